@@ -1,0 +1,158 @@
+/* seghdc_cuda.h — C-ABI of the B200-native SegHDC encode + cluster hot path.
+ *
+ * The reference (arXiv 2303.12753 artifact, /root/reference/proj) exposes this path only as
+ * the C++ API of its static library `seghdc`; it has no FFI. Each entry point below names the
+ * reference interface it replaces (file:line, relative to proj/). The C++ drop-in library
+ * (include/seghdc/seghdc.hpp) and the Python host API (paper_2303_12753_b200) are written
+ * on top of exactly these symbols; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types cross this boundary.
+ *  - Hypervectors use the reference layout: ceil(dim/64) little-endian u64 words, bit i =
+ *    (w[i>>6] >> (i&63)) & 1, tail bits zero (include/seghdc/hypervector.hpp:15-42). A grid is
+ *    h*w*ceil(dim/64) contiguous u64 words, row-major (pixel_pipeline.hpp:38-62).
+ *  - Centroids are k*dim u32 (raw integer member sums, clusterer.hpp:27-34).
+ *  - Return value: SEGHDC_OK, SEGHDC_ECONFIG (the reference would throw ConfigError,
+ *    errors.hpp:9-12) or SEGHDC_ERUNTIME (CUDA failure; the reference has no analogue).
+ *    No exception ever crosses this boundary; seghdc_last_error() holds the message.
+ *  - One context per (host thread, device). Calls are ordered on the context's stream and
+ *    are synchronous unless the name ends in _async.
+ */
+#ifndef SEGHDC_CUDA_H
+#define SEGHDC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEGHDC_OK 0
+#define SEGHDC_ECONFIG 1
+#define SEGHDC_ERUNTIME 2
+
+#define SEGHDC_ENCODER_MANHATTAN 0 /* EncoderKind::manhattan (pixel_pipeline.hpp:64) */
+#define SEGHDC_ENCODER_RPOS 1      /* EncoderKind::rpos */
+#define SEGHDC_ENCODER_RCOLOR 2    /* EncoderKind::rcolor */
+
+typedef struct seghdc_ctx seghdc_ctx;
+
+/* Per-round observer: (user, 1-based round, labels of that round [n_local]). Mirrors
+ * IterationCallback (clusterer.hpp:74); invoked synchronously after each assignment. */
+typedef void (*seghdc_round_cb)(void* user, size_t round, const uint32_t* labels);
+
+/* ---- context -------------------------------------------------------------------------- */
+int seghdc_create(int device, seghdc_ctx** out);
+void seghdc_destroy(seghdc_ctx* ctx);
+/* Last error message of ctx (or of the calling thread when ctx is NULL). */
+const char* seghdc_last_error(const seghdc_ctx* ctx);
+/* Order all further work of ctx on an external cudaStream_t (NULL: the context's own). */
+int seghdc_set_stream(seghdc_ctx* ctx, void* cuda_stream);
+int seghdc_synchronize(seghdc_ctx* ctx);
+/* Number of device kernels this context has launched so far (for launch accounting). */
+uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx);
+
+/* ---- host-side codebooks (stay on the host: mt19937_64 is sequential and cheap) -------- */
+/* run_pipeline's codebook stage (pipeline.cpp:43-59): one Rng(seed), position codebook
+ * (position_encoder.hpp:45, or build_random_position_codebook pixel_pipeline.hpp:79 for
+ * RPOS), then colour codebook (color_encoder.hpp:42, or build_random_color_codebook
+ * pixel_pipeline.hpp:82 for RCOLOR). Outputs row_out[h][wph], col_out[w][wph] and the colour
+ * tables widened to full dim, widened_out[c][256][wph] (pixel_pipeline.cpp:70-88). */
+int seghdc_build_codebooks(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta,
+                           size_t gamma, uint64_t seed, int encoder, uint64_t* row_out,
+                           uint64_t* col_out, uint64_t* widened_out);
+/* RunConfig::validate (pipeline.cpp:25-30) without building anything. */
+int seghdc_validate_run(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta,
+                        size_t gamma, size_t k, size_t iterations);
+
+/* ---- encode_image (pixel_pipeline.hpp:74-75) ----------------------------------------- */
+/* Uploads image + tables, materialises the pixel HV grid on the device (it stays resident
+ * in ctx for cluster), and copies it to grid_out if non-NULL. */
+int seghdc_encode(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c,
+                  size_t dim, const uint64_t* row_words, const uint64_t* col_words,
+                  const uint64_t* widened_words, uint64_t* grid_out);
+
+/* ---- clustering on a host grid (clusterer.hpp:54-80) --------------------------------- */
+/* select_initial_centroids (clusterer.hpp:54-55); seeds as row-major linear indices. */
+int seghdc_select_seeds(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c,
+                        size_t k, uint64_t* seeds_out);
+/* assign_labels (clusterer.hpp:60). grid may be NULL to use the resident grid. */
+int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim,
+                  const uint32_t* centroids, size_t k, uint32_t* labels_out);
+/* update_centroids (clusterer.hpp:65-66). grid may be NULL to use the resident grid.
+ * prev_counts is accepted for API parity and ignored (the reference ignores it too). */
+int seghdc_update(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim,
+                  const uint32_t* labels, const uint32_t* prev_centroids, size_t k,
+                  uint32_t* centroids_out, uint64_t* counts_out);
+/* cluster (clusterer.hpp:79-80). grid may be NULL to use the resident grid (then h, w, dim
+ * must match it). Outputs: labels_out[h*w]; optional centroids_out[k*dim] and
+ * counts_out[k] = the centroid set used by the final assignment round (cluster() itself
+ * hides it; clusterer.hpp:68-71); rounds_out = ClusterResult::iterations_run. */
+int seghdc_cluster(seghdc_ctx* ctx, const uint64_t* grid, const uint8_t* pixels, size_t h,
+                   size_t w, size_t c, size_t dim, size_t k, size_t iterations, int early_stop,
+                   seghdc_round_cb on_round, void* user, uint32_t* labels_out,
+                   uint32_t* centroids_out, uint64_t* counts_out, size_t* rounds_out);
+
+/* ---- whole pipeline (pipeline.hpp:55-56, run_pipeline) ------------------------------- */
+/* timings_ms_out (nullable) receives {encode_position, encode_color, produce_pixels,
+ * cluster, total} in that order (StageTimings, pipeline.hpp:37-45); device stages are
+ * timed with CUDA events. */
+int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c,
+                        size_t dim, double alpha, size_t beta, size_t gamma, size_t k,
+                        size_t iterations, uint64_t seed, int encoder, int early_stop,
+                        seghdc_round_cb on_round, void* user, uint32_t* labels_out,
+                        size_t* rounds_out, double* timings_ms_out);
+
+/* ---- device-resident staging (no reference analogue: keeps HVs in HBM) --------------- */
+/* Image: full image on every rank. Codebooks: tables as produced by seghdc_build_codebooks.
+ * Pointers are host pointers unless the *_device variant is used. */
+int seghdc_load_image(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c);
+int seghdc_load_codebooks(seghdc_ctx* ctx, size_t dim, const uint64_t* row_words,
+                          const uint64_t* col_words, const uint64_t* widened_words);
+/* Encode image rows [row_begin, row_end) (a row-block shard; 0..h for the whole image)
+ * into the resident grid. No host synchronisation. */
+int seghdc_encode_async(seghdc_ctx* ctx, size_t row_begin, size_t row_end);
+/* Resident grid <-> host (reference layout). load_grid sets rows [row_begin,row_end). */
+int seghdc_load_grid(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim,
+                     size_t row_begin, size_t row_end);
+int seghdc_store_grid(seghdc_ctx* ctx, uint64_t* grid_out);
+/* Full clustering loop on the resident grid/image without host synchronisation (no
+ * callback). Results stay on the device until seghdc_fetch_results. */
+int seghdc_cluster_async(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop);
+int seghdc_fetch_results(seghdc_ctx* ctx, uint32_t* labels_out, uint32_t* centroids_out,
+                         uint64_t* counts_out, size_t* rounds_out);
+
+/* ---- row-block sharding across ranks (one process per GPU) --------------------------- */
+/* The caller owns the collective (e.g. torch.distributed / NCCL all_reduce, SUM, int32) on
+ * the device buffer returned by seghdc_exchange_buffer; everything else is local.
+ *   seghdc_shard_begin(k, iterations, early_stop)      seeds (redundant per rank), colsums
+ *   -> all_reduce(exchange)                            init: seed-pixel bits + colsums
+ *   seghdc_shard_init_finish()
+ *   for r in 1..iterations:
+ *     seghdc_shard_assign(r)                            labels + per-shard partial sums
+ *     if seghdc_shard_round_needs_exchange(r):
+ *        -> all_reduce(exchange)                        [k*dim sums | k counts | changed]
+ *        seghdc_shard_finish(r)                         identical finalisation on all ranks
+ * Integer sums are order independent, so every rank holds bit-identical centroids. */
+int seghdc_shard_begin(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop);
+int seghdc_exchange_buffer(seghdc_ctx* ctx, void** device_ptr, size_t* n_int32);
+/* Host-staged exchange (e.g. a gloo/MPI all-reduce, or G shards emulated on one device):
+ * copy the current exchange buffer (n_int32 entries) to / from host memory. */
+int seghdc_exchange_download(seghdc_ctx* ctx, int32_t* host);
+int seghdc_exchange_upload(seghdc_ctx* ctx, const int32_t* host);
+int seghdc_shard_init_finish(seghdc_ctx* ctx);
+int seghdc_shard_assign(seghdc_ctx* ctx, size_t round);
+int seghdc_shard_round_needs_exchange(const seghdc_ctx* ctx, size_t round);
+int seghdc_shard_finish(seghdc_ctx* ctx, size_t round);
+
+/* ---- synthetic inputs (bench/test workloads) --------------------------- */
+/* config_id 0..4 = BASELINE.json configs; config 2 is config 0's construction (use seed
+ * 0..63 per image). Writes h*w*c bytes. Returns the shape through h/w/c when out is NULL. */
+int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w,
+                       size_t* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEGHDC_CUDA_H */

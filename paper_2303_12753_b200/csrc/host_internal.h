@@ -1,0 +1,28 @@
+// Internal host helpers shared by the C-ABI layer (not part of the public interface).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+namespace seghdc_host {
+
+// Carries a C-ABI status code (SEGHDC_ECONFIG / SEGHDC_ERUNTIME) with the message.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void validate_position(size_t dim, size_t h, size_t w, double alpha, size_t beta);
+void validate_color(size_t dim, size_t c, size_t gamma);
+void validate_image(size_t h, size_t w, size_t c);
+void validate_cluster(size_t k, size_t iterations, size_t pixel_count);
+
+void build_position(size_t dim, size_t h, size_t w, double alpha, size_t beta, int encoder, std::mt19937_64& rng,
+                    uint64_t* row_out, uint64_t* col_out);
+void build_color(size_t dim, size_t c, size_t gamma, int encoder, std::mt19937_64& rng, uint64_t* widened_out);
+
+void synth_image(int id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c);
+
+}  // namespace seghdc_host

@@ -1,0 +1,217 @@
+// B200 (sm_100a) kernels for the SegHDC encode + cluster hot path.
+//
+// Device data layout:
+//   grid      u32[n_local][S32]      pixel HV as 32-bit little-endian words (bit i of the HV is
+//                                    bit (i&31) of word i>>5 — the same bytes as the reference's
+//                                    u64 words, hypervector.hpp:15-42), S32 = W32 rounded up to
+//                                    4 words so every pixel row is 16-byte aligned for TMA.
+//   Z         u32[K][D]              centroids: raw member sums (clusterer.hpp:27-34)
+//   bfrag     u64[NT][W32P][32]      Z split into 4 byte planes, laid out as the B fragments of
+//                                    mma.m16n8k32 (column n = 4*c + plane, NT = ceil(K/2)
+//                                    n-tiles of 8), with the k-slot permutation of unpack_a().
+//   partials  u32[CTAs][K][Dp]       per-CTA centroid sums (Dp = 32*W32), exact integers.
+//   xchg      i32[K*Dp | K | 1 | Dp] [sums | counts | changed | column sums]; the only buffer
+//                                    a multi-GPU run all-reduces.
+//
+// Similarity is the reference's exact integer dot (hypervector.cpp:138-151):
+//   dot(y, z_c) = sum_{i: y_i = 1} z_c[i] = sum_p 256^p * (Y . plane_p(z_c))
+// computed as an integer GEMM Y[px x D] * B[D x 4K] on the IMMA tensor pipe (u8 x u8 -> s32,
+// exact), then recombined in u64 and compared with the reference's 128-bit cross
+// multiplication (clusterer.cpp:41-50). Centroid re-bundling (hypervector.cpp:112-121) is a
+// bit-sliced Harley-Seal carry-save counter per 32-bit word column. No floating point.
+#pragma once
+#include <cstdint>
+
+namespace seghdc_dev {
+
+constexpr uint32_t kTileWarpsMax = 16;  // 512 threads: one warp per 32 HV words
+
+// ------------------------------------------------------------------------------------------
+// Device-side round state. Index [p] is the round parity (round r uses p = r & 1); the
+// double buffering lets round r's consumer and round r+1's producer run back to back
+// without host synchronisation.
+struct RoundState {
+    uint32_t done;        // early stop fired (clusterer.cpp:213)
+    uint32_t rounds_run;  // ClusterResult::iterations_run
+    uint32_t uniform;     // seed selection hit the uniform-image fallback
+    uint32_t pad;
+};
+// Followed in memory by (K = number of clusters):
+//   u32 counts[2][K]     members assigned in the round (accumulated by assign)
+//   u32 changed[2]       labels changed vs. the previous round
+//   u32 cur[2][K]        member counts of the centroid set used by the round's assignment
+//   u64 norm2[2][K]      IntVector::norm_squared of that set (hypervector.cpp:123-127)
+struct StateView {
+    RoundState* hdr;
+    uint32_t* counts;
+    uint32_t* changed;
+    uint32_t* cur;
+    unsigned long long* norm2;
+    uint32_t K;
+    __host__ __device__ static size_t bytes(uint32_t K) {
+        size_t b = sizeof(RoundState) + (2 * K + 2 + 2 * K) * 4;
+        b = (b + 7) & ~size_t(7);
+        return b + 2 * K * 8;
+    }
+    __host__ __device__ static StateView at(void* base, uint32_t K) {
+        StateView v;
+        v.hdr = reinterpret_cast<RoundState*>(base);
+        v.counts = reinterpret_cast<uint32_t*>(v.hdr + 1);
+        v.changed = v.counts + 2 * K;
+        v.cur = v.changed + 2;
+        size_t off = sizeof(RoundState) + (2 * K + 2 + 2 * K) * 4;
+        off = (off + 7) & ~size_t(7);
+        v.norm2 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + off);
+        v.K = K;
+        return v;
+    }
+};
+
+// Cluster whose sums are derived as colsum - sum(others) instead of accumulated: the
+// largest cluster of the current centroid set (ties -> lowest index). Any choice is exact.
+__device__ __forceinline__ uint32_t pick_skip(const uint32_t* cur, uint32_t K) {
+    uint32_t best = 0, bv = cur[0];
+    for (uint32_t c = 1; c < K; ++c)
+        if (cur[c] > bv) { bv = cur[c]; best = c; }
+    return best;
+}
+
+// strictly_closer (clusterer.cpp:41-50): dot_c^2 * n2_best > dot_best^2 * n2_c evaluated in
+// unsigned 128-bit arithmetic (wrapping modulo 2^128 exactly like the reference).
+__device__ __forceinline__ bool strictly_closer(unsigned long long dc, unsigned long long n2c,
+                                                unsigned long long db, unsigned long long n2b) {
+    if (n2c == 0) return false;
+    if (n2b == 0) return dc > 0;
+    const unsigned __int128 lhs = (unsigned __int128)dc * dc * n2b;
+    const unsigned __int128 rhs = (unsigned __int128)db * db * n2c;
+    return lhs > rhs;
+}
+
+// ------------------------------------------------------------------------------------------
+// Harley-Seal bit-sliced counter: 32 independent counters (one per bit of a 32-bit word
+// column), count = ones + 2 twos + 4 fours + 8 eights + sum_m 16*2^m hi[m].
+// 15 carry-save adders (2 LOP3 each) per 16 inputs + an H-plane ripple of the weight-16 word.
+template <int H>
+struct BitCounter {
+    uint32_t o, t, f, e, hi[H];
+    __device__ __forceinline__ void reset() {
+        o = t = f = e = 0;
+#pragma unroll
+        for (int m = 0; m < H; ++m) hi[m] = 0;
+    }
+    __device__ __forceinline__ static void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
+        const uint32_t u = a ^ b;
+        h = (a & b) | (u & c);
+        l = u ^ c;
+    }
+    __device__ __forceinline__ void add16(const uint32_t (&x)[16]) {
+        uint32_t tA, tB, fA, fB, eA, eB, s;
+        csa(tA, o, o, x[0], x[1]);
+        csa(tB, o, o, x[2], x[3]);
+        csa(fA, t, t, tA, tB);
+        csa(tA, o, o, x[4], x[5]);
+        csa(tB, o, o, x[6], x[7]);
+        csa(fB, t, t, tA, tB);
+        csa(eA, f, f, fA, fB);
+        csa(tA, o, o, x[8], x[9]);
+        csa(tB, o, o, x[10], x[11]);
+        csa(fA, t, t, tA, tB);
+        csa(tA, o, o, x[12], x[13]);
+        csa(tB, o, o, x[14], x[15]);
+        csa(fB, t, t, tA, tB);
+        csa(eB, f, f, fA, fB);
+        csa(s, e, e, eA, eB);
+#pragma unroll
+        for (int m = 0; m < H; ++m) {
+            const uint32_t c = hi[m] & s;
+            hi[m] ^= s;
+            s = c;
+        }
+    }
+    // capacity of the counter (largest representable count)
+    __host__ __device__ static constexpr uint64_t capacity() { return 15ull + 16ull * ((1ull << H) - 1); }
+    // dst[b] = count of bit b, b = 0..31 (32 consecutive u32)
+    __device__ __forceinline__ void store(uint32_t* dst) const {
+#pragma unroll 4
+        for (int b = 0; b < 32; b += 4) {
+            uint4 v;
+            uint32_t* pv = &v.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int bb = b + q;
+                uint32_t val = ((o >> bb) & 1u) | (((t >> bb) & 1u) << 1) | (((f >> bb) & 1u) << 2) |
+                               (((e >> bb) & 1u) << 3);
+#pragma unroll
+                for (int m = 0; m < H; ++m) val |= ((hi[m] >> bb) & 1u) << (4 + m);
+                pv[q] = val;
+            }
+            *reinterpret_cast<uint4*>(dst + b) = v;
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + bulk async copy (TMA engine, cp.async.bulk) + legacy-path IMMA.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// A fragment of m16n8k32 from two packed 32-bit HV words (rows g and g+8 of the m-tile).
+// Lane (g, q) owns k-slots 4q..4q+3 (a0/a1) and 16+4q..16+4q+3 (a2/a3). Slot 4q+j holds bit
+// 2q+8j and slot 16+4q+j holds bit 2q+1+8j of the word; the same permutation is baked into
+// bfrag, so the dot product is unchanged. Each byte is 0 or 128 (one IMAD + one LOP3 per
+// register, split across the FMA and ALU pipes); the 128 scale is removed after reduction.
+__device__ __forceinline__ void unpack_a(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row,
+                                         uint32_t m_even, uint32_t m_odd) {
+    a[0] = (w_lo_row * m_even) & 0x80808080u;
+    a[1] = (w_hi_row * m_even) & 0x80808080u;
+    a[2] = (w_lo_row * m_odd) & 0x80808080u;
+    a[3] = (w_hi_row * m_odd) & 0x80808080u;
+}
+
+// bfrag address of bit i (within a column n of n-tile nt): byte offset inside u64 lane slot
+__host__ __device__ __forceinline__ size_t bfrag_byte(uint32_t nt, uint32_t n_in_tile, uint32_t i,
+                                                      uint32_t W32P) {
+    const uint32_t word = i >> 5, b = i & 31;
+    const uint32_t q = (b & 7) >> 1, j = b >> 3, half = b & 1;
+    const uint32_t lane = (n_in_tile << 2) | q;
+    return ((size_t(nt) * W32P + word) * 32 + lane) * 8 + half * 4 + j;
+}
+
+}  // namespace seghdc_dev

@@ -1,0 +1,108 @@
+// Internal launcher interface between the C-ABI layer (seghdc_capi.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace seghdc_dev {
+
+struct EncodeArgs {
+    const uint8_t* img;  // full image, h*w*c
+    uint32_t w, c;
+    uint64_t pix_begin, pix_end;  // global pixel range encoded into grid[0..)
+    const uint32_t *row, *col, *wid;
+    uint32_t wref;  // u32 words per table entry (2 * ceil(dim/64))
+    uint32_t S32;
+    uint32_t* grid;
+};
+void launch_encode(const EncodeArgs& a, cudaStream_t s);
+
+struct SeedArgs {
+    const uint8_t* img;
+    uint64_t n;
+    uint32_t h, w, c, K;
+    uint16_t* min_dist;
+    uint64_t* seeds;
+    unsigned long long* slots;
+    struct RoundState* hdr;
+};
+void launch_select_seeds(const SeedArgs& a, cudaStream_t s);
+
+struct InitSeedArgs {
+    const uint32_t* grid;
+    uint32_t S32;
+    uint64_t pix_begin, n_local;
+    const uint64_t* seeds;
+    uint32_t K, W32, Dp;
+    int32_t* xchg;
+};
+void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s);
+
+struct AccumulateArgs {
+    const uint32_t* grid;
+    uint32_t S32, W32;
+    uint64_t n;
+    const uint32_t* labels;  // nullptr: every pixel counts for "cluster 0" (column sums)
+    uint32_t K;
+    int skip_mode;  // -1 none, -2 largest current cluster, >= 0 explicit
+    void* state;    // may be nullptr when skip_mode != -2 and count_members == 0
+    uint32_t parity;
+    uint32_t* partials;
+    uint32_t Dp;
+    int count_members;
+    uint32_t blocks;  // pixel-range CTAs (partials has blocks*K*Dp entries)
+};
+uint32_t accumulate_blocks(uint64_t n, uint32_t sms);
+void launch_accumulate(const AccumulateArgs& a, cudaStream_t s);
+
+struct ReduceArgs {
+    const uint32_t* partials;
+    uint32_t nparts, K, Dp;
+    int skip_mode;
+    void* state;
+    uint32_t parity;
+    int32_t* xchg;
+    int copy_tail;
+};
+void launch_reduce(const ReduceArgs& a, cudaStream_t s);
+
+struct FinishArgs {
+    int mode;  // 0 round, 1 init, 2 given centroids, 3 standalone update
+    uint32_t K, D, W32, W32P, Dp;
+    const int32_t* xchg;
+    const int32_t* colsum;
+    uint32_t* Z;
+    uint8_t* bfrag;
+    void* state;
+    uint32_t round;
+    int early_stop;
+};
+void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s);
+void launch_finish(const FinishArgs& a, cudaStream_t s);
+
+struct RoundPlan {
+    uint32_t nwarp_words = 0;  // 32-word blocks per HV
+    uint32_t nwarps = 0;       // warps per CTA
+    uint32_t mt = 0;           // m-tiles of 16 pixels per tile
+    uint32_t ntg = 0;          // n-tiles per group
+    bool fused = false;        // K <= 2: B in registers + fused accumulation
+};
+struct RoundArgs {
+    const uint32_t* grid;
+    uint64_t n;
+    uint32_t S32, SS, W32, W32P, nwarp_words, K, NT;
+    const uint64_t* bfrag;
+    uint32_t* labels;
+    void* state;
+    uint32_t round;
+    int do_update;
+    uint32_t* partials;
+    uint32_t Dp;
+    uint32_t ctas;
+};
+size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K);
+bool plan_round(uint32_t K, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
+cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
+
+}  // namespace seghdc_dev

@@ -1,0 +1,789 @@
+// C-ABI of the SegHDC B200 hot path (include/seghdc_cuda.h): device context, resident buffers,
+// the round schedule and the reference-API entry points. No exception crosses the boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/seghdc_cuda.h"
+#include "host_internal.h"
+#include "kernels.cuh"
+#include "launch.h"
+
+using seghdc_host::Error;
+using namespace seghdc_dev;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(SEGHDC_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    // grow-only; contents are not preserved when it grows
+    void ensure(size_t count, bool zero = false) {
+        if (count > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            n = 0;
+            ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+            n = count;
+            if (zero) ck(cudaMemset(p, 0, count * sizeof(T)), "cudaMemset");
+        }
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+struct Geometry {
+    uint32_t D = 0, W32 = 0, S32 = 0, SS = 0, nwarp_words = 0, W32P = 0, Dp = 0;
+    void set(size_t dim) {
+        D = uint32_t(dim);
+        W32 = uint32_t((dim + 31) / 32);
+        S32 = (W32 + 3) & ~3u;
+        SS = S32 + ((S32 % 32 == 0) ? 4 : 0);  // keep LDS.128 of adjacent rows on distinct banks
+        nwarp_words = (W32 + 31) / 32;
+        W32P = nwarp_words * 32;
+        Dp = W32 * 32;
+    }
+    size_t wph() const { return (D + 63) / 64; }
+};
+
+}  // namespace
+
+struct seghdc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sms = 148;
+    size_t smem_optin = 0;
+    std::string err;
+    uint64_t launches = 0;
+
+    // image (full image on every rank)
+    DevBuf<uint8_t> img;
+    size_t h = 0, w = 0, c = 0;
+    // codebooks
+    DevBuf<uint32_t> row, col, wid;
+    size_t cb_dim = 0, cb_h = 0, cb_w = 0, cb_c = 0;
+    // grid (rows [row_begin,row_end) of an h_total x w image)
+    DevBuf<uint32_t> grid;
+    Geometry g;
+    size_t g_h = 0, g_w = 0, row_begin = 0, row_end = 0;
+    bool grid_valid = false, colsum_valid = false;
+    uint64_t n_local() const { return uint64_t(row_end - row_begin) * g_w; }
+    uint64_t pix_begin() const { return uint64_t(row_begin) * g_w; }
+    // clustering state
+    size_t K = 0, iterations = 0;
+    int early_stop = 0;
+    RoundPlan plan;
+    uint32_t round_ctas = 0, acc_blocks = 0;
+    DevBuf<uint8_t> state, bfrag;
+    DevBuf<uint32_t> labels, Z, partials;
+    DevBuf<int32_t> xchg;
+    DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
+    DevBuf<uint64_t> seeds;
+    DevBuf<unsigned long long> slots;
+    DevBuf<uint16_t> min_dist;
+    int exchange_phase = 0;  // 0: rounds, 1: init (includes colsums)
+
+    void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+    size_t xchg_round_ints() const { return K * g.Dp + K + 1; }
+    int32_t* colsum_ptr() { return xchg.p + xchg_round_ints(); }
+    void count(uint64_t k = 1) { launches += k; }
+    void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
+};
+
+namespace {
+
+template <class F>
+int guarded(seghdc_ctx* ctx, F&& f) {
+    try {
+        if (ctx) ctx->use();
+        f();
+        return SEGHDC_OK;
+    } catch (const Error& e) {
+        (ctx ? ctx->err : g_thread_err) = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        (ctx ? ctx->err : g_thread_err) = e.what();
+        return SEGHDC_ERUNTIME;
+    }
+}
+
+void require(bool cond, const std::string& msg) {
+    if (!cond) throw Error(SEGHDC_ECONFIG, msg);
+}
+
+// ---- resident data ---------------------------------------------------------------------------
+void load_image(seghdc_ctx& x, const uint8_t* px, size_t h, size_t w, size_t c) {
+    seghdc_host::validate_image(h, w, c);
+    x.img.ensure(h * w * c);
+    ck(cudaMemcpyAsync(x.img.p, px, h * w * c, cudaMemcpyHostToDevice, x.stream), "upload image");
+    x.h = h;
+    x.w = w;
+    x.c = c;
+}
+
+void load_codebooks(seghdc_ctx& x, size_t dim, size_t h, size_t w, size_t c, const uint64_t* row,
+                    const uint64_t* col, const uint64_t* wid) {
+    const size_t wph = (dim + 63) / 64, wref = 2 * wph;
+    x.row.ensure(h * wref);
+    x.col.ensure(w * wref);
+    x.wid.ensure(c * 256 * wref);
+    ck(cudaMemcpyAsync(x.row.p, row, h * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload rows");
+    ck(cudaMemcpyAsync(x.col.p, col, w * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload cols");
+    ck(cudaMemcpyAsync(x.wid.p, wid, c * 256 * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload colour tables");
+    x.cb_dim = dim;
+    x.cb_h = h;
+    x.cb_w = w;
+    x.cb_c = c;
+}
+
+void set_grid_shape(seghdc_ctx& x, size_t h, size_t w, size_t dim, size_t r0, size_t r1) {
+    require(dim >= 1, "hypervector dimension must be >= 1");
+    require(dim <= 65536, "dim > 65536 exceeds the exact-integer range of the IMMA similarity kernel");
+    require(r0 < r1 && r1 <= h, "row range out of bounds");
+    x.g.set(dim);
+    x.g_h = h;
+    x.g_w = w;
+    x.row_begin = r0;
+    x.row_end = r1;
+    x.grid.ensure(size_t(x.n_local()) * x.g.S32);
+    x.colsum_valid = false;
+}
+
+void encode_rows(seghdc_ctx& x, size_t r0, size_t r1) {
+    require(x.cb_dim > 0 && x.cb_h == x.h && x.cb_w == x.w && x.cb_c == x.c,
+            "codebooks do not match the loaded image");
+    set_grid_shape(x, x.h, x.w, x.cb_dim, r0, r1);
+    EncodeArgs a{};
+    a.img = x.img.p;
+    a.w = uint32_t(x.w);
+    a.c = uint32_t(x.c);
+    a.pix_begin = uint64_t(r0) * x.w;
+    a.pix_end = uint64_t(r1) * x.w;
+    a.row = x.row.p;
+    a.col = x.col.p;
+    a.wid = x.wid.p;
+    a.wref = uint32_t(2 * x.g.wph());
+    a.S32 = x.g.S32;
+    a.grid = x.grid.p;
+    launch_encode(a, x.stream);
+    x.count();
+    x.check_launch();
+    x.grid_valid = true;
+}
+
+void load_grid(seghdc_ctx& x, const uint64_t* grid, size_t h, size_t w, size_t dim, size_t r0, size_t r1) {
+    set_grid_shape(x, h, w, dim, r0, r1);
+    ck(cudaMemsetAsync(x.grid.p, 0, size_t(x.n_local()) * x.g.S32 * 4, x.stream), "clear grid");
+    const size_t wph = x.g.wph();
+    ck(cudaMemcpy2DAsync(x.grid.p, x.g.S32 * 4, grid + size_t(r0) * w * wph, wph * 8, wph * 8, x.n_local(),
+                         cudaMemcpyHostToDevice, x.stream),
+       "upload grid");
+    x.grid_valid = true;
+}
+
+void store_grid(seghdc_ctx& x, uint64_t* out) {
+    require(x.grid_valid, "no resident grid");
+    const size_t wph = x.g.wph();
+    ck(cudaMemcpy2DAsync(out, wph * 8, x.grid.p, x.g.S32 * 4, wph * 8, x.n_local(), cudaMemcpyDeviceToHost,
+                         x.stream),
+       "download grid");
+    ck(cudaStreamSynchronize(x.stream), "sync");
+}
+
+// ---- clustering schedule ----------------------------------------------------------------------
+void alloc_cluster(seghdc_ctx& x, size_t K) {
+    require(x.grid_valid, "no resident grid: encode or load a grid first");
+    const Geometry& g = x.g;
+    if (!plan_round(uint32_t(K), g.W32, g.SS, x.plan, x.smem_optin))
+        throw Error(SEGHDC_ERUNTIME, "dim " + std::to_string(g.D) + " does not fit the round kernel's shared memory");
+    x.K = K;
+    const uint64_t n = x.n_local();
+    const uint64_t tp = 16ull * x.plan.mt;
+    x.round_ctas = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(x.sms, (n + tp - 1) / tp)));
+    x.acc_blocks = accumulate_blocks(n, uint32_t(x.sms));
+    const uint32_t NT = uint32_t((K + 1) / 2);
+    x.state.ensure(StateView::bytes(uint32_t(K)));
+    x.labels.ensure(n);
+    x.Z.ensure(K * g.D);
+    // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
+    x.bfrag.ensure(size_t(NT) * g.W32P * 32 * 8);
+    ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
+    const size_t parts = std::max<size_t>(x.round_ctas, x.acc_blocks);
+    x.partials.ensure(parts * K * g.Dp);
+    x.xchg.ensure(x.xchg_round_ints() + g.Dp);
+    x.colsum.ensure(g.Dp);
+    x.seeds.ensure(std::max<size_t>(K, 1));
+    x.slots.ensure(2 + K);
+    x.min_dist.ensure(x.h * x.w);
+}
+
+void compute_colsum(seghdc_ctx& x) {
+    // every pixel as "cluster 0": Harley-Seal column sums, then a 1-cluster reduce into the
+    // colsum region of the exchange buffer
+    AccumulateArgs a{};
+    a.grid = x.grid.p;
+    a.S32 = x.g.S32;
+    a.W32 = x.g.W32;
+    a.n = x.n_local();
+    a.labels = nullptr;
+    a.K = 1;
+    a.skip_mode = -1;
+    a.state = nullptr;
+    a.parity = 0;
+    a.partials = x.partials.p;
+    a.Dp = x.g.Dp;
+    a.count_members = 0;
+    a.blocks = x.acc_blocks;
+    launch_accumulate(a, x.stream);
+    ReduceArgs r{};
+    r.partials = x.partials.p;
+    r.nparts = x.acc_blocks;
+    r.K = 1;
+    r.Dp = x.g.Dp;
+    r.skip_mode = -1;
+    r.state = nullptr;
+    r.xchg = x.colsum.p;
+    r.copy_tail = 0;
+    launch_reduce(r, x.stream);
+    x.count(2);
+    x.check_launch();
+    x.colsum_valid = true;
+}
+
+void select_seeds_dev(seghdc_ctx& x, size_t K) {
+    SeedArgs a{};
+    a.img = x.img.p;
+    a.n = uint64_t(x.h) * x.w;
+    a.h = uint32_t(x.h);
+    a.w = uint32_t(x.w);
+    a.c = uint32_t(x.c);
+    a.K = uint32_t(K);
+    a.min_dist = x.min_dist.p;
+    a.seeds = x.seeds.p;
+    a.slots = x.slots.p;
+    a.hdr = reinterpret_cast<RoundState*>(x.state.p);
+    launch_select_seeds(a, x.stream);
+    x.count(2 + (K > 2 ? (K - 2) + 1 : 0));
+    x.check_launch();
+}
+
+void finish(seghdc_ctx& x, int mode, uint32_t round) {
+    const uint32_t np = (round & 1) ^ 1;
+    launch_prep_finish(x.state.p, uint32_t(x.K), np, x.stream);
+    FinishArgs f{};
+    f.mode = mode;
+    f.K = uint32_t(x.K);
+    f.D = x.g.D;
+    f.W32 = x.g.W32;
+    f.W32P = x.g.W32P;
+    f.Dp = x.g.Dp;
+    f.xchg = x.xchg.p;
+    f.colsum = x.colsum_ptr();
+    f.Z = x.Z.p;
+    f.bfrag = x.bfrag.p;
+    f.state = x.state.p;
+    f.round = round;
+    f.early_stop = x.early_stop;
+    launch_finish(f, x.stream);
+    x.count(2);
+    x.check_launch();
+}
+
+// Everything up to (not including) the all-reduce of the init exchange.
+void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
+    require(x.h > 0 && x.w == x.g_w && x.h == x.g_h, "image and grid shapes differ");
+    seghdc_host::validate_cluster(K, iterations, x.h * x.w);
+    alloc_cluster(x, K);
+    x.iterations = iterations;
+    x.early_stop = early_stop;
+    ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K)), x.stream), "clear state");
+    ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
+    select_seeds_dev(x, K);
+    if (!x.colsum_valid) compute_colsum(x);
+    // local column sums into the exchange tail; the init all-reduce makes them global
+    ck(cudaMemcpyAsync(x.colsum_ptr(), x.colsum.p, x.g.Dp * 4, cudaMemcpyDeviceToDevice, x.stream), "colsum");
+    InitSeedArgs a{};
+    a.grid = x.grid.p;
+    a.S32 = x.g.S32;
+    a.pix_begin = x.pix_begin();
+    a.n_local = x.n_local();
+    a.seeds = x.seeds.p;
+    a.K = uint32_t(K);
+    a.W32 = x.g.W32;
+    a.Dp = x.g.Dp;
+    a.xchg = x.xchg.p;
+    launch_init_seeds(a, x.stream);
+    x.count();
+    x.check_launch();
+    x.exchange_phase = 1;
+}
+
+void init_finish(seghdc_ctx& x) {
+    finish(x, 1, 0);
+    x.exchange_phase = 0;
+}
+
+void round_assign(seghdc_ctx& x, uint32_t r) {
+    const bool do_update = r < x.iterations;
+    RoundArgs a{};
+    a.grid = x.grid.p;
+    a.n = x.n_local();
+    a.S32 = x.g.S32;
+    a.SS = x.g.SS;
+    a.W32 = x.g.W32;
+    a.W32P = x.g.W32P;
+    a.nwarp_words = x.g.nwarp_words;
+    a.K = uint32_t(x.K);
+    a.NT = uint32_t((x.K + 1) / 2);
+    a.bfrag = reinterpret_cast<const uint64_t*>(x.bfrag.p);
+    a.labels = x.labels.p;
+    a.state = x.state.p;
+    a.round = r;
+    a.do_update = do_update ? 1 : 0;
+    a.partials = x.partials.p;
+    a.Dp = x.g.Dp;
+    a.ctas = x.round_ctas;
+    ck(launch_round(a, x.plan, x.stream), "round kernel");
+    x.count();
+    if (do_update && !x.plan.fused) {  // K >= 3: separate single-read accumulation pass
+        AccumulateArgs u{};
+        u.grid = x.grid.p;
+        u.S32 = x.g.S32;
+        u.W32 = x.g.W32;
+        u.n = x.n_local();
+        u.labels = x.labels.p;
+        u.K = uint32_t(x.K);
+        u.skip_mode = -2;
+        u.state = x.state.p;
+        u.parity = r & 1;
+        u.partials = x.partials.p;
+        u.Dp = x.g.Dp;
+        u.count_members = 0;
+        u.blocks = x.acc_blocks;
+        launch_accumulate(u, x.stream);
+        x.count();
+        x.check_launch();
+    }
+}
+
+// Partial sums -> exchange buffer (before the all-reduce).
+void round_reduce(seghdc_ctx& x, uint32_t r) {
+    ReduceArgs a{};
+    a.partials = x.partials.p;
+    a.nparts = x.plan.fused ? x.round_ctas : x.acc_blocks;
+    a.K = uint32_t(x.K);
+    a.Dp = x.g.Dp;
+    a.skip_mode = -2;
+    a.state = x.state.p;
+    a.parity = r & 1;
+    a.xchg = x.xchg.p;
+    a.copy_tail = 1;
+    launch_reduce(a, x.stream);
+    x.count();
+    x.check_launch();
+}
+
+struct HostState {
+    RoundState hdr;
+    std::vector<uint32_t> cur[2];
+};
+
+HostState read_state(seghdc_ctx& x) {
+    std::vector<uint8_t> buf(StateView::bytes(uint32_t(x.K)));
+    ck(cudaMemcpyAsync(buf.data(), x.state.p, buf.size(), cudaMemcpyDeviceToHost, x.stream), "read state");
+    ck(cudaStreamSynchronize(x.stream), "sync");
+    StateView v = StateView::at(buf.data(), uint32_t(x.K));
+    HostState h;
+    h.hdr = *v.hdr;
+    for (int p = 0; p < 2; ++p) h.cur[p].assign(v.cur + p * x.K, v.cur + (p + 1) * x.K);
+    return h;
+}
+
+void run_rounds(seghdc_ctx& x, seghdc_round_cb cb, void* user) {
+    std::vector<uint32_t> host_labels;
+    if (cb) host_labels.resize(x.n_local());
+    for (uint32_t r = 1; r <= x.iterations; ++r) {
+        round_assign(x, r);
+        if (cb) {
+            ck(cudaMemcpyAsync(host_labels.data(), x.labels.p, x.n_local() * 4, cudaMemcpyDeviceToHost, x.stream),
+               "download labels");
+            ck(cudaStreamSynchronize(x.stream), "sync");
+            cb(user, r, host_labels.data());
+        }
+        if (r < x.iterations) {
+            round_reduce(x, r);
+            finish(x, 0, r);
+            if (cb && x.early_stop && read_state(x).hdr.done) break;
+        }
+    }
+}
+
+void fetch(seghdc_ctx& x, uint32_t* labels, uint32_t* centroids, uint64_t* counts, size_t* rounds) {
+    if (labels)
+        ck(cudaMemcpyAsync(labels, x.labels.p, x.n_local() * 4, cudaMemcpyDeviceToHost, x.stream), "download labels");
+    if (centroids)
+        ck(cudaMemcpyAsync(centroids, x.Z.p, x.K * x.g.D * 4, cudaMemcpyDeviceToHost, x.stream), "download centroids");
+    const HostState h = read_state(x);  // synchronises
+    if (rounds) *rounds = h.hdr.rounds_run;
+    if (counts)
+        for (size_t c = 0; c < x.K; ++c) counts[c] = h.cur[h.hdr.rounds_run & 1][c];
+}
+
+void cluster_full(seghdc_ctx& x, size_t K, size_t iterations, int early_stop, seghdc_round_cb cb, void* user) {
+    cluster_begin(x, K, iterations, early_stop);
+    init_finish(x);
+    run_rounds(x, cb, user);
+}
+
+}  // namespace
+
+// ================================ C-ABI ========================================================
+extern "C" {
+
+int seghdc_create(int device, seghdc_ctx** out) {
+    auto ctx = std::make_unique<seghdc_ctx>();
+    ctx->device = device;
+    const int rc = guarded(nullptr, [&] {
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+        int optin = 0;
+        ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
+        ctx->smem_optin = size_t(optin);
+        int major = 0;
+        ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device), "attr");
+        if (major != 10) throw Error(SEGHDC_ERUNTIME, "this build targets sm_100a (B200); device is sm_" + std::to_string(major) + "x");
+        ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+        ctx->own_stream = true;
+    });
+    if (rc != SEGHDC_OK) return rc;
+    *out = ctx.release();
+    return SEGHDC_OK;
+}
+
+void seghdc_destroy(seghdc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* seghdc_last_error(const seghdc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
+
+int seghdc_set_stream(seghdc_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+            ctx->own_stream = false;
+        } else {
+            ck(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+            ctx->own_stream = true;
+        }
+    });
+}
+
+int seghdc_synchronize(seghdc_ctx* ctx) {
+    return guarded(ctx, [&] { ck(cudaStreamSynchronize(ctx->stream), "sync"); });
+}
+
+uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int seghdc_build_codebooks(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta, size_t gamma,
+                           uint64_t seed, int encoder, uint64_t* row_out, uint64_t* col_out, uint64_t* widened_out) {
+    return guarded(nullptr, [&] {
+        seghdc_host::validate_position(dim, h, w, alpha, beta);
+        seghdc_host::validate_color(dim, c, gamma);
+        std::mt19937_64 rng(seed);  // pipeline.cpp:43: one generator, position first, then colour
+        seghdc_host::build_position(dim, h, w, alpha, beta, encoder, rng, row_out, col_out);
+        seghdc_host::build_color(dim, c, gamma, encoder, rng, widened_out);
+    });
+}
+
+int seghdc_validate_run(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta, size_t gamma, size_t k,
+                        size_t iterations) {
+    return guarded(nullptr, [&] {  // RunConfig::validate, pipeline.cpp:25-30
+        seghdc_host::validate_image(h, w, c);
+        seghdc_host::validate_position(dim, h, w, alpha, beta);
+        seghdc_host::validate_color(dim, c, gamma);
+        seghdc_host::validate_cluster(k, iterations, h * w);
+    });
+}
+
+int seghdc_encode(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c, size_t dim,
+                  const uint64_t* row_words, const uint64_t* col_words, const uint64_t* widened_words,
+                  uint64_t* grid_out) {
+    return guarded(ctx, [&] {
+        load_image(*ctx, pixels, h, w, c);
+        load_codebooks(*ctx, dim, h, w, c, row_words, col_words, widened_words);
+        encode_rows(*ctx, 0, h);
+        if (grid_out) store_grid(*ctx, grid_out);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int seghdc_select_seeds(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c, size_t k,
+                        uint64_t* seeds_out) {
+    return guarded(ctx, [&] {
+        load_image(*ctx, pixels, h, w, c);
+        require(k >= 1 && k <= h * w, "select_initial_centroids: k = " + std::to_string(k) + " out of range for " +
+                                          std::to_string(h * w) + " pixels");
+        ctx->K = k;
+        ctx->state.ensure(StateView::bytes(uint32_t(k)));
+        ctx->seeds.ensure(k);
+        ctx->slots.ensure(2 + k);
+        ctx->min_dist.ensure(h * w);
+        select_seeds_dev(*ctx, k);
+        ck(cudaMemcpyAsync(seeds_out, ctx->seeds.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream), "download seeds");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim, const uint32_t* centroids,
+                  size_t k, uint32_t* labels_out) {
+    return guarded(ctx, [&] {
+        require(k >= 1, "assign_labels: empty centroid set");
+        if (grid) load_grid(*ctx, grid, h, w, dim, 0, h);
+        require(ctx->g.D == dim && ctx->g_h == h && ctx->g_w == w, "assign_labels: dimension mismatch");
+        alloc_cluster(*ctx, k);
+        ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
+        ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
+        ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");
+        finish(*ctx, 2, 0);  // norm2 + B fragments of the given set (parity 1)
+        ctx->iterations = 1;
+        ctx->early_stop = 0;
+        round_assign(*ctx, 1);
+        ck(cudaMemcpyAsync(labels_out, ctx->labels.p, ctx->n_local() * 4, cudaMemcpyDeviceToHost, ctx->stream),
+           "download labels");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int seghdc_update(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim, const uint32_t* labels,
+                  const uint32_t* prev_centroids, size_t k, uint32_t* centroids_out, uint64_t* counts_out) {
+    return guarded(ctx, [&] {
+        if (grid) load_grid(*ctx, grid, h, w, dim, 0, h);
+        require(ctx->g_h == h && ctx->g_w == w, "update_centroids: mask shape does not match grid");
+        require(ctx->g.D == dim, "update_centroids: dimension mismatch");
+        for (size_t p = 0; p < h * w; ++p)  // clusterer.cpp:176-179
+            if (labels[p] >= k)
+                throw Error(SEGHDC_ECONFIG, "update_centroids: label " + std::to_string(labels[p]) +
+                                                " out of range for k = " + std::to_string(k));
+        alloc_cluster(*ctx, k);
+        ck(cudaMemcpyAsync(ctx->labels.p, labels, h * w * 4, cudaMemcpyHostToDevice, ctx->stream), "upload labels");
+        ck(cudaMemcpyAsync(ctx->Z.p, prev_centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload prev");
+        ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
+        AccumulateArgs u{};
+        u.grid = ctx->grid.p;
+        u.S32 = ctx->g.S32;
+        u.W32 = ctx->g.W32;
+        u.n = ctx->n_local();
+        u.labels = ctx->labels.p;
+        u.K = uint32_t(k);
+        u.skip_mode = -1;
+        u.state = ctx->state.p;
+        u.parity = 1;
+        u.partials = ctx->partials.p;
+        u.Dp = ctx->g.Dp;
+        u.count_members = 1;
+        u.blocks = ctx->acc_blocks;
+        launch_accumulate(u, ctx->stream);
+        ReduceArgs r{};
+        r.partials = ctx->partials.p;
+        r.nparts = ctx->acc_blocks;
+        r.K = uint32_t(k);
+        r.Dp = ctx->g.Dp;
+        r.skip_mode = -1;
+        r.state = ctx->state.p;
+        r.parity = 1;
+        r.xchg = ctx->xchg.p;
+        r.copy_tail = 1;
+        launch_reduce(r, ctx->stream);
+        ctx->count(2);
+        ctx->check_launch();
+        finish(*ctx, 3, 1);
+        ck(cudaMemcpyAsync(centroids_out, ctx->Z.p, k * dim * 4, cudaMemcpyDeviceToHost, ctx->stream),
+           "download centroids");
+        const HostState hs = read_state(*ctx);
+        for (size_t c = 0; c < k; ++c) counts_out[c] = hs.cur[0][c];
+    });
+}
+
+int seghdc_cluster(seghdc_ctx* ctx, const uint64_t* grid, const uint8_t* pixels, size_t h, size_t w, size_t c,
+                   size_t dim, size_t k, size_t iterations, int early_stop, seghdc_round_cb on_round, void* user,
+                   uint32_t* labels_out, uint32_t* centroids_out, uint64_t* counts_out, size_t* rounds_out) {
+    return guarded(ctx, [&] {
+        seghdc_host::validate_cluster(k, iterations, h * w);  // clusterer.cpp:192 validates first
+        load_image(*ctx, pixels, h, w, c);
+        if (grid) load_grid(*ctx, grid, h, w, dim, 0, h);
+        require(ctx->grid_valid && ctx->g_h == h && ctx->g_w == w && ctx->g.D == dim,
+                "cluster: grid shape does not match image");
+        cluster_full(*ctx, k, iterations, early_stop, on_round, user);
+        fetch(*ctx, labels_out, centroids_out, counts_out, rounds_out);
+    });
+}
+
+int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c, size_t dim, double alpha,
+                        size_t beta, size_t gamma, size_t k, size_t iterations, uint64_t seed, int encoder,
+                        int early_stop, seghdc_round_cb on_round, void* user, uint32_t* labels_out, size_t* rounds_out,
+                        double* timings) {
+    return guarded(ctx, [&] {
+        using Clock = std::chrono::steady_clock;
+        auto ms = [](Clock::time_point t0) {
+            return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        };
+        // RunConfig::validate before any work (pipeline.cpp:25-30, 42)
+        seghdc_host::validate_image(h, w, c);
+        seghdc_host::validate_position(dim, h, w, alpha, beta);
+        seghdc_host::validate_color(dim, c, gamma);
+        seghdc_host::validate_cluster(k, iterations, h * w);
+        const auto t_total = Clock::now();
+        const size_t wph = (dim + 63) / 64;
+        std::vector<uint64_t> row(h * wph), col(w * wph), wid(c * 256 * wph);
+        std::mt19937_64 rng(seed);
+        auto t = Clock::now();
+        seghdc_host::build_position(dim, h, w, alpha, beta, encoder, rng, row.data(), col.data());
+        const double t_pos = ms(t);
+        t = Clock::now();
+        seghdc_host::build_color(dim, c, gamma, encoder, rng, wid.data());
+        const double t_col = ms(t);
+        cudaEvent_t e0, e1, e2;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventCreate(&e2), "event");
+        load_image(*ctx, pixels, h, w, c);
+        load_codebooks(*ctx, dim, h, w, c, row.data(), col.data(), wid.data());
+        ck(cudaEventRecord(e0, ctx->stream), "event");
+        encode_rows(*ctx, 0, h);
+        ck(cudaEventRecord(e1, ctx->stream), "event");
+        cluster_full(*ctx, k, iterations, early_stop, on_round, user);
+        ck(cudaEventRecord(e2, ctx->stream), "event");
+        fetch(*ctx, labels_out, nullptr, nullptr, rounds_out);
+        float enc_ms = 0, clu_ms = 0;
+        cudaEventElapsedTime(&enc_ms, e0, e1);
+        cudaEventElapsedTime(&clu_ms, e1, e2);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaEventDestroy(e2);
+        if (timings) {
+            timings[0] = t_pos;
+            timings[1] = t_col;
+            timings[2] = enc_ms;
+            timings[3] = clu_ms;
+            timings[4] = ms(t_total);
+        }
+    });
+}
+
+int seghdc_load_image(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c) {
+    return guarded(ctx, [&] { load_image(*ctx, pixels, h, w, c); });
+}
+
+int seghdc_load_codebooks(seghdc_ctx* ctx, size_t dim, const uint64_t* row, const uint64_t* col,
+                          const uint64_t* wid) {
+    return guarded(ctx, [&] {
+        require(ctx->h > 0, "load the image before its codebooks");
+        load_codebooks(*ctx, dim, ctx->h, ctx->w, ctx->c, row, col, wid);
+    });
+}
+
+int seghdc_encode_async(seghdc_ctx* ctx, size_t row_begin, size_t row_end) {
+    return guarded(ctx, [&] { encode_rows(*ctx, row_begin, row_end); });
+}
+
+int seghdc_load_grid(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, size_t dim, size_t row_begin,
+                     size_t row_end) {
+    return guarded(ctx, [&] { load_grid(*ctx, grid, h, w, dim, row_begin, row_end); });
+}
+
+int seghdc_store_grid(seghdc_ctx* ctx, uint64_t* grid_out) {
+    return guarded(ctx, [&] { store_grid(*ctx, grid_out); });
+}
+
+int seghdc_cluster_async(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop) {
+    return guarded(ctx, [&] { cluster_full(*ctx, k, iterations, early_stop, nullptr, nullptr); });
+}
+
+int seghdc_fetch_results(seghdc_ctx* ctx, uint32_t* labels_out, uint32_t* centroids_out, uint64_t* counts_out,
+                         size_t* rounds_out) {
+    return guarded(ctx, [&] { fetch(*ctx, labels_out, centroids_out, counts_out, rounds_out); });
+}
+
+int seghdc_shard_begin(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop) {
+    return guarded(ctx, [&] { cluster_begin(*ctx, k, iterations, early_stop); });
+}
+
+int seghdc_exchange_buffer(seghdc_ctx* ctx, void** device_ptr, size_t* n_int32) {
+    return guarded(ctx, [&] {
+        require(ctx->xchg.p != nullptr, "no clustering in progress");
+        *device_ptr = ctx->xchg.p;
+        *n_int32 = ctx->xchg_round_ints() + (ctx->exchange_phase == 1 ? ctx->g.Dp : 0);
+    });
+}
+
+int seghdc_exchange_download(seghdc_ctx* ctx, int32_t* host) {
+    return guarded(ctx, [&] {
+        void* p;
+        size_t n;
+        if (seghdc_exchange_buffer(ctx, &p, &n) != SEGHDC_OK) throw Error(SEGHDC_ECONFIG, ctx->err);
+        ck(cudaMemcpyAsync(host, p, n * 4, cudaMemcpyDeviceToHost, ctx->stream), "download exchange");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int seghdc_exchange_upload(seghdc_ctx* ctx, const int32_t* host) {
+    return guarded(ctx, [&] {
+        void* p;
+        size_t n;
+        if (seghdc_exchange_buffer(ctx, &p, &n) != SEGHDC_OK) throw Error(SEGHDC_ECONFIG, ctx->err);
+        ck(cudaMemcpyAsync(p, host, n * 4, cudaMemcpyHostToDevice, ctx->stream), "upload exchange");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int seghdc_shard_init_finish(seghdc_ctx* ctx) {
+    return guarded(ctx, [&] { init_finish(*ctx); });
+}
+
+int seghdc_shard_assign(seghdc_ctx* ctx, size_t round) {
+    return guarded(ctx, [&] {
+        require(round >= 1 && round <= ctx->iterations, "round out of range");
+        round_assign(*ctx, uint32_t(round));
+        if (round < ctx->iterations) round_reduce(*ctx, uint32_t(round));
+    });
+}
+
+int seghdc_shard_round_needs_exchange(const seghdc_ctx* ctx, size_t round) {
+    return ctx && round >= 1 && round < ctx->iterations ? 1 : 0;
+}
+
+int seghdc_shard_finish(seghdc_ctx* ctx, size_t round) {
+    return guarded(ctx, [&] { finish(*ctx, 0, uint32_t(round)); });
+}
+
+int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c) {
+    return guarded(nullptr, [&] { seghdc_host::synth_image(config_id, seed, out, h, w, c); });
+}
+
+}  // extern "C"

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the reference's goldens.
+
+Bit-exact for everything (labels, centroids, member counts, rounds, seeds, grid words): the
+path is integer-only (no floating point anywhere in assignment)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2303_12753_b200 as S
+from conftest import instance_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- reference suites' instances
+def test_bruteforce_instances(ctx, golden_instances):
+    """test_clusterer.cpp:211-235 and acceptance criterion 5: per-round labels of 60 tiny
+    instances (<= 16 px, d <= 32, k <= 3) equal the reference's brute-force oracle."""
+    for inst in golden_instances:
+        img, grid = instance_arrays(inst)
+        rounds = []
+        res = ctx.cluster(grid, img, inst["dim"], inst["k"], inst["iterations"], False,
+                          on_iteration=lambda r, lab: rounds.append(lab.tolist()))
+        assert rounds == inst["expected_rounds"], (inst["suite"], inst["instance"])
+        assert res["rounds"] == inst["iterations"]
+        assert ctx.select_initial_centroids(img, inst["k"]).tolist() == inst["seeds"]
+
+
+# ---------------------------------------------------------------- encode
+@pytest.mark.parametrize("dim,h,w,c,enc,beta", [
+    (10000, 40, 37, 3, "manhattan", 26), (10000, 23, 50, 1, "manhattan", 3), (16384, 20, 21, 3, "manhattan", 26),
+    (999, 9, 13, 3, "rpos", 2), (1001, 7, 5, 3, "rcolor", 1), (2048, 8, 8, 3, "manhattan", 2), (600, 1, 1, 1, "manhattan", 1),
+    (4096, 16, 16, 1, "manhattan", 1), (31000, 6, 7, 3, "manhattan", 2),
+])
+def test_encode_matches_reference(ctx, port, dim, h, w, c, enc, beta):
+    rng = np.random.default_rng(dim + h)
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    cb = S.build_codebooks(dim, h, w, c, 1.0, beta, 1, 7, enc)
+    grid = ctx.encode_image(img, dim, *cb)
+    assert (grid == port.encode(img, dim, *cb)).all()
+
+
+# ---------------------------------------------------------------- assign / update
+def _rand_grid(rng, n, dim, density=0.5):
+    bits = (rng.random((n, dim)) < density).astype(np.uint8)
+    pad = (-dim) % 64
+    bits = np.concatenate([bits, np.zeros((n, pad), np.uint8)], axis=1)
+    return np.packbits(bits.reshape(n, -1, 8)[:, :, ::-1], axis=2).reshape(n, -1).view("<u8").copy()
+
+
+@pytest.mark.parametrize("dim,k,zmax", [(10000, 2, 1 << 19), (10000, 2, 3), (333, 1, 10), (10000, 4, 1 << 22),
+                                         (16384, 8, 1 << 24), (777, 3, 1000), (64, 9, 50), (40000, 2, 1 << 20),
+                                         (10000, 17, 1 << 16), (5000, 5, (1 << 32) - 1)])
+def test_assign_matches_oracle(ctx, port, dim, k, zmax):
+    rng = np.random.default_rng(dim * 31 + k)
+    h, w = 37, 41
+    grid = _rand_grid(rng, h * w, dim)
+    z = rng.integers(0, zmax, (k, dim), dtype=np.uint64).astype(np.uint32)
+    if k > 2:
+        z[1] = z[0]          # exact tie: lower index wins
+        z[2] = z[0] * 3      # magnitude invariance (clusterer.hpp:27-28)
+    lab = ctx.assign_labels(grid, h, w, dim, z)
+    assert (lab == port.assign(grid, dim, z)).all()
+
+
+def test_assign_zero_centroid_and_ties(ctx, port):
+    # strictly_closer edge rules (clusterer.cpp:43-44) and test_clusterer.cpp:82-104
+    dim = 8
+    grid = np.array([[0b00000011], [0b00001100]], np.uint64)
+    z = np.array([[1, 1, 0, 0, 0, 0, 0, 0], [0, 0, 1, 1, 0, 0, 0, 0]], np.uint32)
+    assert ctx.assign_labels(grid, 1, 2, dim, z).tolist() == [0, 1]
+    tie = np.array([[1, 0, 1, 0, 0, 0, 0, 0]] * 2, np.uint32)
+    assert ctx.assign_labels(grid, 1, 2, dim, tie).tolist() == [0, 0]
+    zero = np.zeros((3, dim), np.uint32)
+    zero[2, 0] = 5
+    assert (ctx.assign_labels(grid, 1, 2, dim, zero) == port.assign(grid, dim, zero)).all()
+
+
+@pytest.mark.parametrize("dim,k", [(10000, 2), (10000, 4), (16384, 8), (100, 3), (40000, 2), (7, 1)])
+def test_update_matches_oracle(ctx, port, dim, k):
+    rng = np.random.default_rng(dim + k)
+    h, w = 53, 61
+    grid = _rand_grid(rng, h * w, dim, density=0.3)
+    labels = rng.integers(0, max(1, k - 1), h * w, dtype=np.uint32)  # cluster k-1 stays empty
+    prev = rng.integers(0, 1000, (k, dim), dtype=np.uint32)
+    z, counts = ctx.update_centroids(grid, h, w, dim, labels, prev)
+    z2, c2 = port.update(grid, dim, labels, prev)
+    assert (z == z2).all() and (counts == c2).all()
+    # update example of test_clusterer.cpp:124-149 ({1100,1010} -> (2,1,1,0), empty keeps previous)
+    g = np.array([[0b0011], [0b0101]], np.uint64)
+    zz, cc = ctx.update_centroids(g, 1, 2, 4, np.array([0, 0], np.uint32), np.array([[0, 0, 0, 1], [1, 1, 1, 1]], np.uint32))
+    assert zz.tolist() == [[2, 1, 1, 0], [1, 1, 1, 1]] and cc.tolist() == [2, 0]
+
+
+def test_update_rejects_rogue_label(ctx):
+    g = np.array([[0b0011], [0b0101]], np.uint64)
+    with pytest.raises(S.ConfigError):
+        ctx.update_centroids(g, 1, 2, 4, np.array([0, 7], np.uint32), np.zeros((2, 4), np.uint32))
+
+
+# ---------------------------------------------------------------- seeds
+def test_seed_selection(ctx, port):
+    img = np.zeros((1, 4, 1), np.uint8)
+    img[0, :, 0] = [0, 100, 255, 120]
+    assert ctx.select_initial_centroids(img, 3).tolist() == [0, 2, 3]  # test_clusterer.cpp:70-80
+    uni = np.full((3, 4, 3), 128, np.uint8)
+    assert ctx.select_initial_centroids(uni, 5).tolist() == [0, 3, 8, 11, 1]  # :51-61
+    img2 = np.full((2, 2, 1), 50, np.uint8)
+    img2[0, 1] = img2[1, 0] = 7
+    assert ctx.select_initial_centroids(img2, 1).tolist() == [1]  # :41-49
+    rng = np.random.default_rng(3)
+    for t in range(8):
+        im = rng.integers(0, 6 if t % 2 else 256, (31, 29, 3 if t < 4 else 1), dtype=np.uint8)
+        for k in (1, 2, 3, 7, 12):
+            assert (ctx.select_initial_centroids(im, k) == port.select_seeds(im, k)).all(), (t, k)
+    with pytest.raises(S.ConfigError):
+        ctx.select_initial_centroids(uni, 13)
+
+
+# ---------------------------------------------------------------- full loop, random
+@pytest.mark.parametrize("case", range(12))
+def test_cluster_random_vs_oracle(ctx, port, case):
+    rng = np.random.default_rng(1000 + case)
+    h, w = int(rng.integers(5, 90)), int(rng.integers(5, 90))
+    c = int(rng.choice([1, 3]))
+    dim = int(rng.choice([800, 1024, 2000, 10000, 16384]))
+    k = int(rng.integers(1, 7))
+    iterations = int(rng.integers(1, 9))
+    es = bool(case % 2)
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    if case % 3 == 0:
+        img = (img // 64) * 64  # many colour ties
+    alpha = 1.0
+    beta = int(rng.integers(1, 5))
+    cb = S.build_codebooks(dim, h, w, c, alpha, beta, 1, case)
+    grid = port.encode(img, dim, *cb)
+    got_rounds = []
+    res = ctx.cluster(grid, img, dim, k, iterations, es, on_iteration=lambda r, lab: got_rounds.append(lab))
+    exp = port.cluster(grid, img, dim, k, iterations, es, per_round=True)
+    assert res["rounds"] == exp["rounds"]
+    assert len(got_rounds) == exp["rounds"]
+    for r in range(exp["rounds"]):
+        assert (got_rounds[r] == exp["labels_rounds"][r]).all(), r
+    assert (res["labels"] == exp["labels"]).all()
+    assert (res["centroids"] == exp["centroids"]).all()
+    assert (res["counts"] == exp["counts"]).all()
+    # the same call without a callback runs with no host synchronisation between rounds
+    res2 = ctx.cluster(None, img, dim, k, iterations, es)
+    assert res2["rounds"] == exp["rounds"] and (res2["labels"] == exp["labels"]).all()
+    assert (res2["centroids"] == exp["centroids"]).all()
+
+
+def test_k1_stops_at_round_two(ctx, port):
+    # test_clusterer.cpp:168-174
+    img = np.full((2, 2, 1), 10, np.uint8)
+    grid = _rand_grid(np.random.default_rng(10), 4, 16)
+    res = ctx.cluster(grid, img, 16, 1, 10, True)
+    assert res["rounds"] == 2 and res["labels"].tolist() == [0, 0, 0, 0]
+
+
+def test_cluster_validation(ctx):
+    img = np.zeros((2, 2, 1), np.uint8)
+    grid = np.zeros((4, 1), np.uint64)
+    with pytest.raises(S.ConfigError):
+        ctx.cluster(grid, img, 16, 5, 10, True)
+    with pytest.raises(S.ConfigError):
+        ctx.cluster(grid, img, 16, 1, 0, True)
+
+
+# ---------------------------------------------------------------- BASELINE.json configs
+def _config_run(ctx, golden_configs, name, image_seed=0, iterations=None, early_stop=False):
+    spec = golden_configs["_meta"]["configs"][name]
+    img = S.synth_image(spec["cid"], image_seed)
+    h, w, c = img.shape
+    cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], 26, 1, 0)
+    ctx.encode_image(img, spec["dim"], *cb, download=False)
+    rounds = []
+    res = ctx.cluster(None, img, spec["dim"], spec["k"], iterations or spec["iterations"], early_stop,
+                      on_iteration=lambda r, lab: rounds.append(sha(lab)))
+    return img, res, rounds
+
+
+@pytest.mark.parametrize("name", ["C0", "C1"])
+def test_config_golden_reference(ctx, golden_configs, name):
+    """C0/C1 goldens come from the reference library itself (tests/golden/make_golden.py)."""
+    g = golden_configs[name]
+    img, res, rounds = _config_run(ctx, golden_configs, name)
+    assert sha(img) == g["image_sha256"]
+    assert rounds == g["round_labels_sha256"]
+    assert sha(res["labels"]) == g["labels_sha256"]
+    assert sha(res["centroids"]) == g["centroids_sha256"]
+    assert res["counts"].tolist() == g["counts"] and res["rounds"] == g["rounds"]
+    _, es, _ = _config_run(ctx, golden_configs, name, early_stop=True)
+    assert es["rounds"] == g["early_stop_rounds"] and sha(es["labels"]) == g["early_stop_labels_sha256"]
+
+
+def test_config_c2_batch(ctx, golden_configs):
+    spec = golden_configs["_meta"]["configs"]["C2"]
+    for s, g in enumerate(golden_configs["C2"]["images"]):
+        img = S.synth_image(2, s)
+        h, w, c = img.shape
+        cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], 26, 1, 0)
+        ctx.encode_image(img, spec["dim"], *cb, download=False)
+        res = ctx.cluster(None, img, spec["dim"], spec["k"], spec["iterations"], False)
+        assert sha(res["labels"]) == g["labels_sha256"], s
+        assert sha(res["centroids"]) == g["centroids_sha256"], s
+        assert res["counts"].tolist() == g["counts"], s
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_config_large_golden(ctx, golden_configs, name):
+    """C3 (20 rounds) / C4 (first 2 rounds) against the validated port."""
+    if name not in golden_configs:
+        pytest.skip(f"{name} golden not generated")
+    g = golden_configs[name]
+    img, res, rounds = _config_run(ctx, golden_configs, name, iterations=g["iterations"])
+    assert sha(img) == g["image_sha256"]
+    assert rounds == g["round_labels_sha256"]
+    assert sha(res["centroids"]) == g["centroids_sha256"]
+    assert res["counts"].tolist() == g["counts"]
