@@ -146,6 +146,13 @@ int seghdc_shard_assign(seghdc_ctx* ctx, size_t round);
 int seghdc_shard_round_needs_exchange(const seghdc_ctx* ctx, size_t round);
 int seghdc_shard_finish(seghdc_ctx* ctx, size_t round);
 
+/* ---- measurement -------------------------------------------------------------------- */
+/* Bracket every round kernel (the dominant kernel) with CUDA events on the context's stream;
+ * profile_read synchronises and returns the summed kernel time and launch count since the
+ * last read (used by bench.py for the roofline fraction). */
+int seghdc_profile_rounds(seghdc_ctx* ctx, int enable);
+int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count);
+
 /* ---- synthetic inputs (bench/test workloads) --------------------------- */
 /* config_id 0..4 = BASELINE.json configs; config 2 is config 0's construction (use seed
  * 0..63 per image). Writes h*w*c bytes. Returns the shape through h/w/c when out is NULL. */

@@ -73,6 +73,8 @@ SIGNATURES = {
     "seghdc_shard_assign": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_round_needs_exchange": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_finish": ([C.c_void_p, _sz], C.c_int),
+    "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
+    "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
     "seghdc_synth_image": ([C.c_int, C.c_uint64, C.c_void_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
 }
 
@@ -187,6 +189,15 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(lib().seghdc_kernel_launches(self.h))
+
+    def profile_rounds(self, enable: bool) -> None:
+        self.check(lib().seghdc_profile_rounds(self.h, int(enable)))
+
+    def profile_read(self):
+        """(summed round-kernel milliseconds, launches) since the last read."""
+        t, n = C.c_double(), C.c_uint64()
+        self.check(lib().seghdc_profile_read(self.h, C.byref(t), C.byref(n)))
+        return t.value, n.value
 
     # ---- reference API ------------------------------------------------------------------
     def encode_image(self, img: np.ndarray, dim: int, row, col, widened, download: bool = True):

@@ -195,15 +195,22 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
 // A fragment of m16n8k32 from two packed 32-bit HV words (rows g and g+8 of the m-tile).
 // Lane (g, q) owns k-slots 4q..4q+3 (a0/a1) and 16+4q..16+4q+3 (a2/a3). Slot 4q+j holds bit
 // 2q+8j and slot 16+4q+j holds bit 2q+1+8j of the word; the same permutation is baked into
-// bfrag, so the dot product is unchanged. Each byte is 0 or 128 (one IMAD + one LOP3 per
-// register, split across the FMA and ALU pipes); the 128 scale is removed after reduction.
-__device__ __forceinline__ void unpack_a(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row,
-                                         uint32_t m_even, uint32_t m_odd) {
-    a[0] = (w_lo_row * m_even) & 0x80808080u;
-    a[1] = (w_hi_row * m_even) & 0x80808080u;
-    a[2] = (w_lo_row * m_odd) & 0x80808080u;
-    a[3] = (w_hi_row * m_odd) & 0x80808080u;
+// bfrag, so the dot product is unchanged. One shift by 6-2q (an IMAD by the lane's opaque
+// power of two, FMA pipe) puts bit 2q+8j at bit 6 and bit 2q+1+8j at bit 7 of byte j, so
+// two LOP3 masks (ALU pipe) give both registers of the row: bytes are 64*bit (a0/a1) and
+// 128*bit (a2/a3). bfrag stores 7-bit centroid planes doubled in the a0/a1 slots, so every
+// product is 128 * bit * plane; the 128 is removed after the reduction.
+__device__ __forceinline__ void unpack_a(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, uint32_t mul) {
+    uint32_t t_lo, t_hi;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(t_lo) : "r"(w_lo_row), "r"(mul));
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(t_hi) : "r"(w_hi_row), "r"(mul));
+    a[0] = t_lo & 0x40404040u;
+    a[1] = t_hi & 0x40404040u;
+    a[2] = t_lo & 0x80808080u;
+    a[3] = t_hi & 0x80808080u;
 }
+// centroid values are split into kPlanes planes of kPlaneBits bits (z < 2^28)
+constexpr uint32_t kPlaneBits = 7, kPlanes = 4;
 
 // bfrag address of bit i (within a column n of n-tile nt): byte offset inside u64 lane slot
 __host__ __device__ __forceinline__ size_t bfrag_byte(uint32_t nt, uint32_t n_in_tile, uint32_t i,

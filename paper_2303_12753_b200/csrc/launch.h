@@ -69,7 +69,7 @@ void launch_reduce(const ReduceArgs& a, cudaStream_t s);
 
 struct FinishArgs {
     int mode;  // 0 round, 1 init, 2 given centroids, 3 standalone update
-    uint32_t K, D, W32, W32P, Dp;
+    uint32_t K, P, D, W32, W32P, Dp;
     const int32_t* xchg;
     const int32_t* colsum;
     uint32_t* Z;
@@ -86,12 +86,13 @@ struct RoundPlan {
     uint32_t nwarps = 0;       // warps per CTA
     uint32_t mt = 0;           // m-tiles of 16 pixels per tile
     uint32_t ntg = 0;          // n-tiles per group
-    bool fused = false;        // K <= 2: B in registers + fused accumulation
+    uint32_t nt = 0;           // n-tiles in total: ceil(K * planes / 8)
+    bool fused = false;        // one n-tile: B in registers (+ fused accumulation when K == 2)
 };
 struct RoundArgs {
     const uint32_t* grid;
     uint64_t n;
-    uint32_t S32, SS, W32, W32P, nwarp_words, K, NT;
+    uint32_t S32, SS, W32, W32P, nwarp_words, K, P, NT;
     const uint64_t* bfrag;
     uint32_t* labels;
     void* state;
@@ -101,8 +102,8 @@ struct RoundArgs {
     uint32_t Dp;
     uint32_t ctas;
 };
-size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K);
-bool plan_round(uint32_t K, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
+size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
+bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
 
 }  // namespace seghdc_dev

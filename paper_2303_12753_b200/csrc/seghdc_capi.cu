@@ -91,6 +91,7 @@ struct seghdc_ctx {
     uint64_t pix_begin() const { return uint64_t(row_begin) * g_w; }
     // clustering state
     size_t K = 0, iterations = 0;
+    uint32_t planes = kPlanes;  // 7-bit centroid planes per cluster (5 when a caller's centroids exceed 2^28)
     int early_stop = 0;
     RoundPlan plan;
     uint32_t round_ctas = 0, acc_blocks = 0;
@@ -102,6 +103,10 @@ struct seghdc_ctx {
     DevBuf<unsigned long long> slots;
     DevBuf<uint16_t> min_dist;
     int exchange_phase = 0;  // 0: rounds, 1: init (includes colsums)
+    // optional CUDA-event timing of every round kernel (bench.py's roofline)
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
 
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
     size_t xchg_round_ints() const { return K * g.Dp + K + 1; }
@@ -211,17 +216,22 @@ void store_grid(seghdc_ctx& x, uint64_t* out) {
 }
 
 // ---- clustering schedule ----------------------------------------------------------------------
-void alloc_cluster(seghdc_ctx& x, size_t K) {
+void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
     require(x.grid_valid, "no resident grid: encode or load a grid first");
+    // centroid entries are member counts <= pixels; the similarity kernel splits them into
+    // four 7-bit planes (kernels.cuh: kPlanes * kPlaneBits = 28 bits)
+    require(uint64_t(x.g_h) * x.g_w < (1ull << (kPlanes * kPlaneBits)),
+            "images of 2^28 pixels or more exceed the 28-bit centroid planes of the similarity kernel");
     const Geometry& g = x.g;
-    if (!plan_round(uint32_t(K), g.W32, g.SS, x.plan, x.smem_optin))
+    x.planes = planes;
+    if (!plan_round(uint32_t(K), planes, g.W32, g.SS, x.plan, x.smem_optin))
         throw Error(SEGHDC_ERUNTIME, "dim " + std::to_string(g.D) + " does not fit the round kernel's shared memory");
     x.K = K;
     const uint64_t n = x.n_local();
     const uint64_t tp = 16ull * x.plan.mt;
     x.round_ctas = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(x.sms, (n + tp - 1) / tp)));
     x.acc_blocks = accumulate_blocks(n, uint32_t(x.sms));
-    const uint32_t NT = uint32_t((K + 1) / 2);
+    const uint32_t NT = x.plan.nt;
     x.state.ensure(StateView::bytes(uint32_t(K)));
     x.labels.ensure(n);
     x.Z.ensure(K * g.D);
@@ -293,6 +303,7 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     FinishArgs f{};
     f.mode = mode;
     f.K = uint32_t(x.K);
+    f.P = x.planes;
     f.D = x.g.D;
     f.W32 = x.g.W32;
     f.W32P = x.g.W32P;
@@ -354,7 +365,8 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.W32P = x.g.W32P;
     a.nwarp_words = x.g.nwarp_words;
     a.K = uint32_t(x.K);
-    a.NT = uint32_t((x.K + 1) / 2);
+    a.P = x.planes;
+    a.NT = x.plan.nt;
     a.bfrag = reinterpret_cast<const uint64_t*>(x.bfrag.p);
     a.labels = x.labels.p;
     a.state = x.state.p;
@@ -363,7 +375,19 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.partials = x.partials.p;
     a.Dp = x.g.Dp;
     a.ctas = x.round_ctas;
+    cudaEvent_t ev_end = nullptr;
+    if (x.profiling) {
+        if (x.prof_used == x.prof_events.size()) {
+            cudaEvent_t e0, e1;
+            ck(cudaEventCreate(&e0), "event");
+            ck(cudaEventCreate(&e1), "event");
+            x.prof_events.emplace_back(e0, e1);
+        }
+        ck(cudaEventRecord(x.prof_events[x.prof_used].first, x.stream), "event");
+        ev_end = x.prof_events[x.prof_used++].second;
+    }
     ck(launch_round(a, x.plan, x.stream), "round kernel");
+    if (ev_end) ck(cudaEventRecord(ev_end, x.stream), "event");
     x.count();
     if (do_update && !x.plan.fused) {  // K >= 3: separate single-read accumulation pass
         AccumulateArgs u{};
@@ -485,6 +509,10 @@ void seghdc_destroy(seghdc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    for (auto& e : ctx->prof_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     delete ctx;
 }
 
@@ -566,7 +594,10 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         require(k >= 1, "assign_labels: empty centroid set");
         if (grid) load_grid(*ctx, grid, h, w, dim, 0, h);
         require(ctx->g.D == dim && ctx->g_h == h && ctx->g_w == w, "assign_labels: dimension mismatch");
-        alloc_cluster(*ctx, k);
+        // caller centroids may hold any u32 (the reference's IntVector): 5 planes above 2^28
+        uint32_t zmax = 0;
+        for (size_t i = 0; i < k * dim; ++i) zmax = std::max(zmax, centroids[i]);
+        alloc_cluster(*ctx, k, zmax >= (1u << (kPlanes * kPlaneBits)) ? kPlanes + 1 : kPlanes);
         ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
         ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
         ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");
@@ -780,6 +811,28 @@ int seghdc_shard_round_needs_exchange(const seghdc_ctx* ctx, size_t round) {
 
 int seghdc_shard_finish(seghdc_ctx* ctx, size_t round) {
     return guarded(ctx, [&] { finish(*ctx, 0, uint32_t(round)); });
+}
+
+int seghdc_profile_rounds(seghdc_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        ctx->profiling = enable != 0;
+        ctx->prof_used = 0;
+    });
+}
+
+int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count) {
+    return guarded(ctx, [&] {
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        double t = 0;
+        for (size_t i = 0; i < ctx->prof_used; ++i) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, ctx->prof_events[i].first, ctx->prof_events[i].second), "elapsed");
+            t += ms;
+        }
+        *total_ms = t;
+        *count = ctx->prof_used;
+        ctx->prof_used = 0;
+    });
 }
 
 int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c) {

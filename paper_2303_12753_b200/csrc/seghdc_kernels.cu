@@ -315,7 +315,7 @@ void launch_reduce(const ReduceArgs& a, cudaStream_t s) {
 //   mode 3 (update): like 0 but no skip and no early stop (update_centroids API).
 // Always: norm2 of the new set, B fragments. One thread per (32-bit word, cluster).
 // =============================================================================================
-__global__ void k_finish(int mode, uint32_t K, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
+__global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
                          const int32_t* __restrict__ xchg, const int32_t* __restrict__ colsum, uint32_t* Z,
                          uint8_t* bfrag, void* state, uint32_t round, int early_stop) {
     StateView st = StateView::at(state, K);
@@ -365,11 +365,10 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t D, uint32_t W32, uint32_
                 z[b] = 0;
             }
         }
-        // B fragments: column n = 4c + plane; lane (n&7)<<2 | q holds bits {2q, 2q+8, 2q+16,
-        // 2q+24} (bytes 0-3) and {2q+1, ...} (bytes 4-7) of this word, one byte plane each.
-#pragma unroll
-        for (uint32_t pl = 0; pl < 4; ++pl) {
-            const uint32_t n = 4 * c + pl, nt = n >> 3, nl = n & 7;
+        // B fragments: column n = P*c + plane; lane (n&7)<<2 | q holds bits {2q, 2q+8, 2q+16,
+        // 2q+24} (bytes 0-3) and {2q+1, ...} (bytes 4-7) of this word, one 7-bit plane each.
+        for (uint32_t pl = 0; pl < P; ++pl) {
+            const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7;
 #pragma unroll
             for (uint32_t q = 0; q < 4; ++q) {
                 uint64_t v = 0;
@@ -377,7 +376,8 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t D, uint32_t W32, uint32_
                 for (uint32_t half = 0; half < 2; ++half)
 #pragma unroll
                     for (uint32_t j = 0; j < 4; ++j)
-                        v |= uint64_t((z[2 * q + half + 8 * j] >> (8 * pl)) & 0xFFu) << (8 * (half * 4 + j));
+                        v |= uint64_t(((z[2 * q + half + 8 * j] >> (kPlaneBits * pl)) & 0x7Fu) << (1 - half))
+                             << (8 * (half * 4 + j));  // a0/a1 slots carry 64*bit: plane doubled
                 const uint32_t lane = (nl << 2) | q;
                 *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + word) * 32 + lane) * 8) = v;
             }
@@ -394,7 +394,7 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t D, uint32_t W32, uint32_
 void launch_finish(const FinishArgs& a, cudaStream_t s) {
     const uint32_t threads = 128;
     const uint32_t total = a.W32 * a.K;
-    k_finish<<<(total + threads - 1) / threads, threads, 0, s>>>(a.mode, a.K, a.D, a.W32, a.W32P, a.Dp, a.xchg,
+    k_finish<<<(total + threads - 1) / threads, threads, 0, s>>>(a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg,
                                                                  a.colsum, a.Z, a.bfrag, a.state, a.round,
                                                                  a.early_stop);
 }
@@ -425,8 +425,9 @@ void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s) {
 template <int MT, int NTG, bool BREG, bool UPD, int H, int TB>
 __global__ void __launch_bounds__(TB, 1)
     k_round(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t W32P,
-            uint32_t nwarp_words, uint32_t K, uint32_t NT, const uint64_t* __restrict__ bfrag, uint32_t* labels,
-            void* state, uint32_t round, int do_update, uint32_t* __restrict__ partials, uint32_t Dp) {
+            uint32_t nwarp_words, uint32_t K, uint32_t P, uint32_t NT, const uint64_t* __restrict__ bfrag,
+            uint32_t* labels, void* state, uint32_t round, int do_update, uint32_t* __restrict__ partials,
+            uint32_t Dp) {
     constexpr uint32_t TP = 16 * MT;
     constexpr uint32_t NC = NTG * 8;  // columns per group
     extern __shared__ __align__(128) uint8_t smem[];
@@ -437,13 +438,14 @@ __global__ void __launch_bounds__(TB, 1)
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t g8 = lane >> 2, q = lane & 3;
     const uint32_t parity = round & 1;
+    const uint32_t NCT = NT * 8;  // all columns (P planes x K clusters, padded to n-tiles)
 
     // shared memory carve-up
     uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
     const size_t tile_words = size_t(TP) * SS;
     int32_t* part = reinterpret_cast<int32_t*>(tiles + 2 * tile_words + 32);  // [nwarps][TP][NC]
-    uint32_t* red = reinterpret_cast<uint32_t*>(part + size_t(nwarps) * TP * NC);  // [TP][NC]
-    uint32_t* s_label = red + TP * NC;                                           // [TP]
+    uint32_t* red = reinterpret_cast<uint32_t*>(part + size_t(nwarps) * TP * NC);  // [TP][NCT]
+    uint32_t* s_label = red + TP * NCT;                                          // [TP]
     uint32_t* s_list = s_label + TP;                                             // [TP]
     uint32_t* s_misc = s_list + TP;  // [0] list_n, [1] changed, [2] skip, [4..4+K) counts
     unsigned long long* s_n2 = reinterpret_cast<unsigned long long*>(s_misc + ((4 + K + 1) & ~1u));  // [K]
@@ -499,7 +501,9 @@ __global__ void __launch_bounds__(TB, 1)
             breg[kk][1] = uint32_t(v >> 32);
         }
     }
-    const uint32_t m_even = 1u << (7 - 2 * q), m_odd = 1u << (6 - 2 * q);
+    // shift of unpack_a as an opaque multiplier so it issues as IMAD (FMA pipe), not SHF (ALU)
+    uint32_t mul;
+    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
 
     BitCounter<UPD ? H : 1> cnt;
     if constexpr (UPD) cnt.reset();
@@ -516,6 +520,8 @@ __global__ void __launch_bounds__(TB, 1)
         const uint32_t* T = tiles + buf * tile_words;
         const uint64_t px0 = tile * TP;
         const uint32_t npx = uint32_t(umin64(TP, n - px0));
+        // previous labels, fetched now so the load latency hides behind the k-loop
+        const uint32_t old = (tid < npx) ? labels[px0 + tid] : 0u;
 
         for (uint32_t grp = 0; grp < ngroups; ++grp) {
             int acc[MT][NTG][4];
@@ -530,30 +536,35 @@ __global__ void __launch_bounds__(TB, 1)
                 const uint32_t wbase = wb * 32;
 #pragma unroll
                 for (int k4 = 0; k4 < 8; ++k4) {
+                    // rows g and g+8 of every m-tile: 4 consecutive words = 4 k-steps
+                    uint4 wl[MT], wh[MT];
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
-                        // rows g and g+8 of m-tile mt: 4 consecutive words = 4 k-steps
-                        const uint4 wl = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
-                        const uint4 wh = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+                        wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
+                        wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+                    }
 #pragma unroll
-                        for (int kq = 0; kq < 4; ++kq) {
-                            const int kk = 4 * k4 + kq;
-                            uint32_t b0[NTG], b1[NTG];
+                    for (int kq = 0; kq < 4; ++kq) {
+                        const int kk = 4 * k4 + kq;
+                        uint32_t b0[NTG], b1[NTG];
 #pragma unroll
-                            for (int nt = 0; nt < NTG; ++nt) {
-                                if constexpr (BREG) {
-                                    b0[nt] = breg[kk][0];
-                                    b1[nt] = breg[kk][1];
-                                } else {
-                                    const uint32_t ntg = grp * NTG + nt;
-                                    uint64_t v = 0;
-                                    if (ntg < NT) v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
-                                    b0[nt] = uint32_t(v);
-                                    b1[nt] = uint32_t(v >> 32);
-                                }
+                        for (int nt = 0; nt < NTG; ++nt) {
+                            if constexpr (BREG) {
+                                b0[nt] = breg[kk][0];
+                                b1[nt] = breg[kk][1];
+                            } else {
+                                const uint32_t ntg = grp * NTG + nt;
+                                uint64_t v = 0;
+                                if (ntg < NT) v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
+                                b0[nt] = uint32_t(v);
+                                b1[nt] = uint32_t(v >> 32);
                             }
+                        }
+                        // consecutive IMMAs target different m-tiles: independent accumulators
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
                             uint32_t a[4];
-                            unpack_a(a, (&wl.x)[kq], (&wh.x)[kq], m_even, m_odd);
+                            unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
 #pragma unroll
                             for (int nt = 0; nt < NTG; ++nt) imma16832(acc[mt][nt], a, b0[nt], b1[nt]);
                         }
@@ -571,33 +582,31 @@ __global__ void __launch_bounds__(TB, 1)
                 }
             __syncthreads();
             for (uint32_t e = tid; e < TP * NC; e += blockDim.x) {
+                const uint32_t px = e / NC, col = grp * NC + e % NC;
+                if (col >= NCT) continue;
                 int32_t s = 0;
                 for (uint32_t w = 0; w < nwarps; ++w) s += part[size_t(w) * TP * NC + e];
-                red[e] = uint32_t(s) >> 7;  // remove the 128 scale of unpack_a (exact)
+                red[px * NCT + col] = uint32_t(s) >> 7;  // remove the 128 scale of unpack_a (exact)
             }
-            __syncthreads();
-            if (tid < TP) {
-                const uint32_t* rr = red + tid * NC;
-                for (uint32_t cl = 0; cl < NC / 4; ++cl) {
-                    const uint32_t c = grp * (NC / 4) + cl;
-                    if (c >= K) break;
-                    const unsigned long long d = (unsigned long long)rr[4 * cl] +
-                                                 ((unsigned long long)rr[4 * cl + 1] << 8) +
-                                                 ((unsigned long long)rr[4 * cl + 2] << 16) +
-                                                 ((unsigned long long)rr[4 * cl + 3] << 24);
-                    const unsigned long long n2 = s_n2[c];
-                    if (c == 0) {
-                        best = 0;
-                        bdot = d;
-                        bn2 = n2;
-                    } else if (strictly_closer(d, n2, bdot, bn2)) {
-                        best = c;
-                        bdot = d;
-                        bn2 = n2;
-                    }
+            __syncthreads();  // red complete for this group; part free for the next group
+        }
+        // exact dots (u64) and the reference's 128-bit argmax, ties to the lower index
+        if (tid < TP) {
+            const uint32_t* rr = red + tid * NCT;
+            for (uint32_t c = 0; c < K; ++c) {
+                unsigned long long d = 0;
+                for (uint32_t pl = 0; pl < P; ++pl) d += (unsigned long long)rr[P * c + pl] << (kPlaneBits * pl);
+                const unsigned long long n2 = s_n2[c];
+                if (c == 0) {
+                    best = 0;
+                    bdot = d;
+                    bn2 = n2;
+                } else if (strictly_closer(d, n2, bdot, bn2)) {
+                    best = c;
+                    bdot = d;
+                    bn2 = n2;
                 }
             }
-            if (ngroups > 1) __syncthreads();  // red reused by the next group
         }
 
         // labels, changed count, member counts, update list
@@ -605,7 +614,6 @@ __global__ void __launch_bounds__(TB, 1)
             const bool live = tid < npx;
             if (live) {
                 const uint64_t p = px0 + tid;
-                const uint32_t old = labels[p];
                 labels[p] = best;
                 if (old != best) atomicAdd(&s_misc[1], 1u);
                 atomicAdd(&s_misc[4 + best], 1u);
@@ -646,11 +654,11 @@ __global__ void __launch_bounds__(TB, 1)
     for (uint32_t c = tid; c < K; c += blockDim.x) atomicAdd(st.counts + parity * K + c, s_misc[4 + c]);
 }
 
-size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K) {
+size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT) {
     const uint32_t TP = 16 * MT, NC = 8 * NTG;
     size_t b = (2 * size_t(TP) * SS + 32) * 4;        // tiles + slack for the last row's overrun
     b += size_t(nwarps) * TP * NC * 4;                 // part
-    b += size_t(TP) * NC * 4;                          // red
+    b += size_t(TP) * NT * 8 * 4;                      // red (all columns)
     b += 2 * size_t(TP) * 4;                           // s_label, s_list
     b += ((4 + K + 1) & ~size_t(1)) * 4;               // s_misc
     b += size_t(K) * 8;                                // s_n2
@@ -662,23 +670,25 @@ template <int MT, int NTG, bool BREG, bool UPD, int H>
 static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStream_t s) {
     // register budget: 1 CTA/SM; <= 12 warps leaves 170 registers per thread, 16 warps 128
     auto kern = nwarps <= 12 ? k_round<MT, NTG, BREG, UPD, H, 384> : k_round<MT, NTG, BREG, UPD, H, 512>;
-    const size_t smem = round_smem_bytes(MT, NTG, a.SS, nwarps, a.K);
+    const size_t smem = round_smem_bytes(MT, NTG, a.SS, nwarps, a.K, a.NT);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<a.ctas, nwarps * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.W32P, a.nwarp_words, a.K, a.NT,
+    kern<<<a.ctas, nwarps * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.W32P, a.nwarp_words, a.K, a.P, a.NT,
                                            a.bfrag, a.labels, a.state, a.round, a.do_update, a.partials, a.Dp);
     return cudaGetLastError();
 }
 
-// Plan: which instantiation handles (K, D). Returns false if no kernel fits.
-bool plan_round(uint32_t K, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit) {
+// Plan: which instantiation handles (K, P, D). Returns false if no kernel fits.
+bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit) {
     p.nwarp_words = (W32 + 31) / 32;
-    p.fused = (K <= 2) && p.nwarp_words <= kTileWarpsMax;
+    p.nt = (K * P + 7) / 8;
+    // one n-tile and <= 16 word blocks: B fragments live in registers, accumulation is fused
+    p.fused = p.nt == 1 && p.nwarp_words <= kTileWarpsMax;
     p.ntg = p.fused ? 1 : 4;
     // at least 2 warps: the epilogue needs one thread per pixel of a 64-pixel tile
     p.nwarps = std::max<uint32_t>(2, p.fused ? p.nwarp_words : std::min<uint32_t>(p.nwarp_words, 16));
     for (uint32_t mt : {4u, 2u, 1u}) {
-        if (round_smem_bytes(mt, p.ntg, SS, p.nwarps, K) <= smem_limit) {
+        if (round_smem_bytes(mt, p.ntg, SS, p.nwarps, K, p.nt) <= smem_limit) {
             p.mt = mt;
             return true;
         }
@@ -689,7 +699,7 @@ bool plan_round(uint32_t K, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
     const uint64_t per_cta = (a.n + a.ctas - 1) / a.ctas;
     if (p.fused) {
-        const bool upd = a.K == 2;
+        const bool upd = a.K == 2;  // the fused Harley-Seal accumulation keeps one counter set
         if (!upd) {
             switch (p.mt) {
                 case 4: return launch_round_t<4, 1, true, false, 1>(a, p.nwarps, s);
