@@ -87,6 +87,8 @@ struct RoundPlan {
     uint32_t mt = 0;           // m-tiles of 16 pixels per tile
     uint32_t ntg = 0;          // n-tiles per group
     uint32_t nt = 0;           // n-tiles in total: ceil(K * planes / 8)
+    uint32_t wpw = 32;         // HV words per warp (split-K)
+    uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
     bool fused = false;        // one n-tile: B in registers (+ fused accumulation when K == 2)
 };
 struct RoundArgs {

@@ -233,10 +233,10 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
     x.acc_blocks = accumulate_blocks(n, uint32_t(x.sms));
     const uint32_t NT = x.plan.nt;
     x.state.ensure(StateView::bytes(uint32_t(K)));
-    x.labels.ensure(n);
+    x.labels.ensure(n + 4);  // +4: the fused kernel's TMA of a tile's labels rounds up to 16 B
     x.Z.ensure(K * g.D);
     // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
-    x.bfrag.ensure(size_t(NT) * g.W32P * 32 * 8);
+    x.bfrag.ensure(size_t(NT) * x.plan.w32p * 32 * 8);
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
     const size_t parts = std::max<size_t>(x.round_ctas, x.acc_blocks);
     x.partials.ensure(parts * K * g.Dp);
@@ -306,7 +306,7 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.P = x.planes;
     f.D = x.g.D;
     f.W32 = x.g.W32;
-    f.W32P = x.g.W32P;
+    f.W32P = x.plan.w32p;
     f.Dp = x.g.Dp;
     f.xchg = x.xchg.p;
     f.colsum = x.colsum_ptr();
@@ -362,7 +362,7 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.S32 = x.g.S32;
     a.SS = x.g.SS;
     a.W32 = x.g.W32;
-    a.W32P = x.g.W32P;
+    a.W32P = x.plan.w32p;
     a.nwarp_words = x.g.nwarp_words;
     a.K = uint32_t(x.K);
     a.P = x.planes;

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "launch.h"
@@ -654,6 +655,466 @@ __global__ void __launch_bounds__(TB, 1)
     for (uint32_t c = tid; c < K; c += blockDim.x) atomicAdd(st.counts + parity * K + c, s_misc[4 + c]);
 }
 
+// =============================================================================================
+// The fused round kernel for one n-tile of centroid planes (K * P <= 8: K <= 2 at P = 4).
+// Same data flow as k_round, tuned for the headline configs:
+//  * warp w owns WPW words (a multiple of 4; warps a multiple of 4 so every SM sub-partition
+//    carries the same k-loop load) and holds their B fragments in 2*WPW registers;
+//  * the previous labels of a tile ride in the tile's TMA transaction (no exposed LDG);
+//  * the split-K reduction and the argmax run on every warp at once (8 lanes per pixel,
+//    planes combined with shuffles), so only three block barriers remain per tile.
+// =============================================================================================
+template <int MT, int WPW, bool UPD, int H, int TB>
+__global__ void __launch_bounds__(TB, 1)
+    k_round_fused(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
+                  uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
+                  int do_update, uint32_t* __restrict__ partials, uint32_t Dp) {
+    constexpr uint32_t TP = 16 * MT;
+    extern __shared__ __align__(128) uint8_t smem[];
+    StateView st = StateView::at(state, K);
+    if (st.hdr->done) return;
+
+    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t g8 = lane >> 2, q = lane & 3;
+    const uint32_t parity = round & 1;
+
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
+    const size_t tile_words = size_t(TP) * SS;
+    uint32_t* s_old = tiles + 2 * tile_words + 32;                         // [2][TP] labels via TMA
+    int32_t* part = reinterpret_cast<int32_t*>(s_old + 2 * TP);             // [nwarps][TP][8]
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + size_t(nwarps) * TP * 8);  // [TP]
+    uint32_t* s_misc = s_list + TP;  // [0] list_n, [1] changed, [2] skip, [4..4+K) counts
+    unsigned long long* s_n2 = reinterpret_cast<unsigned long long*>(s_misc + ((4 + K + 1) & ~1u));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_n2 + K);
+
+    const uint64_t ntiles = (n + TP - 1) / TP;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
+        s_misc[0] = 0;
+        s_misc[1] = 0;
+        s_misc[2] = pick_skip(st.cur + parity * K, K);
+    }
+    for (uint32_t c = tid; c < K; c += blockDim.x) {
+        s_misc[4 + c] = 0;
+        s_n2[c] = st.norm2[parity * K + c];
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        st.hdr->rounds_run = round;
+        for (uint32_t c = 0; c < K; ++c) st.counts[(parity ^ 1) * K + c] = 0;
+        st.changed[parity ^ 1] = 0;
+    }
+    __syncthreads();
+    const uint32_t skip = s_misc[2];
+    const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
+
+    auto issue = [&](uint64_t tile, uint32_t buf) {
+        const uint64_t px0 = tile * TP;
+        const uint32_t npx = uint32_t(umin64(TP, n - px0));
+        const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer is padded to 16 B
+        if (lane == 0) mbar_expect_tx(&bars[buf], npx * S32 * 4 + lab_bytes);
+        __syncwarp();
+        if (lane == 0) bulk_g2s(s_old + buf * TP, labels + px0, lab_bytes, &bars[buf]);
+        for (uint32_t r = lane; r < npx; r += 32)
+            bulk_g2s(tiles + buf * tile_words + size_t(r) * SS, grid + (px0 + r) * S32, S32 * 4, &bars[buf]);
+    };
+    if (warp == 0) {
+        fence_proxy_async();
+        for (uint32_t b = 0; b < 2; ++b) {
+            const uint64_t tile = blockIdx.x + uint64_t(b) * gridDim.x;
+            if (tile < ntiles) issue(tile, b);
+        }
+    }
+
+    uint32_t breg[WPW][2];
+#pragma unroll
+    for (int kk = 0; kk < WPW; ++kk) {
+        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+        breg[kk][0] = uint32_t(v);
+        breg[kk][1] = uint32_t(v >> 32);
+    }
+    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
+    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
+    const uint32_t wbase = warp * WPW;
+
+    BitCounter<UPD ? H : 1> cnt;
+    if constexpr (UPD) cnt.reset();
+
+    uint32_t it = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const uint32_t buf = it & 1;
+        mbar_wait(&bars[buf], (it >> 1) & 1);
+        const uint32_t* T = tiles + buf * tile_words;
+        const uint64_t px0 = tile * TP;
+        const uint32_t npx = uint32_t(umin64(TP, n - px0));
+
+        int acc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
+#pragma unroll
+        for (int k4 = 0; k4 < WPW / 4; ++k4) {
+            uint4 wl[MT], wh[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
+                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+            }
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) {
+                const int kk = 4 * k4 + kq;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint32_t a[4];
+                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
+                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            int32_t* row0 = part + (size_t(warp) * TP + 16 * mt + g8) * 8 + 2 * q;
+            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
+            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
+        }
+        __syncthreads();  // (1) partial dots of every warp are in shared memory
+
+        // split-K reduction + exact argmax: 4 pixels per warp pass, lane = (pixel, column)
+        for (uint32_t pg = warp; pg < TP / 4; pg += nwarps) {
+            const uint32_t px = pg * 4 + (lane >> 3), col = lane & 7;
+            int32_t s = 0;
+            for (uint32_t w = 0; w < nwarps; ++w) s += part[(size_t(w) * TP + px) * 8 + col];
+            const uint32_t c_of = col / P, pl = col - c_of * P;
+            const unsigned long long v =
+                (col < K * P) ? (unsigned long long)(uint32_t(s) >> 7) << (kPlaneBits * pl) : 0ull;
+            const uint32_t base = lane & ~7u;
+            uint32_t best = 0;
+            unsigned long long bdot = 0, bn2 = 0;
+            for (uint32_t c = 0; c < K; ++c) {
+                unsigned long long d = 0;
+                for (uint32_t j = 0; j < P; ++j) d += __shfl_sync(0xffffffffu, v, base + P * c + j);
+                const unsigned long long n2 = s_n2[c];
+                if (c == 0 || strictly_closer(d, n2, bdot, bn2)) {
+                    best = c;
+                    bdot = d;
+                    bn2 = n2;
+                }
+            }
+            const bool leader = col == 0 && px < npx;
+            const uint32_t old = s_old[buf * TP + px];
+            if (leader) labels[px0 + px] = best;
+            const uint32_t chg = __ballot_sync(0xffffffffu, leader && old != best);
+            if (lane == 0 && chg) atomicAdd(&s_misc[1], __popc(chg));
+            for (uint32_t c = 0; c < K; ++c) {
+                const uint32_t m = __ballot_sync(0xffffffffu, leader && best == c);
+                if (lane == 0 && m) atomicAdd(&s_misc[4 + c], __popc(m));
+            }
+            if constexpr (UPD) {
+                const bool take = do_update && leader && best == upd_c;
+                const uint32_t m = __ballot_sync(0xffffffffu, take);
+                uint32_t pos = 0;
+                if (lane == 0 && m) pos = atomicAdd(&s_misc[0], __popc(m));
+                pos = __shfl_sync(0xffffffffu, pos, 0);
+                if (take) s_list[pos + __popc(m & ((1u << lane) - 1))] = px;
+            }
+            (void)c_of;
+        }
+        __syncthreads();  // (2) labels of the tile decided, update list complete
+        if constexpr (UPD) {
+            if (do_update) {
+                const uint32_t m = s_misc[0];
+                if (tid < W32) {
+                    for (uint32_t e = 0; e < m; e += 16) {
+                        uint32_t x[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) x[u] = (e + u < m) ? T[size_t(s_list[e + u]) * SS + tid] : 0u;
+                        cnt.add16(x);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // (3) every read of this buffer is done
+        if (tid == 0) s_misc[0] = 0;
+        if (warp == 0) {
+            const uint64_t nxt = tile + 2ull * gridDim.x;
+            if (nxt < ntiles) {
+                fence_proxy_async();
+                issue(nxt, buf);
+            }
+        }
+    }
+
+    if constexpr (UPD) {
+        if (do_update && tid < W32) cnt.store(partials + (size_t(blockIdx.x) * K + upd_c) * Dp + size_t(tid) * 32);
+    }
+    __syncthreads();
+    if (tid == 0) atomicAdd(st.changed + parity, s_misc[1]);
+    for (uint32_t c = tid; c < K; c += blockDim.x) atomicAdd(st.counts + parity * K + c, s_misc[4 + c]);
+}
+
+// =============================================================================================
+// Warp-specialised round kernel (one n-tile of centroid planes, K * P <= 8).
+//
+//   warps 0..NMW-1  "MMA" warps: wait tile t -> IMMA k-loop over their WPW words -> split-K
+//                   partials to part[t%2] -> then, while the epilogue warp works on tile t,
+//                   fold tile t-1 into the Harley-Seal counters (thread = word column) and
+//                   release its buffer.
+//   warp NMW        epilogue: reduce tile t's partials (lane = pixel), exact u64 dots, 128-bit
+//                   argmax, labels, member counts, change count, update list.
+//   warp NMW+1      producer: cp.async.bulk (TMA engine) of tile rows + previous labels into
+//                   a 3-deep ring, gated by the buffer-free barriers.
+// All hand-offs are mbarriers; no block-wide barrier inside the tile loop, so the k-loop
+// of tile t+1 overlaps the epilogue and re-bundling of tile t.
+// =============================================================================================
+template <int WPW, bool UPD, int H, int NMW>
+__global__ void __launch_bounds__((NMW + 2) * 32, 1)
+    k_round_ws(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
+               uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
+               int do_update, uint32_t* __restrict__ partials, uint32_t Dp) {
+    constexpr uint32_t MT = 2, TP = 32, NB = 3;
+    extern __shared__ __align__(128) uint8_t smem[];
+    StateView st = StateView::at(state, K);
+    if (st.hdr->done) return;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t parity = round & 1;
+
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
+    const size_t tile_words = size_t(TP) * SS;
+    uint32_t* s_old = tiles + NB * tile_words + 32;                        // [NB][TP]
+    int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);           // [2][NMW][TP][8]
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
+    uint32_t* s_listn = s_list + 2 * TP;                                   // [2]
+    uint32_t* s_misc = s_listn + 2;                                        // [0] skip
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ((reinterpret_cast<uintptr_t>(s_misc + 2) -
+                                                           reinterpret_cast<uintptr_t>(smem) + 7) & ~uintptr_t(7)));
+    uint64_t* full = bars;            // [NB] tile data landed (TMA)
+    uint64_t* buf_free = bars + NB;   // [NB] MMA warps done with the buffer
+    uint64_t* part_full = bars + 2 * NB;      // [2] partials written
+    uint64_t* part_free = bars + 2 * NB + 2;  // [2] epilogue done reading partials
+    uint64_t* list_ready = bars + 2 * NB + 4; // [2] labels + update list of the tile ready
+
+    const uint64_t ntiles = (n + TP - 1) / TP;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    if (tid == 0) {
+        for (uint32_t b = 0; b < NB; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&buf_free[b], NMW * 32);
+        }
+        for (uint32_t b = 0; b < 2; ++b) {
+            mbar_init(&part_full[b], NMW * 32);
+            mbar_init(&part_free[b], 32);
+            mbar_init(&list_ready[b], 32);
+        }
+        mbar_fence_init();
+        s_misc[0] = pick_skip(st.cur + parity * K, K);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        st.hdr->rounds_run = round;
+        for (uint32_t c = 0; c < K; ++c) st.counts[(parity ^ 1) * K + c] = 0;
+        st.changed[parity ^ 1] = 0;
+    }
+    __syncthreads();
+    const uint32_t skip = s_misc[0];
+    const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
+
+    if (warp == NMW + 1) {
+        // ------------------------------------------------------------------ producer warp
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t b = it % NB;
+            if (it >= NB) mbar_wait(&buf_free[b], ((it / NB) - 1) & 1);
+            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
+            const uint32_t npx = uint32_t(umin64(TP, n - px0));
+            const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer padded to 16 B
+            if (lane == 0) mbar_expect_tx(&full[b], npx * S32 * 4 + lab_bytes);
+            __syncwarp();
+            if (lane == 0) bulk_g2s(s_old + b * TP, labels + px0, lab_bytes, &full[b]);
+            if (lane < npx)
+                bulk_g2s(tiles + b * tile_words + size_t(lane) * SS, grid + (px0 + lane) * S32, S32 * 4, &full[b]);
+        }
+        return;
+    }
+    if (warp == NMW) {
+        // ------------------------------------------------------------------ epilogue warp
+        unsigned long long n2[2] = {st.norm2[parity * K], K > 1 ? st.norm2[parity * K + 1] : 0ull};
+        uint32_t changed = 0, cnt0 = 0, cnt1 = 0;
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t pb = it & 1, b = it % NB;
+            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
+            const uint32_t npx = uint32_t(umin64(TP, n - px0));
+            mbar_wait(&part_full[pb], (it >> 1) & 1);
+            const int32_t* pp = part + size_t(pb) * NMW * TP * 8 + lane * 8;
+            int32_t col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+            for (uint32_t w = 0; w < NMW; ++w) {
+                const int4 lo = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8);
+                const int4 hi = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8 + 4);
+                col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
+                col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
+            }
+            mbar_arrive(&part_free[pb]);
+            // exact dots: column n = P*c + plane, 7-bit planes, 128 scale removed (exact)
+            unsigned long long d[2] = {0, 0};
+#pragma unroll
+            for (uint32_t cn = 0; cn < 8; ++cn) {
+                const uint32_t c = cn / P, pl = cn - c * P;
+                if (c < K && c < 2) d[c] += (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
+            }
+            uint32_t best = 0;
+            if (K > 1 && strictly_closer(d[1], n2[1], d[0], n2[0])) best = 1;
+            const bool live = lane < npx;
+            const uint32_t old = s_old[b * TP + lane];
+            if (live) {
+                labels[px0 + lane] = best;
+                changed += old != best;
+                cnt0 += best == 0;
+                cnt1 += best == 1;
+            }
+            if constexpr (UPD) {
+                const bool take = do_update && live && best == upd_c;
+                const uint32_t m = __ballot_sync(0xffffffffu, take);
+                if (take) s_list[pb * TP + __popc(m & ((1u << lane) - 1))] = lane;
+                if (lane == 0) s_listn[pb] = __popc(m);
+            }
+            mbar_arrive(&list_ready[pb]);
+        }
+        for (int o = 16; o; o >>= 1) {
+            changed += __shfl_xor_sync(0xffffffffu, changed, o);
+            cnt0 += __shfl_xor_sync(0xffffffffu, cnt0, o);
+            cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
+        }
+        if (lane == 0) {
+            atomicAdd(st.changed + parity, changed);
+            atomicAdd(st.counts + parity * K, cnt0);
+            if (K > 1) atomicAdd(st.counts + parity * K + 1, cnt1);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------------- MMA warps
+    const uint32_t g8 = lane >> 2, q = lane & 3;
+    uint32_t breg[WPW][2];
+#pragma unroll
+    for (int kk = 0; kk < WPW; ++kk) {
+        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+        breg[kk][0] = uint32_t(v);
+        breg[kk][1] = uint32_t(v >> 32);
+    }
+    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
+    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
+    const uint32_t wbase = warp * WPW;
+    BitCounter<UPD ? H : 1> cnt;
+    if constexpr (UPD) cnt.reset();
+
+    auto rebundle = [&](uint32_t jt) {  // fold tile jt's update list into the counters
+        const uint32_t pb = jt & 1, b = jt % NB;
+        mbar_wait(&list_ready[pb], (jt >> 1) & 1);
+        if constexpr (UPD) {
+            if (do_update && tid < W32) {
+                const uint32_t m = s_listn[pb];
+                const uint32_t* T = tiles + b * tile_words;
+                for (uint32_t e = 0; e < m; e += 16) {
+                    uint32_t x[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        x[u] = (e + u < m) ? T[size_t(s_list[pb * TP + e + u]) * SS + tid] : 0u;
+                    cnt.add16(x);
+                }
+            }
+        }
+        mbar_arrive(&buf_free[b]);
+    };
+
+    for (uint32_t it = 0; it < my_tiles; ++it) {
+        const uint32_t b = it % NB, pb = it & 1;
+        mbar_wait(&full[b], (it / NB) & 1);
+        const uint32_t* T = tiles + b * tile_words;
+        int acc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
+#pragma unroll
+        for (int k4 = 0; k4 < WPW / 4; ++k4) {
+            uint4 wl[MT], wh[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
+                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+            }
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) {
+                const int kk = 4 * k4 + kq;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint32_t a[4];
+                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
+                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
+                }
+            }
+        }
+        if (it >= 2) mbar_wait(&part_free[pb], ((it >> 1) - 1) & 1);
+        int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
+            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
+            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
+        }
+        mbar_arrive(&part_full[pb]);
+        if (it >= 1) rebundle(it - 1);
+    }
+    if (my_tiles >= 1) rebundle(my_tiles - 1);
+    if constexpr (UPD) {
+        if (do_update && tid < W32) cnt.store(partials + (size_t(blockIdx.x) * K + upd_c) * Dp + size_t(tid) * 32);
+    }
+}
+
+size_t ws_smem_bytes(uint32_t SS, uint32_t nmw) {
+    const uint32_t TP = 32, NB = 3;
+    size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
+    b += NB * TP * 4;                            // s_old
+    b += 2 * size_t(nmw) * TP * 8 * 4;           // part
+    b += 2 * TP * 4 + 2 * 4 + 2 * 4;             // s_list, s_listn, s_misc
+    b = (b + 7) & ~size_t(7);
+    b += (2 * NB + 6) * 8;                       // mbarriers
+    return b;
+}
+
+template <int WPW, bool UPD, int H, int NMW>
+static cudaError_t launch_ws_t(const RoundArgs& a, cudaStream_t s) {
+    auto kern = k_round_ws<WPW, UPD, H, NMW>;
+    const size_t smem = ws_smem_bytes(a.SS, NMW);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<a.ctas, (NMW + 2) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
+                                              a.round, a.do_update, a.partials, a.Dp);
+    return cudaGetLastError();
+}
+
+template <int WPW, int NMW>
+static cudaError_t launch_ws_h(const RoundArgs& a, cudaStream_t s) {
+    if (a.K != 2) return launch_ws_t<WPW, false, 1, NMW>(a, s);
+    const uint64_t per_cta = (a.n + a.ctas - 1) / a.ctas;
+    if (per_cta <= BitCounter<8>::capacity()) return launch_ws_t<WPW, true, 8, NMW>(a, s);
+    if (per_cta <= BitCounter<12>::capacity()) return launch_ws_t<WPW, true, 12, NMW>(a, s);
+    return launch_ws_t<WPW, true, 20, NMW>(a, s);
+}
+
+size_t fused_smem_bytes(uint32_t MT, uint32_t SS, uint32_t nwarps, uint32_t K) {
+    const uint32_t TP = 16 * MT;
+    size_t b = (2 * size_t(TP) * SS + 32) * 4;  // tiles + overrun slack
+    b += 2 * size_t(TP) * 4;                     // s_old
+    b += size_t(nwarps) * TP * 8 * 4;            // part
+    b += size_t(TP) * 4;                         // s_list
+    b += ((4 + K + 1) & ~size_t(1)) * 4;         // s_misc
+    b += size_t(K) * 8 + 2 * 8;                  // s_n2, mbarriers
+    return b;
+}
+
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT) {
     const uint32_t TP = 16 * MT, NC = 8 * NTG;
     size_t b = (2 * size_t(TP) * SS + 32) * 4;        // tiles + slack for the last row's overrun
@@ -682,11 +1143,32 @@ static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStrea
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit) {
     p.nwarp_words = (W32 + 31) / 32;
     p.nt = (K * P + 7) / 8;
-    // one n-tile and <= 16 word blocks: B fragments live in registers, accumulation is fused
-    p.fused = p.nt == 1 && p.nwarp_words <= kTileWarpsMax;
-    p.ntg = p.fused ? 1 : 4;
+    p.fused = false;
+    if (p.nt == 1) {
+        // warp-specialised kernel: MMA warps in multiples of 4 (equal load per SM sub-partition),
+        // B fragments in 2*wpw registers, one thread per word column for the re-bundling
+        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32},
+                                           {12, 20}, {12, 28}, {16, 20}, {16, 28}};
+        const char* force = getenv("SEGHDC_FUSED_WARPS");
+        if (force && !*force) force = nullptr;
+        for (const auto& c : cand) {
+            if (force && uint32_t(atoi(force)) != c[0]) continue;
+            if (c[0] * c[1] < W32 || c[0] * 32 < W32) continue;
+            if (ws_smem_bytes(SS, c[0]) > smem_limit) continue;
+            p.fused = true;
+            p.nwarps = c[0];
+            p.wpw = c[1];
+            p.w32p = c[0] * c[1];
+            p.mt = 2;
+            p.ntg = 1;
+            return true;
+        }
+    }
+    p.ntg = 4;
+    p.wpw = 32;
+    p.w32p = p.nwarp_words * 32;
     // at least 2 warps: the epilogue needs one thread per pixel of a 64-pixel tile
-    p.nwarps = std::max<uint32_t>(2, p.fused ? p.nwarp_words : std::min<uint32_t>(p.nwarp_words, 16));
+    p.nwarps = std::max<uint32_t>(2, std::min<uint32_t>(p.nwarp_words, 16));
     for (uint32_t mt : {4u, 2u, 1u}) {
         if (round_smem_bytes(mt, p.ntg, SS, p.nwarps, K, p.nt) <= smem_limit) {
             p.mt = mt;
@@ -697,27 +1179,19 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 }
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
-    const uint64_t per_cta = (a.n + a.ctas - 1) / a.ctas;
     if (p.fused) {
-        const bool upd = a.K == 2;  // the fused Harley-Seal accumulation keeps one counter set
-        if (!upd) {
-            switch (p.mt) {
-                case 4: return launch_round_t<4, 1, true, false, 1>(a, p.nwarps, s);
-                case 2: return launch_round_t<2, 1, true, false, 1>(a, p.nwarps, s);
-                default: return launch_round_t<1, 1, true, false, 1>(a, p.nwarps, s);
-            }
-        }
-        const int h = per_cta <= BitCounter<8>::capacity() ? 8 : per_cta <= BitCounter<12>::capacity() ? 12 : 20;
-#define SEGHDC_ROUND_H(MTV)                                                        \
-    if (h == 8) return launch_round_t<MTV, 1, true, true, 8>(a, p.nwarps, s);      \
-    if (h == 12) return launch_round_t<MTV, 1, true, true, 12>(a, p.nwarps, s);    \
-    return launch_round_t<MTV, 1, true, true, 20>(a, p.nwarps, s);
-        switch (p.mt) {
-            case 4: { SEGHDC_ROUND_H(4) }
-            case 2: { SEGHDC_ROUND_H(2) }
-            default: { SEGHDC_ROUND_H(1) }
-        }
-#undef SEGHDC_ROUND_H
+#define SEGHDC_WS(NMW)                                                   \
+    if (p.nwarps == NMW) {                                               \
+        if (p.wpw == 20) return launch_ws_h<20, NMW>(a, s);              \
+        if (p.wpw == 28) return launch_ws_h<28, NMW>(a, s);              \
+        return launch_ws_h<32, NMW>(a, s);                               \
+    }
+        SEGHDC_WS(4)
+        SEGHDC_WS(8)
+        SEGHDC_WS(12)
+        if (p.wpw == 20) return launch_ws_h<20, 16>(a, s);
+        return launch_ws_h<28, 16>(a, s);
+#undef SEGHDC_WS
     }
     switch (p.mt) {
         case 4: return launch_round_t<4, 4, false, false, 1>(a, p.nwarps, s);
