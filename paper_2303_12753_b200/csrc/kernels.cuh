@@ -6,16 +6,17 @@
 //                                    u64 words, hypervector.hpp:15-42), S32 = W32 rounded up to
 //                                    4 words so every pixel row is 16-byte aligned for TMA.
 //   Z         u32[K][D]              centroids: raw member sums (clusterer.hpp:27-34)
-//   bfrag     u64[NT][W32P][32]      Z split into 4 byte planes, laid out as the B fragments of
-//                                    mma.m16n8k32 (column n = 4*c + plane, NT = ceil(K/2)
+//   bfrag     u64[NT][W32P][32]      Z split into P 7-bit planes, laid out as the B fragments of
+//                                    mma.m16n8k32 (column n = P*c + plane, NT = ceil(K*P/8)
 //                                    n-tiles of 8), with the k-slot permutation of unpack_a().
-//   partials  u32[CTAs][K][Dp]       per-CTA centroid sums (Dp = 32*W32), exact integers.
-//   xchg      i32[K*Dp | K | 1 | Dp] [sums | counts | changed | column sums]; the only buffer
-//                                    a multi-GPU run all-reduces.
+//   xchg      i32[K*Dp | K | 1 | Dp] [centroid sums | member counts | changed | column sums],
+//                                    Dp = 32*W32. Every CTA folds its exact integer sums in
+//                                    with coalesced atomics; it is the only buffer a multi-GPU
+//                                    run all-reduces.
 //
 // Similarity is the reference's exact integer dot (hypervector.cpp:138-151):
-//   dot(y, z_c) = sum_{i: y_i = 1} z_c[i] = sum_p 256^p * (Y . plane_p(z_c))
-// computed as an integer GEMM Y[px x D] * B[D x 4K] on the IMMA tensor pipe (u8 x u8 -> s32,
+//   dot(y, z_c) = sum_{i: y_i = 1} z_c[i] = sum_p 128^p * (Y . plane_p(z_c))
+// computed as an integer GEMM Y[px x D] * B[D x P*K] on the IMMA tensor pipe (u8 x u8 -> s32,
 // exact), then recombined in u64 and compared with the reference's 128-bit cross
 // multiplication (clusterer.cpp:41-50). Centroid re-bundling (hypervector.cpp:112-121) is a
 // bit-sliced Harley-Seal carry-save counter per 32-bit word column. No floating point.
@@ -23,8 +24,6 @@
 #include <cstdint>
 
 namespace seghdc_dev {
-
-constexpr uint32_t kTileWarpsMax = 16;  // 512 threads: one warp per 32 HV words
 
 // ------------------------------------------------------------------------------------------
 // Device-side round state. Index [p] is the round parity (round r uses p = r & 1); the
@@ -37,31 +36,22 @@ struct RoundState {
     uint32_t pad;
 };
 // Followed in memory by (K = number of clusters):
-//   u32 counts[2][K]     members assigned in the round (accumulated by assign)
-//   u32 changed[2]       labels changed vs. the previous round
 //   u32 cur[2][K]        member counts of the centroid set used by the round's assignment
 //   u64 norm2[2][K]      IntVector::norm_squared of that set (hypervector.cpp:123-127)
 struct StateView {
     RoundState* hdr;
-    uint32_t* counts;
-    uint32_t* changed;
     uint32_t* cur;
     unsigned long long* norm2;
     uint32_t K;
-    __host__ __device__ static size_t bytes(uint32_t K) {
-        size_t b = sizeof(RoundState) + (2 * K + 2 + 2 * K) * 4;
-        b = (b + 7) & ~size_t(7);
-        return b + 2 * K * 8;
+    __host__ __device__ static size_t norm2_offset(uint32_t K) {
+        return (sizeof(RoundState) + 2 * size_t(K) * 4 + 7) & ~size_t(7);
     }
+    __host__ __device__ static size_t bytes(uint32_t K) { return norm2_offset(K) + 2 * size_t(K) * 8; }
     __host__ __device__ static StateView at(void* base, uint32_t K) {
         StateView v;
         v.hdr = reinterpret_cast<RoundState*>(base);
-        v.counts = reinterpret_cast<uint32_t*>(v.hdr + 1);
-        v.changed = v.counts + 2 * K;
-        v.cur = v.changed + 2;
-        size_t off = sizeof(RoundState) + (2 * K + 2 + 2 * K) * 4;
-        off = (off + 7) & ~size_t(7);
-        v.norm2 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + off);
+        v.cur = reinterpret_cast<uint32_t*>(v.hdr + 1);
+        v.norm2 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + norm2_offset(K));
         v.K = K;
         return v;
     }
@@ -130,6 +120,13 @@ struct BitCounter {
     }
     // capacity of the counter (largest representable count)
     __host__ __device__ static constexpr uint64_t capacity() { return 15ull + 16ull * ((1ull << H) - 1); }
+    // count of bit b
+    __device__ __forceinline__ uint32_t value(int b) const {
+        uint32_t val = ((o >> b) & 1u) | (((t >> b) & 1u) << 1) | (((f >> b) & 1u) << 2) | (((e >> b) & 1u) << 3);
+#pragma unroll
+        for (int m = 0; m < H; ++m) val |= ((hi[m] >> b) & 1u) << (4 + m);
+        return val;
+    }
     // dst[b] = count of bit b, b = 0..31 (32 consecutive u32)
     __device__ __forceinline__ void store(uint32_t* dst) const {
 #pragma unroll 4
@@ -149,6 +146,25 @@ struct BitCounter {
         }
     }
 };
+
+// Fold a warp's counters into dst with coalesced atomics: lane l owns word column
+// (col0 + l) = entries [32*(col0+l), 32*(col0+l)+32). The 32x32 block is transposed through
+// `scratch` (32*33 u32 of shared memory owned by this warp) so each atomic instruction covers
+// 32 consecutive entries (one 128-byte line). Columns >= ncols are skipped.
+template <int H>
+__device__ __forceinline__ void flush_warp_atomic(const BitCounter<H>& cnt, uint32_t* scratch, uint32_t* dst,
+                                                  uint32_t col0, uint32_t ncols) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) scratch[lane * 33 + b] = cnt.value(b);
+    __syncwarp();
+    for (uint32_t r = 0; r < 32; ++r) {
+        if (col0 + r >= ncols) break;
+        const uint32_t val = scratch[r * 33 + lane];
+        if (val) atomicAdd(dst + size_t(col0 + r) * 32 + lane, val);
+    }
+    __syncwarp();
+}
 
 // ------------------------------------------------------------------------------------------
 // PTX helpers: mbarrier + bulk async copy (TMA engine, cp.async.bulk) + legacy-path IMMA.

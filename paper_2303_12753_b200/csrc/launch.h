@@ -7,14 +7,18 @@
 
 namespace seghdc_dev {
 
+struct RoundState;
+
 struct EncodeArgs {
     const uint8_t* img;  // full image, h*w*c
     uint32_t w, c;
     uint64_t pix_begin, pix_end;  // global pixel range encoded into grid[0..)
     const uint32_t *row, *col, *wid;
     uint32_t wref;  // u32 words per table entry (2 * ceil(dim/64))
-    uint32_t S32;
+    uint32_t S32, W32;
     uint32_t* grid;
+    uint32_t* colsum;  // zeroed by the caller; receives the column sums of the encoded rows
+    uint32_t sms;
 };
 void launch_encode(const EncodeArgs& a, cudaStream_t s);
 
@@ -25,7 +29,7 @@ struct SeedArgs {
     uint16_t* min_dist;
     uint64_t* seeds;
     unsigned long long* slots;
-    struct RoundState* hdr;
+    RoundState* hdr;
 };
 void launch_select_seeds(const SeedArgs& a, cudaStream_t s);
 
@@ -46,26 +50,14 @@ struct AccumulateArgs {
     const uint32_t* labels;  // nullptr: every pixel counts for "cluster 0" (column sums)
     uint32_t K;
     int skip_mode;  // -1 none, -2 largest current cluster, >= 0 explicit
-    void* state;    // may be nullptr when skip_mode != -2 and count_members == 0
+    void* state;    // may be nullptr when skip_mode != -2
     uint32_t parity;
-    uint32_t* partials;
+    uint32_t* dst;         // sums land in dst[c * Dp + i] (atomically added)
     uint32_t Dp;
-    int count_members;
-    uint32_t blocks;  // pixel-range CTAs (partials has blocks*K*Dp entries)
+    uint32_t* counts_dst;  // nullable: member counts atomically added to counts_dst[c]
+    uint32_t sms;
 };
-uint32_t accumulate_blocks(uint64_t n, uint32_t sms);
 void launch_accumulate(const AccumulateArgs& a, cudaStream_t s);
-
-struct ReduceArgs {
-    const uint32_t* partials;
-    uint32_t nparts, K, Dp;
-    int skip_mode;
-    void* state;
-    uint32_t parity;
-    int32_t* xchg;
-    int copy_tail;
-};
-void launch_reduce(const ReduceArgs& a, cudaStream_t s);
 
 struct FinishArgs {
     int mode;  // 0 round, 1 init, 2 given centroids, 3 standalone update
@@ -83,13 +75,13 @@ void launch_finish(const FinishArgs& a, cudaStream_t s);
 
 struct RoundPlan {
     uint32_t nwarp_words = 0;  // 32-word blocks per HV
-    uint32_t nwarps = 0;       // warps per CTA
+    uint32_t nwarps = 0;       // (MMA) warps per CTA
     uint32_t mt = 0;           // m-tiles of 16 pixels per tile
     uint32_t ntg = 0;          // n-tiles per group
     uint32_t nt = 0;           // n-tiles in total: ceil(K * planes / 8)
     uint32_t wpw = 32;         // HV words per warp (split-K)
     uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
-    bool fused = false;        // one n-tile: B in registers (+ fused accumulation when K == 2)
+    bool fused = false;        // one n-tile: warp-specialised kernel (+ fused accumulation when K == 2)
 };
 struct RoundArgs {
     const uint32_t* grid;
@@ -100,11 +92,12 @@ struct RoundArgs {
     void* state;
     uint32_t round;
     int do_update;
-    uint32_t* partials;
+    int32_t* xchg;  // [K*Dp sums | K counts | changed], zeroed before the round
     uint32_t Dp;
     uint32_t ctas;
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
+size_t ws_smem_bytes(uint32_t SS, uint32_t nmw);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
 

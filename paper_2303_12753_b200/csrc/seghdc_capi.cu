@@ -94,9 +94,9 @@ struct seghdc_ctx {
     uint32_t planes = kPlanes;  // 7-bit centroid planes per cluster (5 when a caller's centroids exceed 2^28)
     int early_stop = 0;
     RoundPlan plan;
-    uint32_t round_ctas = 0, acc_blocks = 0;
+    uint32_t round_ctas = 0;
     DevBuf<uint8_t> state, bfrag;
-    DevBuf<uint32_t> labels, Z, partials;
+    DevBuf<uint32_t> labels, Z;
     DevBuf<int32_t> xchg;
     DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
     DevBuf<uint64_t> seeds;
@@ -189,11 +189,17 @@ void encode_rows(seghdc_ctx& x, size_t r0, size_t r1) {
     a.wid = x.wid.p;
     a.wref = uint32_t(2 * x.g.wph());
     a.S32 = x.g.S32;
+    a.W32 = x.g.W32;
     a.grid = x.grid.p;
+    x.colsum.ensure(x.g.Dp);
+    ck(cudaMemsetAsync(x.colsum.p, 0, x.g.Dp * 4, x.stream), "clear colsum");
+    a.colsum = reinterpret_cast<uint32_t*>(x.colsum.p);
+    a.sms = uint32_t(x.sms);
     launch_encode(a, x.stream);
     x.count();
     x.check_launch();
     x.grid_valid = true;
+    x.colsum_valid = true;  // the encode kernel accumulates the column sums as it writes
 }
 
 void load_grid(seghdc_ctx& x, const uint64_t* grid, size_t h, size_t w, size_t dim, size_t r0, size_t r1) {
@@ -230,7 +236,6 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
     const uint64_t n = x.n_local();
     const uint64_t tp = 16ull * x.plan.mt;
     x.round_ctas = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(x.sms, (n + tp - 1) / tp)));
-    x.acc_blocks = accumulate_blocks(n, uint32_t(x.sms));
     const uint32_t NT = x.plan.nt;
     x.state.ensure(StateView::bytes(uint32_t(K)));
     x.labels.ensure(n + 4);  // +4: the fused kernel's TMA of a tile's labels rounds up to 16 B
@@ -238,8 +243,6 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
     // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
     x.bfrag.ensure(size_t(NT) * x.plan.w32p * 32 * 8);
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
-    const size_t parts = std::max<size_t>(x.round_ctas, x.acc_blocks);
-    x.partials.ensure(parts * K * g.Dp);
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
     x.colsum.ensure(g.Dp);
     x.seeds.ensure(std::max<size_t>(K, 1));
@@ -247,9 +250,11 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
     x.min_dist.ensure(x.h * x.w);
 }
 
+// Column sums of a grid that did not come from encode (encode computes them on the fly):
+// every pixel counts as "cluster 0" of a Harley-Seal accumulation.
 void compute_colsum(seghdc_ctx& x) {
-    // every pixel as "cluster 0": Harley-Seal column sums, then a 1-cluster reduce into the
-    // colsum region of the exchange buffer
+    x.colsum.ensure(x.g.Dp);
+    ck(cudaMemsetAsync(x.colsum.p, 0, x.g.Dp * 4, x.stream), "clear colsum");
     AccumulateArgs a{};
     a.grid = x.grid.p;
     a.S32 = x.g.S32;
@@ -260,22 +265,12 @@ void compute_colsum(seghdc_ctx& x) {
     a.skip_mode = -1;
     a.state = nullptr;
     a.parity = 0;
-    a.partials = x.partials.p;
+    a.dst = reinterpret_cast<uint32_t*>(x.colsum.p);
     a.Dp = x.g.Dp;
-    a.count_members = 0;
-    a.blocks = x.acc_blocks;
+    a.counts_dst = nullptr;
+    a.sms = uint32_t(x.sms);
     launch_accumulate(a, x.stream);
-    ReduceArgs r{};
-    r.partials = x.partials.p;
-    r.nparts = x.acc_blocks;
-    r.K = 1;
-    r.Dp = x.g.Dp;
-    r.skip_mode = -1;
-    r.state = nullptr;
-    r.xchg = x.colsum.p;
-    r.copy_tail = 0;
-    launch_reduce(r, x.stream);
-    x.count(2);
+    x.count();
     x.check_launch();
     x.colsum_valid = true;
 }
@@ -372,9 +367,11 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.state = x.state.p;
     a.round = r;
     a.do_update = do_update ? 1 : 0;
-    a.partials = x.partials.p;
+    a.xchg = x.xchg.p;
     a.Dp = x.g.Dp;
     a.ctas = x.round_ctas;
+    // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
+    ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     cudaEvent_t ev_end = nullptr;
     if (x.profiling) {
         if (x.prof_used == x.prof_events.size()) {
@@ -400,31 +397,14 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
         u.skip_mode = -2;
         u.state = x.state.p;
         u.parity = r & 1;
-        u.partials = x.partials.p;
+        u.dst = reinterpret_cast<uint32_t*>(x.xchg.p);
         u.Dp = x.g.Dp;
-        u.count_members = 0;
-        u.blocks = x.acc_blocks;
+        u.counts_dst = nullptr;  // member counts come from the round kernel
+        u.sms = uint32_t(x.sms);
         launch_accumulate(u, x.stream);
         x.count();
         x.check_launch();
     }
-}
-
-// Partial sums -> exchange buffer (before the all-reduce).
-void round_reduce(seghdc_ctx& x, uint32_t r) {
-    ReduceArgs a{};
-    a.partials = x.partials.p;
-    a.nparts = x.plan.fused ? x.round_ctas : x.acc_blocks;
-    a.K = uint32_t(x.K);
-    a.Dp = x.g.Dp;
-    a.skip_mode = -2;
-    a.state = x.state.p;
-    a.parity = r & 1;
-    a.xchg = x.xchg.p;
-    a.copy_tail = 1;
-    launch_reduce(a, x.stream);
-    x.count();
-    x.check_launch();
 }
 
 struct HostState {
@@ -455,7 +435,6 @@ void run_rounds(seghdc_ctx& x, seghdc_round_cb cb, void* user) {
             cb(user, r, host_labels.data());
         }
         if (r < x.iterations) {
-            round_reduce(x, r);
             finish(x, 0, r);
             if (cb && x.early_stop && read_state(x).hdr.done) break;
         }
@@ -635,23 +614,13 @@ int seghdc_update(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         u.skip_mode = -1;
         u.state = ctx->state.p;
         u.parity = 1;
-        u.partials = ctx->partials.p;
+        ck(cudaMemsetAsync(ctx->xchg.p, 0, ctx->xchg_round_ints() * 4, ctx->stream), "clear exchange");
+        u.dst = reinterpret_cast<uint32_t*>(ctx->xchg.p);
         u.Dp = ctx->g.Dp;
-        u.count_members = 1;
-        u.blocks = ctx->acc_blocks;
+        u.counts_dst = reinterpret_cast<uint32_t*>(ctx->xchg.p) + k * ctx->g.Dp;
+        u.sms = uint32_t(ctx->sms);
         launch_accumulate(u, ctx->stream);
-        ReduceArgs r{};
-        r.partials = ctx->partials.p;
-        r.nparts = ctx->acc_blocks;
-        r.K = uint32_t(k);
-        r.Dp = ctx->g.Dp;
-        r.skip_mode = -1;
-        r.state = ctx->state.p;
-        r.parity = 1;
-        r.xchg = ctx->xchg.p;
-        r.copy_tail = 1;
-        launch_reduce(r, ctx->stream);
-        ctx->count(2);
+        ctx->count();
         ctx->check_launch();
         finish(*ctx, 3, 1);
         ck(cudaMemcpyAsync(centroids_out, ctx->Z.p, k * dim * 4, cudaMemcpyDeviceToHost, ctx->stream),
@@ -801,7 +770,7 @@ int seghdc_shard_assign(seghdc_ctx* ctx, size_t round) {
     return guarded(ctx, [&] {
         require(round >= 1 && round <= ctx->iterations, "round out of range");
         round_assign(*ctx, uint32_t(round));
-        if (round < ctx->iterations) round_reduce(*ctx, uint32_t(round));
+
     });
 }
 

@@ -14,50 +14,87 @@ namespace seghdc_dev {
 
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
 
+template <int H>
+constexpr uint64_t counter_capacity() {
+    return BitCounter<H>::capacity();
+}
+// Counter planes for a run of at most `count` inputs per counter.
+#define SEGHDC_DISPATCH_H(count, FN, ...)                              \
+    do {                                                               \
+        const uint64_t _c = (count);                                   \
+        if (_c <= counter_capacity<8>()) FN<8>(__VA_ARGS__);           \
+        else if (_c <= counter_capacity<12>()) FN<12>(__VA_ARGS__);    \
+        else if (_c <= counter_capacity<16>()) FN<16>(__VA_ARGS__);    \
+        else FN<24>(__VA_ARGS__);                                      \
+    } while (0)
+
 // =============================================================================================
 // encode_image (reference pixel_pipeline.cpp:92-126): grid[p] = row[i] ^ col[j] ^ ^_ch wid[ch][v]
-// One CTA per PXB consecutive pixels; thread t owns u32 word column t (coalesced 128-B stores
-// per warp per pixel). Tables are the reference's u64 words read as u32 (same bytes).
+// fused with the column sums of the grid (the Harley-Seal counter of every pixel), which the
+// round schedule needs to derive the largest cluster's sums without accumulating them.
+// CTA = (contiguous pixel range, block of <= 512 word columns); thread t = word column, 16
+// pixels per step (16 independent table reads in flight, coalesced 128-B stores per warp).
+// Tables are the reference's u64 words read as u32 (same bytes).
 // =============================================================================================
-template <int C>
-__global__ void __launch_bounds__(256) k_encode(const uint8_t* __restrict__ img, uint32_t w,
-                                                 uint64_t pix_begin, uint64_t pix_end,
-                                                 const uint32_t* __restrict__ row,
-                                                 const uint32_t* __restrict__ col,
-                                                 const uint32_t* __restrict__ wid, uint32_t wref,
-                                                 uint32_t S32, uint32_t pxb, uint32_t* __restrict__ grid) {
-    const uint64_t p0 = pix_begin + uint64_t(blockIdx.x) * pxb;
-    const uint64_t p1 = p0 + pxb < pix_end ? p0 + pxb : pix_end;
-    for (uint32_t t = threadIdx.x; t < S32; t += blockDim.x) {
-        const bool live = t < wref;
-        for (uint64_t p = p0; p < p1; ++p) {
-            const uint32_t i = uint32_t(p / w), j = uint32_t(p - uint64_t(i) * w);
+template <int C, int H>
+__global__ void __launch_bounds__(512) k_encode(const uint8_t* __restrict__ img, uint32_t w, uint64_t pix_begin,
+                                                 uint64_t pix_end, uint64_t ppc, const uint32_t* __restrict__ row,
+                                                 const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
+                                                 uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid,
+                                                 uint32_t* __restrict__ colsum, uint32_t W32) {
+    extern __shared__ uint32_t scratch_all[];  // [warps][32*33] for the final flush
+    const uint32_t t = blockIdx.y * blockDim.x + threadIdx.x;
+    const uint64_t p0 = pix_begin + uint64_t(blockIdx.x) * ppc;
+    const uint64_t p1 = p0 + ppc < pix_end ? p0 + ppc : pix_end;
+    const bool live = t < wref, store = t < S32;
+    BitCounter<H> cnt;
+    cnt.reset();
+    uint32_t i = p0 < p1 ? uint32_t(p0 / w) : 0, j = p0 < p1 ? uint32_t(p0 - uint64_t(i) * w) : 0;
+    for (uint64_t q = p0; q < p1; q += 16) {
+        uint32_t x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const uint64_t p = q + u;
             uint32_t v = 0;
-            if (live) {
+            if (p < p1 && live) {
                 v = __ldg(row + size_t(i) * wref + t) ^ __ldg(col + size_t(j) * wref + t);
 #pragma unroll
-                for (int ch = 0; ch < C; ++ch) {
-                    const uint32_t val = img[p * C + ch];
-                    v ^= __ldg(wid + (size_t(ch) * 256 + val) * wref + t);
-                }
+                for (int ch = 0; ch < C; ++ch) v ^= __ldg(wid + (size_t(ch) * 256 + img[p * C + ch]) * wref + t);
             }
-            grid[(p - pix_begin) * S32 + t] = v;
+            if (p < p1 && store) grid[(p - pix_begin) * S32 + t] = v;
+            x[u] = v;
+            if (++j == w) {
+                j = 0;
+                ++i;
+            }
         }
+        cnt.add16(x);
+    }
+    flush_warp_atomic(cnt, scratch_all + (threadIdx.x >> 5) * (32 * 33), colsum, t & ~31u, W32);
+}
+
+template <int H>
+static void launch_encode_h(const EncodeArgs& a, uint32_t blocks, uint64_t ppc, cudaStream_t s) {
+    const uint32_t threads = std::min<uint32_t>(512, ((a.S32 + 31) / 32) * 32);
+    dim3 g(blocks, (a.S32 + threads - 1) / threads);
+    const size_t smem = size_t(threads / 32) * 32 * 33 * 4;
+    if (a.c == 1) {
+        cudaFuncSetAttribute(k_encode<1, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_encode<1, H><<<g, threads, smem, s>>>(a.img, a.w, a.pix_begin, a.pix_end, ppc, a.row, a.col, a.wid, a.wref,
+                                                a.S32, a.grid, a.colsum, a.W32);
+    } else {
+        cudaFuncSetAttribute(k_encode<3, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_encode<3, H><<<g, threads, smem, s>>>(a.img, a.w, a.pix_begin, a.pix_end, ppc, a.row, a.col, a.wid, a.wref,
+                                                a.S32, a.grid, a.colsum, a.W32);
     }
 }
 
 void launch_encode(const EncodeArgs& a, cudaStream_t s) {
-    const uint32_t pxb = 16;
     const uint64_t n = a.pix_end - a.pix_begin;
     if (n == 0) return;
-    const uint32_t blocks = uint32_t((n + pxb - 1) / pxb);
-    const uint32_t threads = std::min<uint32_t>(256, ((a.S32 + 31) / 32) * 32);
-    if (a.c == 1)
-        k_encode<1><<<blocks, threads, 0, s>>>(a.img, a.w, a.pix_begin, a.pix_end, a.row, a.col, a.wid, a.wref,
-                                               a.S32, pxb, a.grid);
-    else
-        k_encode<3><<<blocks, threads, 0, s>>>(a.img, a.w, a.pix_begin, a.pix_end, a.row, a.col, a.wid, a.wref,
-                                               a.S32, pxb, a.grid);
+    const uint32_t blocks = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(a.sms) * 4, (n + 63) / 64)));
+    const uint64_t ppc = (n + blocks - 1) / blocks;
+    SEGHDC_DISPATCH_H(ppc, launch_encode_h, a, blocks, ppc, s);
 }
 
 // =============================================================================================
@@ -189,20 +226,23 @@ void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s) {
 
 // =============================================================================================
 // Standalone bit-sliced accumulation (update_centroids, clusterer.cpp:164-188, without the
-// fused assignment; also the column sums "colsum" when labels == nullptr).
-// CTA = (pixel range, 1024-word column block). For each cluster c != skip the CTA compacts
+// fused assignment; also the column sums when labels == nullptr).
+// CTA = (pixel range, <= 512-word column block). For each cluster c != skip the CTA compacts
 // the pixels of its range labelled c and feeds their words through one Harley-Seal counter
-// per word column, so every pixel HV is read exactly once regardless of K.
+// per word column, so every pixel HV is read exactly once regardless of K; the counters are
+// folded into dst[c * Dp + ...] with coalesced atomics, member counts into counts_dst[c].
 // =============================================================================================
 template <int H>
 __global__ void __launch_bounds__(512) k_accumulate(const uint32_t* __restrict__ grid, uint32_t S32, uint32_t W32,
                                                      uint64_t n, uint64_t ppc, const uint32_t* __restrict__ labels,
                                                      uint32_t K, int skip_mode, void* state, uint32_t parity,
-                                                     uint32_t* __restrict__ partials, uint32_t Dp, int count_members) {
+                                                     uint32_t* __restrict__ dst, uint32_t Dp,
+                                                     uint32_t* __restrict__ counts_dst) {
     constexpr uint32_t CHUNK = 4096;
-    __shared__ uint32_t list[CHUNK];
-    __shared__ uint32_t list_n;
-    __shared__ uint32_t s_counts_c;
+    extern __shared__ uint32_t dyn[];
+    uint32_t* list = dyn;                        // [CHUNK]
+    uint32_t* scratch = dyn + CHUNK;             // [warps][32*33]
+    __shared__ uint32_t list_n, s_count;
     StateView st = StateView::at(state, K);
     if (state && st.hdr->done) return;
     const uint32_t t = blockIdx.y * blockDim.x + threadIdx.x;  // word column
@@ -216,7 +256,7 @@ __global__ void __launch_bounds__(512) k_accumulate(const uint32_t* __restrict__
     for (uint32_t c = 0; c < nclusters; ++c) {
         if (int(c) == skip) continue;
         cnt.reset();
-        if (threadIdx.x == 0) s_counts_c = 0;
+        if (threadIdx.x == 0) s_count = 0;
         for (uint64_t q0 = p_begin; q0 < p_end; q0 += CHUNK) {
             const uint64_t q1 = q0 + CHUNK < p_end ? q0 + CHUNK : p_end;
             __syncthreads();
@@ -232,7 +272,7 @@ __global__ void __launch_bounds__(512) k_accumulate(const uint32_t* __restrict__
             }
             __syncthreads();
             const uint32_t m = list_n;
-            if (threadIdx.x == 0) s_counts_c += m;
+            if (threadIdx.x == 0) s_count += m;
             if (t < W32) {
                 for (uint32_t e = 0; e < m; e += 16) {
                     uint32_t x[16];
@@ -243,10 +283,9 @@ __global__ void __launch_bounds__(512) k_accumulate(const uint32_t* __restrict__
                 }
             }
         }
-        if (t < W32) cnt.store(partials + (size_t(blockIdx.x) * K + c) * Dp + size_t(t) * 32);
+        flush_warp_atomic(cnt, scratch + (threadIdx.x >> 5) * (32 * 33), dst + size_t(c) * Dp, t & ~31u, W32);
         __syncthreads();
-        if (count_members && threadIdx.x == 0 && blockIdx.y == 0 && state)
-            atomicAdd(st.counts + parity * K + c, s_counts_c);
+        if (counts_dst && threadIdx.x == 0 && blockIdx.y == 0 && s_count) atomicAdd(counts_dst + c, s_count);
     }
 }
 
@@ -254,56 +293,16 @@ template <int H>
 static void launch_accumulate_h(const AccumulateArgs& a, uint32_t blocks_x, uint64_t ppc, cudaStream_t s) {
     const uint32_t threads = std::min<uint32_t>(512, ((a.W32 + 31) / 32) * 32);
     dim3 g(blocks_x, (a.W32 + threads - 1) / threads);
-    k_accumulate<H><<<g, threads, 0, s>>>(a.grid, a.S32, a.W32, a.n, ppc, a.labels, a.K, a.skip_mode, a.state,
-                                          a.parity, a.partials, a.Dp, a.count_members);
-}
-
-uint32_t accumulate_blocks(uint64_t n, uint32_t sms) {
-    return uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(sms) * 2, (n + 255) / 256)));
+    const size_t smem = (4096 + size_t(threads / 32) * 32 * 33) * 4;
+    cudaFuncSetAttribute(k_accumulate<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_accumulate<H><<<g, threads, smem, s>>>(a.grid, a.S32, a.W32, a.n, ppc, a.labels, a.K, a.skip_mode, a.state,
+                                             a.parity, a.dst, a.Dp, a.counts_dst);
 }
 
 void launch_accumulate(const AccumulateArgs& a, cudaStream_t s) {
-    const uint32_t blocks = a.blocks;
+    const uint32_t blocks = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(a.sms) * 2, (a.n + 255) / 256)));
     const uint64_t ppc = (a.n + blocks - 1) / blocks;
-    if (ppc <= BitCounter<8>::capacity())
-        launch_accumulate_h<8>(a, blocks, ppc, s);
-    else if (ppc <= BitCounter<12>::capacity())
-        launch_accumulate_h<12>(a, blocks, ppc, s);
-    else if (ppc <= BitCounter<16>::capacity())
-        launch_accumulate_h<16>(a, blocks, ppc, s);
-    else
-        launch_accumulate_h<24>(a, blocks, ppc, s);
-}
-
-// =============================================================================================
-// Reduce per-CTA partial sums into the exchange buffer (clusters != skip), and copy the
-// round's counts/changed into its tail. xchg entries of the skipped cluster are left 0.
-// =============================================================================================
-__global__ void k_reduce(const uint32_t* __restrict__ partials, uint32_t nparts, uint32_t K, uint32_t Dp,
-                         int skip_mode, void* state, uint32_t parity, int32_t* xchg, int copy_tail) {
-    StateView st = StateView::at(state, K);
-    if (state && st.hdr->done) return;
-    int skip = skip_mode;
-    if (skip_mode == -2) skip = int(pick_skip(st.cur + parity * K, K));
-    const size_t total = size_t(K) * Dp;
-    for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
-        const uint32_t c = uint32_t(e / Dp);
-        uint32_t s = 0;
-        if (int(c) != skip)
-            for (uint32_t b = 0; b < nparts; ++b) s += partials[size_t(b) * total + e];
-        xchg[e] = int32_t(s);
-    }
-    if (copy_tail && blockIdx.x == 0 && threadIdx.x <= K) {
-        const uint32_t v = threadIdx.x < K ? st.counts[parity * K + threadIdx.x] : st.changed[parity];
-        xchg[total + threadIdx.x] = int32_t(v);
-    }
-}
-
-void launch_reduce(const ReduceArgs& a, cudaStream_t s) {
-    const size_t total = size_t(a.K) * a.Dp;
-    const uint32_t blocks = uint32_t(std::min<size_t>((total + 255) / 256, 148 * 4));
-    k_reduce<<<blocks, 256, 0, s>>>(a.partials, a.nparts, a.K, a.Dp, a.skip_mode, a.state, a.parity, a.xchg,
-                                    a.copy_tail);
+    SEGHDC_DISPATCH_H(ppc, launch_accumulate_h, a, blocks, ppc, s);
 }
 
 // =============================================================================================
@@ -314,7 +313,8 @@ void launch_reduce(const ReduceArgs& a, cudaStream_t s) {
 //   mode 1 (init):   centroids = seed HV bits, member counts 1 (clusterer.cpp:197-205).
 //   mode 2 (given):  centroids already in Z (assign_labels on caller centroids).
 //   mode 3 (update): like 0 but no skip and no early stop (update_centroids API).
-// Always: norm2 of the new set, B fragments. One thread per (32-bit word, cluster).
+// Always: norm2 of the new set and its B fragments. One warp per (32-bit word, cluster):
+// lane b owns entry 32*word + b; lanes (plane, q) then gather the 8 entries of one B slot.
 // =============================================================================================
 __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
                          const int32_t* __restrict__ xchg, const int32_t* __restrict__ colsum, uint32_t* Z,
@@ -330,60 +330,47 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
             return;
         }
     }
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t word = idx / K, c = idx % K;
-    const int skip = (mode == 0) ? int(pick_skip(st.cur + p * K, K)) : -1;
-    unsigned long long n2 = 0;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t word = gw / K, c = gw % K;
     if (word < W32) {
-        uint32_t z[32];
-        const size_t base = size_t(word) * 32;
+        const int skip = (mode == 0) ? int(pick_skip(st.cur + p * K, K)) : -1;
+        const size_t i = size_t(word) * 32 + lane;
+        const bool in = i < D;
+        uint32_t z;
         if (mode == 2) {
-#pragma unroll
-            for (int b = 0; b < 32; ++b) z[b] = (base + b < D) ? Z[size_t(c) * D + base + b] : 0u;
+            z = in ? Z[size_t(c) * D + i] : 0u;
         } else if (mode == 1 || counts[c] != 0) {
             if (int(c) == skip) {
-#pragma unroll
-                for (int b = 0; b < 32; ++b) z[b] = uint32_t(colsum[base + b]);
-                for (uint32_t o = 0; o < K; ++o) {
-                    if (int(o) == skip) continue;
-#pragma unroll
-                    for (int b = 0; b < 32; ++b) z[b] -= uint32_t(xchg[size_t(o) * Dp + base + b]);
-                }
+                z = uint32_t(colsum[i]);
+                for (uint32_t o = 0; o < K; ++o)
+                    if (int(o) != skip) z -= uint32_t(xchg[size_t(o) * Dp + i]);
             } else {
-#pragma unroll
-                for (int b = 0; b < 32; ++b) z[b] = uint32_t(xchg[size_t(c) * Dp + base + b]);
+                z = uint32_t(xchg[size_t(c) * Dp + i]);
             }
         } else {  // empty cluster keeps its previous centroid
-#pragma unroll
-            for (int b = 0; b < 32; ++b) z[b] = (base + b < D) ? Z[size_t(c) * D + base + b] : 0u;
+            z = in ? Z[size_t(c) * D + i] : 0u;
         }
+        if (!in) z = 0;
+        if (in && mode != 2) Z[size_t(c) * D + i] = z;
+        unsigned long long n2 = (unsigned long long)z * z;
+        for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        if (lane == 0) atomicAdd(st.norm2 + np * K + c, n2);
+        // B fragments: column n = P*c + plane; slot lane (n&7)<<2 | q holds bits {2q, 2q+8,
+        // 2q+16, 2q+24} (bytes 0-3, doubled: a0/a1 carry 64*bit) and {2q+1, ...} (bytes 4-7).
+        const uint32_t pl = lane >> 2, q = lane & 3;
+        uint64_t v = 0;
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            if (base + b < D) {
-                if (mode != 2) Z[size_t(c) * D + base + b] = z[b];
-                n2 += (unsigned long long)z[b] * z[b];
-            } else {
-                z[b] = 0;
+        for (uint32_t half = 0; half < 2; ++half)
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                const uint32_t zb = __shfl_sync(0xffffffffu, z, 2 * q + half + 8 * j);
+                v |= uint64_t(((zb >> (kPlaneBits * pl)) & 0x7Fu) << (1 - half)) << (8 * (half * 4 + j));
             }
-        }
-        // B fragments: column n = P*c + plane; lane (n&7)<<2 | q holds bits {2q, 2q+8, 2q+16,
-        // 2q+24} (bytes 0-3) and {2q+1, ...} (bytes 4-7) of this word, one 7-bit plane each.
-        for (uint32_t pl = 0; pl < P; ++pl) {
+        if (pl < P) {
             const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7;
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-                uint64_t v = 0;
-#pragma unroll
-                for (uint32_t half = 0; half < 2; ++half)
-#pragma unroll
-                    for (uint32_t j = 0; j < 4; ++j)
-                        v |= uint64_t(((z[2 * q + half + 8 * j] >> (kPlaneBits * pl)) & 0x7Fu) << (1 - half))
-                             << (8 * (half * 4 + j));  // a0/a1 slots carry 64*bit: plane doubled
-                const uint32_t lane = (nl << 2) | q;
-                *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + word) * 32 + lane) * 8) = v;
-            }
+            *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + word) * 32 + ((nl << 2) | q)) * 8) = v;
         }
-        atomicAdd(st.norm2 + np * K + c, n2);
     }
     if (blockIdx.x == 0 && threadIdx.x < K) {
         const uint32_t cc = threadIdx.x;
@@ -393,11 +380,10 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
 }
 
 void launch_finish(const FinishArgs& a, cudaStream_t s) {
-    const uint32_t threads = 128;
-    const uint32_t total = a.W32 * a.K;
-    k_finish<<<(total + threads - 1) / threads, threads, 0, s>>>(a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg,
-                                                                 a.colsum, a.Z, a.bfrag, a.state, a.round,
-                                                                 a.early_stop);
+    const uint32_t threads = 256;
+    const uint64_t total = uint64_t(a.W32) * a.K * 32;
+    k_finish<<<uint32_t((total + threads - 1) / threads), threads, 0, s>>>(
+        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop);
 }
 
 // Zero the accumulators of parity np before k_finish accumulates into them.
@@ -410,25 +396,21 @@ void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s) {
 }
 
 // =============================================================================================
-// The round kernel: assign_labels (clusterer.cpp:132-162) fused with the centroid
-// accumulation of update_centroids (clusterer.cpp:164-188).
+// Generic round kernel (any K): assign_labels (clusterer.cpp:132-162).
 //
-// Persistent CTAs walk tiles of TP = 16*MT pixels. Each tile arrives in shared memory by
-// cp.async.bulk (TMA engine, one copy per pixel row, double buffered on mbarriers). Warp g
-// owns 32-bit words [32g, 32g+32) of every HV (split-K): it unpacks the packed bits into IMMA
-// A fragments in registers (unpack_a) and multiplies them with the byte-plane B fragments of
-// the centroids (held in registers when BREG). Per-warp partial dots meet in shared memory,
-// one thread per pixel recombines the planes in u64 and runs the exact 128-bit argmax. With
-// UPD (K == 2) the words of the pixels assigned to the non-skipped cluster are then folded
-// into a per-thread Harley-Seal counter (thread t = word column t) straight from the same
-// shared-memory tile, so each pixel HV crosses HBM once per round.
+// Persistent CTAs walk tiles of TP = 16*MT pixels, double buffered through cp.async.bulk
+// (TMA engine, one copy per pixel row) on mbarriers. Warp g owns 32-word blocks of every HV
+// (split-K), unpacks the packed bits into IMMA A fragments in registers (unpack_a) and
+// multiplies them with the 7-bit-plane B fragments of the centroids, NTG n-tiles at a time
+// (B streamed from L2). Partial dots meet in shared memory; one thread per pixel recombines
+// the planes in u64 and runs the exact 128-bit argmax. Member counts and the change count
+// go to the exchange-buffer tail; the re-bundling runs in k_accumulate.
 // =============================================================================================
-template <int MT, int NTG, bool BREG, bool UPD, int H, int TB>
+template <int MT, int NTG, int TB>
 __global__ void __launch_bounds__(TB, 1)
-    k_round(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t W32P,
+    k_round(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32P,
             uint32_t nwarp_words, uint32_t K, uint32_t P, uint32_t NT, const uint64_t* __restrict__ bfrag,
-            uint32_t* labels, void* state, uint32_t round, int do_update, uint32_t* __restrict__ partials,
-            uint32_t Dp) {
+            uint32_t* labels, void* state, uint32_t round, uint32_t* __restrict__ tail) {
     constexpr uint32_t TP = 16 * MT;
     constexpr uint32_t NC = NTG * 8;  // columns per group
     extern __shared__ __align__(128) uint8_t smem[];
@@ -441,15 +423,12 @@ __global__ void __launch_bounds__(TB, 1)
     const uint32_t parity = round & 1;
     const uint32_t NCT = NT * 8;  // all columns (P planes x K clusters, padded to n-tiles)
 
-    // shared memory carve-up
     uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
     const size_t tile_words = size_t(TP) * SS;
-    int32_t* part = reinterpret_cast<int32_t*>(tiles + 2 * tile_words + 32);  // [nwarps][TP][NC]
+    int32_t* part = reinterpret_cast<int32_t*>(tiles + 2 * tile_words + 32);     // [nwarps][TP][NC]
     uint32_t* red = reinterpret_cast<uint32_t*>(part + size_t(nwarps) * TP * NC);  // [TP][NCT]
-    uint32_t* s_label = red + TP * NCT;                                          // [TP]
-    uint32_t* s_list = s_label + TP;                                             // [TP]
-    uint32_t* s_misc = s_list + TP;  // [0] list_n, [1] changed, [2] skip, [4..4+K) counts
-    unsigned long long* s_n2 = reinterpret_cast<unsigned long long*>(s_misc + ((4 + K + 1) & ~1u));  // [K]
+    uint32_t* s_misc = red + TP * NCT;  // [0] changed, [2..2+K) counts
+    unsigned long long* s_n2 = reinterpret_cast<unsigned long long*>(s_misc + ((2 + K + 1) & ~1u));  // [K]
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_n2 + K);
 
     const uint64_t ntiles = (n + TP - 1) / TP;
@@ -458,25 +437,15 @@ __global__ void __launch_bounds__(TB, 1)
         mbar_init(&bars[1], 1);
         mbar_fence_init();
         s_misc[0] = 0;
-        s_misc[1] = 0;
-        s_misc[2] = pick_skip(st.cur + parity * K, K);
     }
     for (uint32_t c = tid; c < K; c += blockDim.x) {
-        s_misc[4 + c] = 0;
+        s_misc[2 + c] = 0;
         s_n2[c] = st.norm2[parity * K + c];
     }
-    if (blockIdx.x == 0 && tid == 0) {
-        st.hdr->rounds_run = round;
-        // reset the other parity's accumulators for the next round
-        for (uint32_t c = 0; c < K; ++c) st.counts[(parity ^ 1) * K + c] = 0;
-        st.changed[parity ^ 1] = 0;
-    }
+    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
     __syncthreads();
-    const uint32_t skip = s_misc[2];
-    const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
 
     auto issue = [&](uint64_t tile, uint32_t buf) {
-        // warp 0 issues one bulk copy per pixel row (rows are S32*4 bytes, 16-B aligned)
         const uint64_t px0 = tile * TP;
         const uint32_t npx = uint32_t(umin64(TP, n - px0));
         if (lane == 0) mbar_expect_tx(&bars[buf], npx * S32 * 4);
@@ -491,28 +460,9 @@ __global__ void __launch_bounds__(TB, 1)
             if (tile < ntiles) issue(tile, b);
         }
     }
-
-    // B fragments resident in registers for the whole round (BREG: one word block per warp)
-    uint32_t breg[BREG ? 32 : 1][2];
-    if constexpr (BREG) {
-#pragma unroll
-        for (int kk = 0; kk < 32; ++kk) {
-            const uint64_t v = warp < nwarp_words ? bfrag[(size_t(warp) * 32 + kk) * 32 + lane] : 0ull;
-            breg[kk][0] = uint32_t(v);
-            breg[kk][1] = uint32_t(v >> 32);
-        }
-    }
-    // shift of unpack_a as an opaque multiplier so it issues as IMAD (FMA pipe), not SHF (ALU)
-    uint32_t mul;
+    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
     asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
-
-    BitCounter<UPD ? H : 1> cnt;
-    if constexpr (UPD) cnt.reset();
-
     const uint32_t ngroups = (NT + NTG - 1) / NTG;
-    // epilogue state (threads tid < TP): running argmax across n-tile groups
-    uint32_t best = 0;
-    unsigned long long bdot = 0, bn2 = 0;
 
     uint32_t it = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -521,7 +471,6 @@ __global__ void __launch_bounds__(TB, 1)
         const uint32_t* T = tiles + buf * tile_words;
         const uint64_t px0 = tile * TP;
         const uint32_t npx = uint32_t(umin64(TP, n - px0));
-        // previous labels, fetched now so the load latency hides behind the k-loop
         const uint32_t old = (tid < npx) ? labels[px0 + tid] : 0u;
 
         for (uint32_t grp = 0; grp < ngroups; ++grp) {
@@ -537,7 +486,6 @@ __global__ void __launch_bounds__(TB, 1)
                 const uint32_t wbase = wb * 32;
 #pragma unroll
                 for (int k4 = 0; k4 < 8; ++k4) {
-                    // rows g and g+8 of every m-tile: 4 consecutive words = 4 k-steps
                     uint4 wl[MT], wh[MT];
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
@@ -550,18 +498,12 @@ __global__ void __launch_bounds__(TB, 1)
                         uint32_t b0[NTG], b1[NTG];
 #pragma unroll
                         for (int nt = 0; nt < NTG; ++nt) {
-                            if constexpr (BREG) {
-                                b0[nt] = breg[kk][0];
-                                b1[nt] = breg[kk][1];
-                            } else {
-                                const uint32_t ntg = grp * NTG + nt;
-                                uint64_t v = 0;
-                                if (ntg < NT) v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
-                                b0[nt] = uint32_t(v);
-                                b1[nt] = uint32_t(v >> 32);
-                            }
+                            const uint32_t ntg = grp * NTG + nt;
+                            uint64_t v = 0;
+                            if (ntg < NT) v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
+                            b0[nt] = uint32_t(v);
+                            b1[nt] = uint32_t(v >> 32);
                         }
-                        // consecutive IMMAs target different m-tiles: independent accumulators
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
                             uint32_t a[4];
@@ -572,7 +514,6 @@ __global__ void __launch_bounds__(TB, 1)
                     }
                 }
             }
-            // per-warp partial dots -> shared memory
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -591,211 +532,13 @@ __global__ void __launch_bounds__(TB, 1)
             }
             __syncthreads();  // red complete for this group; part free for the next group
         }
-        // exact dots (u64) and the reference's 128-bit argmax, ties to the lower index
-        if (tid < TP) {
+        if (tid < npx) {
             const uint32_t* rr = red + tid * NCT;
-            for (uint32_t c = 0; c < K; ++c) {
-                unsigned long long d = 0;
-                for (uint32_t pl = 0; pl < P; ++pl) d += (unsigned long long)rr[P * c + pl] << (kPlaneBits * pl);
-                const unsigned long long n2 = s_n2[c];
-                if (c == 0) {
-                    best = 0;
-                    bdot = d;
-                    bn2 = n2;
-                } else if (strictly_closer(d, n2, bdot, bn2)) {
-                    best = c;
-                    bdot = d;
-                    bn2 = n2;
-                }
-            }
-        }
-
-        // labels, changed count, member counts, update list
-        if (tid < TP) {
-            const bool live = tid < npx;
-            if (live) {
-                const uint64_t p = px0 + tid;
-                labels[p] = best;
-                if (old != best) atomicAdd(&s_misc[1], 1u);
-                atomicAdd(&s_misc[4 + best], 1u);
-                s_label[tid] = best;
-                if (UPD && do_update && best == upd_c) s_list[atomicAdd(&s_misc[0], 1u)] = tid;
-            }
-        }
-        __syncthreads();
-        if constexpr (UPD) {
-            if (do_update) {
-                const uint32_t m = s_misc[0];
-                if (tid < W32) {
-                    for (uint32_t e = 0; e < m; e += 16) {
-                        uint32_t x[16];
-#pragma unroll
-                        for (int u = 0; u < 16; ++u) x[u] = (e + u < m) ? T[size_t(s_list[e + u]) * SS + tid] : 0u;
-                        cnt.add16(x);
-                    }
-                }
-            }
-        }
-        __syncthreads();  // every read of this buffer is done
-        if (tid == 0) s_misc[0] = 0;
-        if (warp == 0) {
-            const uint64_t nxt = tile + 2ull * gridDim.x;
-            if (nxt < ntiles) {
-                fence_proxy_async();
-                issue(nxt, buf);
-            }
-        }
-    }
-
-    if constexpr (UPD) {
-        if (do_update && tid < W32) cnt.store(partials + (size_t(blockIdx.x) * K + upd_c) * Dp + size_t(tid) * 32);
-    }
-    __syncthreads();
-    if (tid == 0) atomicAdd(st.changed + parity, s_misc[1]);
-    for (uint32_t c = tid; c < K; c += blockDim.x) atomicAdd(st.counts + parity * K + c, s_misc[4 + c]);
-}
-
-// =============================================================================================
-// The fused round kernel for one n-tile of centroid planes (K * P <= 8: K <= 2 at P = 4).
-// Same data flow as k_round, tuned for the headline configs:
-//  * warp w owns WPW words (a multiple of 4; warps a multiple of 4 so every SM sub-partition
-//    carries the same k-loop load) and holds their B fragments in 2*WPW registers;
-//  * the previous labels of a tile ride in the tile's TMA transaction (no exposed LDG);
-//  * the split-K reduction and the argmax run on every warp at once (8 lanes per pixel,
-//    planes combined with shuffles), so only three block barriers remain per tile.
-// =============================================================================================
-template <int MT, int WPW, bool UPD, int H, int TB>
-__global__ void __launch_bounds__(TB, 1)
-    k_round_fused(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
-                  uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
-                  int do_update, uint32_t* __restrict__ partials, uint32_t Dp) {
-    constexpr uint32_t TP = 16 * MT;
-    extern __shared__ __align__(128) uint8_t smem[];
-    StateView st = StateView::at(state, K);
-    if (st.hdr->done) return;
-
-    const uint32_t nwarps = blockDim.x >> 5;
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t g8 = lane >> 2, q = lane & 3;
-    const uint32_t parity = round & 1;
-
-    uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
-    const size_t tile_words = size_t(TP) * SS;
-    uint32_t* s_old = tiles + 2 * tile_words + 32;                         // [2][TP] labels via TMA
-    int32_t* part = reinterpret_cast<int32_t*>(s_old + 2 * TP);             // [nwarps][TP][8]
-    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + size_t(nwarps) * TP * 8);  // [TP]
-    uint32_t* s_misc = s_list + TP;  // [0] list_n, [1] changed, [2] skip, [4..4+K) counts
-    unsigned long long* s_n2 = reinterpret_cast<unsigned long long*>(s_misc + ((4 + K + 1) & ~1u));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_n2 + K);
-
-    const uint64_t ntiles = (n + TP - 1) / TP;
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_fence_init();
-        s_misc[0] = 0;
-        s_misc[1] = 0;
-        s_misc[2] = pick_skip(st.cur + parity * K, K);
-    }
-    for (uint32_t c = tid; c < K; c += blockDim.x) {
-        s_misc[4 + c] = 0;
-        s_n2[c] = st.norm2[parity * K + c];
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-        st.hdr->rounds_run = round;
-        for (uint32_t c = 0; c < K; ++c) st.counts[(parity ^ 1) * K + c] = 0;
-        st.changed[parity ^ 1] = 0;
-    }
-    __syncthreads();
-    const uint32_t skip = s_misc[2];
-    const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
-
-    auto issue = [&](uint64_t tile, uint32_t buf) {
-        const uint64_t px0 = tile * TP;
-        const uint32_t npx = uint32_t(umin64(TP, n - px0));
-        const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer is padded to 16 B
-        if (lane == 0) mbar_expect_tx(&bars[buf], npx * S32 * 4 + lab_bytes);
-        __syncwarp();
-        if (lane == 0) bulk_g2s(s_old + buf * TP, labels + px0, lab_bytes, &bars[buf]);
-        for (uint32_t r = lane; r < npx; r += 32)
-            bulk_g2s(tiles + buf * tile_words + size_t(r) * SS, grid + (px0 + r) * S32, S32 * 4, &bars[buf]);
-    };
-    if (warp == 0) {
-        fence_proxy_async();
-        for (uint32_t b = 0; b < 2; ++b) {
-            const uint64_t tile = blockIdx.x + uint64_t(b) * gridDim.x;
-            if (tile < ntiles) issue(tile, b);
-        }
-    }
-
-    uint32_t breg[WPW][2];
-#pragma unroll
-    for (int kk = 0; kk < WPW; ++kk) {
-        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
-        breg[kk][0] = uint32_t(v);
-        breg[kk][1] = uint32_t(v >> 32);
-    }
-    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
-    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
-    const uint32_t wbase = warp * WPW;
-
-    BitCounter<UPD ? H : 1> cnt;
-    if constexpr (UPD) cnt.reset();
-
-    uint32_t it = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const uint32_t buf = it & 1;
-        mbar_wait(&bars[buf], (it >> 1) & 1);
-        const uint32_t* T = tiles + buf * tile_words;
-        const uint64_t px0 = tile * TP;
-        const uint32_t npx = uint32_t(umin64(TP, n - px0));
-
-        int acc[MT][4];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
-#pragma unroll
-        for (int k4 = 0; k4 < WPW / 4; ++k4) {
-            uint4 wl[MT], wh[MT];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
-                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
-            }
-#pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-                const int kk = 4 * k4 + kq;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    uint32_t a[4];
-                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
-                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
-                }
-            }
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            int32_t* row0 = part + (size_t(warp) * TP + 16 * mt + g8) * 8 + 2 * q;
-            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
-            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
-        }
-        __syncthreads();  // (1) partial dots of every warp are in shared memory
-
-        // split-K reduction + exact argmax: 4 pixels per warp pass, lane = (pixel, column)
-        for (uint32_t pg = warp; pg < TP / 4; pg += nwarps) {
-            const uint32_t px = pg * 4 + (lane >> 3), col = lane & 7;
-            int32_t s = 0;
-            for (uint32_t w = 0; w < nwarps; ++w) s += part[(size_t(w) * TP + px) * 8 + col];
-            const uint32_t c_of = col / P, pl = col - c_of * P;
-            const unsigned long long v =
-                (col < K * P) ? (unsigned long long)(uint32_t(s) >> 7) << (kPlaneBits * pl) : 0ull;
-            const uint32_t base = lane & ~7u;
             uint32_t best = 0;
             unsigned long long bdot = 0, bn2 = 0;
             for (uint32_t c = 0; c < K; ++c) {
                 unsigned long long d = 0;
-                for (uint32_t j = 0; j < P; ++j) d += __shfl_sync(0xffffffffu, v, base + P * c + j);
+                for (uint32_t pl = 0; pl < P; ++pl) d += (unsigned long long)rr[P * c + pl] << (kPlaneBits * pl);
                 const unsigned long long n2 = s_n2[c];
                 if (c == 0 || strictly_closer(d, n2, bdot, bn2)) {
                     best = c;
@@ -803,41 +546,11 @@ __global__ void __launch_bounds__(TB, 1)
                     bn2 = n2;
                 }
             }
-            const bool leader = col == 0 && px < npx;
-            const uint32_t old = s_old[buf * TP + px];
-            if (leader) labels[px0 + px] = best;
-            const uint32_t chg = __ballot_sync(0xffffffffu, leader && old != best);
-            if (lane == 0 && chg) atomicAdd(&s_misc[1], __popc(chg));
-            for (uint32_t c = 0; c < K; ++c) {
-                const uint32_t m = __ballot_sync(0xffffffffu, leader && best == c);
-                if (lane == 0 && m) atomicAdd(&s_misc[4 + c], __popc(m));
-            }
-            if constexpr (UPD) {
-                const bool take = do_update && leader && best == upd_c;
-                const uint32_t m = __ballot_sync(0xffffffffu, take);
-                uint32_t pos = 0;
-                if (lane == 0 && m) pos = atomicAdd(&s_misc[0], __popc(m));
-                pos = __shfl_sync(0xffffffffu, pos, 0);
-                if (take) s_list[pos + __popc(m & ((1u << lane) - 1))] = px;
-            }
-            (void)c_of;
+            labels[px0 + tid] = best;
+            if (old != best) atomicAdd(&s_misc[0], 1u);
+            atomicAdd(&s_misc[2 + best], 1u);
         }
-        __syncthreads();  // (2) labels of the tile decided, update list complete
-        if constexpr (UPD) {
-            if (do_update) {
-                const uint32_t m = s_misc[0];
-                if (tid < W32) {
-                    for (uint32_t e = 0; e < m; e += 16) {
-                        uint32_t x[16];
-#pragma unroll
-                        for (int u = 0; u < 16; ++u) x[u] = (e + u < m) ? T[size_t(s_list[e + u]) * SS + tid] : 0u;
-                        cnt.add16(x);
-                    }
-                }
-            }
-        }
-        __syncthreads();  // (3) every read of this buffer is done
-        if (tid == 0) s_misc[0] = 0;
+        __syncthreads();  // every read of this buffer (and of red) is done
         if (warp == 0) {
             const uint64_t nxt = tile + 2ull * gridDim.x;
             if (nxt < ntiles) {
@@ -846,56 +559,79 @@ __global__ void __launch_bounds__(TB, 1)
             }
         }
     }
-
-    if constexpr (UPD) {
-        if (do_update && tid < W32) cnt.store(partials + (size_t(blockIdx.x) * K + upd_c) * Dp + size_t(tid) * 32);
-    }
     __syncthreads();
-    if (tid == 0) atomicAdd(st.changed + parity, s_misc[1]);
-    for (uint32_t c = tid; c < K; c += blockDim.x) atomicAdd(st.counts + parity * K + c, s_misc[4 + c]);
+    if (tid == 0 && s_misc[0]) atomicAdd(tail + K, s_misc[0]);
+    for (uint32_t c = tid; c < K; c += blockDim.x)
+        if (s_misc[2 + c]) atomicAdd(tail + c, s_misc[2 + c]);
+}
+
+size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT) {
+    const uint32_t TP = 16 * MT, NC = 8 * NTG;
+    size_t b = (2 * size_t(TP) * SS + 32) * 4;  // tiles + slack for the last row's overrun
+    b += size_t(nwarps) * TP * NC * 4;           // part
+    b += size_t(TP) * NT * 8 * 4;                // red (all columns)
+    b += ((2 + K + 1) & ~size_t(1)) * 4;         // s_misc
+    b += size_t(K) * 8;                          // s_n2
+    b += 2 * 8;                                  // mbarriers
+    return b;
+}
+
+template <int MT, int NTG>
+static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStream_t s) {
+    auto kern = nwarps <= 12 ? k_round<MT, NTG, 384> : k_round<MT, NTG, 512>;
+    const size_t smem = round_smem_bytes(MT, NTG, a.SS, nwarps, a.K, a.NT);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<a.ctas, nwarps * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32P, a.nwarp_words, a.K, a.P, a.NT, a.bfrag,
+                                           a.labels, a.state, a.round, reinterpret_cast<uint32_t*>(a.xchg) +
+                                                                           size_t(a.K) * a.Dp);
+    return cudaGetLastError();
 }
 
 // =============================================================================================
-// Warp-specialised round kernel (one n-tile of centroid planes, K * P <= 8).
+// Warp-specialised round kernel (one n-tile of centroid planes, K * P <= 8): assign_labels
+// (clusterer.cpp:132-162) fused with the accumulation of update_centroids
+// (clusterer.cpp:164-188), each pixel HV crossing HBM once per round.
 //
-//   warps 0..NMW-1  "MMA" warps: wait tile t -> IMMA k-loop over their WPW words -> split-K
-//                   partials to part[t%2] -> then, while the epilogue warp works on tile t,
-//                   fold tile t-1 into the Harley-Seal counters (thread = word column) and
-//                   release its buffer.
+//   warps 0..NMW-1  "MMA" warps: wait tile t -> IMMA k-loop over their WPW words (B fragments
+//                   in 2*WPW registers) -> split-K partials to part[t%2] -> then, while the
+//                   epilogue warp works on tile t, fold tile t-1's update list into the
+//                   Harley-Seal counters (thread = word column) and release its buffer.
 //   warp NMW        epilogue: reduce tile t's partials (lane = pixel), exact u64 dots, 128-bit
 //                   argmax, labels, member counts, change count, update list.
 //   warp NMW+1      producer: cp.async.bulk (TMA engine) of tile rows + previous labels into
-//                   a 3-deep ring, gated by the buffer-free barriers.
-// All hand-offs are mbarriers; no block-wide barrier inside the tile loop, so the k-loop
-// of tile t+1 overlaps the epilogue and re-bundling of tile t.
+//                   a 4-deep ring, gated by the buffer-free barriers.
+// Hand-offs are mbarriers only; the k-loop of tile t+1 overlaps the epilogue and the
+// re-bundling of tile t. Counters are folded into the exchange buffer with coalesced
+// atomics at the end; counts and changes go to its tail.
 // =============================================================================================
 template <int WPW, bool UPD, int H, int NMW>
 __global__ void __launch_bounds__((NMW + 2) * 32, 1)
     k_round_ws(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
                uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
-               int do_update, uint32_t* __restrict__ partials, uint32_t Dp) {
-    constexpr uint32_t MT = 2, TP = 32, NB = 3;
+               int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
+    constexpr uint32_t MT = 2, TP = 32, NB = 4;  // ring: tile t computing, t+1..t+2 in flight, t-1 re-bundling
     extern __shared__ __align__(128) uint8_t smem[];
     StateView st = StateView::at(state, K);
     if (st.hdr->done) return;
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t parity = round & 1;
+    uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
 
     uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
     const size_t tile_words = size_t(TP) * SS;
-    uint32_t* s_old = tiles + NB * tile_words + 32;                        // [NB][TP]
-    int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);           // [2][NMW][TP][8]
+    uint32_t* s_old = tiles + NB * tile_words + 32;                           // [NB][TP]
+    int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);              // [2][NMW][TP][8]
     uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
-    uint32_t* s_listn = s_list + 2 * TP;                                   // [2]
-    uint32_t* s_misc = s_listn + 2;                                        // [0] skip
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ((reinterpret_cast<uintptr_t>(s_misc + 2) -
-                                                           reinterpret_cast<uintptr_t>(smem) + 7) & ~uintptr_t(7)));
-    uint64_t* full = bars;            // [NB] tile data landed (TMA)
-    uint64_t* buf_free = bars + NB;   // [NB] MMA warps done with the buffer
-    uint64_t* part_full = bars + 2 * NB;      // [2] partials written
-    uint64_t* part_free = bars + 2 * NB + 2;  // [2] epilogue done reading partials
-    uint64_t* list_ready = bars + 2 * NB + 4; // [2] labels + update list of the tile ready
+    uint32_t* s_listn = s_list + 2 * TP;                                      // [2]
+    uint32_t* s_misc = s_listn + 2;                                           // [0] skip
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_misc + 2);                 // 8-byte aligned
+    uint64_t* full = bars;                     // [NB] tile data landed (TMA)
+    uint64_t* buf_free = bars + NB;            // [NB] MMA warps done with the buffer
+    uint64_t* part_full = bars + 2 * NB;       // [2] partials written
+    uint64_t* part_free = bars + 2 * NB + 2;   // [2] epilogue done reading partials
+    uint64_t* list_ready = bars + 2 * NB + 4;  // [2] labels + update list of the tile ready
 
     const uint64_t ntiles = (n + TP - 1) / TP;
     const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -912,11 +648,7 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
         mbar_fence_init();
         s_misc[0] = pick_skip(st.cur + parity * K, K);
     }
-    if (blockIdx.x == 0 && tid == 0) {
-        st.hdr->rounds_run = round;
-        for (uint32_t c = 0; c < K; ++c) st.counts[(parity ^ 1) * K + c] = 0;
-        st.changed[parity ^ 1] = 0;
-    }
+    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
     __syncthreads();
     const uint32_t skip = s_misc[0];
     const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
@@ -939,7 +671,7 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
     }
     if (warp == NMW) {
         // ------------------------------------------------------------------ epilogue warp
-        unsigned long long n2[2] = {st.norm2[parity * K], K > 1 ? st.norm2[parity * K + 1] : 0ull};
+        const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
         uint32_t changed = 0, cnt0 = 0, cnt1 = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t pb = it & 1, b = it % NB;
@@ -957,14 +689,15 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
             }
             mbar_arrive(&part_free[pb]);
             // exact dots: column n = P*c + plane, 7-bit planes, 128 scale removed (exact)
-            unsigned long long d[2] = {0, 0};
+            unsigned long long d0 = 0, d1 = 0;  // named registers: no local-memory indexing
 #pragma unroll
             for (uint32_t cn = 0; cn < 8; ++cn) {
                 const uint32_t c = cn / P, pl = cn - c * P;
-                if (c < K && c < 2) d[c] += (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
+                const unsigned long long v = (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
+                if (c == 0) d0 += v;
+                else if (c == 1 && K > 1) d1 += v;
             }
-            uint32_t best = 0;
-            if (K > 1 && strictly_closer(d[1], n2[1], d[0], n2[0])) best = 1;
+            const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
             const bool live = lane < npx;
             const uint32_t old = s_old[b * TP + lane];
             if (live) {
@@ -987,9 +720,9 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
             cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
         }
         if (lane == 0) {
-            atomicAdd(st.changed + parity, changed);
-            atomicAdd(st.counts + parity * K, cnt0);
-            if (K > 1) atomicAdd(st.counts + parity * K + 1, cnt1);
+            if (changed) atomicAdd(tail + K, changed);
+            if (cnt0) atomicAdd(tail, cnt0);
+            if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
         }
         return;
     }
@@ -1069,19 +802,22 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
     }
     if (my_tiles >= 1) rebundle(my_tiles - 1);
     if constexpr (UPD) {
-        if (do_update && tid < W32) cnt.store(partials + (size_t(blockIdx.x) * K + upd_c) * Dp + size_t(tid) * 32);
+        if (do_update) {
+            // all tiles consumed: the ring is free to serve as the transpose scratch
+            asm volatile("bar.sync 1, %0;" ::"r"(NMW * 32));
+            flush_warp_atomic(cnt, tiles + warp * (32 * 33), xchg + size_t(upd_c) * Dp, warp * 32, W32);
+        }
     }
 }
 
 size_t ws_smem_bytes(uint32_t SS, uint32_t nmw) {
-    const uint32_t TP = 32, NB = 3;
+    const uint32_t TP = 32, NB = 4;
     size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
     b += NB * TP * 4;                            // s_old
     b += 2 * size_t(nmw) * TP * 8 * 4;           // part
     b += 2 * TP * 4 + 2 * 4 + 2 * 4;             // s_list, s_listn, s_misc
-    b = (b + 7) & ~size_t(7);
     b += (2 * NB + 6) * 8;                       // mbarriers
-    return b;
+    return std::max<size_t>(b, size_t(nmw) * 32 * 33 * 4);
 }
 
 template <int WPW, bool UPD, int H, int NMW>
@@ -1091,52 +827,25 @@ static cudaError_t launch_ws_t(const RoundArgs& a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, (NMW + 2) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
-                                              a.round, a.do_update, a.partials, a.Dp);
+                                              a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
     return cudaGetLastError();
 }
+
+template <int H>
+struct WsH {
+    template <int WPW, int NMW>
+    static cudaError_t go(const RoundArgs& a, cudaStream_t s) {
+        return launch_ws_t<WPW, true, H, NMW>(a, s);
+    }
+};
 
 template <int WPW, int NMW>
 static cudaError_t launch_ws_h(const RoundArgs& a, cudaStream_t s) {
     if (a.K != 2) return launch_ws_t<WPW, false, 1, NMW>(a, s);
-    const uint64_t per_cta = (a.n + a.ctas - 1) / a.ctas;
-    if (per_cta <= BitCounter<8>::capacity()) return launch_ws_t<WPW, true, 8, NMW>(a, s);
-    if (per_cta <= BitCounter<12>::capacity()) return launch_ws_t<WPW, true, 12, NMW>(a, s);
-    return launch_ws_t<WPW, true, 20, NMW>(a, s);
-}
-
-size_t fused_smem_bytes(uint32_t MT, uint32_t SS, uint32_t nwarps, uint32_t K) {
-    const uint32_t TP = 16 * MT;
-    size_t b = (2 * size_t(TP) * SS + 32) * 4;  // tiles + overrun slack
-    b += 2 * size_t(TP) * 4;                     // s_old
-    b += size_t(nwarps) * TP * 8 * 4;            // part
-    b += size_t(TP) * 4;                         // s_list
-    b += ((4 + K + 1) & ~size_t(1)) * 4;         // s_misc
-    b += size_t(K) * 8 + 2 * 8;                  // s_n2, mbarriers
-    return b;
-}
-
-size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT) {
-    const uint32_t TP = 16 * MT, NC = 8 * NTG;
-    size_t b = (2 * size_t(TP) * SS + 32) * 4;        // tiles + slack for the last row's overrun
-    b += size_t(nwarps) * TP * NC * 4;                 // part
-    b += size_t(TP) * NT * 8 * 4;                      // red (all columns)
-    b += 2 * size_t(TP) * 4;                           // s_label, s_list
-    b += ((4 + K + 1) & ~size_t(1)) * 4;               // s_misc
-    b += size_t(K) * 8;                                // s_n2
-    b += 2 * 8;                                        // mbarriers
-    return b;
-}
-
-template <int MT, int NTG, bool BREG, bool UPD, int H>
-static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStream_t s) {
-    // register budget: 1 CTA/SM; <= 12 warps leaves 170 registers per thread, 16 warps 128
-    auto kern = nwarps <= 12 ? k_round<MT, NTG, BREG, UPD, H, 384> : k_round<MT, NTG, BREG, UPD, H, 512>;
-    const size_t smem = round_smem_bytes(MT, NTG, a.SS, nwarps, a.K, a.NT);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    kern<<<a.ctas, nwarps * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.W32P, a.nwarp_words, a.K, a.P, a.NT,
-                                           a.bfrag, a.labels, a.state, a.round, a.do_update, a.partials, a.Dp);
-    return cudaGetLastError();
+    const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + 31) & ~uint64_t(31);
+    if (per_cta <= counter_capacity<8>()) return WsH<8>::go<WPW, NMW>(a, s);
+    if (per_cta <= counter_capacity<12>()) return WsH<12>::go<WPW, NMW>(a, s);
+    return WsH<20>::go<WPW, NMW>(a, s);
 }
 
 // Plan: which instantiation handles (K, P, D). Returns false if no kernel fits.
@@ -1147,8 +856,7 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     if (p.nt == 1) {
         // warp-specialised kernel: MMA warps in multiples of 4 (equal load per SM sub-partition),
         // B fragments in 2*wpw registers, one thread per word column for the re-bundling
-        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32},
-                                           {12, 20}, {12, 28}, {16, 20}, {16, 28}};
+        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {12, 28}, {16, 20}};
         const char* force = getenv("SEGHDC_FUSED_WARPS");
         if (force && !*force) force = nullptr;
         for (const auto& c : cand) {
@@ -1180,23 +888,21 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
     if (p.fused) {
-#define SEGHDC_WS(NMW)                                                   \
-    if (p.nwarps == NMW) {                                               \
-        if (p.wpw == 20) return launch_ws_h<20, NMW>(a, s);              \
-        if (p.wpw == 28) return launch_ws_h<28, NMW>(a, s);              \
-        return launch_ws_h<32, NMW>(a, s);                               \
-    }
-        SEGHDC_WS(4)
-        SEGHDC_WS(8)
-        SEGHDC_WS(12)
-        if (p.wpw == 20) return launch_ws_h<20, 16>(a, s);
-        return launch_ws_h<28, 16>(a, s);
-#undef SEGHDC_WS
+        switch (p.nwarps * 100 + p.wpw) {
+            case 420: return launch_ws_h<20, 4>(a, s);
+            case 428: return launch_ws_h<28, 4>(a, s);
+            case 432: return launch_ws_h<32, 4>(a, s);
+            case 820: return launch_ws_h<20, 8>(a, s);
+            case 828: return launch_ws_h<28, 8>(a, s);
+            case 832: return launch_ws_h<32, 8>(a, s);
+            case 1228: return launch_ws_h<28, 12>(a, s);
+            default: return launch_ws_h<20, 16>(a, s);
+        }
     }
     switch (p.mt) {
-        case 4: return launch_round_t<4, 4, false, false, 1>(a, p.nwarps, s);
-        case 2: return launch_round_t<2, 4, false, false, 1>(a, p.nwarps, s);
-        default: return launch_round_t<1, 4, false, false, 1>(a, p.nwarps, s);
+        case 4: return launch_round_t<4, 4>(a, p.nwarps, s);
+        case 2: return launch_round_t<2, 4>(a, p.nwarps, s);
+        default: return launch_round_t<1, 4>(a, p.nwarps, s);
     }
 }
 
