@@ -32,69 +32,119 @@ constexpr uint64_t counter_capacity() {
 // encode_image (reference pixel_pipeline.cpp:92-126): grid[p] = row[i] ^ col[j] ^ ^_ch wid[ch][v]
 // fused with the column sums of the grid (the Harley-Seal counter of every pixel), which the
 // round schedule needs to derive the largest cluster's sums without accumulating them.
-// CTA = (contiguous pixel range, block of <= 512 word columns); thread t = word column, 16
-// pixels per step (16 independent table reads in flight, coalesced 128-B stores per warp).
-// Tables are the reference's u64 words read as u32 (same bytes).
+//
+// CTA = (tile of ER x EC pixels, chunk of 32 HV words). The chunk's slice of every table it
+// touches (ER row entries, EC column entries, C x 256 colour entries: <= 120 KB) and the image
+// tile are staged once in shared memory, so L2 serves ~30 B per pixel-chunk instead of the
+// ~4 table words per output word of a direct gather. Warp = one pixel at a time, lane = word:
+// coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane; the CTA folds
+// them in shared memory and adds 1024 column sums to the global array with one atomic each.
 // =============================================================================================
-template <int C, int H>
-__global__ void __launch_bounds__(512) k_encode(const uint8_t* __restrict__ img, uint32_t w, uint64_t pix_begin,
-                                                 uint64_t pix_end, uint64_t ppc, const uint32_t* __restrict__ row,
-                                                 const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
-                                                 uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid,
-                                                 uint32_t* __restrict__ colsum, uint32_t W32) {
-    extern __shared__ uint32_t scratch_all[];  // [warps][32*33] for the final flush
-    const uint32_t t = blockIdx.y * blockDim.x + threadIdx.x;
-    const uint64_t p0 = pix_begin + uint64_t(blockIdx.x) * ppc;
-    const uint64_t p1 = p0 + ppc < pix_end ? p0 + ppc : pix_end;
-    const bool live = t < wref, store = t < S32;
-    BitCounter<H> cnt;
-    cnt.reset();
-    uint32_t i = p0 < p1 ? uint32_t(p0 / w) : 0, j = p0 < p1 ? uint32_t(p0 - uint64_t(i) * w) : 0;
-    for (uint64_t q = p0; q < p1; q += 16) {
-        uint32_t x[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const uint64_t p = q + u;
-            uint32_t v = 0;
-            if (p < p1 && live) {
-                v = __ldg(row + size_t(i) * wref + t) ^ __ldg(col + size_t(j) * wref + t);
-#pragma unroll
-                for (int ch = 0; ch < C; ++ch) v ^= __ldg(wid + (size_t(ch) * 256 + img[p * C + ch]) * wref + t);
-            }
-            if (p < p1 && store) grid[(p - pix_begin) * S32 + t] = v;
-            x[u] = v;
-            if (++j == w) {
-                j = 0;
-                ++i;
-            }
-        }
-        cnt.add16(x);
-    }
-    flush_warp_atomic(cnt, scratch_all + (threadIdx.x >> 5) * (32 * 33), colsum, t & ~31u, W32);
-}
+constexpr uint32_t kEncRows = 32, kEncCols = 64, kEncWarps = 16;
 
-template <int H>
-static void launch_encode_h(const EncodeArgs& a, uint32_t blocks, uint64_t ppc, cudaStream_t s) {
-    const uint32_t threads = std::min<uint32_t>(512, ((a.S32 + 31) / 32) * 32);
-    dim3 g(blocks, (a.S32 + threads - 1) / threads);
-    const size_t smem = size_t(threads / 32) * 32 * 33 * 4;
-    if (a.c == 1) {
-        cudaFuncSetAttribute(k_encode<1, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_encode<1, H><<<g, threads, smem, s>>>(a.img, a.w, a.pix_begin, a.pix_end, ppc, a.row, a.col, a.wid, a.wref,
-                                                a.S32, a.grid, a.colsum, a.W32);
-    } else {
-        cudaFuncSetAttribute(k_encode<3, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_encode<3, H><<<g, threads, smem, s>>>(a.img, a.w, a.pix_begin, a.pix_end, ppc, a.row, a.col, a.wid, a.wref,
-                                                a.S32, a.grid, a.colsum, a.W32);
+template <int C>
+__global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __restrict__ img, uint32_t h_img, uint32_t w,
+                                                            uint32_t row_begin, uint32_t row_end,
+                                                            const uint32_t* __restrict__ row,
+                                                            const uint32_t* __restrict__ col,
+                                                            const uint32_t* __restrict__ wid, uint32_t wref,
+                                                            uint32_t S32, uint32_t* __restrict__ grid,
+                                                            uint32_t* __restrict__ colsum, uint32_t W32) {
+    extern __shared__ __align__(16) uint32_t es[];
+    uint32_t* s_wid = es;                            // [C][256][32]
+    uint32_t* s_col = s_wid + C * 256 * 32;          // [EC][32]
+    uint32_t* s_sum = s_col + kEncCols * 32;         // [32 bits][32 words]
+    (void)h_img;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t w0 = blockIdx.z * 32;             // first word of the chunk
+    const uint32_t rows_per = (row_end - row_begin + gridDim.y - 1) / gridDim.y;
+    const uint32_t r0 = row_begin + blockIdx.y * rows_per, r1 = min(row_end, r0 + rows_per);
+    const uint32_t c0 = blockIdx.x * kEncCols, nc = min(kEncCols, w - c0);
+    const bool wl = w0 + lane < wref;  // this lane's word exists in the tables (else zero)
+
+    // stage the chunk of the colour tables and of the tile's column codes (8 loads in flight)
+    for (uint32_t e0 = tid; e0 < C * 256 * 32; e0 += blockDim.x * 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t e = e0 + k * blockDim.x, wd = e & 31;
+            v[k] = (e < C * 256 * 32 && w0 + wd < wref) ? __ldg(wid + size_t(e >> 5) * wref + w0 + wd) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (e0 + k * blockDim.x < C * 256 * 32) s_wid[e0 + k * blockDim.x] = v[k];
+    }
+    for (uint32_t e = tid; e < nc * 32; e += blockDim.x) {
+        const uint32_t wd = e & 31;
+        s_col[e] = (w0 + wd < wref) ? __ldg(col + size_t(c0 + (e >> 5)) * wref + w0 + wd) : 0u;
+    }
+    for (uint32_t e = tid; e < 1024; e += blockDim.x) s_sum[e] = 0;
+    __syncthreads();
+
+    BitCounter<12> cnt;  // <= rows_per / warps * 64 pixels per warp
+    cnt.reset();
+    const bool st = w0 + lane < S32;
+    for (uint32_t r = r0 + warp; r < r1; r += kEncWarps) {  // warp = one image row of the tile
+        const uint32_t rv = wl ? __ldg(row + size_t(r) * wref + w0 + lane) : 0u;
+        uint32_t* out = grid + (size_t(r - row_begin) * w + c0) * S32 + w0 + lane;
+        // this row's pixel values: lane l holds the bytes of pixels l and l+32
+        uint32_t pv0[C], pv1[C];
+#pragma unroll
+        for (int ch = 0; ch < C; ++ch) {
+            pv0[ch] = lane < nc ? img[(size_t(r) * w + c0 + lane) * C + ch] : 0u;
+            pv1[ch] = lane + 32 < nc ? img[(size_t(r) * w + c0 + lane + 32) * C + ch] : 0u;
+        }
+        for (uint32_t c16 = 0; c16 < nc; c16 += 16) {
+            uint32_t x[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const uint32_t cc = c16 + u;
+                uint32_t v = rv ^ s_col[cc * 32 + lane];
+#pragma unroll
+                for (int ch = 0; ch < C; ++ch) {
+                    const uint32_t val = __shfl_sync(0xffffffffu, c16 < 32 ? pv0[ch] : pv1[ch], cc & 31);
+                    v ^= s_wid[(ch * 256 + val) * 32 + lane];
+                }
+                if (!wl || cc >= nc) v = 0;
+                if (st && cc < nc) out[size_t(cc) * S32] = v;
+                x[u] = v;
+            }
+            cnt.add16(x);
+        }
+    }
+    // fold the warps' counters in shared memory (bit-major: lanes hit distinct banks), then
+    // one global atomic per column sum
+#pragma unroll 4
+    for (int b = 0; b < 32; ++b) {
+        const uint32_t val = cnt.value(b);
+        if (val) atomicAdd(&s_sum[b * 32 + lane], val);
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < 1024; e += blockDim.x) {
+        const uint32_t wd = e & 31, b = e >> 5, word = w0 + wd;
+        if (word < W32 && s_sum[e]) atomicAdd(colsum + size_t(word) * 32 + b, s_sum[e]);
     }
 }
 
 void launch_encode(const EncodeArgs& a, cudaStream_t s) {
     const uint64_t n = a.pix_end - a.pix_begin;
     if (n == 0) return;
-    const uint32_t blocks = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(a.sms) * 4, (n + 63) / 64)));
-    const uint64_t ppc = (n + blocks - 1) / blocks;
-    SEGHDC_DISPATCH_H(ppc, launch_encode_h, a, blocks, ppc, s);
+    const uint32_t row_begin = uint32_t(a.pix_begin / a.w), row_end = uint32_t(a.pix_end / a.w);
+    const uint32_t gx = (a.w + kEncCols - 1) / kEncCols, gz = (a.S32 + 31) / 32;
+    // row groups: ~4 CTAs per SM in total; each CTA stages its table chunk once for all its rows
+    const uint32_t gy = std::max<uint32_t>(
+        1, std::min<uint32_t>(row_end - row_begin, (4 * a.sms + gx * gz - 1) / (gx * gz)));
+    dim3 g(gx, gy, gz);
+    const size_t smem = (size_t(a.c) * 256 * 32 + kEncCols * 32 + 1024) * 4;
+    if (a.c == 1) {
+        cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_encode<1><<<g, kEncWarps * 32, smem, s>>>(a.img, 0, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
+                                                    a.S32, a.grid, a.colsum, a.W32);
+    } else {
+        cudaFuncSetAttribute(k_encode<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_encode<3><<<g, kEncWarps * 32, smem, s>>>(a.img, 0, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
+                                                    a.S32, a.grid, a.colsum, a.W32);
+    }
 }
 
 // =============================================================================================
