@@ -235,7 +235,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     ctx = S.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    # one dedicated stream for our kernels, torch's events and NCCL (torch's default stream is
+    # the legacy NULL stream, which a non-blocking context stream would not order against)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     sharded = world > 1 and args.config in (3, 4)
