@@ -82,6 +82,7 @@ struct RoundPlan {
     uint32_t wpw = 32;         // HV words per warp (split-K)
     uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
     bool fused = false;        // one n-tile: warp-specialised kernel (+ fused accumulation when K == 2)
+    bool dedicated_roles = false;  // fused: separate epilogue/producer warps (k_round_ws) instead of rotating roles
 };
 struct RoundArgs {
     const uint32_t* grid;

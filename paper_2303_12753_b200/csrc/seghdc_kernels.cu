@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "kernels.cuh"
 #include "launch.h"
@@ -84,32 +85,37 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
     BitCounter<12> cnt;  // <= rows_per / warps * 64 pixels per warp
     cnt.reset();
     const bool st = w0 + lane < S32;
+    // staged tables hold 0 for words >= wref, so lanes past the HV need no masking below
+    const uint32_t* s_col_l = s_col + lane;
+    const uint32_t* s_wid_l = s_wid + lane;
     for (uint32_t r = r0 + warp; r < r1; r += kEncWarps) {  // warp = one image row of the tile
         const uint32_t rv = wl ? __ldg(row + size_t(r) * wref + w0 + lane) : 0u;
         uint32_t* out = grid + (size_t(r - row_begin) * w + c0) * S32 + w0 + lane;
-        // this row's pixel values: lane l holds the bytes of pixels l and l+32
-        uint32_t pv0[C], pv1[C];
+        for (uint32_t half = 0; half * 32 < nc; ++half) {
+            // pixel values of columns half*32 + lane (broadcast per pixel with a shuffle)
+            uint32_t pv[C];
 #pragma unroll
-        for (int ch = 0; ch < C; ++ch) {
-            pv0[ch] = lane < nc ? img[(size_t(r) * w + c0 + lane) * C + ch] : 0u;
-            pv1[ch] = lane + 32 < nc ? img[(size_t(r) * w + c0 + lane + 32) * C + ch] : 0u;
-        }
-        for (uint32_t c16 = 0; c16 < nc; c16 += 16) {
-            uint32_t x[16];
+            for (int ch = 0; ch < C; ++ch)
+                pv[ch] = half * 32 + lane < nc ? img[(size_t(r) * w + c0 + half * 32 + lane) * C + ch] : 0u;
+            for (uint32_t c16 = half * 32; c16 < nc && c16 < half * 32 + 32; c16 += 16) {
+                const uint32_t lim = nc - c16;  // >= 16 except in the last group of a ragged tile
+                uint32_t x[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const uint32_t cc = c16 + u;
-                uint32_t v = rv ^ s_col[cc * 32 + lane];
+                for (int u = 0; u < 16; ++u) {
+                    uint32_t v = rv ^ s_col_l[(c16 + u) * 32];
 #pragma unroll
-                for (int ch = 0; ch < C; ++ch) {
-                    const uint32_t val = __shfl_sync(0xffffffffu, c16 < 32 ? pv0[ch] : pv1[ch], cc & 31);
-                    v ^= s_wid[(ch * 256 + val) * 32 + lane];
+                    for (int ch = 0; ch < C; ++ch)
+                        v ^= s_wid_l[(ch * 256 + __shfl_sync(0xffffffffu, pv[ch], (c16 & 31) + u)) * 32];
+                    x[u] = uint32_t(u) < lim ? v : 0u;
                 }
-                if (!wl || cc >= nc) v = 0;
-                if (st && cc < nc) out[size_t(cc) * S32] = v;
-                x[u] = v;
+                uint32_t* o = out + size_t(c16) * S32;
+                if (st) {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        if (uint32_t(u) < lim) o[u * S32] = x[u];
+                }
+                cnt.add16(x);
             }
-            cnt.add16(x);
         }
     }
     // fold the warps' counters in shared memory (bit-major: lanes hit distinct banks), then
@@ -714,8 +720,11 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
             if (lane == 0) mbar_expect_tx(&full[b], npx * S32 * 4 + lab_bytes);
             __syncwarp();
             if (lane == 0) bulk_g2s(s_old + b * TP, labels + px0, lab_bytes, &full[b]);
-            if (lane < npx)
+            if (SS == S32) {  // unpadded rows: the tile is one contiguous 40 KB block
+                if (lane == 1) bulk_g2s(tiles + b * tile_words, grid + px0 * S32, npx * S32 * 4, &full[b]);
+            } else if (lane < npx) {
                 bulk_g2s(tiles + b * tile_words + size_t(lane) * SS, grid + (px0 + lane) * S32, S32 * 4, &full[b]);
+            }
         }
         return;
     }
@@ -860,6 +869,264 @@ __global__ void __launch_bounds__((NMW + 2) * 32, 1)
     }
 }
 
+// =============================================================================================
+// One-role-warp variant (the default): NMW MMA warps + ONE warp that is both the epilogue and
+// the TMA producer. With NMW = 8 the CTA has 9 warps, at most 3 per SM sub-partition, so the
+// MMA warps get ~170 registers (B fragments of WPW = 40 words stay resident) while the
+// k-loop load is still spread evenly over the 4 sub-partitions (2 MMA warps each). Threads
+// own CPT word columns for the re-bundling (CPT = 2 when NMW*32 < W32).
+//   MMA warp:  wait full[t] -> k-loop -> partials -> arrive part_full[t%2]
+//              -> re-bundle tile t-1 (wait list_ready) -> arrive buf_free
+//   role warp: wait part_full[t%2] -> epilogue(t) -> arrive list_ready[t%2]
+//              -> wait buf_free(t-1) -> TMA of tile t-1+NB into the freed buffer
+// part[t%2] needs no free-barrier: an MMA warp rewrites it only after re-bundling tile t,
+// which waits for list_ready[t], signalled after the epilogue has read part[t%2].
+// =============================================================================================
+template <int WPW, bool UPD, int H, int NMW, int CPT>
+__global__ void __launch_bounds__((NMW + 1) * 32, 1)
+    k_round_w1(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
+               uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
+               int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
+    constexpr uint32_t MT = 2, TP = 32, NB = 4;
+    extern __shared__ __align__(128) uint8_t smem[];
+    StateView st = StateView::at(state, K);
+    if (st.hdr->done) return;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t parity = round & 1;
+    uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
+
+    uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
+    const size_t tile_words = size_t(TP) * SS;
+    uint32_t* s_old = tiles + NB * tile_words + 32;                           // [NB][TP]
+    int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);              // [2][NMW][TP][8]
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
+    uint32_t* s_listn = s_list + 2 * TP;                                      // [2]
+    uint32_t* s_misc = s_listn + 2;                                           // [0] skip
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_misc + 2);                 // 8-byte aligned
+    uint64_t* full = bars;                     // [NB] tile data landed (TMA)
+    uint64_t* buf_free = bars + NB;            // [NB] MMA warps done with the buffer
+    uint64_t* part_full = bars + 2 * NB;       // [2] partials written
+    uint64_t* list_ready = bars + 2 * NB + 2;  // [2] labels + update list of the tile ready
+
+    const uint64_t ntiles = (n + TP - 1) / TP;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    if (tid == 0) {
+        for (uint32_t b = 0; b < NB; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&buf_free[b], NMW * 32);
+        }
+        for (uint32_t b = 0; b < 2; ++b) {
+            mbar_init(&part_full[b], NMW * 32);
+            mbar_init(&list_ready[b], 32);
+        }
+        mbar_fence_init();
+        s_misc[0] = pick_skip(st.cur + parity * K, K);
+    }
+    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
+    __syncthreads();
+    const uint32_t upd_c = 1 - s_misc[0];  // K == 2 under UPD
+
+    if (warp == NMW) {
+        // ------------------------------------------------------------- epilogue + producer warp
+        auto issue = [&](uint32_t it) {
+            const uint32_t b = it % NB;
+            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
+            const uint32_t npx = uint32_t(umin64(TP, n - px0));
+            const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer padded to 16 B
+            if (lane == 0) mbar_expect_tx(&full[b], npx * S32 * 4 + lab_bytes);
+            __syncwarp();
+            if (lane == 0) bulk_g2s(s_old + b * TP, labels + px0, lab_bytes, &full[b]);
+            if (SS == S32) {  // unpadded rows: the tile is one contiguous 40 KB block
+                if (lane == 1) bulk_g2s(tiles + b * tile_words, grid + px0 * S32, npx * S32 * 4, &full[b]);
+            } else if (lane < npx) {
+                bulk_g2s(tiles + b * tile_words + size_t(lane) * SS, grid + (px0 + lane) * S32, S32 * 4, &full[b]);
+            }
+        };
+        for (uint32_t it = 0; it < NB && it < my_tiles; ++it) issue(it);
+        const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
+        uint32_t changed = 0, cnt1 = 0, total = 0;
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t pb = it & 1, b = it % NB;
+            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
+            const uint32_t npx = uint32_t(umin64(TP, n - px0));
+            mbar_wait(&part_full[pb], (it >> 1) & 1);
+            const int32_t* pp = part + size_t(pb) * NMW * TP * 8 + lane * 8;
+            int32_t col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+            for (uint32_t w = 0; w < NMW; ++w) {
+                const int4 lo = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8);
+                const int4 hi = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8 + 4);
+                col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
+                col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
+            }
+            // exact dots: column n = P*c + plane, 7-bit planes, 128 scale removed (exact)
+            unsigned long long d0 = 0, d1 = 0;  // named registers: no local-memory indexing
+#pragma unroll
+            for (uint32_t cn = 0; cn < 8; ++cn) {
+                const uint32_t c = cn / P, pl = cn - c * P;
+                const unsigned long long v = (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
+                if (c == 0) d0 += v;
+                else if (c == 1 && K > 1) d1 += v;
+            }
+            const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
+            const bool live = lane < npx;
+            const uint32_t old = s_old[b * TP + lane];
+            if (live) {
+                labels[px0 + lane] = best;
+                changed += old != best;
+                cnt1 += best;
+            }
+            total += npx;
+            if constexpr (UPD) {
+                const bool take = do_update && live && best == upd_c;
+                const uint32_t m = __ballot_sync(0xffffffffu, take);
+                if (take) s_list[pb * TP + __popc(m & ((1u << lane) - 1))] = lane;
+                if (lane == 0) s_listn[pb] = __popc(m);
+            }
+            mbar_arrive(&list_ready[pb]);
+            // refill the buffer of tile it-1 (its re-bundling follows this tile's k-loop)
+            if (it >= 1 && it - 1 + NB < my_tiles) {
+                mbar_wait(&buf_free[(it - 1) % NB], ((it - 1) / NB) & 1);
+                fence_proxy_async();
+                issue(it - 1 + NB);
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            changed += __shfl_xor_sync(0xffffffffu, changed, o);
+            cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
+        }
+        if (lane == 0) {
+            if (changed) atomicAdd(tail + K, changed);
+            if (total - cnt1) atomicAdd(tail, total - cnt1);
+            if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------------- MMA warps
+    const uint32_t g8 = lane >> 2, q = lane & 3;
+    uint32_t breg[WPW][2];
+#pragma unroll
+    for (int kk = 0; kk < WPW; ++kk) {
+        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+        breg[kk][0] = uint32_t(v);
+        breg[kk][1] = uint32_t(v >> 32);
+    }
+    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
+    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
+    const uint32_t wbase = warp * WPW;
+    BitCounter<UPD ? H : 1> cnt[CPT];
+    if constexpr (UPD)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) cnt[c].reset();
+
+    auto rebundle = [&](uint32_t jt) {  // fold tile jt's update list into the counters
+        const uint32_t pb = jt & 1, b = jt % NB;
+        mbar_wait(&list_ready[pb], (jt >> 1) & 1);
+        if constexpr (UPD) {
+            if (do_update) {
+                const uint32_t m = s_listn[pb];
+                const uint32_t* T = tiles + b * tile_words;
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    const uint32_t colw = tid + c * NMW * 32;
+                    if (colw < W32) {
+                        for (uint32_t e = 0; e < m; e += 16) {
+                            uint32_t x[16];
+#pragma unroll
+                            for (int u = 0; u < 16; ++u)
+                                x[u] = (e + u < m) ? T[size_t(s_list[pb * TP + e + u]) * SS + colw] : 0u;
+                            cnt[c].add16(x);
+                        }
+                    }
+                }
+            }
+        }
+        mbar_arrive(&buf_free[b]);
+    };
+
+    for (uint32_t it = 0; it < my_tiles; ++it) {
+        const uint32_t b = it % NB, pb = it & 1;
+        mbar_wait(&full[b], (it / NB) & 1);
+        const uint32_t* T = tiles + b * tile_words;
+        int acc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
+#pragma unroll
+        for (int k4 = 0; k4 < WPW / 4; ++k4) {
+            uint4 wl[MT], wh[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
+                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+            }
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) {
+                const int kk = 4 * k4 + kq;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint32_t a[4];
+                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
+                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
+                }
+            }
+        }
+        int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
+            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
+            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
+        }
+        mbar_arrive(&part_full[pb]);
+        if (it >= 1) rebundle(it - 1);
+    }
+    if (my_tiles >= 1) rebundle(my_tiles - 1);
+    if constexpr (UPD) {
+        if (do_update) {
+            // every tile consumed: the ring is free to serve as the transpose scratch
+            asm volatile("bar.sync 1, %0;" ::"r"(NMW * 32));
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+                flush_warp_atomic(cnt[c], tiles + warp * (32 * 33), xchg + size_t(upd_c) * Dp,
+                                  warp * 32 + c * NMW * 32, W32);
+        }
+    }
+}
+
+size_t w1_smem_bytes(uint32_t SS, uint32_t nmw) {
+    const uint32_t TP = 32, NB = 4;
+    size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
+    b += NB * TP * 4;                            // s_old
+    b += 2 * size_t(nmw) * TP * 8 * 4;           // part
+    b += (2 * TP + 2 + 2) * 4;                   // s_list, s_listn, s_misc
+    b += (2 * NB + 4) * 8;                       // mbarriers
+    return std::max<size_t>(b, size_t(nmw) * 32 * 33 * 4);
+}
+
+template <int WPW, bool UPD, int H, int NMW, int CPT>
+static cudaError_t launch_w1_t(const RoundArgs& a, cudaStream_t s) {
+    auto kern = k_round_w1<WPW, UPD, H, NMW, CPT>;
+    const size_t smem = w1_smem_bytes(a.SS, NMW);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<a.ctas, (NMW + 1) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
+                                              a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
+    return cudaGetLastError();
+}
+
+template <int WPW, int NMW, int CPT>
+static cudaError_t launch_w1_h(const RoundArgs& a, cudaStream_t s) {
+    if (a.K != 2) return launch_w1_t<WPW, false, 1, NMW, CPT>(a, s);
+    const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + 31) & ~uint64_t(31);
+    if (per_cta <= counter_capacity<8>()) return launch_w1_t<WPW, true, 8, NMW, CPT>(a, s);
+    if (per_cta <= counter_capacity<12>()) return launch_w1_t<WPW, true, 12, NMW, CPT>(a, s);
+    return launch_w1_t<WPW, true, 20, NMW, CPT>(a, s);
+}
+
 size_t ws_smem_bytes(uint32_t SS, uint32_t nmw) {
     const uint32_t TP = 32, NB = 4;
     size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
@@ -904,16 +1171,23 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     p.nt = (K * P + 7) / 8;
     p.fused = false;
     if (p.nt == 1) {
-        // warp-specialised kernel: MMA warps in multiples of 4 (equal load per SM sub-partition),
-        // B fragments in 2*wpw registers, one thread per word column for the re-bundling
-        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {12, 28}, {16, 20}};
+        // (MMA warps, words per warp): MMA warps in multiples of 4 (equal k-loop load per SM
+        // sub-partition), B fragments in 2*wpw registers, <= 2 word columns per thread in the
+        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count, SEGHDC_ROUND=ws the kernel with
+        // separate epilogue and producer warps (A/B testing).
+        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {8, 40},
+                                           {12, 28}, {16, 20}};
         const char* force = getenv("SEGHDC_FUSED_WARPS");
         if (force && !*force) force = nullptr;
+        const char* variant = getenv("SEGHDC_ROUND");
+        const bool ws = variant && std::string(variant) == "ws";
         for (const auto& c : cand) {
             if (force && uint32_t(atoi(force)) != c[0]) continue;
-            if (c[0] * c[1] < W32 || c[0] * 32 < W32) continue;
-            if (ws_smem_bytes(SS, c[0]) > smem_limit) continue;
+            if (c[0] * c[1] < W32 || c[0] * 64 < W32) continue;
+            if (ws && (c[0] * 32 < W32 || c[1] == 40)) continue;
+            if (std::max(ws_smem_bytes(SS, c[0]), w1_smem_bytes(SS, c[0])) > smem_limit) continue;
             p.fused = true;
+            p.dedicated_roles = ws;
             p.nwarps = c[0];
             p.wpw = c[1];
             p.w32p = c[0] * c[1];
@@ -937,6 +1211,19 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 }
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
+    if (p.fused && !p.dedicated_roles) {
+        switch (p.nwarps * 100 + p.wpw) {
+            case 420: return launch_w1_h<20, 4, 1>(a, s);
+            case 428: return launch_w1_h<28, 4, 1>(a, s);
+            case 432: return launch_w1_h<32, 4, 1>(a, s);
+            case 820: return launch_w1_h<20, 8, 1>(a, s);
+            case 828: return launch_w1_h<28, 8, 1>(a, s);
+            case 832: return launch_w1_h<32, 8, 1>(a, s);
+            case 840: return launch_w1_h<40, 8, 2>(a, s);
+            case 1228: return launch_w1_h<28, 12, 1>(a, s);
+            default: return launch_w1_h<20, 16, 1>(a, s);
+        }
+    }
     if (p.fused) {
         switch (p.nwarps * 100 + p.wpw) {
             case 420: return launch_ws_h<20, 4>(a, s);
