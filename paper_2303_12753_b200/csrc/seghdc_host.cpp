@@ -143,10 +143,14 @@ void build_color(size_t dim, size_t c, size_t gamma, int encoder, std::mt19937_6
                     cursor += u;
                 }
             }
-            // channel entry placed at its concatenation offset (pixel_pipeline.cpp:70-88)
+            // channel entry placed at its concatenation offset (pixel_pipeline.cpp:70-88), one
+            // shifted word at a time (the entry's tail bits are zero, so OR-ing whole words is exact)
             uint64_t* dst = widened_out + (ch * 256 + size_t(v)) * nw;
-            for (size_t b = 0; b < d_ch; ++b)
-                if ((entry[b >> 6] >> (b & 63)) & 1) dst[(offset + b) >> 6] |= 1ULL << ((offset + b) & 63);
+            const size_t w0 = offset >> 6, sh = offset & 63;
+            for (size_t k = 0; k < entry.size(); ++k) {
+                dst[w0 + k] |= entry[k] << sh;
+                if (sh && w0 + k + 1 < nw) dst[w0 + k + 1] |= entry[k] >> (64 - sh);
+            }
         }
         offset += d_ch;
     }
