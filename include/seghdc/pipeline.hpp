@@ -1,0 +1,3 @@
+// Forwarding header: the reference's seghdc/pipeline.hpp API lives in seghdc/seghdc.hpp.
+#pragma once
+#include "seghdc/seghdc.hpp"

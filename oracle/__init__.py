@@ -43,7 +43,7 @@ def build(force: bool = False) -> None:
     """Compile the checkers (the port always; the reference only if its sources exist)."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/src"):
-        targets.append("ref")
+        targets += ["ref", "suites"]
     subprocess.run(["make", "-s", "-C", HERE] + (["-B"] if force else []) + targets, check=True)
 
 
