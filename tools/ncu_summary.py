@@ -1,0 +1,77 @@
+"""Summarise ncu artefacts into profiles/*.md.
+
+  python tools/ncu_summary.py launches <launches.csv> <out.md>    # per-kernel device-time share
+  python tools/ncu_summary.py kernel   <report.ncu-rep> <out.md>  # key --set full metrics of one kernel
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "DRAM read % of peak"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "IMMA pipe %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__block_size", "block size"),
+    ("launch__grid_size", "grid size"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+]
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    iN, iV, iU = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[start + 1:]:
+        if len(r) <= iV:
+            continue
+        name = r[iN].split("(")[0].replace("void ", "")
+        v = float(r[iV].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[iU], 1)
+        agg[name][0] += 1
+        agg[name][1] += v
+    tot = sum(v for _, v in agg.values())
+    with open(out, "w") as f:
+        f.write(f"# Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`), from `{path}`\n\n")
+        f.write("Cold-cache, serialised per-launch times: compare shares, not absolutes.\n\n")
+        f.write("| kernel | launches | total us | share | avg us |\n|---|---|---|---|---|\n")
+        for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"| `{k}` | {c} | {v / 1e3:.1f} | {100 * v / tot:.1f} % | {v / c / 1e3:.2f} |\n")
+
+
+def kernel(path, out):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {h: (u, v) for h, u, v in zip(hdr, units, vals)}
+    stalls = []
+    for h, (u, v) in d.items():
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+            try:
+                stalls.append((float(v), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+            except ValueError:
+                pass
+    tot = sum(s for s, _ in stalls) or 1
+    with open(out, "w") as f:
+        f.write(f"# ncu --set full summary: `{d.get('Kernel Name', ('', '?'))[1]}`\n\nSource: `{path}`\n\n")
+        f.write("| metric | value | unit |\n|---|---|---|\n")
+        for key, label in KEYS:
+            if key in d:
+                f.write(f"| {label} (`{key}`) | {d[key][1]} | {d[key][0]} |\n")
+        f.write("\n## Warp stall samples\n\n| reason | share |\n|---|---|\n")
+        for s, n in sorted(stalls, reverse=True)[:10]:
+            f.write(f"| {n} | {100 * s / tot:.1f} % |\n")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "kernel": kernel}[sys.argv[1]](sys.argv[2], sys.argv[3])
