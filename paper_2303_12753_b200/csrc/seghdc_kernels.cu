@@ -34,37 +34,35 @@ constexpr uint64_t counter_capacity() {
 // fused with the column sums of the grid (the Harley-Seal counter of every pixel), which the
 // round schedule needs to derive the largest cluster's sums without accumulating them.
 //
-// CTA = (tile of ER x EC pixels, chunk of 32 HV words). The chunk's slice of every table it
-// touches (ER row entries, EC column entries, C x 256 colour entries: <= 120 KB) and the image
-// tile are staged once in shared memory, so L2 serves ~30 B per pixel-chunk instead of the
-// ~4 table words per output word of a direct gather. Warp = one pixel at a time, lane = word:
-// coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane; the CTA folds
-// them in shared memory and adds 1024 column sums to the global array with one atomic each.
+// CTA = (64-column tile, group of rows, chunk of 32 HV words). The chunk's slice of the colour
+// tables (C x 256 entries) and of the tile's 64 column codes is staged once per CTA; row codes
+// and image bytes are staged per batch of 32 rows, so the inner loop touches shared memory only
+// (L2 serves ~30 B per pixel-chunk instead of ~4 table words per output word). Warp = one image
+// row, lane = word: coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane;
+// the CTA folds them in shared memory and adds 1024 column sums to the global array.
 // =============================================================================================
-constexpr uint32_t kEncRows = 32, kEncCols = 64, kEncWarps = 16;
+constexpr uint32_t kEncRows = 32, kEncCols = 64, kEncWarps = 8;
 
 template <int C>
-__global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __restrict__ img, uint32_t h_img, uint32_t w,
-                                                            uint32_t row_begin, uint32_t row_end,
-                                                            const uint32_t* __restrict__ row,
-                                                            const uint32_t* __restrict__ col,
-                                                            const uint32_t* __restrict__ wid, uint32_t wref,
-                                                            uint32_t S32, uint32_t* __restrict__ grid,
-                                                            uint32_t* __restrict__ colsum, uint32_t W32) {
+__global__ void __launch_bounds__(kEncWarps * 32, 3)
+    k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
+             const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
+             uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t* __restrict__ colsum, uint32_t W32) {
     extern __shared__ __align__(16) uint32_t es[];
     uint32_t* s_wid = es;                            // [C][256][32]
     uint32_t* s_col = s_wid + C * 256 * 32;          // [EC][32]
-    uint32_t* s_sum = s_col + kEncCols * 32;         // [32 bits][32 words]
-    (void)h_img;
+    uint32_t* s_row = s_col + kEncCols * 32;         // [ER][32]
+    uint32_t* s_sum = s_row + kEncRows * 32;         // [32 bits][32 words]
+    uint8_t* s_img = reinterpret_cast<uint8_t*>(s_sum + 1024);  // [ER][EC][C]
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t w0 = blockIdx.z * 32;             // first word of the chunk
-    const uint32_t rows_per = (row_end - row_begin + gridDim.y - 1) / gridDim.y;
-    const uint32_t r0 = row_begin + blockIdx.y * rows_per, r1 = min(row_end, r0 + rows_per);
-    const uint32_t c0 = blockIdx.x * kEncCols, nc = min(kEncCols, w - c0);
-    const bool wl = w0 + lane < wref;  // this lane's word exists in the tables (else zero)
+    // chunk index varies fastest, so the CTAs writing the same pixel rows run together and L2
+    // assembles full lines before they are written back
+    const uint32_t w0 = blockIdx.x * 32;             // first word of the chunk
+    const uint32_t rows_per = (row_end - row_begin + gridDim.z - 1) / gridDim.z;
+    const uint32_t r0 = row_begin + blockIdx.z * rows_per, r1 = min(row_end, r0 + rows_per);
+    const uint32_t c0 = blockIdx.y * kEncCols, nc = min(kEncCols, w - c0);
 
-    // stage the chunk of the colour tables and of the tile's column codes (8 loads in flight)
-    for (uint32_t e0 = tid; e0 < C * 256 * 32; e0 += blockDim.x * 8) {
+    for (uint32_t e0 = tid; e0 < C * 256 * 32; e0 += blockDim.x * 8) {  // 8 loads in flight
         uint32_t v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -75,12 +73,11 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
         for (int k = 0; k < 8; ++k)
             if (e0 + k * blockDim.x < C * 256 * 32) s_wid[e0 + k * blockDim.x] = v[k];
     }
-    for (uint32_t e = tid; e < nc * 32; e += blockDim.x) {
-        const uint32_t wd = e & 31;
-        s_col[e] = (w0 + wd < wref) ? __ldg(col + size_t(c0 + (e >> 5)) * wref + w0 + wd) : 0u;
+    for (uint32_t e = tid; e < kEncCols * 32; e += blockDim.x) {
+        const uint32_t wd = e & 31, cc = e >> 5;
+        s_col[e] = (cc < nc && w0 + wd < wref) ? __ldg(col + size_t(c0 + cc) * wref + w0 + wd) : 0u;
     }
     for (uint32_t e = tid; e < 1024; e += blockDim.x) s_sum[e] = 0;
-    __syncthreads();
 
     BitCounter<12> cnt;  // <= rows_per / warps * 64 pixels per warp
     cnt.reset();
@@ -88,31 +85,39 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
     // staged tables hold 0 for words >= wref, so lanes past the HV need no masking below
     const uint32_t* s_col_l = s_col + lane;
     const uint32_t* s_wid_l = s_wid + lane;
-    for (uint32_t r = r0 + warp; r < r1; r += kEncWarps) {  // warp = one image row of the tile
-        const uint32_t rv = wl ? __ldg(row + size_t(r) * wref + w0 + lane) : 0u;
-        uint32_t* out = grid + (size_t(r - row_begin) * w + c0) * S32 + w0 + lane;
-        for (uint32_t half = 0; half * 32 < nc; ++half) {
-            // pixel values of columns half*32 + lane (broadcast per pixel with a shuffle)
-            uint32_t pv[C];
-#pragma unroll
-            for (int ch = 0; ch < C; ++ch)
-                pv[ch] = half * 32 + lane < nc ? img[(size_t(r) * w + c0 + half * 32 + lane) * C + ch] : 0u;
-            for (uint32_t c16 = half * 32; c16 < nc && c16 < half * 32 + 32; c16 += 16) {
+    for (uint32_t rb = r0; rb < r1; rb += kEncRows) {
+        const uint32_t nrb = min(kEncRows, r1 - rb);
+        __syncthreads();  // previous batch's row codes / image bytes consumed (and tables staged)
+        for (uint32_t e = tid; e < nrb * 32; e += blockDim.x) {
+            const uint32_t wd = e & 31;
+            s_row[e] = (w0 + wd < wref) ? __ldg(row + size_t(rb + (e >> 5)) * wref + w0 + wd) : 0u;
+        }
+        for (uint32_t e = tid; e < nrb * nc * C; e += blockDim.x) {
+            const uint32_t rr = e / (nc * C), k = e - rr * nc * C;
+            s_img[rr * kEncCols * C + k] = __ldg(img + (size_t(rb + rr) * w + c0) * C + k);
+        }
+        __syncthreads();
+        for (uint32_t rr = warp; rr < nrb; rr += kEncWarps) {  // warp = one image row
+            const uint32_t rv = s_row[rr * 32 + lane];
+            const uint8_t* px = s_img + rr * kEncCols * C;
+            uint32_t* o = grid + (size_t(rb + rr - row_begin) * w + c0) * S32 + w0 + lane;
+            for (uint32_t c16 = 0; c16 < nc; c16 += 16) {
                 const uint32_t lim = nc - c16;  // >= 16 except in the last group of a ragged tile
                 uint32_t x[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    uint32_t v = rv ^ s_col_l[(c16 + u) * 32];
+                    const uint32_t cc = c16 + u;
+                    uint32_t v = rv ^ s_col_l[cc * 32];
 #pragma unroll
-                    for (int ch = 0; ch < C; ++ch)
-                        v ^= s_wid_l[(ch * 256 + __shfl_sync(0xffffffffu, pv[ch], (c16 & 31) + u)) * 32];
+                    for (int ch = 0; ch < C; ++ch) v ^= s_wid_l[(ch * 256 + px[cc * C + ch]) * 32];
                     x[u] = uint32_t(u) < lim ? v : 0u;
                 }
-                uint32_t* o = out + size_t(c16) * S32;
                 if (st) {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        if (uint32_t(u) < lim) o[u * S32] = x[u];
+                    for (int u = 0; u < 16; ++u) {
+                        if (uint32_t(u) < lim) *o = x[u];
+                        o += S32;
+                    }
                 }
                 cnt.add16(x);
             }
@@ -120,6 +125,7 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
     }
     // fold the warps' counters in shared memory (bit-major: lanes hit distinct banks), then
     // one global atomic per column sum
+    __syncthreads();
 #pragma unroll 4
     for (int b = 0; b < 32; ++b) {
         const uint32_t val = cnt.value(b);
@@ -132,25 +138,28 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode(const uint8_t* __rest
     }
 }
 
+template <int C>
+static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
+    const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
+    cudaFuncSetAttribute(k_encode<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_encode<C><<<g, kEncWarps * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref, a.S32,
+                                                a.grid, a.colsum, a.W32);
+}
+
 void launch_encode(const EncodeArgs& a, cudaStream_t s) {
     const uint64_t n = a.pix_end - a.pix_begin;
     if (n == 0) return;
     const uint32_t row_begin = uint32_t(a.pix_begin / a.w), row_end = uint32_t(a.pix_end / a.w);
     const uint32_t gx = (a.w + kEncCols - 1) / kEncCols, gz = (a.S32 + 31) / 32;
-    // row groups: ~4 CTAs per SM in total; each CTA stages its table chunk once for all its rows
+    // row groups: up to ~6 CTAs per SM in total, but each CTA covers enough rows to amortise
+    // staging its table chunk (C x 32 KB) over >= 32*C rows
+    const uint32_t rows = row_end - row_begin;
+    const uint32_t min_rows = 32 * a.c;
     const uint32_t gy = std::max<uint32_t>(
-        1, std::min<uint32_t>(row_end - row_begin, (4 * a.sms + gx * gz - 1) / (gx * gz)));
-    dim3 g(gx, gy, gz);
-    const size_t smem = (size_t(a.c) * 256 * 32 + kEncCols * 32 + 1024) * 4;
-    if (a.c == 1) {
-        cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_encode<1><<<g, kEncWarps * 32, smem, s>>>(a.img, 0, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
-                                                    a.S32, a.grid, a.colsum, a.W32);
-    } else {
-        cudaFuncSetAttribute(k_encode<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_encode<3><<<g, kEncWarps * 32, smem, s>>>(a.img, 0, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
-                                                    a.S32, a.grid, a.colsum, a.W32);
-    }
+        1, std::min<uint32_t>((rows + min_rows - 1) / min_rows, (6 * a.sms + gx * gz - 1) / (gx * gz)));
+    const dim3 g(gz, gx, gy);
+    if (a.c == 1) launch_encode_c<1>(a, g, row_begin, row_end, s);
+    else launch_encode_c<3>(a, g, row_begin, row_end, s);
 }
 
 // =============================================================================================
