@@ -193,7 +193,7 @@ def run_reference_arm(args, spec):
     total = sum(times)
     value = h * w * args.steps / total
     line = {
-        "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32/u64 (reference integer dot)", "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD_TEXT[args.config], "pixels": h * w, "dim": spec["dim"], "k": spec["k"],
