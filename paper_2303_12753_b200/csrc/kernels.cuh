@@ -8,7 +8,8 @@
 //   Z         u32[K][D]              centroids: raw member sums (clusterer.hpp:27-34)
 //   bfrag     u64[NT][W32P][32]      Z split into P 7-bit planes, laid out as the B fragments of
 //                                    mma.m16n8k32 (column n = P*c + plane, NT = ceil(K*P/8)
-//                                    n-tiles of 8), with the k-slot permutation of unpack_a().
+//                                    n-tiles of 8), MMA index kk = 4*group + m, with the k-slot
+//                                    permutation of unpack_mask()/unpack_shift().
 //   xchg      i32[K*Dp | K | 1 | Dp] [centroid sums | member counts | changed | column sums],
 //                                    Dp = 32*W32. Every CTA folds its exact integer sums in
 //                                    with coalesced atomics; it is the only buffer a multi-GPU
@@ -211,18 +212,26 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// A fragment of m16n8k32 from two packed 32-bit HV words (rows g and g+8 of the m-tile).
-// Lane (g, q) owns k-slots 4q..4q+3 (a0/a1) and 16+4q..16+4q+3 (a2/a3). Slot 4q+j holds bit
-// 2q+8j and slot 16+4q+j holds bit 2q+1+8j of the word; the same permutation is baked into
-// bfrag, so the dot product is unchanged. One shift by 6-2q (an IMAD by the lane's opaque
-// power of two, FMA pipe) puts bit 2q+8j at bit 6 and bit 2q+1+8j at bit 7 of byte j, so
-// two LOP3 masks (ALU pipe) give both registers of the row: bytes are 64*bit (a0/a1) and
-// 128*bit (a2/a3). bfrag stores 7-bit centroid planes doubled in the a0/a1 slots, so every
-// product is 128 * bit * plane; the 128 is removed after the reduction.
-__device__ __forceinline__ void unpack_a(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, uint32_t mul) {
-    uint32_t t_lo, t_hi;
-    asm("mul.lo.u32 %0, %1, %2;" : "=r"(t_lo) : "r"(w_lo_row), "r"(mul));
-    asm("mul.lo.u32 %0, %1, %2;" : "=r"(t_hi) : "r"(w_hi_row), "r"(mul));
+// A fragments of m16n8k32 from packed HV words. The MMAs of a 4-word group (128 bits of the
+// HV) are numbered m = 0..3 (MMA index kk = 4*group + m); lane (g, q) supplies rows g and g+8
+// from word q of the group, so every lane loads one word per row per group and keeps it for
+// all four MMAs. k-slot 4q+j of MMA m is bit 8j+6-2m of word q, slot 16+4q+j is bit 8j+7-2m;
+// bfrag bakes in the same permutation (k_finish), so the dot product is unchanged.
+//   unpack_mask:  masks only (ALU pipe). Bytes are 2^(6-2m)*bit (a0/a1) and 2^(7-2m)*bit
+//                 (a2/a3); with the 7-bit planes doubled in bfrag's a0/a1 slots every product
+//                 is 2^(7-2m)*bit*plane, so MMA m accumulates separately and its scale is
+//                 removed (>> 7-2m, exact) before the accumulators are added.
+//   unpack_shift: one shift by 2m first, so every MMA has the common scale 128 (one
+//                 accumulator for all m; >> 7 after the reduction).
+__device__ __forceinline__ void unpack_mask(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, int m) {
+    const uint32_t m6 = 0x40404040u >> (2 * m), m7 = 0x80808080u >> (2 * m);
+    a[0] = w_lo_row & m6;
+    a[1] = w_hi_row & m6;
+    a[2] = w_lo_row & m7;
+    a[3] = w_hi_row & m7;
+}
+__device__ __forceinline__ void unpack_shift(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, int m) {
+    const uint32_t t_lo = w_lo_row << (2 * m), t_hi = w_hi_row << (2 * m);
     a[0] = t_lo & 0x40404040u;
     a[1] = t_hi & 0x40404040u;
     a[2] = t_lo & 0x80808080u;
@@ -230,14 +239,5 @@ __device__ __forceinline__ void unpack_a(uint32_t (&a)[4], uint32_t w_lo_row, ui
 }
 // centroid values are split into kPlanes planes of kPlaneBits bits (z < 2^28)
 constexpr uint32_t kPlaneBits = 7, kPlanes = 4;
-
-// bfrag address of bit i (within a column n of n-tile nt): byte offset inside u64 lane slot
-__host__ __device__ __forceinline__ size_t bfrag_byte(uint32_t nt, uint32_t n_in_tile, uint32_t i,
-                                                      uint32_t W32P) {
-    const uint32_t word = i >> 5, b = i & 31;
-    const uint32_t q = (b & 7) >> 1, j = b >> 3, half = b & 1;
-    const uint32_t lane = (n_in_tile << 2) | q;
-    return ((size_t(nt) * W32P + word) * 32 + lane) * 8 + half * 4 + j;
-}
 
 }  // namespace seghdc_dev

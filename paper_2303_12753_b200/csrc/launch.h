@@ -82,7 +82,6 @@ struct RoundPlan {
     uint32_t wpw = 32;         // HV words per warp (split-K)
     uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
     bool fused = false;        // one n-tile: warp-specialised kernel (+ fused accumulation when K == 2)
-    bool dedicated_roles = false;  // fused: separate epilogue/producer warps (k_round_ws) instead of rotating roles
 };
 struct RoundArgs {
     const uint32_t* grid;
@@ -98,7 +97,6 @@ struct RoundArgs {
     uint32_t ctas;
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
-size_t ws_smem_bytes(uint32_t SS, uint32_t nmw);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
 

@@ -421,20 +421,22 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
         unsigned long long n2 = (unsigned long long)z * z;
         for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         if (lane == 0) atomicAdd(st.norm2 + np * K + c, n2);
-        // B fragments: column n = P*c + plane; slot lane (n&7)<<2 | q holds bits {2q, 2q+8,
-        // 2q+16, 2q+24} (bytes 0-3, doubled: a0/a1 carry 64*bit) and {2q+1, ...} (bytes 4-7).
-        const uint32_t pl = lane >> 2, q = lane & 3;
+        // B fragments: column n = P*c + plane. This warp's word is word q = word & 3 of its
+        // 4-word group; lane (plane, m) writes the slot of MMA kk = 4*(word >> 2) + m for
+        // column n, lane (n & 7) << 2 | q: bytes j = bit 8j+6-2m (doubled: a0/a1 carry half the
+        // scale) and 4+j = bit 8j+7-2m (unpack_mask / unpack_shift).
+        const uint32_t pl = lane >> 2, m = lane & 3, qw = word & 3;
         uint64_t v = 0;
 #pragma unroll
         for (uint32_t half = 0; half < 2; ++half)
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) {
-                const uint32_t zb = __shfl_sync(0xffffffffu, z, 2 * q + half + 8 * j);
+                const uint32_t zb = __shfl_sync(0xffffffffu, z, 8 * j + 6 - 2 * m + half);
                 v |= uint64_t(((zb >> (kPlaneBits * pl)) & 0x7Fu) << (1 - half)) << (8 * (half * 4 + j));
             }
         if (pl < P) {
-            const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7;
-            *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + word) * 32 + ((nl << 2) | q)) * 8) = v;
+            const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7, kk = 4 * (word >> 2) + m;
+            *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + kk) * 32 + ((nl << 2) | qw)) * 8) = v;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x < K) {
@@ -465,7 +467,7 @@ void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s) {
 //
 // Persistent CTAs walk tiles of TP = 16*MT pixels, double buffered through cp.async.bulk
 // (TMA engine, one copy per pixel row) on mbarriers. Warp g owns 32-word blocks of every HV
-// (split-K), unpacks the packed bits into IMMA A fragments in registers (unpack_a) and
+// (split-K), unpacks the packed bits into IMMA A fragments in registers (unpack_shift) and
 // multiplies them with the 7-bit-plane B fragments of the centroids, NTG n-tiles at a time
 // (B streamed from L2). Partial dots meet in shared memory; one thread per pixel recombines
 // the planes in u64 and runs the exact 128-bit argmax. Member counts and the change count
@@ -525,8 +527,6 @@ __global__ void __launch_bounds__(TB, 1)
             if (tile < ntiles) issue(tile, b);
         }
     }
-    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
-    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
     const uint32_t ngroups = (NT + NTG - 1) / NTG;
 
     uint32_t it = 0;
@@ -549,17 +549,18 @@ __global__ void __launch_bounds__(TB, 1)
 
             for (uint32_t wb = warp; wb < nwarp_words; wb += nwarps) {
                 const uint32_t wbase = wb * 32;
+                const uint32_t* Tq = T + wbase + q;
 #pragma unroll
                 for (int k4 = 0; k4 < 8; ++k4) {
-                    uint4 wl[MT], wh[MT];
+                    uint32_t wl[MT], wh[MT];
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
-                        wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
-                        wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+                        wl[mt] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
+                        wh[mt] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
                     }
 #pragma unroll
-                    for (int kq = 0; kq < 4; ++kq) {
-                        const int kk = 4 * k4 + kq;
+                    for (int m = 0; m < 4; ++m) {
+                        const int kk = 4 * k4 + m;
                         uint32_t b0[NTG], b1[NTG];
 #pragma unroll
                         for (int nt = 0; nt < NTG; ++nt) {
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(TB, 1)
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
                             uint32_t a[4];
-                            unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
+                            unpack_shift(a, wl[mt], wh[mt], m);
 #pragma unroll
                             for (int nt = 0; nt < NTG; ++nt) imma16832(acc[mt][nt], a, b0[nt], b1[nt]);
                         }
@@ -593,7 +594,7 @@ __global__ void __launch_bounds__(TB, 1)
                 if (col >= NCT) continue;
                 int32_t s = 0;
                 for (uint32_t w = 0; w < nwarps; ++w) s += part[size_t(w) * TP * NC + e];
-                red[px * NCT + col] = uint32_t(s) >> 7;  // remove the 128 scale of unpack_a (exact)
+                red[px * NCT + col] = uint32_t(s) >> 7;  // remove the 128 scale of unpack_shift (exact)
             }
             __syncthreads();  // red complete for this group; part free for the next group
         }
@@ -651,231 +652,6 @@ static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStrea
                                            a.labels, a.state, a.round, reinterpret_cast<uint32_t*>(a.xchg) +
                                                                            size_t(a.K) * a.Dp);
     return cudaGetLastError();
-}
-
-// =============================================================================================
-// Warp-specialised round kernel (one n-tile of centroid planes, K * P <= 8): assign_labels
-// (clusterer.cpp:132-162) fused with the accumulation of update_centroids
-// (clusterer.cpp:164-188), each pixel HV crossing HBM once per round.
-//
-//   warps 0..NMW-1  "MMA" warps: wait tile t -> IMMA k-loop over their WPW words (B fragments
-//                   in 2*WPW registers) -> split-K partials to part[t%2] -> then, while the
-//                   epilogue warp works on tile t, fold tile t-1's update list into the
-//                   Harley-Seal counters (thread = word column) and release its buffer.
-//   warp NMW        epilogue: reduce tile t's partials (lane = pixel), exact u64 dots, 128-bit
-//                   argmax, labels, member counts, change count, update list.
-//   warp NMW+1      producer: cp.async.bulk (TMA engine) of tile rows + previous labels into
-//                   a 4-deep ring, gated by the buffer-free barriers.
-// Hand-offs are mbarriers only; the k-loop of tile t+1 overlaps the epilogue and the
-// re-bundling of tile t. Counters are folded into the exchange buffer with coalesced
-// atomics at the end; counts and changes go to its tail.
-// =============================================================================================
-template <int WPW, bool UPD, int H, int NMW>
-__global__ void __launch_bounds__((NMW + 2) * 32, 1)
-    k_round_ws(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
-               uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
-               int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
-    constexpr uint32_t MT = 2, TP = 32, NB = 4;  // ring: tile t computing, t+1..t+2 in flight, t-1 re-bundling
-    extern __shared__ __align__(128) uint8_t smem[];
-    StateView st = StateView::at(state, K);
-    if (st.hdr->done) return;
-
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t parity = round & 1;
-    uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
-
-    uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
-    const size_t tile_words = size_t(TP) * SS;
-    uint32_t* s_old = tiles + NB * tile_words + 32;                           // [NB][TP]
-    int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);              // [2][NMW][TP][8]
-    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
-    uint32_t* s_listn = s_list + 2 * TP;                                      // [2]
-    uint32_t* s_misc = s_listn + 2;                                           // [0] skip
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_misc + 2);                 // 8-byte aligned
-    uint64_t* full = bars;                     // [NB] tile data landed (TMA)
-    uint64_t* buf_free = bars + NB;            // [NB] MMA warps done with the buffer
-    uint64_t* part_full = bars + 2 * NB;       // [2] partials written
-    uint64_t* part_free = bars + 2 * NB + 2;   // [2] epilogue done reading partials
-    uint64_t* list_ready = bars + 2 * NB + 4;  // [2] labels + update list of the tile ready
-
-    const uint64_t ntiles = (n + TP - 1) / TP;
-    const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-    if (tid == 0) {
-        for (uint32_t b = 0; b < NB; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&buf_free[b], NMW * 32);
-        }
-        for (uint32_t b = 0; b < 2; ++b) {
-            mbar_init(&part_full[b], NMW * 32);
-            mbar_init(&part_free[b], 32);
-            mbar_init(&list_ready[b], 32);
-        }
-        mbar_fence_init();
-        s_misc[0] = pick_skip(st.cur + parity * K, K);
-    }
-    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
-    __syncthreads();
-    const uint32_t skip = s_misc[0];
-    const uint32_t upd_c = 1 - skip;  // K == 2 under UPD
-
-    if (warp == NMW + 1) {
-        // ------------------------------------------------------------------ producer warp
-        for (uint32_t it = 0; it < my_tiles; ++it) {
-            const uint32_t b = it % NB;
-            if (it >= NB) mbar_wait(&buf_free[b], ((it / NB) - 1) & 1);
-            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
-            const uint32_t npx = uint32_t(umin64(TP, n - px0));
-            const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer padded to 16 B
-            if (lane == 0) mbar_expect_tx(&full[b], npx * S32 * 4 + lab_bytes);
-            __syncwarp();
-            if (lane == 0) bulk_g2s(s_old + b * TP, labels + px0, lab_bytes, &full[b]);
-            if (SS == S32) {  // unpadded rows: the tile is one contiguous 40 KB block
-                if (lane == 1) bulk_g2s(tiles + b * tile_words, grid + px0 * S32, npx * S32 * 4, &full[b]);
-            } else if (lane < npx) {
-                bulk_g2s(tiles + b * tile_words + size_t(lane) * SS, grid + (px0 + lane) * S32, S32 * 4, &full[b]);
-            }
-        }
-        return;
-    }
-    if (warp == NMW) {
-        // ------------------------------------------------------------------ epilogue warp
-        const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
-        uint32_t changed = 0, cnt0 = 0, cnt1 = 0;
-        for (uint32_t it = 0; it < my_tiles; ++it) {
-            const uint32_t pb = it & 1, b = it % NB;
-            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
-            const uint32_t npx = uint32_t(umin64(TP, n - px0));
-            mbar_wait(&part_full[pb], (it >> 1) & 1);
-            const int32_t* pp = part + size_t(pb) * NMW * TP * 8 + lane * 8;
-            int32_t col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-            for (uint32_t w = 0; w < NMW; ++w) {
-                const int4 lo = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8);
-                const int4 hi = *reinterpret_cast<const int4*>(pp + size_t(w) * TP * 8 + 4);
-                col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
-                col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
-            }
-            mbar_arrive(&part_free[pb]);
-            // exact dots: column n = P*c + plane, 7-bit planes, 128 scale removed (exact)
-            unsigned long long d0 = 0, d1 = 0;  // named registers: no local-memory indexing
-#pragma unroll
-            for (uint32_t cn = 0; cn < 8; ++cn) {
-                const uint32_t c = cn / P, pl = cn - c * P;
-                const unsigned long long v = (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
-                if (c == 0) d0 += v;
-                else if (c == 1 && K > 1) d1 += v;
-            }
-            const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
-            const bool live = lane < npx;
-            const uint32_t old = s_old[b * TP + lane];
-            if (live) {
-                labels[px0 + lane] = best;
-                changed += old != best;
-                cnt0 += best == 0;
-                cnt1 += best == 1;
-            }
-            if constexpr (UPD) {
-                const bool take = do_update && live && best == upd_c;
-                const uint32_t m = __ballot_sync(0xffffffffu, take);
-                if (take) s_list[pb * TP + __popc(m & ((1u << lane) - 1))] = lane;
-                if (lane == 0) s_listn[pb] = __popc(m);
-            }
-            mbar_arrive(&list_ready[pb]);
-        }
-        for (int o = 16; o; o >>= 1) {
-            changed += __shfl_xor_sync(0xffffffffu, changed, o);
-            cnt0 += __shfl_xor_sync(0xffffffffu, cnt0, o);
-            cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
-        }
-        if (lane == 0) {
-            if (changed) atomicAdd(tail + K, changed);
-            if (cnt0) atomicAdd(tail, cnt0);
-            if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
-        }
-        return;
-    }
-
-    // ---------------------------------------------------------------------- MMA warps
-    const uint32_t g8 = lane >> 2, q = lane & 3;
-    uint32_t breg[WPW][2];
-#pragma unroll
-    for (int kk = 0; kk < WPW; ++kk) {
-        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
-        breg[kk][0] = uint32_t(v);
-        breg[kk][1] = uint32_t(v >> 32);
-    }
-    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
-    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
-    const uint32_t wbase = warp * WPW;
-    BitCounter<UPD ? H : 1> cnt;
-    if constexpr (UPD) cnt.reset();
-
-    auto rebundle = [&](uint32_t jt) {  // fold tile jt's update list into the counters
-        const uint32_t pb = jt & 1, b = jt % NB;
-        mbar_wait(&list_ready[pb], (jt >> 1) & 1);
-        if constexpr (UPD) {
-            if (do_update && tid < W32) {
-                const uint32_t m = s_listn[pb];
-                const uint32_t* T = tiles + b * tile_words;
-                for (uint32_t e = 0; e < m; e += 16) {
-                    uint32_t x[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        x[u] = (e + u < m) ? T[size_t(s_list[pb * TP + e + u]) * SS + tid] : 0u;
-                    cnt.add16(x);
-                }
-            }
-        }
-        mbar_arrive(&buf_free[b]);
-    };
-
-    for (uint32_t it = 0; it < my_tiles; ++it) {
-        const uint32_t b = it % NB, pb = it & 1;
-        mbar_wait(&full[b], (it / NB) & 1);
-        const uint32_t* T = tiles + b * tile_words;
-        int acc[MT][4];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
-#pragma unroll
-        for (int k4 = 0; k4 < WPW / 4; ++k4) {
-            uint4 wl[MT], wh[MT];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
-                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
-            }
-#pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-                const int kk = 4 * k4 + kq;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    uint32_t a[4];
-                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
-                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
-                }
-            }
-        }
-        if (it >= 2) mbar_wait(&part_free[pb], ((it >> 1) - 1) & 1);
-        int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
-            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
-            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
-        }
-        mbar_arrive(&part_full[pb]);
-        if (it >= 1) rebundle(it - 1);
-    }
-    if (my_tiles >= 1) rebundle(my_tiles - 1);
-    if constexpr (UPD) {
-        if (do_update) {
-            // all tiles consumed: the ring is free to serve as the transpose scratch
-            asm volatile("bar.sync 1, %0;" ::"r"(NMW * 32));
-            flush_warp_atomic(cnt, tiles + warp * (32 * 33), xchg + size_t(upd_c) * Dp, warp * 32, W32);
-        }
-    }
 }
 
 // =============================================================================================
@@ -969,12 +745,12 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
                 col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
                 col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
             }
-            // exact dots: column n = P*c + plane, 7-bit planes, 128 scale removed (exact)
+            // exact dots: column n = P*c + plane, 7-bit planes (MMA scales already removed)
             unsigned long long d0 = 0, d1 = 0;  // named registers: no local-memory indexing
 #pragma unroll
             for (uint32_t cn = 0; cn < 8; ++cn) {
                 const uint32_t c = cn / P, pl = cn - c * P;
-                const unsigned long long v = (unsigned long long)(uint32_t(col[cn]) >> 7) << (kPlaneBits * pl);
+                const unsigned long long v = (unsigned long long)uint32_t(col[cn]) << (kPlaneBits * pl);
                 if (c == 0) d0 += v;
                 else if (c == 1 && K > 1) d1 += v;
             }
@@ -1022,8 +798,6 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
         breg[kk][0] = uint32_t(v);
         breg[kk][1] = uint32_t(v >> 32);
     }
-    uint32_t mul;  // opaque power of two: the unpack shift issues as IMAD on the FMA pipe
-    asm volatile("mov.b32 %0, %1;" : "=r"(mul) : "r"(1u << (6 - 2 * q)));
     const uint32_t wbase = warp * WPW;
     BitCounter<UPD ? H : 1> cnt[CPT];
     if constexpr (UPD)
@@ -1059,36 +833,46 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
         const uint32_t b = it % NB, pb = it & 1;
         mbar_wait(&full[b], (it / NB) & 1);
         const uint32_t* T = tiles + b * tile_words;
-        int acc[MT][4];
+        // one accumulator per MMA m of a word group (mask-only unpack: scale 2^(7-2m))
+        int acc[4][MT][4];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[m][mt][r] = 0;
+        const uint32_t* Tq = T + wbase + q;
 #pragma unroll
         for (int k4 = 0; k4 < WPW / 4; ++k4) {
-            uint4 wl[MT], wh[MT];
+            uint32_t wl[MT], wh[MT];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-                wl[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8) * SS + wbase + 4 * k4);
-                wh[mt] = *reinterpret_cast<const uint4*>(T + size_t(16 * mt + g8 + 8) * SS + wbase + 4 * k4);
+                wl[mt] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
+                wh[mt] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
             }
 #pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-                const int kk = 4 * k4 + kq;
+            for (int m = 0; m < 4; ++m) {
+                const int kk = 4 * k4 + m;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     uint32_t a[4];
-                    unpack_a(a, (&wl[mt].x)[kq], (&wh[mt].x)[kq], mul);
-                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
+                    unpack_mask(a, wl[mt], wh[mt], m);
+                    imma16832(acc[m][mt], a, breg[kk][0], breg[kk][1]);
                 }
             }
         }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                acc[0][mt][r] = int((uint32_t(acc[0][mt][r]) >> 7) + (uint32_t(acc[1][mt][r]) >> 5) +
+                                    (uint32_t(acc[2][mt][r]) >> 3) + (uint32_t(acc[3][mt][r]) >> 1));
         int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
-            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
-            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
+            *reinterpret_cast<int2*>(row0) = make_int2(acc[0][mt][0], acc[0][mt][1]);
+            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[0][mt][2], acc[0][mt][3]);
         }
         mbar_arrive(&part_full[pb]);
         if (it >= 1) rebundle(it - 1);
@@ -1136,44 +920,6 @@ static cudaError_t launch_w1_h(const RoundArgs& a, cudaStream_t s) {
     return launch_w1_t<WPW, true, 20, NMW, CPT>(a, s);
 }
 
-size_t ws_smem_bytes(uint32_t SS, uint32_t nmw) {
-    const uint32_t TP = 32, NB = 4;
-    size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
-    b += NB * TP * 4;                            // s_old
-    b += 2 * size_t(nmw) * TP * 8 * 4;           // part
-    b += 2 * TP * 4 + 2 * 4 + 2 * 4;             // s_list, s_listn, s_misc
-    b += (2 * NB + 6) * 8;                       // mbarriers
-    return std::max<size_t>(b, size_t(nmw) * 32 * 33 * 4);
-}
-
-template <int WPW, bool UPD, int H, int NMW>
-static cudaError_t launch_ws_t(const RoundArgs& a, cudaStream_t s) {
-    auto kern = k_round_ws<WPW, UPD, H, NMW>;
-    const size_t smem = ws_smem_bytes(a.SS, NMW);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    kern<<<a.ctas, (NMW + 2) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
-                                              a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
-    return cudaGetLastError();
-}
-
-template <int H>
-struct WsH {
-    template <int WPW, int NMW>
-    static cudaError_t go(const RoundArgs& a, cudaStream_t s) {
-        return launch_ws_t<WPW, true, H, NMW>(a, s);
-    }
-};
-
-template <int WPW, int NMW>
-static cudaError_t launch_ws_h(const RoundArgs& a, cudaStream_t s) {
-    if (a.K != 2) return launch_ws_t<WPW, false, 1, NMW>(a, s);
-    const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + 31) & ~uint64_t(31);
-    if (per_cta <= counter_capacity<8>()) return WsH<8>::go<WPW, NMW>(a, s);
-    if (per_cta <= counter_capacity<12>()) return WsH<12>::go<WPW, NMW>(a, s);
-    return WsH<20>::go<WPW, NMW>(a, s);
-}
-
 // Plan: which instantiation handles (K, P, D). Returns false if no kernel fits.
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit) {
     p.nwarp_words = (W32 + 31) / 32;
@@ -1182,21 +928,16 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     if (p.nt == 1) {
         // (MMA warps, words per warp): MMA warps in multiples of 4 (equal k-loop load per SM
         // sub-partition), B fragments in 2*wpw registers, <= 2 word columns per thread in the
-        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count, SEGHDC_ROUND=ws the kernel with
-        // separate epilogue and producer warps (A/B testing).
+        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count (A/B testing).
         static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {8, 40},
                                            {12, 28}, {16, 20}};
         const char* force = getenv("SEGHDC_FUSED_WARPS");
         if (force && !*force) force = nullptr;
-        const char* variant = getenv("SEGHDC_ROUND");
-        const bool ws = variant && std::string(variant) == "ws";
         for (const auto& c : cand) {
             if (force && uint32_t(atoi(force)) != c[0]) continue;
             if (c[0] * c[1] < W32 || c[0] * 64 < W32) continue;
-            if (ws && (c[0] * 32 < W32 || c[1] == 40)) continue;
-            if (std::max(ws_smem_bytes(SS, c[0]), w1_smem_bytes(SS, c[0])) > smem_limit) continue;
+            if (w1_smem_bytes(SS, c[0]) > smem_limit) continue;
             p.fused = true;
-            p.dedicated_roles = ws;
             p.nwarps = c[0];
             p.wpw = c[1];
             p.w32p = c[0] * c[1];
@@ -1220,7 +961,7 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 }
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
-    if (p.fused && !p.dedicated_roles) {
+    if (p.fused) {
         switch (p.nwarps * 100 + p.wpw) {
             case 420: return launch_w1_h<20, 4, 1>(a, s);
             case 428: return launch_w1_h<28, 4, 1>(a, s);
@@ -1231,18 +972,6 @@ cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s)
             case 840: return launch_w1_h<40, 8, 2>(a, s);
             case 1228: return launch_w1_h<28, 12, 1>(a, s);
             default: return launch_w1_h<20, 16, 1>(a, s);
-        }
-    }
-    if (p.fused) {
-        switch (p.nwarps * 100 + p.wpw) {
-            case 420: return launch_ws_h<20, 4>(a, s);
-            case 428: return launch_ws_h<28, 4>(a, s);
-            case 432: return launch_ws_h<32, 4>(a, s);
-            case 820: return launch_ws_h<20, 8>(a, s);
-            case 828: return launch_ws_h<28, 8>(a, s);
-            case 832: return launch_ws_h<32, 8>(a, s);
-            case 1228: return launch_ws_h<28, 12>(a, s);
-            default: return launch_ws_h<20, 16>(a, s);
         }
     }
     switch (p.mt) {
