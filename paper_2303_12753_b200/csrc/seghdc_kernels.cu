@@ -745,15 +745,16 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
                 col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
                 col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
             }
-            // exact dots: column n = P*c + plane, 7-bit planes (MMA scales already removed)
-            unsigned long long d0 = 0, d1 = 0;  // named registers: no local-memory indexing
-#pragma unroll
-            for (uint32_t cn = 0; cn < 8; ++cn) {
-                const uint32_t c = cn / P, pl = cn - c * P;
-                const unsigned long long v = (unsigned long long)uint32_t(col[cn]) << (kPlaneBits * pl);
-                if (c == 0) d0 += v;
-                else if (c == 1 && K > 1) d1 += v;
-            }
+            // exact dots: column n = 4*c + plane, 7-bit planes (MMA scales already removed). The
+            // fused kernel runs K*P <= 8, so K == 2 means P == 4; K == 1 needs no dots at all.
+            const unsigned long long d0 = (unsigned long long)uint32_t(col[0]) +
+                                          ((unsigned long long)uint32_t(col[1]) << kPlaneBits) +
+                                          ((unsigned long long)uint32_t(col[2]) << (2 * kPlaneBits)) +
+                                          ((unsigned long long)uint32_t(col[3]) << (3 * kPlaneBits));
+            const unsigned long long d1 = (unsigned long long)uint32_t(col[4]) +
+                                          ((unsigned long long)uint32_t(col[5]) << kPlaneBits) +
+                                          ((unsigned long long)uint32_t(col[6]) << (2 * kPlaneBits)) +
+                                          ((unsigned long long)uint32_t(col[7]) << (3 * kPlaneBits));
             const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
             const bool live = lane < npx;
             const uint32_t old = s_old[b * TP + lane];
