@@ -620,7 +620,6 @@ __global__ void __launch_bounds__(TB, 1)
         if (warp == 0) {
             const uint64_t nxt = tile + 2ull * gridDim.x;
             if (nxt < ntiles) {
-                fence_proxy_async();
                 issue(nxt, buf);
             }
         }
@@ -774,7 +773,6 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
             // refill the buffer of tile it-1 (its re-bundling follows this tile's k-loop)
             if (it >= 1 && it - 1 + NB < my_tiles) {
                 mbar_wait(&buf_free[(it - 1) % NB], ((it - 1) / NB) & 1);
-                fence_proxy_async();
                 issue(it - 1 + NB);
             }
         }
