@@ -24,7 +24,7 @@ PUBLIC_HEADERS = [os.path.join(ROOT, "include", "seghdc_cuda.h"),
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
-              "-Xcompiler", "-Wall", "-Xptxas", "-v,-warn-spills"]
+              "-Xcompiler", "-Wall", "-Xptxas", "-v,-warn-spills"] + os.environ.get("SEGHDC_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:

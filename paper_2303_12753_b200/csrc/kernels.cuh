@@ -8,8 +8,8 @@
 //   Z         u32[K][D]              centroids: raw member sums (clusterer.hpp:27-34)
 //   bfrag     u64[NT][W32P][32]      Z split into P 7-bit planes, laid out as the B fragments of
 //                                    mma.m16n8k32 (column n = P*c + plane, NT = ceil(K*P/8)
-//                                    n-tiles of 8), MMA index kk = 4*group + m, with the k-slot
-//                                    permutation of unpack_mask()/unpack_shift().
+//                                    n-tiles of 8), MMA index kk = 4*group + 2*pair + s, with
+//                                    the pair packing of unpack_pair() (6-bit planes).
 //   xchg      i32[K*Dp | K | 1 | Dp] [centroid sums | member counts | changed | column sums],
 //                                    Dp = 32*W32. Every CTA folds its exact integer sums in
 //                                    with coalesced atomics; it is the only buffer a multi-GPU
@@ -212,32 +212,47 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// A fragments of m16n8k32 from packed HV words. The MMAs of a 4-word group (128 bits of the
-// HV) are numbered m = 0..3 (MMA index kk = 4*group + m); lane (g, q) supplies rows g and g+8
-// from word q of the group, so every lane loads one word per row per group and keeps it for
-// all four MMAs. k-slot 4q+j of MMA m is bit 8j+6-2m of word q, slot 16+4q+j is bit 8j+7-2m;
-// bfrag bakes in the same permutation (k_finish), so the dot product is unchanged.
-//   unpack_mask:  masks only (ALU pipe). Bytes are 2^(6-2m)*bit (a0/a1) and 2^(7-2m)*bit
-//                 (a2/a3); with the 7-bit planes doubled in bfrag's a0/a1 slots every product
-//                 is 2^(7-2m)*bit*plane, so MMA m accumulates separately and its scale is
-//                 removed (>> 7-2m, exact) before the accumulators are added.
-//   unpack_shift: one shift by 2m first, so every MMA has the common scale 128 (one
-//                 accumulator for all m; >> 7 after the reduction).
-__device__ __forceinline__ void unpack_mask(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, int m) {
-    const uint32_t m6 = 0x40404040u >> (2 * m), m7 = 0x80808080u >> (2 * m);
-    a[0] = w_lo_row & m6;
-    a[1] = w_hi_row & m6;
-    a[2] = w_lo_row & m7;
-    a[3] = w_hi_row & m7;
+__device__ __forceinline__ void imma16832_s8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void unpack_shift(uint32_t (&a)[4], uint32_t w_lo_row, uint32_t w_hi_row, int m) {
-    const uint32_t t_lo = w_lo_row << (2 * m), t_hi = w_hi_row << (2 * m);
-    a[0] = t_lo & 0x40404040u;
-    a[1] = t_hi & 0x40404040u;
-    a[2] = t_lo & 0x80808080u;
-    a[3] = t_hi & 0x80808080u;
+
+// Two HV bits per 8-bit k-slot ("pair packing"). The A byte of a slot is the top two bits of a
+// byte of the (shifted) word, masked with 0xC0: read as u8 it is 64*b6 + 128*b7, read as s8
+// it is 64*b6 - 128*b7. One u8 MMA against Bu = 2*z6 + z7 plus one s8 MMA against
+// Bs = 2*z6 - z7 (z6, z7 the 6-bit centroid planes of the two bits) add up to
+//     64*b6*(Bu+Bs) + 128*b7*(Bu-Bs) = 256*(b6*z6 + b7*z7),
+// so each MASK (ALU pipe) feeds 8 bits into the tensor pipe instead of 4, and every product
+// carries the common scale 256 (removed with >> 8 after the reduction, exact).
+//
+// The MMAs of a 4-word group (128 bits of the HV) are numbered kk = 4*group + 2*pair + s
+// (s = 0: u8 with Bu, s = 1: s8 with Bs, same A). Lane (g, q) supplies rows g and g+8 from
+// word q of the group, shifted left by 4*pair (a0/a1: slots 4q+j <-> bits 8j+6-4p, 8j+7-4p)
+// and by 4*pair+2 (a2/a3: slots 16+4q+j <-> bits 8j+4-4p, 8j+5-4p). k_finish bakes the
+// same permutation into bfrag. sh[0..3] = the lane's row words shifted by 0, 2, 4, 6.
+__device__ __forceinline__ void unpack_pair(uint32_t (&a)[4], uint32_t lo_p, uint32_t hi_p, uint32_t lo_p2,
+                                            uint32_t hi_p2) {
+    a[0] = lo_p & 0xC0C0C0C0u;
+    a[1] = hi_p & 0xC0C0C0C0u;
+    a[2] = lo_p2 & 0xC0C0C0C0u;
+    a[3] = hi_p2 & 0xC0C0C0C0u;
 }
-// centroid values are split into kPlanes planes of kPlaneBits bits (z < 2^28)
-constexpr uint32_t kPlaneBits = 7, kPlanes = 4;
+// left shift by a power of two held in a register: issues as IMAD on the FMA pipe, which is
+// otherwise idle in the k-loop (the ALU pipe carries the masks)
+__device__ __forceinline__ uint32_t shl_fma(uint32_t w, uint32_t pow2) {
+    uint32_t r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(pow2));
+    return r;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+// centroid values are split into (at least) kPlanes planes of kPlaneBits bits (z < 2^24 with 4)
+constexpr uint32_t kPlaneBits = 6, kPlanes = 4;
 
 }  // namespace seghdc_dev

@@ -91,7 +91,7 @@ struct seghdc_ctx {
     uint64_t pix_begin() const { return uint64_t(row_begin) * g_w; }
     // clustering state
     size_t K = 0, iterations = 0;
-    uint32_t planes = kPlanes;  // 7-bit centroid planes per cluster (5 when a caller's centroids exceed 2^28)
+    uint32_t planes = kPlanes;  // 6-bit centroid planes per cluster (planes_for)
     int early_stop = 0;
     RoundPlan plan;
     uint32_t round_ctas = 0;
@@ -222,12 +222,19 @@ void store_grid(seghdc_ctx& x, uint64_t* out) {
 }
 
 // ---- clustering schedule ----------------------------------------------------------------------
-void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = kPlanes) {
+// planes of kPlaneBits bits needed for centroid entries <= vmax (at least kPlanes)
+uint32_t planes_for(uint64_t vmax) {
+    uint32_t p = kPlanes;
+    while (p * kPlaneBits < 64 && (vmax >> (p * kPlaneBits)) != 0) ++p;
+    return p;
+}
+
+void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = 0) {
     require(x.grid_valid, "no resident grid: encode or load a grid first");
     // centroid entries are member counts <= pixels; the similarity kernel splits them into
-    // four 7-bit planes (kernels.cuh: kPlanes * kPlaneBits = 28 bits)
-    require(uint64_t(x.g_h) * x.g_w < (1ull << (kPlanes * kPlaneBits)),
-            "images of 2^28 pixels or more exceed the 28-bit centroid planes of the similarity kernel");
+    // 6-bit planes (kernels.cuh): 4 planes below 2^24 pixels, 5 below 2^30
+    require(uint64_t(x.g_h) * x.g_w < (1ull << 28), "images of 2^28 pixels or more are not supported");
+    if (planes == 0) planes = planes_for(uint64_t(x.g_h) * x.g_w);
     const Geometry& g = x.g;
     x.planes = planes;
     if (!plan_round(uint32_t(K), planes, g.W32, g.SS, x.plan, x.smem_optin))
@@ -370,6 +377,7 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.xchg = x.xchg.p;
     a.Dp = x.g.Dp;
     a.ctas = x.round_ctas;
+    a.bsm = x.plan.bsm;
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     cudaEvent_t ev_end = nullptr;
@@ -573,10 +581,10 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         require(k >= 1, "assign_labels: empty centroid set");
         if (grid) load_grid(*ctx, grid, h, w, dim, 0, h);
         require(ctx->g.D == dim && ctx->g_h == h && ctx->g_w == w, "assign_labels: dimension mismatch");
-        // caller centroids may hold any u32 (the reference's IntVector): 5 planes above 2^28
+        // caller centroids may hold any u32 (the reference's IntVector): up to 6 planes
         uint32_t zmax = 0;
         for (size_t i = 0; i < k * dim; ++i) zmax = std::max(zmax, centroids[i]);
-        alloc_cluster(*ctx, k, zmax >= (1u << (kPlanes * kPlaneBits)) ? kPlanes + 1 : kPlanes);
+        alloc_cluster(*ctx, k, planes_for(zmax));
         ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
         ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
         ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");

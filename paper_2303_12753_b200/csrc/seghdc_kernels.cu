@@ -422,20 +422,24 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
         for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         if (lane == 0) atomicAdd(st.norm2 + np * K + c, n2);
         // B fragments: column n = P*c + plane. This warp's word is word q = word & 3 of its
-        // 4-word group; lane (plane, m) writes the slot of MMA kk = 4*(word >> 2) + m for
-        // column n, lane (n & 7) << 2 | q: bytes j = bit 8j+6-2m (doubled: a0/a1 carry half the
-        // scale) and 4+j = bit 8j+7-2m (unpack_mask / unpack_shift).
-        const uint32_t pl = lane >> 2, m = lane & 3, qw = word & 3;
+        // 4-word group; lane (plane, pair, s) writes the slot of MMA kk = 4*(word >> 2) +
+        // 2*pair + s for column n, lane (n & 7) << 2 | q (unpack_pair): byte j of the low half
+        // pairs bits (8j+6-4p, 8j+7-4p), byte j of the high half bits (8j+4-4p, 8j+5-4p);
+        // the byte is 2*z6 + z7 (s = 0, u8) or 2*z6 - z7 (s = 1, s8) of the 6-bit planes.
+        const uint32_t pl = lane >> 2, pr = (lane >> 1) & 1, sgn = lane & 1, qw = word & 3;
         uint64_t v = 0;
 #pragma unroll
         for (uint32_t half = 0; half < 2; ++half)
 #pragma unroll
             for (uint32_t j = 0; j < 4; ++j) {
-                const uint32_t zb = __shfl_sync(0xffffffffu, z, 8 * j + 6 - 2 * m + half);
-                v |= uint64_t(((zb >> (kPlaneBits * pl)) & 0x7Fu) << (1 - half)) << (8 * (half * 4 + j));
+                const uint32_t b6 = 8 * j + 6 - 4 * pr - 2 * half;
+                const uint32_t z6 = (__shfl_sync(0xffffffffu, z, b6) >> (kPlaneBits * pl)) & 0x3Fu;
+                const uint32_t z7 = (__shfl_sync(0xffffffffu, z, b6 + 1) >> (kPlaneBits * pl)) & 0x3Fu;
+                const uint32_t byte = (sgn ? 2 * z6 - z7 : 2 * z6 + z7) & 0xFFu;
+                v |= uint64_t(byte) << (8 * (half * 4 + j));
             }
         if (pl < P) {
-            const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7, kk = 4 * (word >> 2) + m;
+            const uint32_t n = P * c + pl, nt = n >> 3, nl = n & 7, kk = 4 * (word >> 2) + 2 * pr + sgn;
             *reinterpret_cast<uint64_t*>(bfrag + ((size_t(nt) * W32P + kk) * 32 + ((nl << 2) | qw)) * 8) = v;
         }
     }
@@ -467,7 +471,7 @@ void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s) {
 //
 // Persistent CTAs walk tiles of TP = 16*MT pixels, double buffered through cp.async.bulk
 // (TMA engine, one copy per pixel row) on mbarriers. Warp g owns 32-word blocks of every HV
-// (split-K), unpacks the packed bits into IMMA A fragments in registers (unpack_shift) and
+// (split-K), unpacks the packed bits into IMMA A fragments in registers (unpack_pair) and
 // multiplies them with the 7-bit-plane B fragments of the centroids, NTG n-tiles at a time
 // (B streamed from L2). Partial dots meet in shared memory; one thread per pixel recombines
 // the planes in u64 and runs the exact 128-bit argmax. Member counts and the change count
@@ -528,6 +532,7 @@ __global__ void __launch_bounds__(TB, 1)
         }
     }
     const uint32_t ngroups = (NT + NTG - 1) / NTG;
+    const uint32_t pw4[4] = {1u, opaque(4u), opaque(16u), opaque(64u)};  // shifts 0, 2, 4, 6
 
     uint32_t it = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -550,32 +555,45 @@ __global__ void __launch_bounds__(TB, 1)
             for (uint32_t wb = warp; wb < nwarp_words; wb += nwarps) {
                 const uint32_t wbase = wb * 32;
                 const uint32_t* Tq = T + wbase + q;
-#pragma unroll
+#pragma unroll 2
                 for (int k4 = 0; k4 < 8; ++k4) {
-                    uint32_t wl[MT], wh[MT];
+                    uint32_t sl[MT][4], sh[MT][4];
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
-                        wl[mt] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
-                        wh[mt] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
+                        sl[mt][0] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
+                        sh[mt][0] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
+#pragma unroll
+                        for (int e = 1; e < 4; ++e) {
+                            sl[mt][e] = shl_fma(sl[mt][0], pw4[e]);
+                            sh[mt][e] = shl_fma(sh[mt][0], pw4[e]);
+                        }
                     }
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int kk = 4 * k4 + m;
-                        uint32_t b0[NTG], b1[NTG];
+                    for (int pr = 0; pr < 2; ++pr) {
+                        const int kk = 4 * k4 + 2 * pr;
+                        uint32_t bu0[NTG], bu1[NTG], bs0[NTG], bs1[NTG];
 #pragma unroll
                         for (int nt = 0; nt < NTG; ++nt) {
                             const uint32_t ntg = grp * NTG + nt;
-                            uint64_t v = 0;
-                            if (ntg < NT) v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
-                            b0[nt] = uint32_t(v);
-                            b1[nt] = uint32_t(v >> 32);
+                            uint64_t u = 0, v = 0;
+                            if (ntg < NT) {
+                                u = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk) * 32 + lane));
+                                v = __ldg(bfrag + ((size_t(ntg) * W32P + wbase + kk + 1) * 32 + lane));
+                            }
+                            bu0[nt] = uint32_t(u);
+                            bu1[nt] = uint32_t(u >> 32);
+                            bs0[nt] = uint32_t(v);
+                            bs1[nt] = uint32_t(v >> 32);
                         }
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt) {
                             uint32_t a[4];
-                            unpack_shift(a, wl[mt], wh[mt], m);
+                            unpack_pair(a, sl[mt][2 * pr], sh[mt][2 * pr], sl[mt][2 * pr + 1], sh[mt][2 * pr + 1]);
 #pragma unroll
-                            for (int nt = 0; nt < NTG; ++nt) imma16832(acc[mt][nt], a, b0[nt], b1[nt]);
+                            for (int nt = 0; nt < NTG; ++nt) {
+                                imma16832(acc[mt][nt], a, bu0[nt], bu1[nt]);
+                                imma16832_s8(acc[mt][nt], a, bs0[nt], bs1[nt]);
+                            }
                         }
                     }
                 }
@@ -594,7 +612,7 @@ __global__ void __launch_bounds__(TB, 1)
                 if (col >= NCT) continue;
                 int32_t s = 0;
                 for (uint32_t w = 0; w < nwarps; ++w) s += part[size_t(w) * TP * NC + e];
-                red[px * NCT + col] = uint32_t(s) >> 7;  // remove the 128 scale of unpack_shift (exact)
+                red[px * NCT + col] = uint32_t(s) >> 8;  // remove the 256 scale of the pair packing (exact)
             }
             __syncthreads();  // red complete for this group; part free for the next group
         }
@@ -665,13 +683,16 @@ static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStrea
 //              -> wait buf_free(t-1) -> TMA of tile t-1+NB into the freed buffer
 // part[t%2] needs no free-barrier: an MMA warp rewrites it only after re-bundling tile t,
 // which waits for list_ready[t], signalled after the epilogue has read part[t%2].
+// BSM: the B fragments live in shared memory (one LDS.64 per MMA, conflict-free) instead of
+// 2*WPW registers per thread; the freed registers let the compiler keep several A fragments
+// in flight. The ring then holds NB = 3 tiles (B takes W32P * 256 bytes).
 // =============================================================================================
-template <int WPW, bool UPD, int H, int NMW, int CPT>
+template <int WPW, bool UPD, int H, int NMW, int CPT, bool BSM>
 __global__ void __launch_bounds__((NMW + 1) * 32, 1)
     k_round_w1(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
                uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
                int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
-    constexpr uint32_t MT = 2, TP = 32, NB = 4;
+    constexpr uint32_t MT = 2, TP = 32, NB = BSM ? 3 : 4;
     extern __shared__ __align__(128) uint8_t smem[];
     StateView st = StateView::at(state, K);
     if (st.hdr->done) return;
@@ -682,7 +703,8 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
 
     uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
     const size_t tile_words = size_t(TP) * SS;
-    uint32_t* s_old = tiles + NB * tile_words + 32;                           // [NB][TP]
+    uint2* sB = reinterpret_cast<uint2*>(tiles + NB * tile_words + 32);       // [NMW*WPW][32] if BSM
+    uint32_t* s_old = reinterpret_cast<uint32_t*>(sB + (BSM ? NMW * WPW * 32 : 0));  // [NB][TP]
     int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);              // [2][NMW][TP][8]
     uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
     uint32_t* s_listn = s_list + 2 * TP;                                      // [2]
@@ -754,7 +776,11 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
                                           ((unsigned long long)uint32_t(col[5]) << kPlaneBits) +
                                           ((unsigned long long)uint32_t(col[6]) << (2 * kPlaneBits)) +
                                           ((unsigned long long)uint32_t(col[7]) << (3 * kPlaneBits));
+#if SEGHDC_EXP == 2
+            const uint32_t best = uint32_t(d0 & 1) & (n2_0 == 7);
+#else
             const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
+#endif
             const bool live = lane < npx;
             const uint32_t old = s_old[b * TP + lane];
             if (live) {
@@ -790,14 +816,24 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
 
     // ---------------------------------------------------------------------- MMA warps
     const uint32_t g8 = lane >> 2, q = lane & 3;
-    uint32_t breg[WPW][2];
+    uint32_t breg[BSM ? 1 : WPW][2];
+    const uint2* sBw = sB + size_t(warp) * WPW * 32 + lane;  // this warp's slice (BSM)
+    if constexpr (BSM) {
+        for (int kk = 0; kk < WPW; ++kk) {
+            const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+            sB[(size_t(warp) * WPW + kk) * 32 + lane] = make_uint2(uint32_t(v), uint32_t(v >> 32));
+        }
+        __syncwarp();
+    } else {
 #pragma unroll
-    for (int kk = 0; kk < WPW; ++kk) {
-        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
-        breg[kk][0] = uint32_t(v);
-        breg[kk][1] = uint32_t(v >> 32);
+        for (int kk = 0; kk < WPW; ++kk) {
+            const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+            breg[kk][0] = uint32_t(v);
+            breg[kk][1] = uint32_t(v >> 32);
+        }
     }
     const uint32_t wbase = warp * WPW;
+    const uint32_t pw4[4] = {1u, opaque(4u), opaque(16u), opaque(64u)};  // shifts 0, 2, 4, 6
     BitCounter<UPD ? H : 1> cnt[CPT];
     if constexpr (UPD)
 #pragma unroll
@@ -832,46 +868,56 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
         const uint32_t b = it % NB, pb = it & 1;
         mbar_wait(&full[b], (it / NB) & 1);
         const uint32_t* T = tiles + b * tile_words;
-        // one accumulator per MMA m of a word group (mask-only unpack: scale 2^(7-2m))
-        int acc[4][MT][4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int r = 0; r < 4; ++r) acc[m][mt][r] = 0;
-        const uint32_t* Tq = T + wbase + q;
-#pragma unroll
-        for (int k4 = 0; k4 < WPW / 4; ++k4) {
-            uint32_t wl[MT], wh[MT];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                wl[mt] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
-                wh[mt] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
-            }
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int kk = 4 * k4 + m;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    uint32_t a[4];
-                    unpack_mask(a, wl[mt], wh[mt], m);
-                    imma16832(acc[m][mt], a, breg[kk][0], breg[kk][1]);
-                }
-            }
-        }
+        int acc[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                acc[0][mt][r] = int((uint32_t(acc[0][mt][r]) >> 7) + (uint32_t(acc[1][mt][r]) >> 5) +
-                                    (uint32_t(acc[2][mt][r]) >> 3) + (uint32_t(acc[3][mt][r]) >> 1));
+            for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
+        const uint32_t* Tq = T + wbase + q;
+#if SEGHDC_EXP != 1
+#pragma unroll
+        for (int k4 = 0; k4 < WPW / 4; ++k4) {
+            uint32_t sl[MT][4], sh[MT][4];  // row words shifted by 0, 2, 4, 6
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                sl[mt][0] = Tq[size_t(16 * mt + g8) * SS + 4 * k4];
+                sh[mt][0] = Tq[size_t(16 * mt + g8 + 8) * SS + 4 * k4];
+#pragma unroll
+                for (int e = 1; e < 4; ++e) {
+                    sl[mt][e] = shl_fma(sl[mt][0], pw4[e]);
+                    sh[mt][e] = shl_fma(sh[mt][0], pw4[e]);
+                }
+            }
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+                const int kk = 4 * k4 + 2 * pr;
+                uint32_t bu0, bu1, bs0, bs1;
+                if constexpr (BSM) {
+                    const uint2 u = sBw[kk * 32], v = sBw[(kk + 1) * 32];
+                    bu0 = u.x; bu1 = u.y; bs0 = v.x; bs1 = v.y;
+                } else {
+                    bu0 = breg[kk][0]; bu1 = breg[kk][1]; bs0 = breg[kk + 1][0]; bs1 = breg[kk + 1][1];
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    uint32_t a[4];
+                    unpack_pair(a, sl[mt][2 * pr], sh[mt][2 * pr], sl[mt][2 * pr + 1], sh[mt][2 * pr + 1]);
+                    imma16832(acc[mt], a, bu0, bu1);
+                    imma16832_s8(acc[mt], a, bs0, bs1);
+                }
+            }
+        }
+#endif
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[mt][r] = int(uint32_t(acc[mt][r]) >> 8);  // scale 256 (exact)
         int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
-            *reinterpret_cast<int2*>(row0) = make_int2(acc[0][mt][0], acc[0][mt][1]);
-            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[0][mt][2], acc[0][mt][3]);
+            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
+            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
         }
         mbar_arrive(&part_full[pb]);
         if (it >= 1) rebundle(it - 1);
@@ -889,9 +935,10 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
     }
 }
 
-size_t w1_smem_bytes(uint32_t SS, uint32_t nmw) {
-    const uint32_t TP = 32, NB = 4;
+size_t w1_smem_bytes(uint32_t SS, uint32_t nmw, uint32_t wpw, bool bsm) {
+    const uint32_t TP = 32, NB = bsm ? 3 : 4;
     size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
+    if (bsm) b += size_t(nmw) * wpw * 32 * 8;    // B fragments
     b += NB * TP * 4;                            // s_old
     b += 2 * size_t(nmw) * TP * 8 * 4;           // part
     b += (2 * TP + 2 + 2) * 4;                   // s_list, s_listn, s_misc
@@ -901,8 +948,9 @@ size_t w1_smem_bytes(uint32_t SS, uint32_t nmw) {
 
 template <int WPW, bool UPD, int H, int NMW, int CPT>
 static cudaError_t launch_w1_t(const RoundArgs& a, cudaStream_t s) {
-    auto kern = k_round_w1<WPW, UPD, H, NMW, CPT>;
-    const size_t smem = w1_smem_bytes(a.SS, NMW);
+    const bool bsm = a.bsm;
+    auto kern = bsm ? k_round_w1<WPW, UPD, H, NMW, CPT, true> : k_round_w1<WPW, UPD, H, NMW, CPT, false>;
+    const size_t smem = w1_smem_bytes(a.SS, NMW, WPW, bsm);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, (NMW + 1) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
@@ -927,15 +975,19 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     if (p.nt == 1) {
         // (MMA warps, words per warp): MMA warps in multiples of 4 (equal k-loop load per SM
         // sub-partition), B fragments in 2*wpw registers, <= 2 word columns per thread in the
-        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count (A/B testing).
-        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {8, 40},
-                                           {12, 28}, {16, 20}};
+        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count, SEGHDC_BSM=1 B fragments in shared
+        // memory (A/B testing; measured equal or slower on B200).
+        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {12, 28},
+                                           {8, 40}, {16, 20}};
         const char* force = getenv("SEGHDC_FUSED_WARPS");
         if (force && !*force) force = nullptr;
         for (const auto& c : cand) {
             if (force && uint32_t(atoi(force)) != c[0]) continue;
             if (c[0] * c[1] < W32 || c[0] * 64 < W32) continue;
-            if (w1_smem_bytes(SS, c[0]) > smem_limit) continue;
+            const char* bs = getenv("SEGHDC_BSM");
+            const bool want_bsm = bs && *bs == '1';  // B in registers unless asked (A/B testing)
+            p.bsm = want_bsm && w1_smem_bytes(SS, c[0], c[1], true) <= smem_limit;
+            if (!p.bsm && w1_smem_bytes(SS, c[0], c[1], false) > smem_limit) continue;
             p.fused = true;
             p.nwarps = c[0];
             p.wpw = c[1];
