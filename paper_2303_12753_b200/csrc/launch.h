@@ -82,7 +82,7 @@ struct RoundPlan {
     uint32_t wpw = 32;         // HV words per warp (split-K)
     uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
     bool fused = false;        // one n-tile: warp-specialised kernel (+ fused accumulation when K == 2)
-    bool bsm = false;          // fused: B fragments in shared memory instead of registers
+    uint32_t nrw = 0;          // fused: dedicated re-bundling warps (0: the MMA warps re-bundle)
 };
 struct RoundArgs {
     const uint32_t* grid;
@@ -96,7 +96,6 @@ struct RoundArgs {
     int32_t* xchg;  // [K*Dp sums | K counts | changed], zeroed before the round
     uint32_t Dp;
     uint32_t ctas;
-    bool bsm;  // RoundPlan::bsm
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);

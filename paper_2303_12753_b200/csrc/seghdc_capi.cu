@@ -377,7 +377,6 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.xchg = x.xchg.p;
     a.Dp = x.g.Dp;
     a.ctas = x.round_ctas;
-    a.bsm = x.plan.bsm;
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     cudaEvent_t ev_end = nullptr;
@@ -817,3 +816,11 @@ int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, si
 }
 
 }  // extern "C"
+
+#ifdef SEGHDC_TRACE
+namespace seghdc_dev {
+void read_trace(void* dst);
+}
+// diagnostic build only: 148 x 64 x 8 u64 clock64() stamps of the fused round kernel
+extern "C" void seghdc_debug_trace(void* dst) { seghdc_dev::read_trace(dst); }
+#endif

@@ -672,27 +672,47 @@ static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStrea
 }
 
 // =============================================================================================
-// One-role-warp variant (the default): NMW MMA warps + ONE warp that is both the epilogue and
-// the TMA producer. With NMW = 8 the CTA has 9 warps, at most 3 per SM sub-partition, so the
-// MMA warps get ~170 registers (B fragments of WPW = 40 words stay resident) while the
-// k-loop load is still spread evenly over the 4 sub-partitions (2 MMA warps each). Threads
-// own CPT word columns for the re-bundling (CPT = 2 when NMW*32 < W32).
-//   MMA warp:  wait full[t] -> k-loop -> partials -> arrive part_full[t%2]
-//              -> re-bundle tile t-1 (wait list_ready) -> arrive buf_free
-//   role warp: wait part_full[t%2] -> epilogue(t) -> arrive list_ready[t%2]
-//              -> wait buf_free(t-1) -> TMA of tile t-1+NB into the freed buffer
-// part[t%2] needs no free-barrier: an MMA warp rewrites it only after re-bundling tile t,
-// which waits for list_ready[t], signalled after the epilogue has read part[t%2].
-// BSM: the B fragments live in shared memory (one LDS.64 per MMA, conflict-free) instead of
-// 2*WPW registers per thread; the freed registers let the compiler keep several A fragments
-// in flight. The ring then holds NB = 3 tiles (B takes W32P * 256 bytes).
+// Fused round kernel (one n-tile of centroid planes, K * P <= 8): assign_labels
+// (clusterer.cpp:132-162) fused with the accumulation of update_centroids
+// (clusterer.cpp:164-188), each pixel HV crossing HBM once per round. Persistent CTAs, one per
+// SM, walk 32-pixel tiles through an NB-deep ring of TMA bulk copies. Warp roles:
+//   NMW MMA warps   wait tile t -> pair-packed IMMA k-loop over their WPW words (B fragments in
+//                   2*WPW registers) -> arrive buf_free[t] -> split-K partials to part[t%2]
+//                   -> arrive part_full[t%2].
+//   epilogue warp   wait part_full -> reduce the partials (lane = pixel), exact u64 dots,
+//                   128-bit argmax, labels, counts, update list -> arrive list_ready[t].
+//   NRW fold warps  wait list_ready[t] -> fold tile t's update list (the pixels of the cluster
+//                   not derived from the column sums) into Harley-Seal counters, one thread
+//                   per word column (<= 4 columns each) -> arrive buf_free[t].
+//   producer warp   wait buf_free[t] -> TMA of tile t+NB into that buffer.
+// Every hand-off is an mbarrier; a buffer is refilled the moment its last reader is done.
+// Ring-slot indexed list[] / list_ready[]: the epilogue writes list[t%NB] for tile t only
+// after tile t landed, i.e. after buf_free[t-NB] (all folding of t-NB) - no overwrite race.
+// part[] is two-deep: an MMA warp waits list_ready[t-2] (the epilogue of t-2 has read part)
+// before it overwrites part[t%2].
 // =============================================================================================
-template <int WPW, bool UPD, int H, int NMW, int CPT, bool BSM>
-__global__ void __launch_bounds__((NMW + 1) * 32, 1)
-    k_round_w1(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
-               uint32_t P, const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round,
-               int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
-    constexpr uint32_t MT = 2, TP = 32, NB = BSM ? 3 : 4;
+#ifdef SEGHDC_TRACE
+// diagnostic build only (-DSEGHDC_TRACE): per-CTA clock64() stamps of the first 64 tiles
+// events 0..7 as in tools/trace_round.py, 8 + 2w / 9 + 2w: k-loop start / end of MMA warp w
+constexpr int kTraceEv = 48;
+__device__ unsigned long long g_trace[148 * 64 * kTraceEv];
+#define SEGHDC_TR(ev, it)                                                              \
+    do {                                                                               \
+        if (lane == 0 && blockIdx.x < 148 && (it) < 64 && (ev) < kTraceEv)             \
+            g_trace[(size_t(blockIdx.x) * 64 + (it)) * kTraceEv + (ev)] = clock64();   \
+    } while (0)
+#else
+#define SEGHDC_TR(ev, it) ((void)0)
+#endif
+template <int WPW, bool UPD, int H, int NMW, int NRW>
+__global__ void __launch_bounds__((NMW + NRW + 2) * 32, 1)
+    k_round_fused(const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32, uint32_t SS, uint32_t W32, uint32_t K,
+                  const uint64_t* __restrict__ bfrag, uint32_t* labels, void* state, uint32_t round, int do_update,
+                  uint32_t* __restrict__ xchg, uint32_t Dp) {
+    constexpr uint32_t MT = 2, TP = 32, NB = 4;
+    constexpr int CPTMAX = 4;  // word columns per fold thread
+    constexpr uint32_t NRT = NRW * 32;
+    constexpr uint32_t NTHREADS = (NMW + NRW + 2) * 32;
     extern __shared__ __align__(128) uint8_t smem[];
     StateView st = StateView::at(state, K);
     if (st.hdr->done) return;
@@ -703,38 +723,39 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
 
     uint32_t* tiles = reinterpret_cast<uint32_t*>(smem);
     const size_t tile_words = size_t(TP) * SS;
-    uint2* sB = reinterpret_cast<uint2*>(tiles + NB * tile_words + 32);       // [NMW*WPW][32] if BSM
-    uint32_t* s_old = reinterpret_cast<uint32_t*>(sB + (BSM ? NMW * WPW * 32 : 0));  // [NB][TP]
+    uint32_t* s_old = tiles + NB * tile_words + 32;                           // [NB][TP] previous labels
     int32_t* part = reinterpret_cast<int32_t*>(s_old + NB * TP);              // [2][NMW][TP][8]
-    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [2][TP]
-    uint32_t* s_listn = s_list + 2 * TP;                                      // [2]
-    uint32_t* s_misc = s_listn + 2;                                           // [0] skip
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(part + 2 * NMW * TP * 8);  // [NB][TP]
+    uint32_t* s_listn = s_list + NB * TP;                                     // [NB]
+    uint32_t* s_misc = s_listn + NB;                                          // [0] skip
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_misc + 2);                 // 8-byte aligned
-    uint64_t* full = bars;                     // [NB] tile data landed (TMA)
-    uint64_t* buf_free = bars + NB;            // [NB] MMA warps done with the buffer
-    uint64_t* part_full = bars + 2 * NB;       // [2] partials written
-    uint64_t* list_ready = bars + 2 * NB + 2;  // [2] labels + update list of the tile ready
+    uint64_t* full = bars;                   // [NB] tile data landed (TMA)
+    uint64_t* buf_free = bars + NB;          // [NB] MMA + fold warps done with the buffer
+    uint64_t* list_ready = bars + 2 * NB;    // [NB] labels + update list of the tile ready
+    uint64_t* part_full = bars + 3 * NB;     // [2] partials written
 
     const uint64_t ntiles = (n + TP - 1) / TP;
     const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
     if (tid == 0) {
         for (uint32_t b = 0; b < NB; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&buf_free[b], NMW * 32);
-        }
-        for (uint32_t b = 0; b < 2; ++b) {
-            mbar_init(&part_full[b], NMW * 32);
+            mbar_init(&buf_free[b], (NMW + NRW) * 32);
             mbar_init(&list_ready[b], 32);
         }
+        for (uint32_t b = 0; b < 2; ++b) mbar_init(&part_full[b], NMW * 32);
         mbar_fence_init();
         s_misc[0] = pick_skip(st.cur + parity * K, K);
     }
     if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
     __syncthreads();
     const uint32_t upd_c = 1 - s_misc[0];  // K == 2 under UPD
+    const bool folding = UPD && do_update;
+    auto end_barrier = [&]() {  // all tiles consumed: the ring becomes the flush scratch
+        if (folding) asm volatile("bar.sync 1, %0;" ::"r"(NTHREADS));
+    };
 
-    if (warp == NMW) {
-        // ------------------------------------------------------------- epilogue + producer warp
+    if (warp == NMW + NRW + 1) {
+        // ----------------------------------------------------------------------- producer warp
         auto issue = [&](uint32_t it) {
             const uint32_t b = it % NB;
             const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
@@ -742,14 +763,26 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
             const uint32_t lab_bytes = (npx * 4 + 15) & ~15u;  // labels buffer padded to 16 B
             if (lane == 0) mbar_expect_tx(&full[b], npx * S32 * 4 + lab_bytes);
             __syncwarp();
+            SEGHDC_TR(0, it);
             if (lane == 0) bulk_g2s(s_old + b * TP, labels + px0, lab_bytes, &full[b]);
-            if (SS == S32) {  // unpadded rows: the tile is one contiguous 40 KB block
+            if (SS == S32) {  // unpadded rows: the tile is one contiguous block
                 if (lane == 1) bulk_g2s(tiles + b * tile_words, grid + px0 * S32, npx * S32 * 4, &full[b]);
             } else if (lane < npx) {
                 bulk_g2s(tiles + b * tile_words + size_t(lane) * SS, grid + (px0 + lane) * S32, S32 * 4, &full[b]);
             }
         };
         for (uint32_t it = 0; it < NB && it < my_tiles; ++it) issue(it);
+        for (uint32_t it = 0; it + NB < my_tiles; ++it) {
+            mbar_wait(&buf_free[it % NB], (it / NB) & 1);
+            SEGHDC_TR(5, it);
+            issue(it + NB);
+        }
+        end_barrier();
+        return;
+    }
+
+    if (warp == NMW + NRW) {
+        // ----------------------------------------------------------------------- epilogue warp
         const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
         uint32_t changed = 0, cnt1 = 0, total = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
@@ -757,6 +790,7 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
             const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
             const uint32_t npx = uint32_t(umin64(TP, n - px0));
             mbar_wait(&part_full[pb], (it >> 1) & 1);
+            SEGHDC_TR(3, it);
             const int32_t* pp = part + size_t(pb) * NMW * TP * 8 + lane * 8;
             int32_t col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
@@ -766,8 +800,8 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
                 col[0] += lo.x; col[1] += lo.y; col[2] += lo.z; col[3] += lo.w;
                 col[4] += hi.x; col[5] += hi.y; col[6] += hi.z; col[7] += hi.w;
             }
-            // exact dots: column n = 4*c + plane, 7-bit planes (MMA scales already removed). The
-            // fused kernel runs K*P <= 8, so K == 2 means P == 4; K == 1 needs no dots at all.
+            // exact dots: column n = 4*c + plane (MMA scale already removed). K*P <= 8 here, so
+            // K == 2 means P == 4; K == 1 needs no dots at all.
             const unsigned long long d0 = (unsigned long long)uint32_t(col[0]) +
                                           ((unsigned long long)uint32_t(col[1]) << kPlaneBits) +
                                           ((unsigned long long)uint32_t(col[2]) << (2 * kPlaneBits)) +
@@ -776,11 +810,7 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
                                           ((unsigned long long)uint32_t(col[5]) << kPlaneBits) +
                                           ((unsigned long long)uint32_t(col[6]) << (2 * kPlaneBits)) +
                                           ((unsigned long long)uint32_t(col[7]) << (3 * kPlaneBits));
-#if SEGHDC_EXP == 2
-            const uint32_t best = uint32_t(d0 & 1) & (n2_0 == 7);
-#else
             const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
-#endif
             const bool live = lane < npx;
             const uint32_t old = s_old[b * TP + lane];
             if (live) {
@@ -792,15 +822,11 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
             if constexpr (UPD) {
                 const bool take = do_update && live && best == upd_c;
                 const uint32_t m = __ballot_sync(0xffffffffu, take);
-                if (take) s_list[pb * TP + __popc(m & ((1u << lane) - 1))] = lane;
-                if (lane == 0) s_listn[pb] = __popc(m);
+                if (take) s_list[b * TP + __popc(m & ((1u << lane) - 1))] = lane;
+                if (lane == 0) s_listn[b] = __popc(m);
             }
-            mbar_arrive(&list_ready[pb]);
-            // refill the buffer of tile it-1 (its re-bundling follows this tile's k-loop)
-            if (it >= 1 && it - 1 + NB < my_tiles) {
-                mbar_wait(&buf_free[(it - 1) % NB], ((it - 1) / NB) & 1);
-                issue(it - 1 + NB);
-            }
+            mbar_arrive(&list_ready[b]);
+            SEGHDC_TR(4, it);
         }
         for (int o = 16; o; o >>= 1) {
             changed += __shfl_xor_sync(0xffffffffu, changed, o);
@@ -811,70 +837,79 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
             if (total - cnt1) atomicAdd(tail, total - cnt1);
             if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
         }
+        end_barrier();
+        return;
+    }
+
+    if (warp >= NMW) {
+        // --------------------------------------------------------------------------- fold warps
+        const uint32_t rt = tid - NMW * 32;
+        const uint32_t cpt = (W32 + NRT - 1) / NRT;
+        BitCounter<UPD ? H : 1> cnt[CPTMAX];
+        if constexpr (UPD)
+#pragma unroll
+            for (int c = 0; c < CPTMAX; ++c) cnt[c].reset();
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t b = it % NB;
+            mbar_wait(&list_ready[b], (it / NB) & 1);
+            if constexpr (UPD) {
+                if (do_update) {
+                    const uint32_t m = s_listn[b];
+                    const uint32_t* T = tiles + b * tile_words;
+                    const uint32_t* L = s_list + b * TP;
+#pragma unroll
+                    for (int c = 0; c < CPTMAX; ++c) {
+                        const uint32_t colw = rt + c * NRT;
+                        if (uint32_t(c) < cpt && colw < W32) {
+                            for (uint32_t e = 0; e < m; e += 16) {
+                                uint32_t x[16];
+#pragma unroll
+                                for (int u = 0; u < 16; ++u) x[u] = (e + u < m) ? T[size_t(L[e + u]) * SS + colw] : 0u;
+                                cnt[c].add16(x);
+                            }
+                        }
+                    }
+                }
+            }
+            if (warp == NMW) SEGHDC_TR(6, it);
+            mbar_arrive(&buf_free[b]);
+        }
+        end_barrier();
+        if constexpr (UPD) {
+            if (do_update) {
+#pragma unroll
+                for (int c = 0; c < CPTMAX; ++c)
+                    if (uint32_t(c) < cpt)
+                        flush_warp_atomic(cnt[c], tiles + (rt >> 5) * (32 * 33), xchg + size_t(upd_c) * Dp,
+                                          (rt & ~31u) + c * NRT, W32);
+            }
+        }
         return;
     }
 
     // ---------------------------------------------------------------------- MMA warps
     const uint32_t g8 = lane >> 2, q = lane & 3;
-    uint32_t breg[BSM ? 1 : WPW][2];
-    const uint2* sBw = sB + size_t(warp) * WPW * 32 + lane;  // this warp's slice (BSM)
-    if constexpr (BSM) {
-        for (int kk = 0; kk < WPW; ++kk) {
-            const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
-            sB[(size_t(warp) * WPW + kk) * 32 + lane] = make_uint2(uint32_t(v), uint32_t(v >> 32));
-        }
-        __syncwarp();
-    } else {
+    uint32_t breg[WPW][2];
 #pragma unroll
-        for (int kk = 0; kk < WPW; ++kk) {
-            const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
-            breg[kk][0] = uint32_t(v);
-            breg[kk][1] = uint32_t(v >> 32);
-        }
+    for (int kk = 0; kk < WPW; ++kk) {
+        const uint64_t v = bfrag[(size_t(warp) * WPW + kk) * 32 + lane];
+        breg[kk][0] = uint32_t(v);
+        breg[kk][1] = uint32_t(v >> 32);
     }
     const uint32_t wbase = warp * WPW;
     const uint32_t pw4[4] = {1u, opaque(4u), opaque(16u), opaque(64u)};  // shifts 0, 2, 4, 6
-    BitCounter<UPD ? H : 1> cnt[CPT];
-    if constexpr (UPD)
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) cnt[c].reset();
-
-    auto rebundle = [&](uint32_t jt) {  // fold tile jt's update list into the counters
-        const uint32_t pb = jt & 1, b = jt % NB;
-        mbar_wait(&list_ready[pb], (jt >> 1) & 1);
-        if constexpr (UPD) {
-            if (do_update) {
-                const uint32_t m = s_listn[pb];
-                const uint32_t* T = tiles + b * tile_words;
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) {
-                    const uint32_t colw = tid + c * NMW * 32;
-                    if (colw < W32) {
-                        for (uint32_t e = 0; e < m; e += 16) {
-                            uint32_t x[16];
-#pragma unroll
-                            for (int u = 0; u < 16; ++u)
-                                x[u] = (e + u < m) ? T[size_t(s_list[pb * TP + e + u]) * SS + colw] : 0u;
-                            cnt[c].add16(x);
-                        }
-                    }
-                }
-            }
-        }
-        mbar_arrive(&buf_free[b]);
-    };
 
     for (uint32_t it = 0; it < my_tiles; ++it) {
         const uint32_t b = it % NB, pb = it & 1;
         mbar_wait(&full[b], (it / NB) & 1);
-        const uint32_t* T = tiles + b * tile_words;
+        if (warp == 0) SEGHDC_TR(1, it);
+        SEGHDC_TR(8 + 2 * warp, it);
+        const uint32_t* Tq = tiles + b * tile_words + wbase + q;
         int acc[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) acc[mt][r] = 0;
-        const uint32_t* Tq = T + wbase + q;
-#if SEGHDC_EXP != 1
 #pragma unroll
         for (int k4 = 0; k4 < WPW / 4; ++k4) {
             uint32_t sl[MT][4], sh[MT][4];  // row words shifted by 0, 2, 4, 6
@@ -891,80 +926,61 @@ __global__ void __launch_bounds__((NMW + 1) * 32, 1)
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
                 const int kk = 4 * k4 + 2 * pr;
-                uint32_t bu0, bu1, bs0, bs1;
-                if constexpr (BSM) {
-                    const uint2 u = sBw[kk * 32], v = sBw[(kk + 1) * 32];
-                    bu0 = u.x; bu1 = u.y; bs0 = v.x; bs1 = v.y;
-                } else {
-                    bu0 = breg[kk][0]; bu1 = breg[kk][1]; bs0 = breg[kk + 1][0]; bs1 = breg[kk + 1][1];
-                }
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     uint32_t a[4];
                     unpack_pair(a, sl[mt][2 * pr], sh[mt][2 * pr], sl[mt][2 * pr + 1], sh[mt][2 * pr + 1]);
-                    imma16832(acc[mt], a, bu0, bu1);
-                    imma16832_s8(acc[mt], a, bs0, bs1);
+                    imma16832(acc[mt], a, breg[kk][0], breg[kk][1]);
+                    imma16832_s8(acc[mt], a, breg[kk + 1][0], breg[kk + 1][1]);
                 }
             }
         }
-#endif
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[mt][r] = int(uint32_t(acc[mt][r]) >> 8);  // scale 256 (exact)
+        if (warp == 0) SEGHDC_TR(2, it);
+        if (warp == NMW - 1) SEGHDC_TR(7, it);
+        SEGHDC_TR(9 + 2 * warp, it);
+        mbar_arrive(&buf_free[b]);  // this warp is done reading the tile
+        if (it >= 2) mbar_wait(&list_ready[(it - 2) % NB], ((it - 2) / NB) & 1);  // part[pb] consumed
         int32_t* pw = part + (size_t(pb) * NMW + warp) * TP * 8;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-            int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;
-            *reinterpret_cast<int2*>(row0) = make_int2(acc[mt][0], acc[mt][1]);
-            *reinterpret_cast<int2*>(row0 + 64) = make_int2(acc[mt][2], acc[mt][3]);
+            int32_t* row0 = pw + (16 * mt + g8) * 8 + 2 * q;  // scale 256 removed (exact)
+            *reinterpret_cast<int2*>(row0) = make_int2(int(uint32_t(acc[mt][0]) >> 8), int(uint32_t(acc[mt][1]) >> 8));
+            *reinterpret_cast<int2*>(row0 + 64) =
+                make_int2(int(uint32_t(acc[mt][2]) >> 8), int(uint32_t(acc[mt][3]) >> 8));
         }
         mbar_arrive(&part_full[pb]);
-        if (it >= 1) rebundle(it - 1);
     }
-    if (my_tiles >= 1) rebundle(my_tiles - 1);
-    if constexpr (UPD) {
-        if (do_update) {
-            // every tile consumed: the ring is free to serve as the transpose scratch
-            asm volatile("bar.sync 1, %0;" ::"r"(NMW * 32));
-#pragma unroll
-            for (int c = 0; c < CPT; ++c)
-                flush_warp_atomic(cnt[c], tiles + warp * (32 * 33), xchg + size_t(upd_c) * Dp,
-                                  warp * 32 + c * NMW * 32, W32);
-        }
-    }
+    end_barrier();
 }
 
-size_t w1_smem_bytes(uint32_t SS, uint32_t nmw, uint32_t wpw, bool bsm) {
-    const uint32_t TP = 32, NB = bsm ? 3 : 4;
+size_t fused_smem_bytes(uint32_t SS, uint32_t nmw, uint32_t nrw) {
+    const uint32_t TP = 32, NB = 4;
     size_t b = (NB * size_t(TP) * SS + 32) * 4;  // tile ring + overrun slack
-    if (bsm) b += size_t(nmw) * wpw * 32 * 8;    // B fragments
     b += NB * TP * 4;                            // s_old
     b += 2 * size_t(nmw) * TP * 8 * 4;           // part
-    b += (2 * TP + 2 + 2) * 4;                   // s_list, s_listn, s_misc
-    b += (2 * NB + 4) * 8;                       // mbarriers
-    return std::max<size_t>(b, size_t(nmw) * 32 * 33 * 4);
+    b += (NB * TP + NB + 2) * 4;                 // s_list, s_listn, s_misc
+    b += (3 * NB + 2) * 8 + 8;                   // mbarriers (+ alignment)
+    return std::max<size_t>(b, size_t(nrw) * 32 * 33 * 4);
 }
 
-template <int WPW, bool UPD, int H, int NMW, int CPT>
-static cudaError_t launch_w1_t(const RoundArgs& a, cudaStream_t s) {
-    const bool bsm = a.bsm;
-    auto kern = bsm ? k_round_w1<WPW, UPD, H, NMW, CPT, true> : k_round_w1<WPW, UPD, H, NMW, CPT, false>;
-    const size_t smem = w1_smem_bytes(a.SS, NMW, WPW, bsm);
+template <int WPW, bool UPD, int H, int NMW, int NRW>
+static cudaError_t launch_fused_t(const RoundArgs& a, cudaStream_t s) {
+    auto kern = k_round_fused<WPW, UPD, H, NMW, NRW>;
+    const size_t smem = fused_smem_bytes(a.SS, NMW, NRW);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    kern<<<a.ctas, (NMW + 1) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.P, a.bfrag, a.labels, a.state,
-                                              a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
+    kern<<<a.ctas, (NMW + NRW + 2) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.bfrag, a.labels, a.state,
+                                                    a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
     return cudaGetLastError();
 }
 
-template <int WPW, int NMW, int CPT>
-static cudaError_t launch_w1_h(const RoundArgs& a, cudaStream_t s) {
-    if (a.K != 2) return launch_w1_t<WPW, false, 1, NMW, CPT>(a, s);
+template <int WPW, int NMW, int NRW>
+static cudaError_t launch_fused_h(const RoundArgs& a, cudaStream_t s) {
+    if (a.K != 2) return launch_fused_t<WPW, false, 1, NMW, NRW>(a, s);
     const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + 31) & ~uint64_t(31);
-    if (per_cta <= counter_capacity<8>()) return launch_w1_t<WPW, true, 8, NMW, CPT>(a, s);
-    if (per_cta <= counter_capacity<12>()) return launch_w1_t<WPW, true, 12, NMW, CPT>(a, s);
-    return launch_w1_t<WPW, true, 20, NMW, CPT>(a, s);
+    if (per_cta <= counter_capacity<8>()) return launch_fused_t<WPW, true, 8, NMW, NRW>(a, s);
+    if (per_cta <= counter_capacity<12>()) return launch_fused_t<WPW, true, 12, NMW, NRW>(a, s);
+    return launch_fused_t<WPW, true, 20, NMW, NRW>(a, s);
 }
 
 // Plan: which instantiation handles (K, P, D). Returns false if no kernel fits.
@@ -973,24 +989,23 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     p.nt = (K * P + 7) / 8;
     p.fused = false;
     if (p.nt == 1) {
-        // (MMA warps, words per warp): MMA warps in multiples of 4 (equal k-loop load per SM
-        // sub-partition), B fragments in 2*wpw registers, <= 2 word columns per thread in the
-        // re-bundling. SEGHDC_FUSED_WARPS forces a warp count, SEGHDC_BSM=1 B fragments in shared
-        // memory (A/B testing; measured equal or slower on B200).
-        static const uint32_t cand[][2] = {{4, 20}, {4, 28}, {4, 32}, {8, 20}, {8, 28}, {8, 32}, {12, 28},
-                                           {8, 40}, {16, 20}};
-        const char* force = getenv("SEGHDC_FUSED_WARPS");
-        if (force && !*force) force = nullptr;
+        // (MMA warps, words per warp, fold warps): MMA warps in multiples of 4 (equal k-loop
+        // load per SM sub-partition), B fragments in 2*wpw registers, fold threads own <= 4
+        // word columns.
+        // SEGHDC_FUSED=<nmw>,<nrw> forces a shape (A/B testing).
+        static const uint32_t cand[][3] = {{4, 20, 1}, {4, 28, 1}, {4, 32, 1}, {8, 20, 2}, {8, 28, 2}, {8, 32, 2},
+                                           {8, 40, 4}, {12, 28, 4}, {16, 20, 4}};
+        uint32_t f_nmw = 0, f_nrw = 0;
+        const char* force = getenv("SEGHDC_FUSED");
+        const bool forced = force && *force && sscanf(force, "%u,%u", &f_nmw, &f_nrw) == 2;
         for (const auto& c : cand) {
-            if (force && uint32_t(atoi(force)) != c[0]) continue;
-            if (c[0] * c[1] < W32 || c[0] * 64 < W32) continue;
-            const char* bs = getenv("SEGHDC_BSM");
-            const bool want_bsm = bs && *bs == '1';  // B in registers unless asked (A/B testing)
-            p.bsm = want_bsm && w1_smem_bytes(SS, c[0], c[1], true) <= smem_limit;
-            if (!p.bsm && w1_smem_bytes(SS, c[0], c[1], false) > smem_limit) continue;
+            if (forced && (c[0] != f_nmw || c[2] != f_nrw)) continue;
+            if (c[0] * c[1] < W32 || c[2] * 32 * 4 < W32) continue;
+            if (fused_smem_bytes(SS, c[0], c[2]) > smem_limit) continue;
             p.fused = true;
             p.nwarps = c[0];
             p.wpw = c[1];
+            p.nrw = c[2];
             p.w32p = c[0] * c[1];
             p.mt = 2;
             p.ntg = 1;
@@ -1013,16 +1028,17 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
     if (p.fused) {
-        switch (p.nwarps * 100 + p.wpw) {
-            case 420: return launch_w1_h<20, 4, 1>(a, s);
-            case 428: return launch_w1_h<28, 4, 1>(a, s);
-            case 432: return launch_w1_h<32, 4, 1>(a, s);
-            case 820: return launch_w1_h<20, 8, 1>(a, s);
-            case 828: return launch_w1_h<28, 8, 1>(a, s);
-            case 832: return launch_w1_h<32, 8, 1>(a, s);
-            case 840: return launch_w1_h<40, 8, 2>(a, s);
-            case 1228: return launch_w1_h<28, 12, 1>(a, s);
-            default: return launch_w1_h<20, 16, 1>(a, s);
+        switch (p.nwarps * 1000 + p.wpw * 10 + p.nrw) {
+            case 4201: return launch_fused_h<20, 4, 1>(a, s);
+            case 4281: return launch_fused_h<28, 4, 1>(a, s);
+            case 4321: return launch_fused_h<32, 4, 1>(a, s);
+            case 8202: return launch_fused_h<20, 8, 2>(a, s);
+            case 8282: return launch_fused_h<28, 8, 2>(a, s);
+            case 8322: return launch_fused_h<32, 8, 2>(a, s);
+            case 12284: return launch_fused_h<28, 12, 4>(a, s);
+            case 8404: return launch_fused_h<40, 8, 4>(a, s);
+            case 16204: return launch_fused_h<20, 16, 4>(a, s);
+            default: return cudaErrorInvalidConfiguration;
         }
     }
     switch (p.mt) {
@@ -1032,4 +1048,7 @@ cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s)
     }
 }
 
+#ifdef SEGHDC_TRACE
+void read_trace(void* dst) { cudaMemcpyFromSymbol(dst, g_trace, sizeof(g_trace)); }
+#endif
 }  // namespace seghdc_dev
