@@ -83,6 +83,7 @@ struct RoundPlan {
     uint32_t w32p = 0;         // words covered by the B-fragment layout (>= W32)
     bool fused = false;        // one n-tile: warp-specialised kernel (+ fused accumulation when K == 2)
     uint32_t nrw = 0;          // fused: dedicated re-bundling warps (0: the MMA warps re-bundle)
+    bool tc = false;           // tcgen05 kernel (seghdc_tc.cu) instead of the IMMA kernels
 };
 struct RoundArgs {
     const uint32_t* grid;
@@ -96,9 +97,24 @@ struct RoundArgs {
     int32_t* xchg;  // [K*Dp sums | K counts | changed], zeroed before the round
     uint32_t Dp;
     uint32_t ctas;
+    // tcgen05 kernel only
+    const void* tmap;     // CUtensorMap of the grid (tc_make_grid_map)
+    const uint8_t* bimg;  // centroid B image (launch_build_bimg)
+    uint32_t nks;         // k-steps of 64 HV dims (tc_ksteps)
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
+
+// tcgen05 round kernel (seghdc_tc.cu)
+bool tc_supported(uint32_t W32);
+uint32_t tc_ksteps(uint32_t W32);
+size_t tc_smem_bytes(uint32_t W32);
+size_t tc_bimg_bytes(uint32_t W32);
+uint32_t tc_tile_pixels();
+bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32);
+void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint8_t* bimg,
+                       const void* state, cudaStream_t s);
+cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s);
 
 }  // namespace seghdc_dev

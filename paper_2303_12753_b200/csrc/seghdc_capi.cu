@@ -96,6 +96,8 @@ struct seghdc_ctx {
     RoundPlan plan;
     uint32_t round_ctas = 0;
     DevBuf<uint8_t> state, bfrag;
+    DevBuf<uint8_t> bimg;                     // tcgen05 kernel: centroid B image
+    alignas(64) unsigned char tmap[128] = {};  // tcgen05 kernel: CUtensorMap of the grid
     DevBuf<uint32_t> labels, Z;
     DevBuf<int32_t> xchg;
     DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
@@ -241,7 +243,8 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = 0) {
         throw Error(SEGHDC_ERUNTIME, "dim " + std::to_string(g.D) + " does not fit the round kernel's shared memory");
     x.K = K;
     const uint64_t n = x.n_local();
-    const uint64_t tp = 16ull * x.plan.mt;
+    if (x.plan.tc && !tc_make_grid_map(x.tmap, x.grid.p, n, g.S32)) x.plan.tc = false;  // no driver entry point
+    const uint64_t tp = x.plan.tc ? tc_tile_pixels() : 16ull * x.plan.mt;
     x.round_ctas = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(x.sms, (n + tp - 1) / tp)));
     const uint32_t NT = x.plan.nt;
     x.state.ensure(StateView::bytes(uint32_t(K)));
@@ -250,6 +253,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = 0) {
     // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
     x.bfrag.ensure(size_t(NT) * x.plan.w32p * 32 * 8);
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
+    if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(g.W32));
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
     x.colsum.ensure(g.Dp);
     x.seeds.ensure(std::max<size_t>(K, 1));
@@ -319,6 +323,11 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.early_stop = x.early_stop;
     launch_finish(f, x.stream);
     x.count(2);
+    if (x.plan.tc) {
+        launch_build_bimg(x.Z.p, uint32_t(x.K), x.planes, x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr,
+                          x.stream);
+        x.count();
+    }
     x.check_launch();
 }
 
@@ -377,6 +386,9 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.xchg = x.xchg.p;
     a.Dp = x.g.Dp;
     a.ctas = x.round_ctas;
+    a.tmap = x.tmap;
+    a.bimg = x.bimg.p;
+    a.nks = tc_ksteps(x.g.W32);
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     cudaEvent_t ev_end = nullptr;
@@ -823,4 +835,16 @@ void read_trace(void* dst);
 }
 // diagnostic build only: 148 x 64 x 8 u64 clock64() stamps of the fused round kernel
 extern "C" void seghdc_debug_trace(void* dst) { seghdc_dev::read_trace(dst); }
+namespace seghdc_dev {
+void read_trace_tc(void* dst);
+}
+extern "C" void seghdc_debug_trace_tc(void* dst) { seghdc_dev::read_trace_tc(dst); }
+#endif
+
+#ifdef SEGHDC_HANGDBG
+namespace seghdc_dev {
+void* setup_hang();
+}
+// diagnostic build only: host-mapped log of timed-out barrier waits of the tcgen05 kernel
+extern "C" void* seghdc_debug_hang_setup() { return seghdc_dev::setup_hang(); }
 #endif

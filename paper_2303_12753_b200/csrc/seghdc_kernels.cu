@@ -988,6 +988,12 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     p.nwarp_words = (W32 + 31) / 32;
     p.nt = (K * P + 7) / 8;
     p.fused = false;
+    p.tc = false;
+    const char* tcenv = getenv("SEGHDC_TC");
+    if (K * P <= 8 && !(tcenv && *tcenv == '0') && tc_supported(W32) && tc_smem_bytes(W32) <= smem_limit) {
+        // tcgen05 kernel; the IMMA plan below stays valid as the fallback (bfrag layout)
+        p.tc = true;
+    }
     if (p.nt == 1) {
         // (MMA warps, words per warp, fold warps): MMA warps in multiples of 4 (equal k-loop
         // load per SM sub-partition), B fragments in 2*wpw registers, fold threads own <= 4
@@ -1027,6 +1033,7 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 }
 
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s) {
+    if (p.tc) return launch_round_tc(a, s);
     if (p.fused) {
         switch (p.nwarps * 1000 + p.wpw * 10 + p.nrw) {
             case 4201: return launch_fused_h<20, 4, 1>(a, s);

@@ -1,0 +1,586 @@
+// tcgen05 round kernel: assign_labels (clusterer.cpp:132-162) fused with the accumulation of
+// update_centroids (clusterer.cpp:164-188) on the 5th-generation tensor cores.
+//
+// Per CTA (one per SM) and per tile of 128 pixels (the MMA's M):
+//   producer warp   2-D TMA (cp.async.bulk.tensor, 128B swizzle) of 128 pixel rows x 32 words
+//                   ("chunk") into an NSTAGE-deep smem ring; once, the centroid B image.
+//   unpack warps    2 per TMEM lane quarter: thread = pixel row. Each 32-bit HV word becomes
+//                   four A registers (w << 2e) & 0xC0C0C0C0 - two HV bits per 8-bit k-slot,
+//                   the pair packing of kernels.cuh - stored to TMEM with tcgen05.st (A lives
+//                   in TMEM, double-buffered per chunk).
+//   MMA thread      per k-step of 64 HV dims: tcgen05.mma.kind::i8 M128 N8 K32 twice on the
+//                   same A - unsigned against Bu = 2*z6 + z7, signed against Bs = 2*z6 - z7 -
+//                   accumulating 256 * (exact plane dots) in a TMEM s32 accumulator;
+//                   tcgen05.commit frees the A buffer / publishes the tile's D.
+//   epilogue warps  one per lane quarter: tcgen05.ld of the 8 accumulator columns of its
+//                   pixel, exact u64 dots, 128-bit argmax, labels, counts, update list.
+//   fold warps      the pixels of the updated cluster (update list) are folded into
+//                   Harley-Seal counters, thread = word column, reading the rows back from
+//                   L2 (the tile streamed through moments before).
+// All hand-offs are mbarriers; the counters and counts leave through the exchange buffer
+// exactly as in the IMMA kernel (seghdc_kernels.cu), so results are bit-identical.
+#include <cuda.h>
+
+#include "kernels.cuh"
+#include "launch.h"
+
+namespace seghdc_dev {
+namespace {
+
+constexpr uint32_t kTP = 128;      // pixels per tile (MMA M)
+constexpr uint32_t kCW = 32;       // HV words per chunk (one 128-byte swizzle span per row)
+constexpr uint32_t kKS = kCW / 2;  // k-steps (64 HV dims) per chunk
+constexpr uint32_t kStages = 9;    // smem ring depth (16 KB each); a multiple of kUW, so slot g % kStages
+                                   // is always unpacked by warp g % kUW (mbarrier phases stay in order)
+constexpr uint32_t kChunkBytes = kTP * kCW * 4;
+constexpr uint32_t kUW = 3;        // unpack warps per TMEM lane quarter (chunk g goes to warp g % kUW)
+constexpr uint32_t kAB = 3;        // A buffers in TMEM (128 columns each)
+static_assert(kStages % kUW == 0 && kAB == kUW, "unpack warp u owns ring slots and A buffers == u mod kUW");
+constexpr uint32_t kN = 8;         // accumulator columns: 2 clusters x 4 planes
+// warp layout (SM sub-partition = warp % 4): [0, 12) unpack (3 per lane quarter), [12, 16)
+// epilogue (one per lane quarter), 16/17/21/22 fold, 18/19 MMA issue (sub-partitions 2 and 3,
+// away from the producer), 20 producer. Two MMA-issuing warps split the chunks of a tile
+// (even / odd) into two accumulators, halving the issue load on any one sub-partition.
+constexpr uint32_t kWEpi = 4 * kUW, kWMma0 = 18, kWProd = 20, kWarps = 23, kNRW = 4;
+static_assert(kWEpi == 12, "warp layout assumes 12 unpack warps");
+__device__ __forceinline__ int fold_index(uint32_t warp) {
+    return warp == 16 ? 0 : warp == 17 ? 1 : warp == 21 ? 2 : warp == 22 ? 3 : -1;
+}
+// TMEM columns: A buffers [128*i, 128*i+128), then accumulators D[tile parity][MMA warp]
+// (8 columns each)
+constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB;
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// One chunk (kKS k-steps) of MMAs, issued by an elected lane of the calling warp from a single
+// asm block: addresses advance inside PTX, so the whole block runs on the uniform datapath
+// (one tcgen05.mma every ~10 cycles instead of ~45 with per-MMA operand conversion).
+// Per k-step: u8 MMA with B block 2kg (Bu), s8 MMA with B block 2kg+1 (Bs), same A columns.
+#define SEGHDC_KSTEP                                                                    \
+    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"                     \
+    "add.u64 b, b, 16;\n\t"                                                             \
+    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %4, q;\n\t"                     \
+    "add.u64 b, b, 16;\n\tadd.u32 a, a, 8;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+__device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idu, uint32_t ids,
+                                             uint32_t accum) {
+    static_assert(kKS == 16, "tc_mma_chunk issues 16 k-steps");
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.ne.b32 q, 1, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
+            SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
+                SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
+        "r"(a_t), "l"(bdesc), "r"(idu), "r"(ids), "r"(accum)
+        : "memory");
+}
+#undef SEGHDC_KSTEP
+// commit all prior MMAs of the calling thread to an mbarrier (elected lane)
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+// smem matrix descriptor: K-major, no swizzle, core matrices of 8 rows x 16 B; LBO = 128 (next
+// core matrix along K), SBO = 256 (next 8 rows), version 1 (tcgen05)
+__device__ __forceinline__ uint64_t bdesc_at(uint32_t saddr) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor kind::i8: D s32 (bits 4-5 = 2), A/B signedness (bits 7, 10), both
+// K-major, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t idesc_i8(bool sgn, uint32_t n, uint32_t m) {
+    return (2u << 4) | (uint32_t(sgn) << 7) | (uint32_t(sgn) << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+#ifdef SEGHDC_HANGDBG
+// diagnostic build only: bounded mbarrier waits. Timeouts are logged (block, warp, barrier id,
+// parity, iteration) into host-mapped memory, then the kernel traps, so the log survives.
+__device__ unsigned int* g_hang;  // [0] count, then 5 words per record
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t id, uint32_t it) {
+    uint32_t ok = 0;
+    for (uint32_t round = 0; round < 4 && !ok; ++round) {
+        for (uint32_t i = 0; i < (1u << 22) && !ok; ++i)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (!ok && round == 0 && (threadIdx.x & 31) == 0) {  // log once, keep waiting so others log too
+            const unsigned k = atomicAdd(&g_hang[0], 1u);
+            if (k < 200) {
+                volatile unsigned* r = g_hang + 1 + 5 * k;
+                r[0] = blockIdx.x; r[1] = threadIdx.x >> 5; r[2] = id; r[3] = parity; r[4] = it;
+                __threadfence_system();
+            }
+        }
+    }
+    if (!ok) asm volatile("trap;");
+}
+#define TCW(id, it, bar, par) (PRG((id) * 100000 + (it)), tc_wait(bar, par, id, it), PRG((id) * 100000 + (it) + 50000))
+// per-warp progress of block 0 (host-mapped): last code written by lane 0
+#define PRG(code) ((blockIdx.x == 0 && (threadIdx.x & 31) == 0) ? (void)(((volatile unsigned*)g_hang)[4096 + (threadIdx.x >> 5)] = (code)) : (void)0)
+#else
+#define TCW(id, it, bar, par) mbar_wait(bar, par)
+#define PRG(code) ((void)0)
+#endif
+
+struct TcSmem {
+    static constexpr size_t ring = 0;  // [kStages][128][32] u32, 1024-aligned (128B swizzle)
+    __host__ __device__ static size_t b(uint32_t nks) { return size_t(kStages) * kChunkBytes; }                   // [2*nks][kN*32] B image
+    __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * 2 * kN * 32; }           // [2][4][32] u32
+    __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + 2 * 4 * 32 * 4; }                   // [2][4] u32
+    __host__ __device__ static size_t misc(uint32_t nks) { return listn(nks) + 2 * 4 * 4; }                        // tmem base, skip
+    __host__ __device__ static size_t bars(uint32_t nks) { return (misc(nks) + 16 + 7) & ~size_t(7); }
+    static constexpr uint32_t nbars = 2 * kStages + 3 * kAB + 2 + 2 + 2 + 2 + 1;
+    __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
+};
+
+}  // namespace
+
+#ifdef SEGHDC_TRACE
+__device__ unsigned long long g_trace_tc[148 * 64 * 8];
+#define TC_TR(ev, it)                                                                 \
+    do {                                                                              \
+        if (lane == 0 && blockIdx.x < 148 && (it) < 64)                               \
+            g_trace_tc[(size_t(blockIdx.x) * 64 + (it)) * 8 + (ev)] = clock64();      \
+    } while (0)
+void read_trace_tc(void* dst) { cudaMemcpyFromSymbol(dst, g_trace_tc, sizeof(g_trace_tc)); }
+// kernel-level events in slot 63 with %globaltimer (ns, comparable across SMs)
+#define TC_TG(ev)                                                                     \
+    do {                                                                              \
+        if (lane == 0 && blockIdx.x < 148) {                                          \
+            unsigned long long t_;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+            g_trace_tc[(size_t(blockIdx.x) * 64 + 63) * 8 + (ev)] = t_;               \
+        }                                                                             \
+    } while (0)
+// accumulated wait cycles in slot 62: 0 unpack slot_full, 1 unpack a_free, 2 MMA a_full,
+// 3 MMA issue (wait-free part), 4 producer slot_free, 5 epilogue d_full
+#define TC_ACC(ev, cyc)                                                               \
+    do {                                                                              \
+        if (lane == 0 && blockIdx.x < 148)                                            \
+            atomicAdd(&g_trace_tc[(size_t(blockIdx.x) * 64 + 62) * 8 + (ev)], (cyc));  \
+    } while (0)
+#define TC_CLK(v) const unsigned long long v = clock64()
+#else
+#define TC_TR(ev, it) ((void)0)
+#define TC_TG(ev) ((void)0)
+#define TC_ACC(ev, cyc) ((void)0)
+#define TC_CLK(v) ((void)0)
+#endif
+
+template <bool UPD, int H>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
+               uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
+               void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
+    constexpr uint32_t NRT = kNRW * 32;
+    constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
+    extern __shared__ __align__(1024) uint8_t smem[];
+    StateView st = StateView::at(state, K);
+    if (st.hdr->done) return;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t parity = round & 1;
+    uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
+    if (warp == 0) TC_TG(0);
+    uint8_t* ring = smem + TcSmem::ring;
+    uint8_t* sB = smem + TcSmem::b(nks);
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + TcSmem::list(nks));
+    uint32_t* s_listn = reinterpret_cast<uint32_t*>(smem + TcSmem::listn(nks));
+    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + TcSmem::misc(nks));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TcSmem::bars(nks));
+    uint64_t* slot_full = bars;                 // [kStages] TMA landed
+    uint64_t* slot_free = bars + kStages;       // [kStages] unpack warps read the chunk
+    // a_full[ab][m]: chunk g (buffer ab = g % kAB) written for MMA warp m = g % 2. One barrier
+    // per (buffer, consumer) keeps every parity wait in order (a shared barrier consumed by two
+    // warps alternately would alias phases)
+    uint64_t* a_full = bars + 2 * kStages;      // [kAB][2] A buffer written (tcgen05.st)
+    uint64_t* a_free = a_full + 2 * kAB;        // [kAB] MMAs on the A buffer done (commit)
+    uint64_t* d_full = a_free + kAB;            // [2] tile accumulator complete (commit)
+    uint64_t* d_free = d_full + 2;              // [2] epilogue read the accumulator
+    uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
+    uint64_t* list_free = list_ready + 2;       // [2] fold warps done with the list
+    uint64_t* b_full = list_free + 2;           // B image landed
+
+    const uint32_t nch = (W32 + kCW - 1) / kCW;  // chunks per tile
+    const uint64_t ntiles = (n + kTP - 1) / kTP;
+    const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+    if (tid == 0) {
+        for (uint32_t s = 0; s < kStages; ++s) {
+            mbar_init(&slot_full[s], 1);
+            mbar_init(&slot_free[s], 4 * 32);
+        }
+        for (uint32_t b = 0; b < kAB; ++b) {
+            mbar_init(&a_full[2 * b], 4 * 32);
+            mbar_init(&a_full[2 * b + 1], 4 * 32);
+            mbar_init(&a_free[b], 1);
+        }
+        for (uint32_t b = 0; b < 2; ++b) {
+            mbar_init(&d_full[b], 2);  // both MMA warps commit
+            mbar_init(&d_free[b], 4 * 32);
+            mbar_init(&list_ready[b], 4 * 32);
+            mbar_init(&list_free[b], NRT);
+        }
+        mbar_init(b_full, 1);
+        mbar_fence_init();
+        s_misc[1] = pick_skip(st.cur + parity * K, K);
+    }
+    if (warp == kWMma0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_misc)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = s_misc[0];
+    const uint32_t upd_c = 1 - s_misc[1];  // K == 2 under UPD
+    if (warp == 0) TC_TG(1);
+    const bool folding = UPD && do_update;
+
+    if (warp < kWEpi) {
+        // ------------------------------------------------------------------------ unpack warps
+        // warp (qd, u) unpacks the 32 rows of lane quarter qd of every chunk g with
+        // g % kUW == u, so kUW chunks are in flight per quarter (each warp's chain of LDS ->
+        // masks -> tcgen05.st -> wait::st is latency-bound)
+        const uint32_t qd = warp & 3, u = warp >> 2;  // lane quarter, chunk phase
+        const uint32_t r = 32 * qd + lane;            // pixel row of the tile
+        const uint32_t lane_addr = tbase + ((32 * qd) << 16);
+        const uint32_t nchunks = my_tiles * nch;
+        for (uint32_t g = u; g < nchunks; g += kUW) {
+            const uint32_t s = g % kStages, ab = g % kAB;
+            TC_CLK(c0);
+            TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
+            TC_CLK(c1);
+            if (warp == 0 && g == 0) TC_TG(3);
+            TCW(2, g, &a_free[ab], ((g / kAB) & 1) ^ 1);
+            __syncwarp();  // lanes leave the spin loops independently; tcgen05.st is .sync.aligned
+            TC_CLK(c2);
+            if (warp == 0) { TC_ACC(0, c1 - c0); TC_ACC(1, c2 - c1); }
+            tc_fence_after();
+            if (warp == 0 && g % nch == 0) TC_TR(1, g / nch);
+            const uint8_t* row = ring + size_t(s) * kChunkBytes + r * 128;
+#pragma unroll
+            for (uint32_t c16 = 0; c16 < 8; ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
+                const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+                uint32_t a[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) a[4 * i + e] = (w4[i] << (2 * e)) & 0xC0C0C0C0u;
+                tc_st16(lane_addr + ab * 128 + c16 * 16, a);  // k-steps 2*c16, 2*c16+1: 8 columns each
+            }
+            PRG(10 * 100000 + g);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            PRG(11 * 100000 + g);
+            mbar_arrive(&slot_free[s]);
+            tc_fence_before();
+            mbar_arrive(&a_full[2 * ab + (g & 1)]);
+            if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
+        }
+    } else if (warp < kWEpi + 4) {
+        // ---------------------------------------------------------------------- epilogue warps
+        const uint32_t qd = warp & 3;
+        const uint32_t lane_addr = tbase + ((32 * qd) << 16);
+        const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
+        uint32_t changed = 0, cnt1 = 0, total = 0;
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t db = it & 1;
+            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * kTP;
+            const uint64_t px = px0 + 32 * qd + lane;
+            const bool live = px < n;
+            const uint32_t old = live ? labels[px] : 0u;
+            TC_CLK(c0);
+            TCW(3, it, &d_full[db], (it >> 1) & 1);
+            __syncwarp();  // converge before the .sync.aligned tcgen05.ld
+            TC_CLK(c1);
+            if (qd == 0) TC_ACC(5, c1 - c0);
+            tc_fence_after();
+            if (qd == 0) TC_TR(4, it);
+            uint32_t col[8], col2[8];
+            tc_ld8(lane_addr + kColD + 16 * db, col);
+            tc_ld8(lane_addr + kColD + 16 * db + 8, col2);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) col[c] += col2[c];
+            tc_fence_before();
+            mbar_arrive(&d_free[db]);
+            // exact dots: column n = 4*c + plane, scale 256 removed (exact). K == 2 here means P == 4.
+            unsigned long long d[2] = {0, 0};
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl)
+                    d[c] += (unsigned long long)(col[4 * c + pl] >> 8) << (kPlaneBits * pl);
+            const uint32_t best = (K > 1 && strictly_closer(d[1], n2_1, d[0], n2_0)) ? 1u : 0u;
+            if (live) {
+                labels[px] = best;
+                changed += old != best;
+                cnt1 += best;
+                ++total;
+            }
+            TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
+            if constexpr (UPD) {
+                const bool take = do_update && live && best == upd_c;
+                const uint32_t m = __ballot_sync(0xffffffffu, take);
+                if (take) s_list[(db * 4 + qd) * 32 + __popc(m & ((1u << lane) - 1))] = 32 * qd + lane;
+                if (lane == 0) s_listn[db * 4 + qd] = __popc(m);
+            }
+            mbar_arrive(&list_ready[db]);
+            if (qd == 0) TC_TR(5, it);
+        }
+        for (int o = 16; o; o >>= 1) {
+            changed += __shfl_xor_sync(0xffffffffu, changed, o);
+            cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
+            total += __shfl_xor_sync(0xffffffffu, total, o);
+        }
+        if (qd == 0) TC_TG(4);
+        if (lane == 0) {
+            if (changed) atomicAdd(tail + K, changed);
+            if (total - cnt1) atomicAdd(tail, total - cnt1);
+            if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
+        }
+    } else if (warp == kWMma0 || warp == kWMma0 + 1) {
+        // ------------------------------------------------------------------------ MMA warps
+        // warp m issues the chunks g = m, m+2, ... (global chunk parity) into accumulator
+        // D[db][m] of their tile; the whole warp walks the loop (barrier waits are
+        // warp-uniform), one elected lane issues inside tc_mma_chunk / tc_commit
+        constexpr uint32_t idu = idesc_i8(false, kN, kTP), ids = idesc_i8(true, kN, kTP);
+        const uint32_t m = warp - kWMma0;
+        const uint32_t b0 = smem_u32(sB);
+        TCW(5, 0, b_full, 0);
+        __syncwarp();
+        TC_TG(2);
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t db = it & 1;
+            const uint32_t d_t = tbase + kColD + 16 * db + 8 * m;
+            TCW(6, it, &d_free[db], ((it >> 1) & 1) ^ 1);
+            __syncwarp();
+            for (uint32_t ch = (it * nch + m) & 1; ch < nch; ch += 2) {  // chunks with g % 2 == m
+                const uint32_t g = it * nch + ch, ab = g % kAB;
+                TC_CLK(c0);
+                TCW(7, g, &a_full[2 * ab + m], (g / (2 * kAB)) & 1);  // g = x + 6k on this barrier
+                __syncwarp();  // converge before elect.sync / tcgen05.mma
+                TC_CLK(c1);
+                if (m == 0) TC_ACC(2, c1 - c0);
+                tc_fence_after();
+                PRG(12 * 100000 + g);
+                tc_mma_chunk(d_t, tbase + ab * 128, bdesc_at(b0 + (2 * ch * kKS) * (kN * 32)), idu, ids, ch >= 2);
+                tc_commit(&a_free[ab]);
+                PRG(13 * 100000 + g);
+                {
+                    TC_CLK(c2);
+                    if (m == 0) TC_ACC(3, c2 - c1);
+                }
+            }
+            tc_commit(&d_full[db]);
+            if (m == 0) TC_TR(3, it);
+        }
+        __syncwarp();
+    } else if (warp == kWProd) {
+        // ----------------------------------------------------------------------- producer warp
+        if (lane == 0) {
+            const uint32_t bbytes = nks * 2 * kN * 32;
+            mbar_expect_tx(b_full, bbytes);
+            bulk_g2s(sB, bimg, bbytes, b_full);
+            uint32_t g = 0;
+            for (uint32_t it = 0; it < my_tiles; ++it) {
+                const int y = int((blockIdx.x + uint64_t(it) * gridDim.x) * kTP);
+                for (uint32_t ch = 0; ch < nch; ++ch, ++g) {
+                    const uint32_t s = g % kStages;
+                    TC_CLK(c0);
+                    TCW(8, g, &slot_free[s], ((g / kStages) & 1) ^ 1);
+                    TC_CLK(c1);
+                    TC_ACC(4, c1 - c0);
+                    if (ch == 0) TC_TR(0, it);
+                    mbar_expect_tx(&slot_full[s], kChunkBytes);
+                    tma_load_2d(ring + size_t(s) * kChunkBytes, &tmap, int(ch * kCW), y, &slot_full[s]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---------------------------------------------------------------------------- fold warps
+    BitCounter<UPD ? H : 1> cnt[CPTMAX];
+    const int fw = fold_index(warp);
+    const uint32_t rt = uint32_t(fw) * 32 + lane;
+    const uint32_t cpt = (W32 + NRT - 1) / NRT;
+    if (fw >= 0) {
+        if constexpr (UPD)
+#pragma unroll
+            for (int c = 0; c < CPTMAX; ++c) cnt[c].reset();
+        for (uint32_t it = 0; it < my_tiles; ++it) {
+            const uint32_t db = it & 1;
+            TCW(9, it, &list_ready[db], (it >> 1) & 1);
+            if (fw == 0) TC_TR(6, it);
+            if constexpr (UPD) {
+                if (do_update) {
+                    const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * kTP;
+                    const uint32_t* G = grid + px0 * S32;
+#pragma unroll 1
+                    for (uint32_t qd = 0; qd < 4; ++qd) {
+                        const uint32_t m = s_listn[db * 4 + qd];
+                        const uint32_t* L = s_list + (db * 4 + qd) * 32;
+#pragma unroll
+                        for (int c = 0; c < CPTMAX; ++c) {
+                            const uint32_t colw = rt + c * NRT;
+                            if (uint32_t(c) < cpt && colw < W32) {
+                                for (uint32_t e = 0; e < m; e += 16) {
+                                    uint32_t x[16];
+#pragma unroll
+                                    for (int v = 0; v < 16; ++v)
+                                        x[v] = (e + v < m) ? __ldg(G + size_t(L[e + v]) * S32 + colw) : 0u;
+                                    cnt[c].add16(x);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            if (fw == 0) TC_TR(7, it);
+            mbar_arrive(&list_free[db]);
+        }
+    }
+    if (fw == 0) TC_TG(5);
+    // all roles done: the ring becomes the counters' transpose scratch; free TMEM
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) TC_TG(6);
+    if (fw >= 0 && folding) {
+#pragma unroll
+        for (int c = 0; c < CPTMAX; ++c)
+            if (uint32_t(c) < cpt)
+                flush_warp_atomic(cnt[c], reinterpret_cast<uint32_t*>(ring) + (rt >> 5) * (32 * 33),
+                                  xchg + size_t(upd_c) * Dp, (rt & ~31u) + c * NRT, W32);
+    }
+    if (fw == 0) TC_TG(7);
+    if (warp == kWMma0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+    }
+}
+
+// B image: for global k-step ks and variant s (0: u8 2*z6 + z7, 1: s8 2*z6 - z7), the kN x 32
+// bytes of B in the canonical K-major no-swizzle layout: core matrix cm (k-slots 16cm..16cm+15)
+// at +128*cm, row n at +16n. k-slot kappa = 4*col + j of the A register column col = 4h + e
+// (word h of the k-step, shift 2e) carries bits 8j+6-2e (weight 64) and 8j+7-2e (weight 128).
+__global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t P, uint32_t D, uint32_t nks,
+                             uint8_t* __restrict__ bimg, const void* state) {
+    if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
+    const uint32_t total = nks * 2 * kN * 32;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t blk = i / (kN * 32), rem = i % (kN * 32);
+        const uint32_t ks = blk >> 1, sgn = blk & 1;
+        const uint32_t ngrp = rem / 256, r2 = rem % 256, cm = r2 / 128, nrow = (r2 % 128) / 16, b = r2 % 16;
+        const uint32_t ncol = ngrp * 8 + nrow;  // B column = 4*cluster + plane
+        const uint32_t kappa = cm * 16 + b, colr = kappa >> 2, j = kappa & 3, h = colr >> 2, e = colr & 3;
+        const uint32_t dim6 = 32 * (2 * ks + h) + 8 * j + 6 - 2 * e;
+        uint32_t z6 = 0, z7 = 0;
+        const uint32_t c = ncol / P, pl = ncol % P;
+        if (c < K) {
+            if (dim6 < D) z6 = (Z[size_t(c) * D + dim6] >> (kPlaneBits * pl)) & 0x3Fu;
+            if (dim6 + 1 < D) z7 = (Z[size_t(c) * D + dim6 + 1] >> (kPlaneBits * pl)) & 0x3Fu;
+        }
+        bimg[i] = uint8_t(sgn ? 2 * z6 - z7 : 2 * z6 + z7);
+    }
+}
+
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+template <bool UPD, int H>
+cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
+    auto kern = k_round_tc<UPD, H>;
+    const size_t smem = tc_smem_bytes(a.W32);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<a.ctas, kWarps * 32, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(a.tmap), a.grid, a.n,
+                                                   a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round,
+                                                   a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
+    return cudaGetLastError();
+}
+}  // namespace
+
+bool tc_supported(uint32_t W32) { return W32 > kCW && W32 <= 3 * kNRW * 32; }  // >= 2 chunks: both MMA warps
+uint32_t tc_ksteps(uint32_t W32) { return ((W32 + kCW - 1) / kCW) * kKS; }
+size_t tc_smem_bytes(uint32_t W32) { return TcSmem::total(tc_ksteps(W32)); }
+size_t tc_bimg_bytes(uint32_t W32) { return size_t(tc_ksteps(W32)) * 2 * kN * 32; }
+uint32_t tc_tile_pixels() { return kTP; }
+
+bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32) {
+    EncodeFn fn = encode_fn();
+    if (!fn || rows == 0) return false;
+    const cuuint64_t dims[2] = {S32, rows};
+    const cuuint64_t strides[1] = {cuuint64_t(S32) * 4};
+    const cuuint32_t box[2] = {kCW, kTP};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(reinterpret_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+              const_cast<uint32_t*>(grid), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint8_t* bimg,
+                       const void* state, cudaStream_t s) {
+    const uint32_t nks = tc_ksteps(W32);
+    const uint32_t total = nks * 2 * kN * 32;
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, P, D, nks, bimg, state);
+}
+
+#ifdef SEGHDC_HANGDBG
+void* setup_hang() {
+    unsigned int* h = nullptr;
+    cudaHostAlloc(&h, 65536, cudaHostAllocMapped);
+    memset(h, 0, 65536);
+    unsigned int* d = nullptr;
+    cudaHostGetDevicePointer(&d, h, 0);
+    cudaMemcpyToSymbol(g_hang, &d, sizeof(d));
+    return h;
+}
+#endif
+
+cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
+    if (a.K != 2) return launch_tc_t<false, 1>(a, s);
+    const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + kTP - 1) / kTP * kTP;
+    if (per_cta <= BitCounter<8>::capacity()) return launch_tc_t<true, 8>(a, s);
+    if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12>(a, s);
+    return launch_tc_t<true, 20>(a, s);
+}
+
+}  // namespace seghdc_dev
