@@ -19,7 +19,8 @@ from typing import Callable, Optional
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libseghdc_b200.so")
+# SEGHDC_LIB selects a diagnostic build of the same library (trace / hang-debug variants)
+LIB_PATH = os.environ.get("SEGHDC_LIB") or os.path.join(PKG, "lib", "libseghdc_b200.so")
 
 SEGHDC_OK, SEGHDC_ECONFIG, SEGHDC_ERUNTIME = 0, 1, 2
 ENCODERS = {"manhattan": 0, "rpos": 1, "rcolor": 2}

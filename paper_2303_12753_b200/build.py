@@ -41,17 +41,20 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra: list[str] | None = None) -> str:
+    """Compile + link the library to ``out`` (default: the product path). ``extra`` adds nvcc
+    flags to the .cu compiles (e.g. -DSEGHDC_TRACE for a diagnostic build)."""
+    extra = list(extra or [])
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + PUBLIC_HEADERS + [__file__]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(out, deps):
+        return out
     objs = []
     logs = []
     for src in srcs:
-        obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
-        cmd = [nvcc()] + ARCH + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = out + "." + os.path.basename(src) + ".o"
+        cmd = [nvcc()] + ARCH + NVCC_FLAGS + extra + ["-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc()] + ARCH + ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-x", "c++",
                                      "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
@@ -61,20 +64,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     r = subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     for o in objs:
         os.remove(o)
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
+    with open(out + ".ptxas.log", "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=LIB)
+    ap.add_argument("extra", nargs="*", help="extra nvcc flags, e.g. -DSEGHDC_TRACE")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, extra=a.extra))

@@ -113,8 +113,9 @@ size_t tc_smem_bytes(uint32_t W32);
 size_t tc_bimg_bytes(uint32_t W32);
 uint32_t tc_tile_pixels();
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32);
-void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint8_t* bimg,
-                       const void* state, cudaStream_t s);
+uint64_t tc_max_value();  // centroid entries above this need the IMMA kernels
+void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
+                       cudaStream_t s);
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s);
 
 }  // namespace seghdc_dev

@@ -231,16 +231,20 @@ uint32_t planes_for(uint64_t vmax) {
     return p;
 }
 
-void alloc_cluster(seghdc_ctx& x, size_t K, uint32_t planes = 0) {
+// vmax: largest centroid entry the round kernels must represent (0: member counts, i.e. the
+// image's pixel count)
+void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     require(x.grid_valid, "no resident grid: encode or load a grid first");
-    // centroid entries are member counts <= pixels; the similarity kernel splits them into
-    // 6-bit planes (kernels.cuh): 4 planes below 2^24 pixels, 5 below 2^30
+    // centroid entries are member counts <= pixels; the IMMA kernels split them into 6-bit
+    // planes (kernels.cuh): 4 planes below 2^24 pixels, 5 below 2^30
     require(uint64_t(x.g_h) * x.g_w < (1ull << 28), "images of 2^28 pixels or more are not supported");
-    if (planes == 0) planes = planes_for(uint64_t(x.g_h) * x.g_w);
+    if (vmax == 0) vmax = uint64_t(x.g_h) * x.g_w;
+    const uint32_t planes = planes_for(vmax);
     const Geometry& g = x.g;
     x.planes = planes;
     if (!plan_round(uint32_t(K), planes, g.W32, g.SS, x.plan, x.smem_optin))
         throw Error(SEGHDC_ERUNTIME, "dim " + std::to_string(g.D) + " does not fit the round kernel's shared memory");
+    if (x.plan.tc && vmax > tc_max_value()) x.plan.tc = false;  // beyond kP8 base-8 digits
     x.K = K;
     const uint64_t n = x.n_local();
     if (x.plan.tc && !tc_make_grid_map(x.tmap, x.grid.p, n, g.S32)) x.plan.tc = false;  // no driver entry point
@@ -324,8 +328,7 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     launch_finish(f, x.stream);
     x.count(2);
     if (x.plan.tc) {
-        launch_build_bimg(x.Z.p, uint32_t(x.K), x.planes, x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr,
-                          x.stream);
+        launch_build_bimg(x.Z.p, uint32_t(x.K), x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr, x.stream);
         x.count();
     }
     x.check_launch();
@@ -595,7 +598,7 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         // caller centroids may hold any u32 (the reference's IntVector): up to 6 planes
         uint32_t zmax = 0;
         for (size_t i = 0; i < k * dim; ++i) zmax = std::max(zmax, centroids[i]);
-        alloc_cluster(*ctx, k, planes_for(zmax));
+        alloc_cluster(*ctx, k, std::max<uint64_t>(zmax, 1));
         ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
         ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
         ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");

@@ -1,22 +1,29 @@
 // tcgen05 round kernel: assign_labels (clusterer.cpp:132-162) fused with the accumulation of
-// update_centroids (clusterer.cpp:164-188) on the 5th-generation tensor cores.
+// update_centroids (clusterer.cpp:164-188) on the 5th-generation tensor cores, as a block-scaled
+// FP4 product (kind::mxf4, e2m1 x e2m1 -> f32, every scale factor 1.0) that is exact by
+// construction.
 //
 // Per CTA (one per SM) and per tile of 128 pixels (the MMA's M):
 //   producer warp   2-D TMA (cp.async.bulk.tensor, 128B swizzle) of 128 pixel rows x 32 words
 //                   ("chunk") into an NSTAGE-deep smem ring; once, the centroid B image.
-//   unpack warps    2 per TMEM lane quarter: thread = pixel row. Each 32-bit HV word becomes
-//                   four A registers (w << 2e) & 0xC0C0C0C0 - two HV bits per 8-bit k-slot,
-//                   the pair packing of kernels.cuh - stored to TMEM with tcgen05.st (A lives
-//                   in TMEM, double-buffered per chunk).
-//   MMA thread      per k-step of 64 HV dims: tcgen05.mma.kind::i8 M128 N8 K32 twice on the
-//                   same A - unsigned against Bu = 2*z6 + z7, signed against Bs = 2*z6 - z7 -
-//                   accumulating 256 * (exact plane dots) in a TMEM s32 accumulator;
-//                   tcgen05.commit frees the A buffer / publishes the tile's D.
-//   epilogue warps  one per lane quarter: tcgen05.ld of the 8 accumulator columns of its
-//                   pixel, exact u64 dots, 128-bit argmax, labels, counts, update list.
+//   unpack warps    3 per TMEM lane quarter: thread = pixel row. Each 32-bit HV word w becomes
+//                   four A registers of eight e2m1 nibbles, one HV bit per nibble:
+//                     w & 0x22222222          bits 4j+1 as 1.0      (w << 1) & 0x22222222  bits 4j   as 1.0
+//                     w & 0x44444444          bits 4j+2 as 2.0      (w >> 1) & 0x44444444  bits 4j+3 as 2.0
+//                   stored to TMEM with tcgen05.st (A lives in TMEM, one buffer per chunk).
+//   MMA warps       per k-step of 64 HV dims ONE tcgen05.mma.kind::mxf4 M128 N16 K64 against
+//                   B = the centroid digits d (weight-1 nibbles) or d/2 (weight-2 nibbles), so
+//                   every product is bit * d exactly; two warps take alternate chunks into their
+//                   own accumulators. tcgen05.commit frees the A buffer / publishes the tile.
+//   epilogue warps  one per lane quarter: tcgen05.ld of the 2 x 16 accumulator columns of its
+//                   pixel, exact integer dots, 128-bit argmax, labels, counts, update list.
 //   fold warps      the pixels of the updated cluster (update list) are folded into
 //                   Harley-Seal counters, thread = word column, reading the rows back from
 //                   L2 (the tile streamed through moments before).
+// Centroid entries z are written in balanced base 8, z = sum_p d_p 8^p with d_p in [-4, 3]
+// (kP8 = 8 digits cover z <= 3 (8^8 - 1) / 7): every digit and every half-digit is an e2m1
+// value, each digit column's dot is an integer of magnitude <= 4 D < 2^24 (exact in f32), and
+// the epilogue recombines the digit dots in int64.
 // All hand-offs are mbarriers; the counters and counts leave through the exchange buffer
 // exactly as in the IMMA kernel (seghdc_kernels.cu), so results are bit-identical.
 #include <cuda.h>
@@ -36,7 +43,9 @@ constexpr uint32_t kChunkBytes = kTP * kCW * 4;
 constexpr uint32_t kUW = 3;        // unpack warps per TMEM lane quarter (chunk g goes to warp g % kUW)
 constexpr uint32_t kAB = 3;        // A buffers in TMEM (128 columns each)
 static_assert(kStages % kUW == 0 && kAB == kUW, "unpack warp u owns ring slots and A buffers == u mod kUW");
-constexpr uint32_t kN = 8;         // accumulator columns: 2 clusters x 4 planes
+constexpr uint32_t kP8 = 8;        // balanced base-8 digits per centroid entry
+constexpr uint32_t kN = 16;        // accumulator columns: 2 clusters x kP8 digits (MMA N)
+constexpr uint32_t kKB = kN * 32;  // B image bytes per k-step: kN rows x 64 e2m1
 // warp layout (SM sub-partition = warp % 4): [0, 12) unpack (3 per lane quarter), [12, 16)
 // epilogue (one per lane quarter), 16/17/21/22 fold, 18/19 MMA issue (sub-partitions 2 and 3,
 // away from the producer), 20 producer. Two MMA-issuing warps split the chunks of a tile
@@ -47,8 +56,9 @@ __device__ __forceinline__ int fold_index(uint32_t warp) {
     return warp == 16 ? 0 : warp == 17 ? 1 : warp == 21 ? 2 : warp == 22 ? 3 : -1;
 }
 // TMEM columns: A buffers [128*i, 128*i+128), then accumulators D[tile parity][MMA warp]
-// (8 columns each)
-constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB;
+// (kN columns each), then the (all 1.0) scale factors of A and B
+constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB, kColSF = kColD + 4 * kN;
+static_assert(kColSF + 8 <= kTmemCols, "TMEM budget");
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -60,32 +70,32 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
-__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr)
-                 : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
 }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // One chunk (kKS k-steps) of MMAs, issued by an elected lane of the calling warp from a single
-// asm block: addresses advance inside PTX, so the whole block runs on the uniform datapath
-// (one tcgen05.mma every ~10 cycles instead of ~45 with per-MMA operand conversion).
-// Per k-step: u8 MMA with B block 2kg (Bu), s8 MMA with B block 2kg+1 (Bs), same A columns.
-#define SEGHDC_KSTEP                                                                    \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"                     \
-    "add.u64 b, b, 16;\n\t"                                                             \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %4, q;\n\t"                     \
-    "add.u64 b, b, 16;\n\tadd.u32 a, a, 8;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-__device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idu, uint32_t ids,
+// asm block: addresses advance inside PTX, so the whole block runs on the uniform datapath.
+// Per k-step ONE block-scaled FP4 MMA: A = 8 TMEM columns (64 e2m1), B = kN x 64 e2m1 at b;
+// the scale factors (all ue8m0 127 = 1.0) sit at sf.
+#define SEGHDC_KSTEP                                                                                  \
+    "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a], b, %3, [%4], [%5], p;\n\t" \
+    "add.u64 b, b, %6;\n\tadd.u32 a, a, 8;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+__device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
                                              uint32_t accum) {
     static_assert(kKS == 16, "tc_mma_chunk issues 16 k-steps");
     asm volatile(
-        "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.ne.b32 q, 1, 0;\n\t"
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
         "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
             SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
                 SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
-        "r"(a_t), "l"(bdesc), "r"(idu), "r"(ids), "r"(accum)
+        "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(kKB >> 4), "r"(accum)
         : "memory");
 }
 #undef SEGHDC_KSTEP
@@ -108,10 +118,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ uint64_t bdesc_at(uint32_t saddr) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) | (1ull << 46);
 }
-// instruction descriptor kind::i8: D s32 (bits 4-5 = 2), A/B signedness (bits 7, 10), both
-// K-major, N >> 3 at bit 17, M >> 4 at bit 24
-constexpr uint32_t idesc_i8(bool sgn, uint32_t n, uint32_t m) {
-    return (2u << 4) | (uint32_t(sgn) << 7) | (uint32_t(sgn) << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+// instruction descriptor, block-scaled kinds: A/B format E2M1 (1) at bits 7 / 10, both K-major,
+// N >> 3 at bit 17, scale format UE8M0 (bit 23), M >> 4 at bit 24, scale-factor ids 0, K = 64
+constexpr uint32_t idesc_mxf4(uint32_t n, uint32_t m) {
+    return (1u << 7) | (1u << 10) | ((n >> 3) << 17) | (1u << 23) | ((m >> 4) << 24);
 }
 
 #ifdef SEGHDC_HANGDBG
@@ -145,8 +155,8 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t
 
 struct TcSmem {
     static constexpr size_t ring = 0;  // [kStages][128][32] u32, 1024-aligned (128B swizzle)
-    __host__ __device__ static size_t b(uint32_t nks) { return size_t(kStages) * kChunkBytes; }                   // [2*nks][kN*32] B image
-    __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * 2 * kN * 32; }           // [2][4][32] u32
+    __host__ __device__ static size_t b(uint32_t nks) { return size_t(kStages) * kChunkBytes; }                   // [nks][kKB] B image
+    __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * kKB; }                  // [2][4][32] u32
     __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + 2 * 4 * 32 * 4; }                   // [2][4] u32
     __host__ __device__ static size_t misc(uint32_t nks) { return listn(nks) + 2 * 4 * 4; }                        // tmem base, skip
     __host__ __device__ static size_t bars(uint32_t nks) { return (misc(nks) + 16 + 7) & ~size_t(7); }
@@ -257,6 +267,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     tc_fence_after();
     const uint32_t tbase = s_misc[0];
     const uint32_t upd_c = 1 - s_misc[1];  // K == 2 under UPD
+    if (warp < 4) {  // scale factors of A and B: every ue8m0 byte 127 (2^0), whatever the layout
+        const uint32_t one = 0x7F7F7F7Fu;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                         tbase + ((32 * warp) << 16) + kColSF),
+                     "r"(one)
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     if (warp == 0) TC_TG(1);
     const bool folding = UPD && do_update;
 
@@ -288,9 +309,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
                 uint32_t a[16];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) a[4 * i + e] = (w4[i] << (2 * e)) & 0xC0C0C0C0u;
+                for (int i = 0; i < 4; ++i) {  // A column 4i + c: class c of word i (see header)
+                    a[4 * i + 0] = w4[i] & 0x22222222u;
+                    a[4 * i + 1] = w4[i] & 0x44444444u;
+                    a[4 * i + 2] = (w4[i] << 1) & 0x22222222u;
+                    a[4 * i + 3] = (w4[i] >> 1) & 0x44444444u;
+                }
                 tc_st16(lane_addr + ab * 128 + c16 * 16, a);  // k-steps 2*c16, 2*c16+1: 8 columns each
             }
             PRG(10 * 100000 + g);
@@ -320,21 +344,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             if (qd == 0) TC_ACC(5, c1 - c0);
             tc_fence_after();
             if (qd == 0) TC_TR(4, it);
-            uint32_t col[8], col2[8];
-            tc_ld8(lane_addr + kColD + 16 * db, col);
-            tc_ld8(lane_addr + kColD + 16 * db + 8, col2);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) col[c] += col2[c];
+            uint32_t c0r[16], c1r[16];  // the two MMA warps' accumulators of this tile
+            tc_ld16(lane_addr + kColD + (2 * db) * kN, c0r);
+            tc_ld16(lane_addr + kColD + (2 * db + 1) * kN, c1r);
+            tc_wait_ld();
             tc_fence_before();
             mbar_arrive(&d_free[db]);
-            // exact dots: column n = 4*c + plane, scale 256 removed (exact). K == 2 here means P == 4.
-            unsigned long long d[2] = {0, 0};
+            // exact dots: column n = kP8 * c + p holds sum_i y_i d_p(z_c[i]) (an integer in f32);
+            // dot_c = sum_p digit_dot_p * 8^p
+            long long d[2] = {0, 0};
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int pl = 0; pl < 4; ++pl)
-                    d[c] += (unsigned long long)(col[4 * c + pl] >> 8) << (kPlaneBits * pl);
-            const uint32_t best = (K > 1 && strictly_closer(d[1], n2_1, d[0], n2_0)) ? 1u : 0u;
+                for (int p = kP8 - 1; p >= 0; --p)
+                    d[c] = d[c] * 8 + (long long)(__float2int_rn(__uint_as_float(c0r[kP8 * c + p])) +
+                                                  __float2int_rn(__uint_as_float(c1r[kP8 * c + p])));
+            const uint32_t best =
+                (K > 1 && strictly_closer((unsigned long long)d[1], n2_1, (unsigned long long)d[0], n2_0)) ? 1u : 0u;
             if (live) {
                 labels[px] = best;
                 changed += old != best;
@@ -367,7 +393,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         // warp m issues the chunks g = m, m+2, ... (global chunk parity) into accumulator
         // D[db][m] of their tile; the whole warp walks the loop (barrier waits are
         // warp-uniform), one elected lane issues inside tc_mma_chunk / tc_commit
-        constexpr uint32_t idu = idesc_i8(false, kN, kTP), ids = idesc_i8(true, kN, kTP);
+        constexpr uint32_t idesc = idesc_mxf4(kN, kTP);
         const uint32_t m = warp - kWMma0;
         const uint32_t b0 = smem_u32(sB);
         TCW(5, 0, b_full, 0);
@@ -375,7 +401,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         TC_TG(2);
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
-            const uint32_t d_t = tbase + kColD + 16 * db + 8 * m;
+            const uint32_t d_t = tbase + kColD + (2 * db + m) * kN;
             TCW(6, it, &d_free[db], ((it >> 1) & 1) ^ 1);
             __syncwarp();
             for (uint32_t ch = (it * nch + m) & 1; ch < nch; ch += 2) {  // chunks with g % 2 == m
@@ -387,7 +413,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 if (m == 0) TC_ACC(2, c1 - c0);
                 tc_fence_after();
                 PRG(12 * 100000 + g);
-                tc_mma_chunk(d_t, tbase + ab * 128, bdesc_at(b0 + (2 * ch * kKS) * (kN * 32)), idu, ids, ch >= 2);
+                tc_mma_chunk(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * kKB), idesc, tbase + kColSF, ch >= 2);
                 tc_commit(&a_free[ab]);
                 PRG(13 * 100000 + g);
                 {
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     } else if (warp == kWProd) {
         // ----------------------------------------------------------------------- producer warp
         if (lane == 0) {
-            const uint32_t bbytes = nks * 2 * kN * 32;
+            const uint32_t bbytes = nks * kKB;
             mbar_expect_tx(b_full, bbytes);
             bulk_g2s(sB, bimg, bbytes, b_full);
             uint32_t g = 0;
@@ -483,28 +509,41 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
 }
 
-// B image: for global k-step ks and variant s (0: u8 2*z6 + z7, 1: s8 2*z6 - z7), the kN x 32
-// bytes of B in the canonical K-major no-swizzle layout: core matrix cm (k-slots 16cm..16cm+15)
-// at +128*cm, row n at +16n. k-slot kappa = 4*col + j of the A register column col = 4h + e
-// (word h of the k-step, shift 2e) carries bits 8j+6-2e (weight 64) and 8j+7-2e (weight 128).
-__global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t P, uint32_t D, uint32_t nks,
+// B image: for k-step ks the kN x 64 e2m1 of B (kKB bytes) in the canonical K-major no-swizzle
+// layout: 8-row group g at +256g, core matrix cm (k-slots 32cm..32cm+31) at +128cm, row at +16r,
+// k-slot pair (2b, 2b+1) in byte b (low nibble = even slot). k-slot k is nibble j = k % 8 of A
+// column col = k / 8 = 4h + c, i.e. class c of HV word 2ks + h (header): c = 0 / 2 carry bits
+// 4j+1 / 4j as 1.0, c = 1 / 3 carry bits 4j+2 / 4j+3 as 2.0. Row n = kP8 * cluster + p holds
+// digit p of the centroid entry (weight 1) or half of it (weight 2), so every product is bit * d.
+__device__ __forceinline__ int digit8(long long z, uint32_t p) {  // balanced base 8: [-4, 3]
+    for (uint32_t q = 0;; ++q) {
+        int r = int(z & 7);
+        if (r >= 4) r -= 8;
+        if (q == p) return r;
+        z = (z - r) >> 3;
+    }
+}
+__device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t ks, uint32_t n,
+                                             uint32_t k) {
+    const uint32_t col = k >> 3, j = k & 7, h = col >> 2, c = col & 3;
+    const uint32_t dim = 32 * (2 * ks + h) + 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
+    const uint32_t cl = n / kP8, p = n % kP8;
+    if (cl >= K || dim >= D) return 0;
+    const int d = digit8((long long)Z[size_t(cl) * D + dim], p);
+    const uint32_t a = uint32_t(d < 0 ? -d : d);
+    // weight 1: |d| in 0..4 -> e2m1 {0, 1, 2, 3, 4}; weight 2: |d|/2 in {0, .5, 1, 1.5, 2}
+    const uint32_t code = (c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u);
+    return code | (d < 0 ? 8u : 0u);
+}
+__global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks,
                              uint8_t* __restrict__ bimg, const void* state) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
-    const uint32_t total = nks * 2 * kN * 32;
+    const uint32_t total = nks * kKB;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t blk = i / (kN * 32), rem = i % (kN * 32);
-        const uint32_t ks = blk >> 1, sgn = blk & 1;
-        const uint32_t ngrp = rem / 256, r2 = rem % 256, cm = r2 / 128, nrow = (r2 % 128) / 16, b = r2 % 16;
-        const uint32_t ncol = ngrp * 8 + nrow;  // B column = 4*cluster + plane
-        const uint32_t kappa = cm * 16 + b, colr = kappa >> 2, j = kappa & 3, h = colr >> 2, e = colr & 3;
-        const uint32_t dim6 = 32 * (2 * ks + h) + 8 * j + 6 - 2 * e;
-        uint32_t z6 = 0, z7 = 0;
-        const uint32_t c = ncol / P, pl = ncol % P;
-        if (c < K) {
-            if (dim6 < D) z6 = (Z[size_t(c) * D + dim6] >> (kPlaneBits * pl)) & 0x3Fu;
-            if (dim6 + 1 < D) z7 = (Z[size_t(c) * D + dim6 + 1] >> (kPlaneBits * pl)) & 0x3Fu;
-        }
-        bimg[i] = uint8_t(sgn ? 2 * z6 - z7 : 2 * z6 + z7);
+        const uint32_t ks = i / kKB, rem = i % kKB;
+        const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
+        const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
+        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k) | (b_nibble(Z, K, D, ks, n, k + 1) << 4));
     }
 }
 
@@ -538,9 +577,11 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
 }  // namespace
 
 bool tc_supported(uint32_t W32) { return W32 > kCW && W32 <= 3 * kNRW * 32; }  // >= 2 chunks: both MMA warps
+// largest centroid entry kP8 balanced base-8 digits represent: 3 (8^kP8 - 1) / 7
+uint64_t tc_max_value() { return 3ull * ((1ull << (3 * kP8)) - 1) / 7; }
 uint32_t tc_ksteps(uint32_t W32) { return ((W32 + kCW - 1) / kCW) * kKS; }
 size_t tc_smem_bytes(uint32_t W32) { return TcSmem::total(tc_ksteps(W32)); }
-size_t tc_bimg_bytes(uint32_t W32) { return size_t(tc_ksteps(W32)) * 2 * kN * 32; }
+size_t tc_bimg_bytes(uint32_t W32) { return size_t(tc_ksteps(W32)) * kKB; }
 uint32_t tc_tile_pixels() { return kTP; }
 
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32) {
@@ -556,11 +597,11 @@ bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint8_t* bimg,
-                       const void* state, cudaStream_t s) {
+void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
+                       cudaStream_t s) {
     const uint32_t nks = tc_ksteps(W32);
-    const uint32_t total = nks * 2 * kN * 32;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, P, D, nks, bimg, state);
+    const uint32_t total = nks * kKB;
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, bimg, state);
 }
 
 #ifdef SEGHDC_HANGDBG
