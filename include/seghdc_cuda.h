@@ -152,6 +152,8 @@ int seghdc_shard_finish(seghdc_ctx* ctx, size_t round);
  * last read (used by bench.py for the roofline fraction). */
 int seghdc_profile_rounds(seghdc_ctx* ctx, int enable);
 int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count);
+/* as profile_read, plus the first `cap` per-launch times (in launch order) into each_ms */
+int seghdc_profile_read_each(seghdc_ctx* ctx, double* total_ms, uint64_t* count, double* each_ms, size_t cap);
 
 /* ---- synthetic inputs (bench/test workloads) --------------------------- */
 /* config_id 0..4 = BASELINE.json configs; config 2 is config 0's construction (use seed

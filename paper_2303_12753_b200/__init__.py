@@ -76,6 +76,7 @@ SIGNATURES = {
     "seghdc_shard_finish": ([C.c_void_p, _sz], C.c_int),
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
+    "seghdc_profile_read_each": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_void_p, _sz], C.c_int),
     "seghdc_synth_image": ([C.c_int, C.c_uint64, C.c_void_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
 }
 
@@ -199,6 +200,13 @@ class Context:
         t, n = C.c_double(), C.c_uint64()
         self.check(lib().seghdc_profile_read(self.h, C.byref(t), C.byref(n)))
         return t.value, n.value
+
+    def profile_read_each(self, cap: int = 4096) -> np.ndarray:
+        """Per-launch round-kernel milliseconds (launch order) since the last read."""
+        t, n = C.c_double(), C.c_uint64()
+        out = np.zeros(cap, np.float64)
+        self.check(lib().seghdc_profile_read_each(self.h, C.byref(t), C.byref(n), out.ctypes.data, cap))
+        return out[:min(n.value, cap)].copy()
 
     # ---- reference API ------------------------------------------------------------------
     def encode_image(self, img: np.ndarray, dim: int, row, col, widened, download: bool = True):

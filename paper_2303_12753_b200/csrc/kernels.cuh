@@ -119,6 +119,40 @@ struct BitCounter {
             s = c;
         }
     }
+    // plane k (weight 2^k) of the 32 counters to dst[k * stride], k < 4 + H
+    __device__ __forceinline__ void planes(uint32_t* dst, size_t stride) const {
+        dst[0] = o;
+        dst[stride] = t;
+        dst[2 * stride] = f;
+        dst[3 * stride] = e;
+#pragma unroll
+        for (int m = 0; m < H; ++m) dst[(4 + m) * stride] = hi[m];
+    }
+    __device__ __forceinline__ bool any() const {
+        uint32_t v = o | t | f | e;
+#pragma unroll
+        for (int m = 0; m < H; ++m) v |= hi[m];
+        return v != 0;
+    }
+    __device__ __forceinline__ void add8(const uint32_t (&x)[8]) {
+        uint32_t tA, tB, fA, fB, s;
+        csa(tA, o, o, x[0], x[1]);
+        csa(tB, o, o, x[2], x[3]);
+        csa(fA, t, t, tA, tB);
+        csa(tA, o, o, x[4], x[5]);
+        csa(tB, o, o, x[6], x[7]);
+        csa(fB, t, t, tA, tB);
+        csa(s, f, f, fA, fB);  // s: weight 8
+        const uint32_t c8 = e & s;
+        e ^= s;
+        s = c8;  // weight 16
+#pragma unroll
+        for (int m = 0; m < H; ++m) {
+            const uint32_t c = hi[m] & s;
+            hi[m] ^= s;
+            s = c;
+        }
+    }
     // capacity of the counter (largest representable count)
     __host__ __device__ static constexpr uint64_t capacity() { return 15ull + 16ull * ((1ull << H) - 1); }
     // count of bit b
@@ -151,13 +185,14 @@ struct BitCounter {
 // Fold a warp's counters into dst with coalesced atomics: lane l owns word column
 // (col0 + l) = entries [32*(col0+l), 32*(col0+l)+32). The 32x32 block is transposed through
 // `scratch` (32*33 u32 of shared memory owned by this warp) so each atomic instruction covers
-// 32 consecutive entries (one 128-byte line). Columns >= ncols are skipped.
+// 32 consecutive entries (one 128-byte line). Columns >= ncols are skipped. `bias` is
+// subtracted from every count (mod 2^32: the incremental re-bundling adds signed deltas).
 template <int H>
 __device__ __forceinline__ void flush_warp_atomic(const BitCounter<H>& cnt, uint32_t* scratch, uint32_t* dst,
-                                                  uint32_t col0, uint32_t ncols) {
+                                                  uint32_t col0, uint32_t ncols, uint32_t bias = 0) {
     const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
-    for (int b = 0; b < 32; ++b) scratch[lane * 33 + b] = cnt.value(b);
+    for (int b = 0; b < 32; ++b) scratch[lane * 33 + b] = cnt.value(b) - bias;
     __syncwarp();
     for (uint32_t r = 0; r < 32; ++r) {
         if (col0 + r >= ncols) break;
@@ -165,6 +200,24 @@ __device__ __forceinline__ void flush_warp_atomic(const BitCounter<H>& cnt, uint
         if (val) atomicAdd(dst + size_t(col0 + r) * 32 + lane, val);
     }
     __syncwarp();
+}
+
+// Whole-CTA flush of bit-sliced counters that their owners spilled plane-major to shared
+// memory (planes[k * ncols + col], k < 4 + H; one 32-bit word column per col): every thread
+// expands entries e = 32 col + b and adds count - bias (mod 2^32) into dst[e]; each warp's
+// atomics cover one 128-byte line. Spreading the bit gathers over all warps keeps the flush
+// off the kernel's tail (four fold warps alone took ~12 us).
+template <int H>
+__device__ __forceinline__ void flush_planes_cta(const uint32_t* planes, uint32_t ncols, uint32_t bias,
+                                                 uint32_t* dst) {
+    for (uint32_t e = threadIdx.x; e < ncols * 32; e += blockDim.x) {
+        const uint32_t col = e >> 5, b = e & 31;
+        uint32_t v = 0;
+#pragma unroll
+        for (int k = 0; k < 4 + H; ++k) v |= ((planes[size_t(k) * ncols + col] >> b) & 1u) << k;
+        v -= bias;
+        if (v) atomicAdd(dst + e, v);
+    }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -7,6 +7,10 @@
 
 namespace seghdc_dev {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) costs host microseconds per call; the
+// launchers raise each kernel's limit once per (function, device) instead of per launch.
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes);
+
 struct RoundState;
 
 struct EncodeArgs {
@@ -69,6 +73,10 @@ struct FinishArgs {
     void* state;
     uint32_t round;
     int early_stop;
+    // incremental re-bundling (tcgen05 kernel, K == 2): xchg row 1 holds the round's delta of
+    // cluster 1's member sums; run1[parity][Dp] are the running sums (read p, write p ^ 1)
+    int inc;
+    uint32_t* run1;
 };
 void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);

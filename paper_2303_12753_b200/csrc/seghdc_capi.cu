@@ -6,7 +6,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <string>
 #include <vector>
@@ -18,6 +20,22 @@
 
 using seghdc_host::Error;
 using namespace seghdc_dev;
+
+namespace seghdc_dev {
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[{func, dev}];
+    if (cur >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
+}  // namespace seghdc_dev
 
 namespace {
 
@@ -99,6 +117,7 @@ struct seghdc_ctx {
     DevBuf<uint8_t> bimg;                     // tcgen05 kernel: centroid B image
     alignas(64) unsigned char tmap[128] = {};  // tcgen05 kernel: CUtensorMap of the grid
     DevBuf<uint32_t> labels, Z;
+    DevBuf<uint32_t> run1;  // tcgen05 K == 2: running member sums of cluster 1, [2][Dp] by parity
     DevBuf<int32_t> xchg;
     DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
     DevBuf<uint64_t> seeds;
@@ -112,6 +131,8 @@ struct seghdc_ctx {
 
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
     size_t xchg_round_ints() const { return K * g.Dp + K + 1; }
+    // the tcgen05 round kernel re-bundles K == 2 incrementally (deltas of cluster 1)
+    bool incremental() const { return plan.tc && K == 2; }
     int32_t* colsum_ptr() { return xchg.p + xchg_round_ints(); }
     void count(uint64_t k = 1) { launches += k; }
     void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
@@ -259,6 +280,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
     if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(g.W32));
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
+    if (x.incremental()) x.run1.ensure(2 * size_t(g.Dp));
     x.colsum.ensure(g.Dp);
     x.seeds.ensure(std::max<size_t>(K, 1));
     x.slots.ensure(2 + K);
@@ -325,6 +347,8 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.state = x.state.p;
     f.round = round;
     f.early_stop = x.early_stop;
+    f.inc = x.incremental() ? 1 : 0;
+    f.run1 = x.run1.p;
     launch_finish(f, x.stream);
     x.count(2);
     if (x.plan.tc) {
@@ -343,6 +367,7 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     x.early_stop = early_stop;
     ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K)), x.stream), "clear state");
     ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
+    if (x.incremental()) ck(cudaMemsetAsync(x.run1.p, 0, 2 * size_t(x.g.Dp) * 4, x.stream), "clear running sums");
     select_seeds_dev(x, K);
     if (!x.colsum_valid) compute_colsum(x);
     // local column sums into the exchange tail; the init all-reduce makes them global
@@ -812,6 +837,10 @@ int seghdc_profile_rounds(seghdc_ctx* ctx, int enable) {
 }
 
 int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count) {
+    return seghdc_profile_read_each(ctx, total_ms, count, nullptr, 0);
+}
+
+int seghdc_profile_read_each(seghdc_ctx* ctx, double* total_ms, uint64_t* count, double* each_ms, size_t cap) {
     return guarded(ctx, [&] {
         ck(cudaStreamSynchronize(ctx->stream), "sync");
         double t = 0;
@@ -819,6 +848,7 @@ int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count) {
             float ms = 0;
             ck(cudaEventElapsedTime(&ms, ctx->prof_events[i].first, ctx->prof_events[i].second), "elapsed");
             t += ms;
+            if (each_ms && i < cap) each_ms[i] = ms;
         }
         *total_ms = t;
         *count = ctx->prof_used;

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, 3)
 template <int C>
 static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
     const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
-    cudaFuncSetAttribute(k_encode<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_dynamic_smem((const void*)k_encode<C>, smem);
     k_encode<C><<<g, kEncWarps * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref, a.S32,
                                                 a.grid, a.colsum, a.W32);
 }
@@ -359,7 +359,7 @@ static void launch_accumulate_h(const AccumulateArgs& a, uint32_t blocks_x, uint
     const uint32_t threads = std::min<uint32_t>(512, ((a.W32 + 31) / 32) * 32);
     dim3 g(blocks_x, (a.W32 + threads - 1) / threads);
     const size_t smem = (4096 + size_t(threads / 32) * 32 * 33) * 4;
-    cudaFuncSetAttribute(k_accumulate<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    ensure_dynamic_smem((const void*)k_accumulate<H>, smem);
     k_accumulate<H><<<g, threads, smem, s>>>(a.grid, a.S32, a.W32, a.n, ppc, a.labels, a.K, a.skip_mode, a.state,
                                              a.parity, a.dst, a.Dp, a.counts_dst);
 }
@@ -383,7 +383,7 @@ void launch_accumulate(const AccumulateArgs& a, cudaStream_t s) {
 // =============================================================================================
 __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
                          const int32_t* __restrict__ xchg, const int32_t* __restrict__ colsum, uint32_t* Z,
-                         uint8_t* bfrag, void* state, uint32_t round, int early_stop) {
+                         uint8_t* bfrag, void* state, uint32_t round, int early_stop, int inc, uint32_t* run1) {
     StateView st = StateView::at(state, K);
     const uint32_t p = round & 1, np = p ^ 1;  // set produced here is used by round+1
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(xchg) + size_t(K) * Dp;
@@ -403,7 +403,12 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
         const size_t i = size_t(word) * 32 + lane;
         const bool in = i < D;
         uint32_t z;
-        if (mode == 2) {
+        if (mode == 0 && inc) {  // K == 2: S1 = running sums + this round's delta, S0 = colsum - S1
+            const uint32_t s1 = run1[size_t(p) * Dp + i] + uint32_t(xchg[Dp + i]);
+            if (c == 1) run1[size_t(np) * Dp + i] = s1;
+            if (counts[c] != 0) z = c == 1 ? s1 : uint32_t(colsum[i]) - s1;
+            else z = in ? Z[size_t(c) * D + i] : 0u;  // empty cluster keeps its previous centroid
+        } else if (mode == 2) {
             z = in ? Z[size_t(c) * D + i] : 0u;
         } else if (mode == 1 || counts[c] != 0) {
             if (int(c) == skip) {
@@ -454,7 +459,8 @@ void launch_finish(const FinishArgs& a, cudaStream_t s) {
     const uint32_t threads = 256;
     const uint64_t total = uint64_t(a.W32) * a.K * 32;
     k_finish<<<uint32_t((total + threads - 1) / threads), threads, 0, s>>>(
-        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop);
+        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop,
+        a.inc, a.run1);
 }
 
 // Zero the accumulators of parity np before k_finish accumulates into them.
@@ -663,7 +669,7 @@ template <int MT, int NTG>
 static cudaError_t launch_round_t(const RoundArgs& a, uint32_t nwarps, cudaStream_t s) {
     auto kern = nwarps <= 12 ? k_round<MT, NTG, 384> : k_round<MT, NTG, 512>;
     const size_t smem = round_smem_bytes(MT, NTG, a.SS, nwarps, a.K, a.NT);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, nwarps * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32P, a.nwarp_words, a.K, a.P, a.NT, a.bfrag,
                                            a.labels, a.state, a.round, reinterpret_cast<uint32_t*>(a.xchg) +
@@ -967,7 +973,7 @@ template <int WPW, bool UPD, int H, int NMW, int NRW>
 static cudaError_t launch_fused_t(const RoundArgs& a, cudaStream_t s) {
     auto kern = k_round_fused<WPW, UPD, H, NMW, NRW>;
     const size_t smem = fused_smem_bytes(a.SS, NMW, NRW);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, (NMW + NRW + 2) * 32, smem, s>>>(a.grid, a.n, a.S32, a.SS, a.W32, a.K, a.bfrag, a.labels, a.state,
                                                     a.round, a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);

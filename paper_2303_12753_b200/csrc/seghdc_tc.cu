@@ -17,9 +17,13 @@
 //                   own accumulators. tcgen05.commit frees the A buffer / publishes the tile.
 //   epilogue warps  one per lane quarter: tcgen05.ld of the 2 x 16 accumulator columns of its
 //                   pixel, exact integer dots, 128-bit argmax, labels, counts, update list.
-//   fold warps      the pixels of the updated cluster (update list) are folded into
-//                   Harley-Seal counters, thread = word column, reading the rows back from
-//                   L2 (the tile streamed through moments before).
+//   fold warps      incremental re-bundling of cluster 1: only pixels whose membership of
+//                   cluster 1 changed this round are folded into Harley-Seal counters (thread
+//                   = word column, rows read back from L2): a pixel entering adds its HV, a
+//                   pixel leaving adds its complement, and the flush subtracts the number of
+//                   leavers, so the exchange buffer receives the exact delta of cluster 1's
+//                   member sums (k_finish keeps the running sums; cluster 0 = colsum - S1).
+//                   After the first rounds almost no pixel changes and the fold is idle.
 // Centroid entries z are written in balanced base 8, z = sum_p d_p 8^p with d_p in [-4, 3]
 // (kP8 = 8 digits cover z <= 3 (8^8 - 1) / 7): every digit and every half-digit is an e2m1
 // value, each digit column's dot is an integer of magnitude <= 4 D < 2^24 (exact in f32), and
@@ -168,16 +172,30 @@ struct TcSmem {
 
 #ifdef SEGHDC_TRACE
 __device__ unsigned long long g_trace_tc[148 * 64 * 8];
+__device__ int g_trace_round;  // 0: trace every launch (the last one wins), r: only round r
+#define TC_ON (g_trace_round == 0 || int(round) == g_trace_round)
 #define TC_TR(ev, it)                                                                 \
     do {                                                                              \
-        if (lane == 0 && blockIdx.x < 148 && (it) < 64)                               \
+        if (lane == 0 && blockIdx.x < 148 && (it) < 64 && TC_ON)                      \
             g_trace_tc[(size_t(blockIdx.x) * 64 + (it)) * 8 + (ev)] = clock64();      \
     } while (0)
-void read_trace_tc(void* dst) { cudaMemcpyFromSymbol(dst, g_trace_tc, sizeof(g_trace_tc)); }
+static cudaEvent_t* g_tc_events = nullptr;
+void read_trace_tc(void* dst) {
+    cudaMemcpyFromSymbol(dst, g_trace_tc, sizeof(g_trace_tc));
+    if (g_tc_events) {  // last launch: event ms of [stamp0], [round], [stamp1] into slot 60 of CTA 0
+        cudaEventSynchronize(g_tc_events[3]);
+        unsigned long long* o = static_cast<unsigned long long*>(dst) + 60 * 8;
+        for (int i = 0; i < 3; ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, g_tc_events[i], g_tc_events[i + 1]);
+            o[i] = (unsigned long long)(ms * 1e6);  // ns
+        }
+    }
+}
 // kernel-level events in slot 63 with %globaltimer (ns, comparable across SMs)
 #define TC_TG(ev)                                                                     \
     do {                                                                              \
-        if (lane == 0 && blockIdx.x < 148) {                                          \
+        if (lane == 0 && blockIdx.x < 148 && TC_ON) {                                 \
             unsigned long long t_;                                                    \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
             g_trace_tc[(size_t(blockIdx.x) * 64 + 63) * 8 + (ev)] = t_;               \
@@ -187,7 +205,7 @@ void read_trace_tc(void* dst) { cudaMemcpyFromSymbol(dst, g_trace_tc, sizeof(g_t
 // 3 MMA issue (wait-free part), 4 producer slot_free, 5 epilogue d_full
 #define TC_ACC(ev, cyc)                                                               \
     do {                                                                              \
-        if (lane == 0 && blockIdx.x < 148)                                            \
+        if (lane == 0 && blockIdx.x < 148 && TC_ON)                                   \
             atomicAdd(&g_trace_tc[(size_t(blockIdx.x) * 64 + 62) * 8 + (ev)], (cyc));  \
     } while (0)
 #define TC_CLK(v) const unsigned long long v = clock64()
@@ -254,7 +272,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         mbar_init(b_full, 1);
         mbar_fence_init();
-        s_misc[1] = pick_skip(st.cur + parity * K, K);
+        s_listn[0] = s_listn[1] = 0;
     }
     if (warp == kWMma0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_misc)),
@@ -266,7 +284,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = s_misc[0];
-    const uint32_t upd_c = 1 - s_misc[1];  // K == 2 under UPD
     if (warp < 4) {  // scale factors of A and B: every ue8m0 byte 127 (2^0), whatever the layout
         const uint32_t one = 0x7F7F7F7Fu;
         asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
@@ -369,10 +386,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             }
             TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
             if constexpr (UPD) {
-                const bool take = do_update && live && best == upd_c;
+                // membership of cluster 1 changed (old = 0xFFFFFFFF before round 1): entering
+                // pixels add their HV, leaving pixels their complement (flag 0x100)
+                const bool enter = live && best == 1 && old != 1, leave = live && old == 1 && best != 1;
+                const bool take = do_update && (enter || leave);
+                // one compacted list per tile: the four quarters reserve their ranges with an
+                // shared-memory atomic (the fold warps reset the count once they have read it)
                 const uint32_t m = __ballot_sync(0xffffffffu, take);
-                if (take) s_list[(db * 4 + qd) * 32 + __popc(m & ((1u << lane) - 1))] = 32 * qd + lane;
-                if (lane == 0) s_listn[db * 4 + qd] = __popc(m);
+                uint32_t base = 0;
+                if (lane == 0 && m) base = atomicAdd(&s_listn[db], uint32_t(__popc(m)));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (take)
+                    s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
             mbar_arrive(&list_ready[db]);
             if (qd == 0) TC_TR(5, it);
@@ -454,6 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int fw = fold_index(warp);
     const uint32_t rt = uint32_t(fw) * 32 + lane;
     const uint32_t cpt = (W32 + NRT - 1) / NRT;
+    uint32_t nleave = 0;  // leaving pixels folded by this CTA (same count in every fold thread)
     if (fw >= 0) {
         if constexpr (UPD)
 #pragma unroll
@@ -466,22 +492,36 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 if (do_update) {
                     const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * kTP;
                     const uint32_t* G = grid + px0 * S32;
-#pragma unroll 1
-                    for (uint32_t qd = 0; qd < 4; ++qd) {
-                        const uint32_t m = s_listn[db * 4 + qd];
-                        const uint32_t* L = s_list + (db * 4 + qd) * 32;
+                    const uint32_t M = s_listn[db];
+                    const uint32_t* L = s_list + db * kTP;
+                    __syncwarp();
+                    asm volatile("bar.sync 1, %0;" ::"n"(kNRW * 32) : "memory");  // all fold threads read M
+                    if (rt == 0) s_listn[db] = 0;
+                    // batches of 8 listed rows: the 8 x CPTMAX loads of a batch are issued together
+                    // (columns clamped to W32 - 1: the extra counters are never flushed)
+                    uint32_t cw[CPTMAX];
+#pragma unroll
+                    for (int c = 0; c < CPTMAX; ++c) cw[c] = min(rt + c * NRT, W32 - 1);
+                    for (uint32_t e = 0; e < M; e += 8) {
+                        uint32_t row[8], neg[8], val[8];
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            const uint32_t en = (e + v < M) ? L[e + v] : 0u;
+                            row[v] = en & 0xFFu;
+                            neg[v] = (en >> 8) ? 0xFFFFFFFFu : 0u;
+                            val[v] = (e + v < M) ? 0xFFFFFFFFu : 0u;
+                            nleave += en >> 8;
+                        }
+                        uint32_t x[CPTMAX][8];
+#pragma unroll
+                        for (int c = 0; c < CPTMAX; ++c)
+#pragma unroll
+                            for (int v = 0; v < 8; ++v) x[c][v] = __ldg(G + size_t(row[v]) * S32 + cw[c]);
 #pragma unroll
                         for (int c = 0; c < CPTMAX; ++c) {
-                            const uint32_t colw = rt + c * NRT;
-                            if (uint32_t(c) < cpt && colw < W32) {
-                                for (uint32_t e = 0; e < m; e += 16) {
-                                    uint32_t x[16];
 #pragma unroll
-                                    for (int v = 0; v < 16; ++v)
-                                        x[v] = (e + v < m) ? __ldg(G + size_t(L[e + v]) * S32 + colw) : 0u;
-                                    cnt[c].add16(x);
-                                }
-                            }
+                            for (int v = 0; v < 8; ++v) x[c][v] = (x[c][v] ^ neg[v]) & val[v];
+                            cnt[c].add8(x[c]);
                         }
                     }
                 }
@@ -495,17 +535,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 0) TC_TG(6);
-    if (fw >= 0 && folding) {
+    if (folding) {  // CTA-uniform: counters -> planes in the ring -> whole-CTA expansion + atomics
+        uint32_t* planes = reinterpret_cast<uint32_t*>(ring);
+        bool nz = false;
+        if (fw >= 0) {
 #pragma unroll
-        for (int c = 0; c < CPTMAX; ++c)
-            if (uint32_t(c) < cpt)
-                flush_warp_atomic(cnt[c], reinterpret_cast<uint32_t*>(ring) + (rt >> 5) * (32 * 33),
-                                  xchg + size_t(upd_c) * Dp, (rt & ~31u) + c * NRT, W32);
+            for (int c = 0; c < CPTMAX; ++c) {
+                const uint32_t colw = rt + c * NRT;
+                if (uint32_t(c) < cpt && colw < W32) {
+                    cnt[c].planes(planes + colw, W32);
+                    nz |= cnt[c].any();
+                }
+            }
+            if (rt == 0) s_misc[1] = nleave;
+            nz |= nleave != 0;
+        }
+        if (__syncthreads_or(nz)) flush_planes_cta<UPD ? H : 1>(planes, W32, s_misc[1], xchg + Dp);
     }
     if (fw == 0) TC_TG(7);
     if (warp == kWMma0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+#ifdef SEGHDC_TRACE
+        if (lane == 0 && blockIdx.x < 148) {  // slot 61: [0] stamp before, [1] after dealloc, [2] stamp after
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            g_trace_tc[(size_t(blockIdx.x) * 64 + 61) * 8 + 1] = t_;
+        }
+#endif
     }
 }
 
@@ -563,11 +620,18 @@ EncodeFn encode_fn() {
     return fn;
 }
 
+#ifdef SEGHDC_TRACE
+__global__ void k_tc_stamp(int ev) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_trace_tc[(size_t(blockIdx.x) * 64 + 61) * 8 + ev] = t_;
+}
+#endif
 template <bool UPD, int H>
 cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     auto kern = k_round_tc<UPD, H>;
     const size_t smem = tc_smem_bytes(a.W32);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, kWarps * 32, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(a.tmap), a.grid, a.n,
                                                    a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round,
@@ -616,12 +680,41 @@ void* setup_hang() {
 }
 #endif
 
-cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
-    if (a.K != 2) return launch_tc_t<false, 1>(a, s);
+static cudaError_t launch_round_tc_body(const RoundArgs& a, cudaStream_t s) {
     const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + kTP - 1) / kTP * kTP;
     if (per_cta <= BitCounter<8>::capacity()) return launch_tc_t<true, 8>(a, s);
     if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12>(a, s);
     return launch_tc_t<true, 20>(a, s);
+}
+cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
+#ifdef SEGHDC_TRACE
+    // events around [stamp0], [round kernel], [stamp1] separately (read with read_tc_events)
+    static cudaEvent_t ev[4] = {};
+    if (!ev[0]) {
+        for (auto& e : ev) cudaEventCreate(&e);
+        const char* tr = getenv("SEGHDC_TRACE_ROUND");
+        const int r = tr ? atoi(tr) : 0;
+        cudaMemcpyToSymbol(g_trace_round, &r, sizeof(r));
+    }
+    const char* tr = getenv("SEGHDC_TRACE_ROUND");
+    if (tr && int(a.round) != atoi(tr)) {  // only the traced round records events and stamps
+        return a.K != 2 ? launch_tc_t<false, 1>(a, s) : launch_round_tc_body(a, s);
+    }
+    cudaEventRecord(ev[0], s);
+    k_tc_stamp<<<148, 1, 0, s>>>(0);
+    cudaEventRecord(ev[1], s);
+    struct After {
+        cudaStream_t s;
+        cudaEvent_t* ev;
+        ~After() {
+            cudaEventRecord(ev[2], s);
+            k_tc_stamp<<<148, 1, 0, s>>>(2);
+            cudaEventRecord(ev[3], s);
+        }
+    } after{s, ev};
+    g_tc_events = ev;
+#endif
+    return a.K != 2 ? launch_tc_t<false, 1>(a, s) : launch_round_tc_body(a, s);
 }
 
 }  // namespace seghdc_dev
