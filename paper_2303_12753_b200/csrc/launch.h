@@ -73,10 +73,6 @@ struct FinishArgs {
     void* state;
     uint32_t round;
     int early_stop;
-    // incremental re-bundling (tcgen05 kernel, K == 2): xchg row 1 holds the round's delta of
-    // cluster 1's member sums; run1[parity][Dp] are the running sums (read p, write p ^ 1)
-    int inc;
-    uint32_t* run1;
 };
 void launch_prep_finish(void* state, uint32_t K, uint32_t np, cudaStream_t s);
 void launch_finish(const FinishArgs& a, cudaStream_t s);
@@ -121,7 +117,12 @@ size_t tc_smem_bytes(uint32_t W32);
 size_t tc_bimg_bytes(uint32_t W32);
 uint32_t tc_tile_pixels();
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32);
-uint64_t tc_max_value();  // centroid entries above this need the IMMA kernels
+uint64_t tc_max_value();
+// incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of
+// cluster 1's member sums, run1[parity][Dp] the running sums (read p, write p ^ 1)
+void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
+                      uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
+                      cudaStream_t s);  // centroid entries above this need the IMMA kernels
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
                        cudaStream_t s);
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s);

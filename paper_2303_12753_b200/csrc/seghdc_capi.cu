@@ -117,7 +117,9 @@ struct seghdc_ctx {
     DevBuf<uint8_t> bimg;                     // tcgen05 kernel: centroid B image
     alignas(64) unsigned char tmap[128] = {};  // tcgen05 kernel: CUtensorMap of the grid
     DevBuf<uint32_t> labels, Z;
-    DevBuf<uint32_t> run1;  // tcgen05 K == 2: running member sums of cluster 1, [2][Dp] by parity
+    DevBuf<uint32_t> run1;    // tcgen05 K == 2: running member sums of cluster 1, [2][Dp] by parity
+    DevBuf<uint32_t> ticket;  // k_finish_tc: last-block detection
+    bool xchg_clean = false;  // the fused finish left the exchange buffer zeroed
     DevBuf<int32_t> xchg;
     DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
     DevBuf<uint64_t> seeds;
@@ -280,7 +282,12 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
     if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(g.W32));
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
-    if (x.incremental()) x.run1.ensure(2 * size_t(g.Dp));
+    if (x.incremental()) {
+        x.run1.ensure(2 * size_t(g.Dp));
+        x.ticket.ensure(1);
+        ck(cudaMemsetAsync(x.ticket.p, 0, 4, x.stream), "clear ticket");
+    }
+    x.xchg_clean = false;
     x.colsum.ensure(g.Dp);
     x.seeds.ensure(std::max<size_t>(K, 1));
     x.slots.ensure(2 + K);
@@ -330,6 +337,14 @@ void select_seeds_dev(seghdc_ctx& x, size_t K) {
 }
 
 void finish(seghdc_ctx& x, int mode, uint32_t round) {
+    if (mode == 0 && x.incremental()) {  // one fused kernel per round
+        launch_finish_tc(x.g.D, x.g.W32, x.g.Dp, x.xchg.p, x.colsum_ptr(), x.Z.p, x.run1.p, x.bimg.p, x.state.p,
+                         round, x.early_stop, x.ticket.p, x.stream);
+        x.count();
+        x.check_launch();
+        x.xchg_clean = true;
+        return;
+    }
     const uint32_t np = (round & 1) ^ 1;
     launch_prep_finish(x.state.p, uint32_t(x.K), np, x.stream);
     FinishArgs f{};
@@ -347,8 +362,6 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.state = x.state.p;
     f.round = round;
     f.early_stop = x.early_stop;
-    f.inc = x.incremental() ? 1 : 0;
-    f.run1 = x.run1.p;
     launch_finish(f, x.stream);
     x.count(2);
     if (x.plan.tc) {
@@ -418,7 +431,8 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.bimg = x.bimg.p;
     a.nks = tc_ksteps(x.g.W32);
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
-    ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
+    if (!x.xchg_clean) ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
+    x.xchg_clean = false;
     cudaEvent_t ev_end = nullptr;
     if (x.profiling) {
         if (x.prof_used == x.prof_events.size()) {

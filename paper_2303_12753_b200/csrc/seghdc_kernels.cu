@@ -383,7 +383,7 @@ void launch_accumulate(const AccumulateArgs& a, cudaStream_t s) {
 // =============================================================================================
 __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
                          const int32_t* __restrict__ xchg, const int32_t* __restrict__ colsum, uint32_t* Z,
-                         uint8_t* bfrag, void* state, uint32_t round, int early_stop, int inc, uint32_t* run1) {
+                         uint8_t* bfrag, void* state, uint32_t round, int early_stop) {
     StateView st = StateView::at(state, K);
     const uint32_t p = round & 1, np = p ^ 1;  // set produced here is used by round+1
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(xchg) + size_t(K) * Dp;
@@ -403,12 +403,7 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
         const size_t i = size_t(word) * 32 + lane;
         const bool in = i < D;
         uint32_t z;
-        if (mode == 0 && inc) {  // K == 2: S1 = running sums + this round's delta, S0 = colsum - S1
-            const uint32_t s1 = run1[size_t(p) * Dp + i] + uint32_t(xchg[Dp + i]);
-            if (c == 1) run1[size_t(np) * Dp + i] = s1;
-            if (counts[c] != 0) z = c == 1 ? s1 : uint32_t(colsum[i]) - s1;
-            else z = in ? Z[size_t(c) * D + i] : 0u;  // empty cluster keeps its previous centroid
-        } else if (mode == 2) {
+        if (mode == 2) {
             z = in ? Z[size_t(c) * D + i] : 0u;
         } else if (mode == 1 || counts[c] != 0) {
             if (int(c) == skip) {
@@ -459,8 +454,7 @@ void launch_finish(const FinishArgs& a, cudaStream_t s) {
     const uint32_t threads = 256;
     const uint64_t total = uint64_t(a.W32) * a.K * 32;
     k_finish<<<uint32_t((total + threads - 1) / threads), threads, 0, s>>>(
-        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop,
-        a.inc, a.run1);
+        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop);
 }
 
 // Zero the accumulators of parity np before k_finish accumulates into them.

@@ -604,6 +604,94 @@ __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_
     }
 }
 
+// Per-round finish of the incremental K == 2 schedule, fused (replaces the exchange memset,
+// k_prep_finish, k_finish and k_build_bimg of a round): one warp per HV word.
+//   early stop (clusterer.cpp:213); S1 = running sums + delta (all-reduced xchg row 1);
+//   Z1 = S1, Z0 = colsum - S1, empty clusters keep their centroid (clusterer.cpp:184-186);
+//   norm2 of the new set (hypervector.cpp:123-127) into parity np, norm2[p] zeroed for the
+//   next finish; the word's 16 x 16 B-image bytes (digits via the offset trick: for
+//   O = 4 (8^kP8 - 1) / 7, digit p of z is ((z + O) >> 3p & 7) - 4); the word's exchange
+//   sums are cleared after use, and the last block clears the counts / changed tail.
+__global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* __restrict__ xchg,
+                                                   const int32_t* __restrict__ colsum, uint32_t* __restrict__ Z,
+                                                   uint32_t* __restrict__ run1, uint8_t* __restrict__ bimg,
+                                                   void* state, uint32_t round, int early_stop,
+                                                   uint32_t* __restrict__ ticket) {
+    constexpr uint32_t K = 2;
+    StateView st = StateView::at(state, K);
+    const uint32_t p = round & 1, np = p ^ 1;
+    uint32_t* tail = reinterpret_cast<uint32_t*>(xchg) + size_t(K) * Dp;  // [counts[2] | changed]
+    if (st.hdr->done) return;
+    const uint32_t cnt0 = tail[0], cnt1 = tail[1];
+    if (early_stop && round > 1 && tail[K] == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st.hdr->done = 1;
+        return;
+    }
+    const uint32_t lane = threadIdx.x & 31, word = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (word < W32) {
+        const uint32_t i = 32 * word + lane;
+        const bool in = i < D;
+        const uint32_t s1 = run1[size_t(p) * Dp + i] + uint32_t(xchg[Dp + i]);
+        run1[size_t(np) * Dp + i] = s1;
+        xchg[i] = 0;
+        xchg[Dp + i] = 0;
+        uint32_t z0 = cnt0 ? uint32_t(colsum[i]) - s1 : (in ? Z[i] : 0u);
+        uint32_t z1 = cnt1 ? s1 : (in ? Z[D + i] : 0u);
+        if (!in) z0 = z1 = 0;
+        if (in) {
+            Z[i] = z0;
+            Z[D + i] = z1;
+        }
+        unsigned long long n0 = (unsigned long long)z0 * z0, n1 = (unsigned long long)z1 * z1;
+        for (int o = 16; o; o >>= 1) {
+            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+        }
+        if (lane == 0) {
+            atomicAdd(st.norm2 + np * K, n0);
+            atomicAdd(st.norm2 + np * K + 1, n1);
+        }
+        // B image bytes of this word: word h = word & 1 of k-step word >> 1 is core matrix h;
+        // lane = (row n, half): row n = kP8 * cluster + digit, bytes 8 * half .. + 7
+        constexpr uint32_t kOff = 4u * ((1u << (3 * kP8)) - 1) / 7u;
+        const uint32_t n = lane >> 1, hb = lane & 1, cl = n / kP8, pd = n % kP8;
+        uint64_t v = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 16; ++q) {  // nibble q of the lane's 8 bytes: k = 16 hb + q
+            const uint32_t k = 16 * hb + q, c = k >> 3, j = k & 7;
+            const uint32_t src = 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
+            const uint32_t za = __shfl_sync(0xffffffffu, z0, src), zb = __shfl_sync(0xffffffffu, z1, src);
+            const int d = int(((cl ? zb : za) + kOff) >> (3 * pd) & 7u) - 4;
+            const uint32_t a = uint32_t(d < 0 ? -d : d);
+            const uint32_t code = ((c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u)) |
+                                  (d < 0 ? 8u : 0u);
+            v |= uint64_t(code) << (4 * q);
+        }
+        *reinterpret_cast<uint64_t*>(bimg + size_t(word >> 1) * kKB + (n >> 3) * 256 + (word & 1) * 128 +
+                                     (n & 7) * 16 + 8 * hb) = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < K) {
+        st.norm2[p * K + threadIdx.x] = 0;
+        st.cur[np * K + threadIdx.x] = threadIdx.x ? cnt1 : cnt0;
+    }
+    // the last block to finish clears the counts / changed tail for the next round
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            tail[0] = tail[1] = tail[K] = 0;
+            *ticket = 0;
+        }
+    }
+}
+
+void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
+                      uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
+                      cudaStream_t s) {
+    k_finish_tc<<<(W32 + 7) / 8, 256, 0, s>>>(D, W32, Dp, xchg, colsum, Z, run1, bimg, state, round, early_stop,
+                                              ticket);
+}
+
 namespace {
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
