@@ -117,6 +117,12 @@ size_t tc_smem_bytes(uint32_t W32);
 size_t tc_bimg_bytes(uint32_t W32);
 uint32_t tc_tile_pixels();
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32);
+struct ExpandArgs {  // closed-form Manhattan codebooks (seghdc_host::manhattan_bases)
+    uint32_t dim, h, w, c, beta, x_row, x_col, wref;
+    uint32_t off[3], unit[3];
+};
+void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_t* row, uint32_t* col, uint32_t* wid,
+                             cudaStream_t s);
 uint64_t tc_max_value();
 // incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of
 // cluster 1's member sums, run1[parity][Dp] the running sums (read p, write p ^ 1)

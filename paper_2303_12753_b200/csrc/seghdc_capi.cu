@@ -99,6 +99,7 @@ struct seghdc_ctx {
     size_t h = 0, w = 0, c = 0;
     // codebooks
     DevBuf<uint32_t> row, col, wid;
+    DevBuf<uint64_t> cb_bases;  // closed-form Manhattan codebooks: bases expanded on the device
     size_t cb_dim = 0, cb_h = 0, cb_w = 0, cb_c = 0;
     // grid (rows [row_begin,row_end) of an h_total x w image)
     DevBuf<uint32_t> grid;
@@ -184,6 +185,37 @@ void load_codebooks(seghdc_ctx& x, size_t dim, size_t h, size_t w, size_t c, con
     x.cb_h = h;
     x.cb_w = w;
     x.cb_c = c;
+}
+
+// Manhattan codebooks from their bases: only (2 + C) HVs cross PCIe, the tables are expanded
+// on the device (k_expand_codebooks); same tables as load_codebooks of the host-built ones.
+void load_codebooks_closed(seghdc_ctx& x, const seghdc_host::ManhattanParams& p, const uint64_t* bases) {
+    const size_t wph = (p.dim + 63) / 64, wref = 2 * wph;
+    x.row.ensure(size_t(p.h) * wref);
+    x.col.ensure(size_t(p.w) * wref);
+    x.wid.ensure(size_t(p.c) * 256 * wref);
+    x.cb_bases.ensure((2 + p.c) * wph);
+    ck(cudaMemcpyAsync(x.cb_bases.p, bases, (2 + p.c) * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload bases");
+    ExpandArgs a{};
+    a.dim = p.dim;
+    a.h = p.h;
+    a.w = p.w;
+    a.c = p.c;
+    a.beta = p.beta;
+    a.x_row = p.x_row;
+    a.x_col = p.x_col;
+    a.wref = uint32_t(wref);
+    for (int i = 0; i < 3; ++i) {
+        a.off[i] = p.off[i];
+        a.unit[i] = p.unit[i];
+    }
+    launch_expand_codebooks(reinterpret_cast<const uint32_t*>(x.cb_bases.p), a, x.row.p, x.col.p, x.wid.p, x.stream);
+    x.count();
+    x.check_launch();
+    x.cb_dim = p.dim;
+    x.cb_h = p.h;
+    x.cb_w = p.w;
+    x.cb_c = p.c;
 }
 
 void set_grid_shape(seghdc_ctx& x, size_t h, size_t w, size_t dim, size_t r0, size_t r1) {
@@ -721,20 +753,30 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
         seghdc_host::validate_cluster(k, iterations, h * w);
         const auto t_total = Clock::now();
         const size_t wph = (dim + 63) / 64;
-        std::vector<uint64_t> row(h * wph), col(w * wph), wid(c * 256 * wph);
-        std::mt19937_64 rng(seed);
-        auto t = Clock::now();
-        seghdc_host::build_position(dim, h, w, alpha, beta, encoder, rng, row.data(), col.data());
-        const double t_pos = ms(t);
-        t = Clock::now();
-        seghdc_host::build_color(dim, c, gamma, encoder, rng, wid.data());
-        const double t_col = ms(t);
+        std::mt19937_64 rng(seed);  // one stream: position codebook, then colour (pipeline.cpp:43-59)
+        double t_pos = 0, t_col = 0;
         cudaEvent_t e0, e1, e2;
         ck(cudaEventCreate(&e0), "event");
         ck(cudaEventCreate(&e1), "event");
         ck(cudaEventCreate(&e2), "event");
         load_image(*ctx, pixels, h, w, c);
-        load_codebooks(*ctx, dim, h, w, c, row.data(), col.data(), wid.data());
+        if (encoder == SEGHDC_ENCODER_MANHATTAN) {  // closed form: bases on the host, tables on the device
+            std::vector<uint64_t> bases((2 + c) * wph);
+            auto t = Clock::now();
+            const auto p = seghdc_host::manhattan_bases(dim, h, w, c, alpha, beta, gamma, rng, bases.data());
+            t_pos = ms(t);
+            load_codebooks_closed(*ctx, p, bases.data());
+        } else {
+            std::vector<uint64_t> row(h * wph), col(w * wph), wid(c * 256 * wph);
+            auto t = Clock::now();
+            seghdc_host::build_position(dim, h, w, alpha, beta, encoder, rng, row.data(), col.data());
+            t_pos = ms(t);
+            t = Clock::now();
+            seghdc_host::build_color(dim, c, gamma, encoder, rng, wid.data());
+            t_col = ms(t);
+            load_codebooks(*ctx, dim, h, w, c, row.data(), col.data(), wid.data());
+            ck(cudaStreamSynchronize(ctx->stream), "sync");  // the host tables go out of scope
+        }
         ck(cudaEventRecord(e0, ctx->stream), "event");
         encode_rows(*ctx, 0, h);
         ck(cudaEventRecord(e1, ctx->stream), "event");

@@ -156,6 +156,40 @@ void build_color(size_t dim, size_t c, size_t gamma, int encoder, std::mt19937_6
     }
 }
 
+ManhattanParams manhattan_bases(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta, size_t gamma,
+                                std::mt19937_64& rng, uint64_t* bases) {
+    validate_position(dim, h, w, alpha, beta);
+    validate_color(dim, c, gamma);
+    const size_t nw = words_for(dim);
+    ManhattanParams p{};
+    p.dim = uint32_t(dim);
+    p.h = uint32_t(h);
+    p.w = uint32_t(w);
+    p.c = uint32_t(c);
+    p.beta = uint32_t(beta);
+    p.x_row = uint32_t(flip_unit(alpha, dim, h));
+    p.x_col = uint32_t(flip_unit(alpha, dim, w));
+    random_hv(bases, dim, rng);       // position_axis(rows): Hypervector::random
+    random_hv(bases + nw, dim, rng);  // position_axis(cols)
+    std::memset(bases + 2 * nw, 0, c * nw * 8);
+    size_t offset = 0;
+    for (size_t ch = 0; ch < c; ++ch) {
+        const size_t d_ch = channel_dim(dim, c, ch);
+        std::vector<uint64_t> entry(words_for(d_ch));
+        random_hv(entry.data(), d_ch, rng);  // build_color_codebook: the channel's base entry
+        uint64_t* dst = bases + (2 + ch) * nw;
+        const size_t w0 = offset >> 6, sh = offset & 63;
+        for (size_t k = 0; k < entry.size(); ++k) {
+            dst[w0 + k] |= entry[k] << sh;
+            if (sh && w0 + k + 1 < nw) dst[w0 + k + 1] |= entry[k] >> (64 - sh);
+        }
+        p.off[ch] = uint32_t(offset);
+        p.unit[ch] = uint32_t(unit_flip(dim, c, gamma, ch));
+        offset += d_ch;
+    }
+    return p;
+}
+
 // ---- synthetic nuclei images -----------------------------------------------
 // One std::mt19937_64(seed) stream; uniforms u = (x >> 11) * 2^-53; normals by Box-Muller
 // (cos branch only); ellipses drawn as (cy, cx, a, b, theta, class); inside test at pixel

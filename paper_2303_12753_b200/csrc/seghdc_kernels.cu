@@ -30,6 +30,44 @@ constexpr uint64_t counter_capacity() {
     } while (0)
 
 // =============================================================================================
+// Manhattan codebooks expanded on the device from their bases (seghdc_host::manhattan_bases):
+// entry e < h is row e, then the w columns, then the C x 256 widened colour entries; each is
+// its base XOR one run of ones. Output in the u32 table layout of seghdc_encode (wref words).
+// =============================================================================================
+__device__ __forceinline__ uint32_t run_mask32(uint32_t q, uint32_t s, uint32_t e) {  // bits [s, e) of word q
+    const uint32_t lo = max(s, 32 * q), hi = min(e, 32 * q + 32);
+    if (lo >= hi) return 0u;
+    const uint32_t len = hi - lo, sh = lo - 32 * q;
+    return (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << sh;
+}
+__global__ void k_expand_codebooks(const uint32_t* __restrict__ bases, ExpandArgs a, uint32_t* __restrict__ row,
+                                   uint32_t* __restrict__ col, uint32_t* __restrict__ wid) {
+    const uint32_t ne = a.h + a.w + a.c * 256;
+    const size_t total = size_t(ne) * a.wref;
+    for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t e = uint32_t(t / a.wref), q = uint32_t(t % a.wref);
+        uint32_t b, s, len;
+        uint32_t* out;
+        if (e < a.h) {
+            b = 0, s = 0, len = (e / a.beta) * a.x_row, out = row + size_t(e) * a.wref;
+        } else if (e < a.h + a.w) {
+            const uint32_t j = e - a.h;
+            b = 1, s = a.dim / 2, len = (j / a.beta) * a.x_col, out = col + size_t(j) * a.wref;
+        } else {
+            const uint32_t ch = (e - a.h - a.w) >> 8, v = (e - a.h - a.w) & 255;
+            b = 2 + ch, s = a.off[ch], len = v * a.unit[ch], out = wid + size_t(ch * 256 + v) * a.wref;
+        }
+        out[q] = bases[size_t(b) * a.wref + q] ^ run_mask32(q, s, s + len);
+    }
+}
+void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_t* row, uint32_t* col, uint32_t* wid,
+                             cudaStream_t s) {
+    const size_t total = size_t(a.h + a.w + a.c * 256) * a.wref;
+    const uint32_t blocks = uint32_t(std::min<size_t>((total + 255) / 256, 148 * 8));
+    k_expand_codebooks<<<blocks, 256, 0, s>>>(bases, a, row, col, wid);
+}
+
+// =============================================================================================
 // encode_image (reference pixel_pipeline.cpp:92-126): grid[p] = row[i] ^ col[j] ^ ^_ch wid[ch][v]
 // fused with the column sums of the grid (the Harley-Seal counter of every pixel), which the
 // round schedule needs to derive the largest cluster's sums without accumulating them.
