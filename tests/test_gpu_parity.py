@@ -223,3 +223,39 @@ def test_config_large_golden(ctx, golden_configs, name):
     assert rounds == g["round_labels_sha256"]
     assert sha(res["centroids"]) == g["centroids_sha256"]
     assert res["counts"].tolist() == g["counts"]
+
+
+# ---------------------------------------------------------------- run_pipeline (closed-form codebooks)
+@pytest.mark.parametrize("dim,h,w,c,enc,alpha,beta,gamma,k,its,seed", [
+    (10000, 30, 41, 1, "manhattan", 1.0, 26, 1, 2, 6, 0), (10000, 64, 80, 3, "manhattan", 1.0, 26, 1, 2, 5, 3),
+    (2003, 17, 19, 3, "manhattan", 1.0, 3, 2, 3, 4, 11), (4096, 12, 9, 1, "manhattan", 0.5, 1, 4, 2, 7, 5),
+    (1500, 10, 11, 3, "rpos", 1.0, 2, 1, 2, 4, 9), (1500, 10, 11, 3, "rcolor", 1.0, 2, 1, 2, 4, 9),
+    (16384, 21, 23, 3, "manhattan", 1.0, 5, 1, 4, 3, 1),
+])
+def test_run_pipeline_matches_oracle(ctx, port, dim, h, w, c, enc, alpha, beta, gamma, k, its, seed):
+    """run_pipeline (pipeline.cpp:40-75): the Manhattan codebooks are expanded on the device from
+    their bases; labels and rounds equal the oracle's encode + cluster of the host-built tables."""
+    rng = np.random.default_rng(dim + h * w + seed)
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    img[: h // 2] //= 4  # a dark half: two clear clusters
+    cfg = S.RunConfig(dim=dim, alpha=alpha, beta=beta, gamma=gamma, clusters=k, iterations=its, seed=seed,
+                      encoder=enc, early_stop=False)
+    res = ctx.run_pipeline(img, cfg)
+    cb = S.build_codebooks(dim, h, w, c, alpha, beta, gamma, seed, enc)
+    exp = port.cluster(port.encode(img, dim, *cb), img, dim, k, its, False)
+    assert res.iterations_run == exp["rounds"]
+    assert (res.mask.reshape(-1) == exp["labels"]).all()
+
+
+def test_run_pipeline_c1_golden(ctx, golden_configs):
+    """The bench's end-to-end call on config C1 reproduces the reference's golden labels."""
+    g, spec = golden_configs["C1"], golden_configs["_meta"]["configs"]["C1"]
+    img = S.synth_image(1, 0)
+    cfg = S.RunConfig(dim=spec["dim"], alpha=spec["alpha"], beta=26, gamma=1, clusters=spec["k"],
+                      iterations=spec["iterations"], seed=0, early_stop=False)
+    res = ctx.run_pipeline(img, cfg)
+    assert sha(res.mask.astype(np.uint32).reshape(-1)) == g["labels_sha256"] and res.iterations_run == g["rounds"]
+    cfg.early_stop = True
+    res = ctx.run_pipeline(img, cfg)
+    assert sha(res.mask.astype(np.uint32).reshape(-1)) == g["early_stop_labels_sha256"]
+    assert res.iterations_run == g["early_stop_rounds"]
