@@ -158,6 +158,11 @@ int seghdc_profile_read_each(seghdc_ctx* ctx, double* total_ms, uint64_t* count,
 /* ---- synthetic inputs (bench/test workloads) --------------------------- */
 /* config_id 0..4 = BASELINE.json configs; config 2 is config 0's construction (use seed
  * 0..63 per image). Writes h*w*c bytes. Returns the shape through h/w/c when out is NULL. */
+/* Page-locked host memory (cudaHostAlloc, portable) for result buffers: device->host copies
+ * of labels into it run at full PCIe rate instead of through the driver's pageable staging. */
+int seghdc_pinned_alloc(size_t bytes, void** out);
+int seghdc_pinned_free(void* p);
+
 int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w,
                        size_t* c);
 

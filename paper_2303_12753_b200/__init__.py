@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+import weakref
 from typing import Callable, Optional
 
 import numpy as np
@@ -77,6 +78,8 @@ SIGNATURES = {
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
     "seghdc_profile_read_each": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_void_p, _sz], C.c_int),
+    "seghdc_pinned_alloc": ([_sz, C.POINTER(C.c_void_p)], C.c_int),
+    "seghdc_pinned_free": ([C.c_void_p], C.c_int),
     "seghdc_synth_image": ([C.c_int, C.c_uint64, C.c_void_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
 }
 
@@ -139,6 +142,30 @@ def build_codebooks(dim: int, h: int, w: int, channels: int, alpha: float = 0.2,
     _check(lib().seghdc_build_codebooks(dim, h, w, channels, float(alpha), beta, gamma, seed, ENCODERS[encoder], row,
                                         col, wid))
     return row.reshape(h, wph), col.reshape(w, wph), wid.reshape(channels, 256, wph)
+
+
+_pinned_free: dict = {}  # nbytes -> [pointers]: page-locked buffers returned by dead arrays
+
+
+def _return_pinned(nbytes: int, ptr: int) -> None:
+    _pinned_free.setdefault(nbytes, []).append(ptr)
+
+
+def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
+    """An uninitialised array in page-locked host memory (seghdc_pinned_alloc), recycled
+    through a process-wide pool once every view of it is gone."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    free = _pinned_free.get(nbytes)
+    if free:
+        ptr = free.pop()
+    else:
+        p = C.c_void_p()
+        _check(lib().seghdc_pinned_alloc(nbytes, C.byref(p)))
+        ptr = p.value
+    raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(max(nbytes, 1),))
+    weakref.finalize(raw.base, _return_pinned, nbytes, ptr)
+    return raw[:nbytes].view(dtype).reshape(shape)
 
 
 def synth_image(config_id: int, seed: int = 0) -> np.ndarray:
@@ -280,7 +307,7 @@ class Context:
         """run_pipeline (pipeline.hpp:55-56)."""
         img = _img3(img)
         h, w, c = img.shape
-        labels = np.zeros(h * w, np.uint32)
+        labels = pinned_empty(h * w, np.uint32)  # page-locked: the label download runs at PCIe rate
         rounds = _sz(0)
         timings = (C.c_double * 5)()
         cb = ROUND_CB(0)

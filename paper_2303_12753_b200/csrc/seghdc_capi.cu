@@ -912,6 +912,17 @@ int seghdc_profile_read_each(seghdc_ctx* ctx, double* total_ms, uint64_t* count,
     });
 }
 
+int seghdc_pinned_alloc(size_t bytes, void** out) {
+    return guarded(nullptr, [&] {
+        require(out != nullptr, "pinned_alloc: null output pointer");
+        ck(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable), "cudaHostAlloc");
+    });
+}
+
+int seghdc_pinned_free(void* p) {
+    return guarded(nullptr, [&] { ck(cudaFreeHost(p), "cudaFreeHost"); });
+}
+
 int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c) {
     return guarded(nullptr, [&] { seghdc_host::synth_image(config_id, seed, out, h, w, c); });
 }
