@@ -52,6 +52,9 @@ int seghdc_set_stream(seghdc_ctx* ctx, void* cuda_stream);
 int seghdc_synchronize(seghdc_ctx* ctx);
 /* Number of device kernels this context has launched so far (for launch accounting). */
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx);
+/* Name of the round kernel the last clustering plan selected ("k_round_tc", "k_round_fused",
+ * "k_round"; "" before any plan). */
+const char* seghdc_round_kernel(const seghdc_ctx* ctx);
 
 /* ---- host-side codebooks (stay on the host: mt19937_64 is sequential and cheap) -------- */
 /* run_pipeline's codebook stage (pipeline.cpp:43-59): one Rng(seed), position codebook

@@ -49,6 +49,7 @@ SIGNATURES = {
     "seghdc_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
     "seghdc_synchronize": ([C.c_void_p], C.c_int),
     "seghdc_kernel_launches": ([C.c_void_p], C.c_uint64),
+    "seghdc_round_kernel": ([C.c_void_p], C.c_char_p),
     "seghdc_build_codebooks": ([_sz, _sz, _sz, _sz, C.c_double, _sz, _sz, C.c_uint64, C.c_int, _u64p, _u64p, _u64p],
                                C.c_int),
     "seghdc_validate_run": ([_sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz], C.c_int),
@@ -218,6 +219,11 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(lib().seghdc_kernel_launches(self.h))
+
+    @property
+    def round_kernel(self) -> str:
+        """Round kernel of the current clustering plan (k_round_tc / k_round_fused / k_round)."""
+        return lib().seghdc_round_kernel(self.h).decode()
 
     def profile_rounds(self, enable: bool) -> None:
         self.check(lib().seghdc_profile_rounds(self.h, int(enable)))

@@ -610,6 +610,11 @@ int seghdc_synchronize(seghdc_ctx* ctx) {
 
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+const char* seghdc_round_kernel(const seghdc_ctx* ctx) {
+    if (!ctx || ctx->K == 0) return "";
+    return ctx->plan.tc ? "k_round_tc" : ctx->plan.fused ? "k_round_fused" : "k_round";
+}
+
 int seghdc_build_codebooks(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta, size_t gamma,
                            uint64_t seed, int encoder, uint64_t* row_out, uint64_t* col_out, uint64_t* widened_out) {
     return guarded(nullptr, [&] {

@@ -320,6 +320,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             tc_fence_after();
             if (warp == 0 && g % nch == 0) TC_TR(1, g / nch);
             const uint8_t* row = ring + size_t(s) * kChunkBytes + r * 128;
+            // both shifts run on the FMA pipe (IMAD.SHL, IMAD.HI with an opaque 2^31), leaving the
+            // ALU pipe the four masks per word
+            const uint32_t half = opaque(0x80000000u), two = opaque(2u);
 #pragma unroll
             for (uint32_t c16 = 0; c16 < 8; ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
                 const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
@@ -329,8 +332,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 for (int i = 0; i < 4; ++i) {  // A column 4i + c: class c of word i (see header)
                     a[4 * i + 0] = w4[i] & 0x22222222u;
                     a[4 * i + 1] = w4[i] & 0x44444444u;
-                    a[4 * i + 2] = (w4[i] << 1) & 0x22222222u;
-                    a[4 * i + 3] = (w4[i] >> 1) & 0x44444444u;
+                    a[4 * i + 2] = (w4[i] * two) & 0x22222222u;
+                    a[4 * i + 3] = __umulhi(w4[i], half) & 0x44444444u;
                 }
                 tc_st16(lane_addr + ab * 128 + c16 * 16, a);  // k-steps 2*c16, 2*c16+1: 8 columns each
             }

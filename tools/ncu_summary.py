@@ -32,21 +32,27 @@ def launches(path, out):
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[start]
     iN, iV, iU = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = collections.defaultdict(lambda: [0, 0.0])
+    iM = hdr.index("Metric Name")
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])  # launches, ns, DRAM bytes
+    scale = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for r in rows[start + 1:]:
         if len(r) <= iV:
             continue
         name = r[iN].split("(")[0].replace("void ", "")
-        v = float(r[iV].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[iU], 1)
-        agg[name][0] += 1
-        agg[name][1] += v
-    tot = sum(v for _, v in agg.values())
+        v = float(r[iV].replace(",", "")) * scale.get(r[iU], 1)
+        if r[iM] == "gpu__time_duration.sum":
+            agg[name][0] += 1
+            agg[name][1] += v
+        elif r[iM].startswith("dram__bytes_"):
+            agg[name][2] += v
+    tot = sum(v[1] for v in agg.values())
     with open(out, "w") as f:
-        f.write(f"# Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`), from `{path}`\n\n")
+        f.write(f"# Launch list (`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                f"--clock-control none`), from `{path}`\n\n")
         f.write("Cold-cache, serialised per-launch times: compare shares, not absolutes.\n\n")
-        f.write("| kernel | launches | total us | share | avg us |\n|---|---|---|---|---|\n")
-        for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
-            f.write(f"| `{k}` | {c} | {v / 1e3:.1f} | {100 * v / tot:.1f} % | {v / c / 1e3:.2f} |\n")
+        f.write("| kernel | launches | total us | share | avg us | DRAM MB / launch |\n|---|---|---|---|---|---|\n")
+        for k, (c, v, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"| `{k}` | {c} | {v / 1e3:.1f} | {100 * v / tot:.1f} % | {v / c / 1e3:.2f} | {b / c / 1e6:.1f} |\n")
 
 
 def kernel(path, out):
