@@ -105,6 +105,9 @@ struct RoundArgs {
     const void* tmap;     // CUtensorMap of the grid (tc_make_grid_map)
     const uint8_t* bimg;  // centroid B image (launch_build_bimg)
     uint32_t nks;         // k-steps of 64 HV dims (tc_ksteps)
+    uint32_t* flist;        // non-null: append changed pixels here (k_fold_list folds them) instead of folding
+    uint32_t* flist_count;  // entries appended (zeroed before the round)
+    uint32_t serpentine;     // odd rounds walk the tiles backwards
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);
@@ -126,6 +129,8 @@ void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_
 uint64_t tc_max_value();
 // incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of
 // cluster 1's member sums, run1[parity][Dp] the running sums (read p, write p ^ 1)
+void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, const uint32_t* grid,
+                      uint32_t S32, uint32_t W32, int32_t* dst, uint32_t sms, cudaStream_t s);
 void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
                       uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
                       cudaStream_t s);  // centroid entries above this need the IMMA kernels

@@ -91,6 +91,7 @@ struct seghdc_ctx {
     bool own_stream = false;
     int sms = 148;
     size_t smem_optin = 0;
+    size_t l2_bytes = 126u << 20;
     std::string err;
     uint64_t launches = 0;
 
@@ -120,6 +121,7 @@ struct seghdc_ctx {
     DevBuf<uint32_t> labels, Z;
     DevBuf<uint32_t> run1;    // tcgen05 K == 2: running member sums of cluster 1, [2][Dp] by parity
     DevBuf<uint32_t> ticket;  // k_finish_tc: last-block detection
+    DevBuf<uint32_t> flist;   // round 1 of the incremental schedule: changed pixels, then their count
     bool xchg_clean = false;  // the fused finish left the exchange buffer zeroed
     DevBuf<int32_t> xchg;
     DevBuf<int32_t> colsum;  // this rank's column sums of its grid (valid while colsum_valid)
@@ -316,6 +318,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
     if (x.incremental()) {
         x.run1.ensure(2 * size_t(g.Dp));
+        x.flist.ensure(n + 1);
         x.ticket.ensure(1);
         ck(cudaMemsetAsync(x.ticket.p, 0, 4, x.stream), "clear ticket");
     }
@@ -462,6 +465,17 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.tmap = x.tmap;
     a.bimg = x.bimg.p;
     a.nks = tc_ksteps(x.g.W32);
+    // round 1 of the incremental schedule folds every member of cluster 1: a global list and a
+    // whole-GPU fold kernel instead of the per-CTA fold warps (whose load is the nuclei's layout)
+    static const char* fe = getenv("SEGHDC_FLIST");
+    const bool use_flist = do_update && r == 1 && x.incremental() && !(fe && *fe == '0');
+    {
+        static const char* se = getenv("SEGHDC_SERPENTINE");
+        a.serpentine = (se && *se == '0') ? 0u : 1u;
+    }
+    a.flist = use_flist ? x.flist.p : nullptr;
+    a.flist_count = use_flist ? x.flist.p + x.n_local() : nullptr;
+    if (use_flist) ck(cudaMemsetAsync(a.flist_count, 0, 4, x.stream), "clear fold list");
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     if (!x.xchg_clean) ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     x.xchg_clean = false;
@@ -479,6 +493,12 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     ck(launch_round(a, x.plan, x.stream), "round kernel");
     if (ev_end) ck(cudaEventRecord(ev_end, x.stream), "event");
     x.count();
+    if (use_flist) {
+        launch_fold_list(a.flist, a.flist_count, x.n_local(), x.grid.p, x.g.S32, x.g.W32, x.xchg.p + x.g.Dp,
+                         uint32_t(x.sms), x.stream);
+        x.count();
+        x.check_launch();
+    }
     if (do_update && !x.plan.fused) {  // K >= 3: separate single-read accumulation pass
         AccumulateArgs u{};
         u.grid = x.grid.p;
@@ -565,6 +585,9 @@ int seghdc_create(int device, seghdc_ctx** out) {
         int optin = 0;
         ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
         ctx->smem_optin = size_t(optin);
+        int l2 = 0;
+        ck(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device), "attr");
+        if (l2 > 0) ctx->l2_bytes = size_t(l2);
         int major = 0;
         ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device), "attr");
         if (major != 10) throw Error(SEGHDC_ERUNTIME, "this build targets sm_100a (B200); device is sm_" + std::to_string(major) + "x");

@@ -117,6 +117,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                                 uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 // smem matrix descriptor: K-major, no swizzle, core matrices of 8 rows x 16 B; LBO = 128 (next
 // core matrix along K), SBO = 256 (next 8 rows), version 1 (tcgen05)
 __device__ __forceinline__ uint64_t bdesc_at(uint32_t saddr) {
@@ -220,7 +234,8 @@ template <bool UPD, int H>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
-               void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp) {
+               void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp,
+               uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine) {
     constexpr uint32_t NRT = kNRW * 32;
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -253,6 +268,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const uint32_t nch = (W32 + kCW - 1) / kCW;  // chunks per tile
     const uint64_t ntiles = (n + kTP - 1) / kTP;
     const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    // serpentine traversal: odd rounds walk the tiles from the end of the grid, even rounds from
+    // the start, so each round begins with the ~100 MB the previous pass (the encode, or the
+    // previous round) left in L2 and only the rest streams from HBM
+    const bool reverse = serpentine && (round & 1) != 0;
+    auto tile_px0 = [&](uint32_t it) -> uint64_t {
+        const uint64_t t = blockIdx.x + uint64_t(it) * gridDim.x;
+        return (reverse ? ntiles - 1 - t : t) * kTP;
+    };
 
     if (tid == 0) {
         for (uint32_t s = 0; s < kStages; ++s) {
@@ -296,7 +319,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     __syncthreads();
     tc_fence_after();
     if (warp == 0) TC_TG(1);
-    const bool folding = UPD && do_update;
+    // flist != nullptr (round 1: every member of cluster 1 enters): the changed pixels are
+    // appended to a global list that k_fold_list folds with the whole GPU after this kernel,
+    // instead of the fold warps reading them back tile by tile
+    const bool folding = UPD && do_update && flist == nullptr;
 
     if (warp < kWEpi) {
         // ------------------------------------------------------------------------ unpack warps
@@ -353,7 +379,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         uint32_t changed = 0, cnt1 = 0, total = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
-            const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * kTP;
+            const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
             const uint32_t old = live ? labels[px] : 0u;
@@ -397,10 +423,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 // shared-memory atomic (the fold warps reset the count once they have read it)
                 const uint32_t m = __ballot_sync(0xffffffffu, take);
                 uint32_t base = 0;
-                if (lane == 0 && m) base = atomicAdd(&s_listn[db], uint32_t(__popc(m)));
+                if (lane == 0 && m) base = atomicAdd(flist ? flist_count : &s_listn[db], uint32_t(__popc(m)));
                 base = __shfl_sync(0xffffffffu, base, 0);
-                if (take)
-                    s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
+                const uint32_t rank = __popc(m & ((1u << lane) - 1));
+                if (take && flist) flist[base + rank] = uint32_t(px) | (leave ? 0x80000000u : 0u);
+                else if (take) s_list[db * kTP + base + rank] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
             mbar_arrive(&list_ready[db]);
             if (qd == 0) TC_TR(5, it);
@@ -457,11 +484,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         // ----------------------------------------------------------------------- producer warp
         if (lane == 0) {
             const uint32_t bbytes = nks * kKB;
+            // the grid streams through L2 with evict_first (measured: evict_last on the tiles read
+            // last slows every round; evict_first takes round 1 from 98 to 82 us at C1)
+            const uint64_t pol_stream = policy_evict_first();
             mbar_expect_tx(b_full, bbytes);
             bulk_g2s(sB, bimg, bbytes, b_full);
             uint32_t g = 0;
             for (uint32_t it = 0; it < my_tiles; ++it) {
-                const int y = int((blockIdx.x + uint64_t(it) * gridDim.x) * kTP);
+                const int y = int(tile_px0(it));
                 for (uint32_t ch = 0; ch < nch; ++ch, ++g) {
                     const uint32_t s = g % kStages;
                     TC_CLK(c0);
@@ -470,7 +500,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                     TC_ACC(4, c1 - c0);
                     if (ch == 0) TC_TR(0, it);
                     mbar_expect_tx(&slot_full[s], kChunkBytes);
-                    tma_load_2d(ring + size_t(s) * kChunkBytes, &tmap, int(ch * kCW), y, &slot_full[s]);
+                    tma_load_2d_hint(ring + size_t(s) * kChunkBytes, &tmap, int(ch * kCW), y, &slot_full[s],
+                                     pol_stream);
                 }
             }
         }
@@ -492,8 +523,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             TCW(9, it, &list_ready[db], (it >> 1) & 1);
             if (fw == 0) TC_TR(6, it);
             if constexpr (UPD) {
-                if (do_update) {
-                    const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * kTP;
+                if (folding) {
+                    const uint64_t px0 = tile_px0(it);
                     const uint32_t* G = grid + px0 * S32;
                     const uint32_t M = s_listn[db];
                     const uint32_t* L = s_list + db * kTP;
@@ -695,6 +726,70 @@ void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, cons
                                               ticket);
 }
 
+// Fold of a global list of changed pixels (bit 31: leaving) into xchg row 1, as signed deltas:
+// CTA = 2 row groups x ceil(W32 / 32) warps, thread = word column; each CTA takes a contiguous
+// slice of the list, the groups interleave its rows (16 loads in flight per thread), their
+// counts meet in shared memory (u32[32][W32], bit-major: conflict-free both ways) and leave
+// with one global atomic per entry.
+template <int H>
+__global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
+                                                   const uint32_t* __restrict__ grid, uint32_t S32, uint32_t W32,
+                                                   uint32_t* __restrict__ dst) {
+    extern __shared__ uint32_t s_val[];  // [32][W32]
+    const uint32_t nw = (W32 + 31) / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t grp = warp / nw, col = (warp % nw) * 32 + lane, colc = min(col, W32 - 1);
+    const uint32_t M = *count;
+    const uint32_t r0 = uint32_t(uint64_t(M) * blockIdx.x / gridDim.x);
+    const uint32_t r1 = uint32_t(uint64_t(M) * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t e = threadIdx.x; e < 32 * W32; e += blockDim.x) s_val[e] = 0;
+    BitCounter<H> cnt;
+    cnt.reset();
+    uint32_t nleave = 0;
+    for (uint32_t e = r0 + grp; e < r1; e += 32) {  // 16 rows of this group: e, e + 2, ..., e + 30
+        uint32_t x[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+            const uint32_t i = e + 2 * v;
+            const uint32_t en = i < r1 ? list[i] : 0u;
+            const uint32_t neg = (en >> 31) ? 0xFFFFFFFFu : 0u;
+            const uint32_t word = i < r1 ? __ldg(grid + size_t(en & 0x7FFFFFFFu) * S32 + colc) : 0u;
+            x[v] = (word ^ neg) & (i < r1 ? 0xFFFFFFFFu : 0u);
+            nleave += (i < r1) ? (en >> 31) : 0u;
+        }
+        cnt.add16(x);
+    }
+    __syncthreads();
+    if (col < W32)
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t v = cnt.value(b) - nleave;
+            if (v) atomicAdd(&s_val[b * W32 + col], v);
+        }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < 32 * W32; e += blockDim.x) {
+        const uint32_t v = s_val[(e & 31) * W32 + (e >> 5)];
+        if (v) atomicAdd(dst + e, v);
+    }
+}
+
+void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, const uint32_t* grid,
+                      uint32_t S32, uint32_t W32, int32_t* dst, uint32_t sms, cudaStream_t s) {
+    const uint32_t ctas = sms;
+    const uint32_t threads = 2 * 32 * ((W32 + 31) / 32);
+    const size_t smem = size_t(32) * W32 * 4;
+    const uint64_t per_group = (max_rows + 2 * ctas - 1) / (2 * ctas);  // inputs per counter
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    if (per_group <= BitCounter<8>::capacity()) {
+        ensure_dynamic_smem((const void*)k_fold_list<8>, smem);
+        k_fold_list<8><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+    } else if (per_group <= BitCounter<12>::capacity()) {
+        ensure_dynamic_smem((const void*)k_fold_list<12>, smem);
+        k_fold_list<12><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+    } else {
+        ensure_dynamic_smem((const void*)k_fold_list<20>, smem);
+        k_fold_list<20><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+    }
+}
+
 namespace {
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -726,7 +821,8 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     kern<<<a.ctas, kWarps * 32, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(a.tmap), a.grid, a.n,
                                                    a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round,
-                                                   a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp);
+                                                   a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp, a.flist,
+                                                   a.flist_count, a.serpentine);
     return cudaGetLastError();
 }
 }  // namespace
