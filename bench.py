@@ -359,7 +359,7 @@ def main():
         "config": {"workload": WORKLOAD_TEXT[args.config], "pixels_per_rank": n_local, "dim": dim, "k": k,
                    "iterations": iters, "early_stop": False, "parallelism": (f"row-shard x{world}" if sharded else
                                                                             f"replicas x{world}"),
-                   "l2": f"grid {n_local * (((dim + 31) // 32 + 3) // 4 * 16) / 1e6:.0f} MB per rank > 126 MB L2: "
+                   "l2": f"grid {n_local * (((dim + 31) // 32 + 31) // 32 * 128) / 1e6:.0f} MB per rank > 126 MB L2: "
                          "every round streams from HBM (no flush needed)",
                    "labels_sha256_16": labels_sha},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
