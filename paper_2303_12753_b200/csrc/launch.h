@@ -11,6 +11,24 @@ namespace seghdc_dev {
 // launchers raise each kernel's limit once per (function, device) instead of per launch.
 cudaError_t ensure_dynamic_smem(const void* func, size_t bytes);
 
+// Launch with programmatic dependent launch allowed: the kernel may start before the previous
+// kernel in the stream completes and must execute griddepcontrol.wait before reading anything
+// that kernel wrote.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 struct RoundState;
 
 struct EncodeArgs {

@@ -240,7 +240,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
     extern __shared__ __align__(1024) uint8_t smem[];
     StateView st = StateView::at(state, K);
-    if (st.hdr->done) return;
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t parity = round & 1;
@@ -302,7 +301,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                      "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -315,9 +313,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                      : "memory");
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+    // programmatic dependent launch: everything above (barriers, TMEM, scale factors) overlaps
+    // the previous kernel; state, B image, labels and the exchange buffer are read after it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool done = *reinterpret_cast<volatile uint32_t*>(&st.hdr->done) != 0;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (done) {  // early stop reached (clusterer.cpp:213): nothing left to do
+        if (warp == kWMma0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+        return;
+    }
+    if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
     if (warp == 0) TC_TG(1);
     // flist != nullptr (round 1: every member of cluster 1 enters): the changed pixels are
     // appended to a global list that k_fold_list folds with the whole GPU after this kernel,
@@ -568,6 +576,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // all roles done: the ring becomes the counters' transpose scratch; free TMEM
     tc_fence_before();
     __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the finish may launch
     if (warp == 0) TC_TG(6);
     if (folding) {  // CTA-uniform: counters -> planes in the ring -> whole-CTA expansion + atomics
         uint32_t* planes = reinterpret_cast<uint32_t*>(ring);
@@ -652,6 +661,8 @@ __global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uin
                                                    void* state, uint32_t round, int early_stop,
                                                    uint32_t* __restrict__ ticket) {
     constexpr uint32_t K = 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL) behind the round kernel
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     StateView st = StateView::at(state, K);
     const uint32_t p = round & 1, np = p ^ 1;
     uint32_t* tail = reinterpret_cast<uint32_t*>(xchg) + size_t(K) * Dp;  // [counts[2] | changed]
@@ -722,8 +733,8 @@ __global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uin
 void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
                       uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
                       cudaStream_t s) {
-    k_finish_tc<<<(W32 + 7) / 8, 256, 0, s>>>(D, W32, Dp, xchg, colsum, Z, run1, bimg, state, round, early_stop,
-                                              ticket);
+    launch_pdl(k_finish_tc, dim3((W32 + 7) / 8), dim3(256), 0, s, D, W32, Dp, xchg, colsum, Z, run1, bimg, state,
+               round, early_stop, ticket);
 }
 
 // Fold of a global list of changed pixels (bit 31: leaving) into xchg row 1, as signed deltas:
@@ -819,11 +830,9 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     const size_t smem = tc_smem_bytes(a.W32);
     cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    kern<<<a.ctas, kWarps * 32, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(a.tmap), a.grid, a.n,
-                                                   a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round,
-                                                   a.do_update, reinterpret_cast<uint32_t*>(a.xchg), a.Dp, a.flist,
-                                                   a.flist_count, a.serpentine);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(a.ctas), dim3(kWarps * 32), smem, s, *reinterpret_cast<const CUtensorMap*>(a.tmap),
+                      a.grid, a.n, a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round, a.do_update,
+                      reinterpret_cast<uint32_t*>(a.xchg), a.Dp, a.flist, a.flist_count, a.serpentine);
 }
 }  // namespace
 
