@@ -218,6 +218,20 @@ __device__ __forceinline__ uint32_t l1_color(const uint8_t* img, uint64_t p, uin
     return s;
 }
 
+// Minimum over the block (result valid in thread 0); blockDim.x a multiple of 32, <= 1024.
+__device__ __forceinline__ unsigned long long block_min64(unsigned long long v) {
+    __shared__ unsigned long long part[32];
+    for (int o = 16; o; o >>= 1) v = umin64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();  // part[] may still be read by a previous call
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : ~0ull;
+        for (int o = 16; o; o >>= 1) v = umin64(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    return v;
+}
+
 __global__ void k_seed_minmax(const uint8_t* __restrict__ img, uint64_t n, uint32_t c,
                               unsigned long long* slots) {
     unsigned long long mn = ~0ull, mx = ~0ull;
@@ -226,11 +240,9 @@ __global__ void k_seed_minmax(const uint8_t* __restrict__ img, uint64_t n, uint3
         mn = umin64(mn, (key << 32) | p);
         mx = umin64(mx, ((0xFFFFull - key) << 32) | p);
     }
-    for (int o = 16; o; o >>= 1) {
-        mn = umin64(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = umin64(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
+    mn = block_min64(mn);
+    mx = block_min64(mx);
+    if (threadIdx.x == 0) {  // one atomic per block (per-warp atomics on two addresses serialised)
         atomicMin(slots + 0, mn);
         atomicMin(slots + 1, mx);
     }
@@ -287,8 +299,8 @@ __global__ void k_seed_greedy(const uint8_t* __restrict__ img, uint64_t n, uint3
             for (uint32_t i = 64; i < nch; ++i) taken |= (slots[2 + i] & 0xFFFFFFFFull) == p;
         if (!taken) best = umin64(best, ((0xFFFFFFFFull - d) << 32) | p);
     }
-    for (int o = 16; o; o >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, o));
-    if ((threadIdx.x & 31) == 0) atomicMin(slots + 2 + s, best);
+    best = block_min64(best);
+    if (threadIdx.x == 0) atomicMin(slots + 2 + s, best);
 }
 
 __global__ void k_seed_collect(uint64_t* seeds, const unsigned long long* slots, uint32_t K, const RoundState* hdr) {
@@ -298,7 +310,7 @@ __global__ void k_seed_collect(uint64_t* seeds, const unsigned long long* slots,
 
 void launch_select_seeds(const SeedArgs& a, cudaStream_t s) {
     cudaMemsetAsync(a.slots, 0xFF, (2 + a.K) * sizeof(unsigned long long), s);
-    const uint32_t blocks = uint32_t(std::min<uint64_t>((a.n + 255) / 256, 148 * 8));
+    const uint32_t blocks = uint32_t(std::min<uint64_t>((a.n + 255) / 256, 148 * 2));
     k_seed_minmax<<<blocks, 256, 0, s>>>(a.img, a.n, a.c, a.slots);
     k_seed_post<<<1, 1, 0, s>>>(a.slots, a.seeds, a.K, a.h, a.w, a.hdr);
     for (uint32_t st = 2; st < a.K; ++st)
