@@ -154,6 +154,29 @@ class Port(_Lib):
         return res
 
 
+    def cluster_stream(self, img, dim, row, col, widened, k, iterations, early_stop=False, per_round=False):
+        """cluster() without a stored grid: pixels re-encoded from the tables every pass
+        (so_cluster_stream) — for grids that do not fit host memory (C4)."""
+        h, w, c = img.shape
+        n = h * w
+        rounds_buf = np.zeros(iterations * n, np.uint32) if per_round else None
+        labels = np.zeros(n, np.uint32)
+        z = np.zeros((k, dim), np.uint32)
+        counts = np.zeros(k, np.uint64)
+        rounds = _sz(0)
+        f = self.lib.so_cluster_stream
+        f.argtypes = [_u8p, _sz, _sz, _sz, _sz, _u64p, _u64p, _u64p, _sz, _sz, C.c_int, C.c_void_p, _u32p, _u32p,
+                      _u64p, C.POINTER(_sz)]
+        self._check(f(np.ascontiguousarray(img), h, w, c, dim, np.ascontiguousarray(row).ravel(),
+                      np.ascontiguousarray(col).ravel(), np.ascontiguousarray(widened).ravel(), k, iterations,
+                      int(early_stop), None if rounds_buf is None else rounds_buf.ctypes.data, labels, z.ravel(),
+                      counts, C.byref(rounds)))
+        res = {"labels": labels, "centroids": z, "counts": counts, "rounds": rounds.value}
+        if per_round:
+            res["labels_rounds"] = rounds_buf.reshape(iterations, n)[: rounds.value]
+        return res
+
+
 class Ref(_Lib):
     """The unmodified reference library (oracle/_ref/libseghdc_ref.so)."""
 

@@ -415,3 +415,127 @@ int so_cluster(const uint64_t* grid, const uint8_t* px, size_t h, size_t w, size
     free(counts);
     return 0;
 }
+
+/* cluster (clusterer.cpp:190-218) without a stored grid: every pass re-encodes each pixel's HV
+ * from the tables (pixel_pipeline.cpp:92-126) and fuses assign_labels with the accumulation of
+ * the following update_centroids (both use the same round's labels). For configurations whose
+ * grid does not fit host memory (C4: 34 GB). Centroids are kept interleaved (z[i * k + c]) so
+ * the per-set-bit dot update is one k-wide vector add. Same results as so_cluster. */
+int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t dim, const uint64_t* row,
+                      const uint64_t* col, const uint64_t* widened, size_t k, size_t iterations, int early_stop,
+                      uint32_t* labels_rounds, uint32_t* labels_final, uint32_t* centroids_out,
+                      uint64_t* counts_out, size_t* rounds_out) {
+    const size_t n = h * w, nw = so_words_for(dim);
+    if (k == 0) return fail(1, "cluster config: k must be >= 1");
+    if (iterations == 0) return fail(1, "cluster config: iterations must be >= 1");
+    if (k > n) return fail(1, "cluster config: k = %zu exceeds pixel count %zu", k, n);
+    if (k > 64) return fail(2, "so_cluster_stream: k <= 64 only");
+    uint64_t* seeds = malloc(k * 8);
+    int rc = so_select_seeds(px, h, w, c, k, seeds);
+    if (rc) {
+        free(seeds);
+        return rc;
+    }
+    uint32_t* zt = calloc(dim * k, 4); /* interleaved centroid set of the current round */
+    uint64_t* counts = malloc(k * 8);
+    uint64_t* y = malloc(nw * 8);
+    for (size_t s2 = 0; s2 < k; s2++) { /* :197-205 seed centroid = the seed pixel's HV */
+        const size_t p = seeds[s2];
+        for (size_t q = 0; q < nw; q++) {
+            uint64_t v = row[(p / w) * nw + q] ^ col[(p % w) * nw + q];
+            for (size_t ch = 0; ch < c; ch++) v ^= widened[(ch * 256 + px[p * c + ch]) * nw + q];
+            y[q] = v;
+        }
+        for (size_t i = 0; i < dim; i++) zt[i * k + s2] = (uint32_t)((y[i >> 6] >> (i & 63)) & 1);
+        counts[s2] = 1;
+    }
+    free(y);
+    const int T = nthreads();
+    uint32_t* part = malloc((size_t)T * k * dim * 4);
+    uint64_t* cnt = malloc((size_t)T * k * 8);
+    uint32_t* prev = malloc(n * 4);
+    uint64_t* norm2 = malloc(k * 8);
+    size_t rounds = 0;
+    for (size_t r = 1; r <= iterations; r++) {
+        const int do_update = r < iterations;
+        for (size_t cc = 0; cc < k; cc++) { /* IntVector::norm_squared */
+            norm2[cc] = 0;
+            for (size_t i = 0; i < dim; i++) norm2[cc] += (uint64_t)zt[i * k + cc] * zt[i * k + cc];
+        }
+        memset(part, 0, (size_t)T * k * dim * 4);
+        memset(cnt, 0, (size_t)T * k * 8);
+#pragma omp parallel num_threads(T)
+        {
+            const int t = omp_get_thread_num();
+            uint32_t* acc = part + (size_t)t * k * dim;
+            uint64_t* ct = cnt + (size_t)t * k;
+            uint64_t* yy = malloc(nw * 8);
+            uint64_t d[64];
+#pragma omp for schedule(dynamic, 1024)
+            for (size_t p = 0; p < n; p++) {
+                const uint64_t* rr = row + (p / w) * nw;
+                const uint64_t* cl = col + (p % w) * nw;
+                for (size_t q = 0; q < nw; q++) yy[q] = rr[q] ^ cl[q];
+                for (size_t ch = 0; ch < c; ch++) {
+                    const uint64_t* tb = widened + (ch * 256 + px[p * c + ch]) * nw;
+                    for (size_t q = 0; q < nw; q++) yy[q] ^= tb[q];
+                }
+                for (size_t cc = 0; cc < k; cc++) d[cc] = 0;
+                for (size_t q = 0; q < nw; q++) { /* dot_words for all clusters at once */
+                    uint64_t x = yy[q];
+                    while (x) {
+                        const uint32_t* zi = zt + ((q << 6) + (size_t)__builtin_ctzll(x)) * k;
+                        for (size_t cc = 0; cc < k; cc++) d[cc] += zi[cc];
+                        x &= x - 1;
+                    }
+                }
+                uint32_t best = 0; /* assign_labels, clusterer.cpp:132-162 */
+                for (size_t cc = 1; cc < k; cc++)
+                    if (strictly_closer(d[cc], norm2[cc], d[best], norm2[best])) best = (uint32_t)cc;
+                labels_final[p] = best;
+                if (do_update) { /* IntVector::add_words into this thread's partial sums */
+                    uint32_t* zc = acc + (size_t)best * dim;
+                    for (size_t q = 0; q < nw; q++) {
+                        uint64_t x = yy[q];
+                        while (x) {
+                            zc[(q << 6) + (size_t)__builtin_ctzll(x)]++;
+                            x &= x - 1;
+                        }
+                    }
+                    ct[best]++;
+                }
+            }
+            free(yy);
+        }
+        rounds = r;
+        if (labels_rounds) memcpy(labels_rounds + (r - 1) * n, labels_final, n * 4);
+        if (early_stop && r > 1 && memcmp(labels_final, prev, n * 4) == 0) break;
+        if (do_update) { /* update_centroids, clusterer.cpp:164-188: empty clusters keep theirs */
+            for (size_t cc = 0; cc < k; cc++) {
+                uint64_t total = 0;
+                for (int t = 0; t < T; t++) total += cnt[(size_t)t * k + cc];
+                counts[cc] = total;
+                if (!total) continue;
+                for (size_t i = 0; i < dim; i++) {
+                    uint32_t s2 = 0;
+                    for (int t = 0; t < T; t++) s2 += part[((size_t)t * k + cc) * dim + i];
+                    zt[i * k + cc] = s2;
+                }
+            }
+        }
+        memcpy(prev, labels_final, n * 4);
+    }
+    if (centroids_out)
+        for (size_t cc = 0; cc < k; cc++)
+            for (size_t i = 0; i < dim; i++) centroids_out[cc * dim + i] = zt[i * k + cc];
+    if (counts_out) memcpy(counts_out, counts, k * 8);
+    *rounds_out = rounds;
+    free(prev);
+    free(seeds);
+    free(zt);
+    free(counts);
+    free(part);
+    free(cnt);
+    free(norm2);
+    return 0;
+}

@@ -53,6 +53,13 @@ int so_cluster(const uint64_t* grid, const uint8_t* px, size_t h, size_t w, size
                uint32_t* labels_final, uint32_t* centroids_out, uint64_t* counts_out,
                size_t* rounds_out);
 
+/* so_cluster without a stored grid (pixels re-encoded from the tables every pass); for
+ * configurations whose grid does not fit host memory. Same outputs as so_cluster. */
+int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t dim, const uint64_t* row,
+                      const uint64_t* col, const uint64_t* widened, size_t k, size_t iterations, int early_stop,
+                      uint32_t* labels_rounds, uint32_t* labels_final, uint32_t* centroids_out,
+                      uint64_t* counts_out, size_t* rounds_out);
+
 /* threads used by the OpenMP loops (0 = OpenMP default). */
 void so_set_threads(int n);
 int so_get_threads(void);

@@ -112,3 +112,19 @@ def test_golden_configs_pinned_to_reference(golden_configs):
         assert golden_configs[name]["source"].startswith("reference")
     imgs = golden_configs["C2"]["images"]
     assert all(r["source"].startswith("reference") for r in imgs[:4])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_streaming_cluster_equals_stored_grid(port, seed):
+    """so_cluster_stream (used for the C4 golden, whose grid does not fit host memory) gives the
+    same per-round labels, centroids, counts and rounds as so_cluster on the stored grid."""
+    rng = np.random.default_rng(50 + seed)
+    h, w, c = int(rng.integers(4, 40)), int(rng.integers(4, 40)), int(rng.choice([1, 3]))
+    dim, k, its = int(rng.choice([800, 1024, 3000])) * c, int(rng.integers(1, 9)), int(rng.integers(1, 6))
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    cb = port.build_codebooks(dim, h, w, c, 1.0, int(rng.integers(1, 4)), 1, seed)
+    exp = port.cluster(port.encode(img, dim, *cb), img, dim, k, its, bool(seed % 2), per_round=True)
+    got = port.cluster_stream(img, dim, *cb, k, its, bool(seed % 2), per_round=True)
+    assert got["rounds"] == exp["rounds"]
+    assert (got["labels_rounds"] == exp["labels_rounds"]).all()
+    assert (got["centroids"] == exp["centroids"]).all() and (got["counts"] == exp["counts"]).all()
