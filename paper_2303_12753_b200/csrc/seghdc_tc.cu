@@ -655,11 +655,13 @@ __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_
 //   next finish; the word's 16 x 16 B-image bytes (digits via the offset trick: for
 //   O = 4 (8^kP8 - 1) / 7, digit p of z is ((z + O) >> 3p & 7) - 4); the word's exchange
 //   sums are cleared after use, and the last block clears the counts / changed tail.
-__global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* __restrict__ xchg,
-                                                   const int32_t* __restrict__ colsum, uint32_t* __restrict__ Z,
-                                                   uint32_t* __restrict__ run1, uint8_t* __restrict__ bimg,
-                                                   void* state, uint32_t round, int early_stop,
-                                                   uint32_t* __restrict__ ticket) {
+constexpr uint32_t kFinWarps = 2;  // HV words (warps) per k_finish_tc block: ~one block per SM at C1
+__global__ void __launch_bounds__(kFinWarps * 32) k_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp,
+                                                            int32_t* __restrict__ xchg,
+                                                            const int32_t* __restrict__ colsum,
+                                                            uint32_t* __restrict__ Z, uint32_t* __restrict__ run1,
+                                                            uint8_t* __restrict__ bimg, void* state, uint32_t round,
+                                                            int early_stop, uint32_t* __restrict__ ticket) {
     constexpr uint32_t K = 2;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL) behind the round kernel
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -672,7 +674,9 @@ __global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uin
         if (blockIdx.x == 0 && threadIdx.x == 0) st.hdr->done = 1;
         return;
     }
-    const uint32_t lane = threadIdx.x & 31, word = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    __shared__ unsigned long long s_n2[kFinWarps][2];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, word = blockIdx.x * kFinWarps + wib;
+    unsigned long long n0 = 0, n1 = 0;
     if (word < W32) {
         const uint32_t i = 32 * word + lane;
         const bool in = i < D;
@@ -687,40 +691,47 @@ __global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uin
             Z[i] = z0;
             Z[D + i] = z1;
         }
-        unsigned long long n0 = (unsigned long long)z0 * z0, n1 = (unsigned long long)z1 * z1;
+        n0 = (unsigned long long)z0 * z0;
+        n1 = (unsigned long long)z1 * z1;
         for (int o = 16; o; o >>= 1) {
             n0 += __shfl_xor_sync(0xffffffffu, n0, o);
             n1 += __shfl_xor_sync(0xffffffffu, n1, o);
         }
-        if (lane == 0) {
-            atomicAdd(st.norm2 + np * K, n0);
-            atomicAdd(st.norm2 + np * K + 1, n1);
-        }
         // B image bytes of this word: word h = word & 1 of k-step word >> 1 is core matrix h;
-        // lane = (row n, half): row n = kP8 * cluster + digit, bytes 8 * half .. + 7
+        // lane = (row n, half): row n = kP8 * cluster + digit, bytes 8 * half .. + 7. Digit pd of
+        // z is u - 4 with u = ((z + O) >> 3 pd) & 7, O = 4 (8^kP8 - 1) / 7; its e2m1 code for a
+        // weight-1 (d) or weight-2 (d / 2) nibble class comes from a packed 8-entry table by u.
         constexpr uint32_t kOff = 4u * ((1u << (3 * kP8)) - 1) / 7u;
-        const uint32_t n = lane >> 1, hb = lane & 1, cl = n / kP8, pd = n % kP8;
+        constexpr uint32_t kLut1 = 0x5420ACDEu, kLut2 = 0x32109ABCu;  // u = 0..7 -> code
+        const uint32_t zb0 = z0 + kOff, zb1 = z1 + kOff;
+        const uint32_t n = lane >> 1, hb = lane & 1, cl = n / kP8, sh = 3 * (n % kP8);
         uint64_t v = 0;
 #pragma unroll
         for (uint32_t q = 0; q < 16; ++q) {  // nibble q of the lane's 8 bytes: k = 16 hb + q
             const uint32_t k = 16 * hb + q, c = k >> 3, j = k & 7;
             const uint32_t src = 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
-            const uint32_t za = __shfl_sync(0xffffffffu, z0, src), zb = __shfl_sync(0xffffffffu, z1, src);
-            const int d = int(((cl ? zb : za) + kOff) >> (3 * pd) & 7u) - 4;
-            const uint32_t a = uint32_t(d < 0 ? -d : d);
-            const uint32_t code = ((c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u)) |
-                                  (d < 0 ? 8u : 0u);
-            v |= uint64_t(code) << (4 * q);
+            const uint32_t za = __shfl_sync(0xffffffffu, zb0, src), zb = __shfl_sync(0xffffffffu, zb1, src);
+            const uint32_t u = ((cl ? zb : za) >> sh) & 7u;
+            v |= uint64_t((((c & 1) ? kLut2 : kLut1) >> (4 * u)) & 0xFu) << (4 * q);
         }
         *reinterpret_cast<uint64_t*>(bimg + size_t(word >> 1) * kKB + (n >> 3) * 256 + (word & 1) * 128 +
                                      (n & 7) * 16 + 8 * hb) = v;
+    }
+    if (lane == 0) {
+        s_n2[wib][0] = n0;
+        s_n2[wib][1] = n1;
     }
     if (blockIdx.x == 0 && threadIdx.x < K) {
         st.norm2[p * K + threadIdx.x] = 0;
         st.cur[np * K + threadIdx.x] = threadIdx.x ? cnt1 : cnt0;
     }
-    // the last block to finish clears the counts / changed tail for the next round
     __syncthreads();
+    if (threadIdx.x < K) {  // one atomic per block and cluster
+        unsigned long long t = 0;
+        for (uint32_t w2 = 0; w2 < kFinWarps; ++w2) t += s_n2[w2][threadIdx.x];
+        atomicAdd(st.norm2 + np * K + threadIdx.x, t);
+    }
+    // the last block to finish clears the counts / changed tail for the next round
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
@@ -733,8 +744,8 @@ __global__ void __launch_bounds__(256) k_finish_tc(uint32_t D, uint32_t W32, uin
 void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
                       uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
                       cudaStream_t s) {
-    launch_pdl(k_finish_tc, dim3((W32 + 7) / 8), dim3(256), 0, s, D, W32, Dp, xchg, colsum, Z, run1, bimg, state,
-               round, early_stop, ticket);
+    launch_pdl(k_finish_tc, dim3((W32 + kFinWarps - 1) / kFinWarps), dim3(kFinWarps * 32), 0, s, D, W32, Dp, xchg,
+               colsum, Z, run1, bimg, state, round, early_stop, ticket);
 }
 
 // Fold of a global list of changed pixels (bit 31: leaving) into xchg row 1, as signed deltas:
