@@ -132,10 +132,10 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
 cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s);
 
 // tcgen05 round kernel (seghdc_tc.cu)
-bool tc_supported(uint32_t W32);
+bool tc_supported(uint32_t K, uint32_t W32);
 uint32_t tc_ksteps(uint32_t W32);
-size_t tc_smem_bytes(uint32_t W32);
-size_t tc_bimg_bytes(uint32_t W32);
+size_t tc_smem_bytes(uint32_t K, uint32_t W32);
+size_t tc_bimg_bytes(uint32_t K, uint32_t W32);
 uint32_t tc_tile_pixels();
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32);
 struct ExpandArgs {  // closed-form Manhattan codebooks (seghdc_host::manhattan_bases)

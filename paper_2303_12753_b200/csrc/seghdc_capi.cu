@@ -317,7 +317,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
     x.bfrag.ensure(size_t(NT) * x.plan.w32p * 32 * 8);
     ck(cudaMemsetAsync(x.bfrag.p, 0, x.bfrag.bytes(), x.stream), "clear bfrag");
-    if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(g.W32));
+    if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(uint32_t(K), g.W32));
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
     if (x.incremental()) {
         x.run1.ensure(2 * size_t(g.Dp));

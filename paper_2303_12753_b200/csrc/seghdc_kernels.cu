@@ -1040,7 +1040,7 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     p.fused = false;
     p.tc = false;
     const char* tcenv = getenv("SEGHDC_TC");
-    if (K <= 2 && !(tcenv && *tcenv == '0') && tc_supported(W32) && tc_smem_bytes(W32) <= smem_limit) {
+    if (!(tcenv && *tcenv == '0') && tc_supported(K, W32) && tc_smem_bytes(K, W32) <= smem_limit) {
         // tcgen05 kernel; the IMMA plan below stays valid as the fallback (bfrag layout)
         p.tc = true;
     }

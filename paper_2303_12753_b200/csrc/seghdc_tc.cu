@@ -41,15 +41,11 @@ namespace {
 constexpr uint32_t kTP = 128;      // pixels per tile (MMA M)
 constexpr uint32_t kCW = 32;       // HV words per chunk (one 128-byte swizzle span per row)
 constexpr uint32_t kKS = kCW / 2;  // k-steps (64 HV dims) per chunk
-constexpr uint32_t kStages = 9;    // smem ring depth (16 KB each); a multiple of kUW, so slot g % kStages
-                                   // is always unpacked by warp g % kUW (mbarrier phases stay in order)
 constexpr uint32_t kChunkBytes = kTP * kCW * 4;
 constexpr uint32_t kUW = 3;        // unpack warps per TMEM lane quarter (chunk g goes to warp g % kUW)
 constexpr uint32_t kAB = 3;        // A buffers in TMEM (128 columns each)
-static_assert(kStages % kUW == 0 && kAB == kUW, "unpack warp u owns ring slots and A buffers == u mod kUW");
+static_assert(kAB == kUW, "unpack warp u owns ring slots and A buffers == u mod kUW");
 constexpr uint32_t kP8 = 8;        // balanced base-8 digits per centroid entry
-constexpr uint32_t kN = 16;        // accumulator columns: 2 clusters x kP8 digits (MMA N)
-constexpr uint32_t kKB = kN * 32;  // B image bytes per k-step: kN rows x 64 e2m1
 // warp layout (SM sub-partition = warp % 4): [0, 12) unpack (3 per lane quarter), [12, 16)
 // epilogue (one per lane quarter), 16/17/21/22 fold, 18/19 MMA issue (sub-partitions 2 and 3,
 // away from the producer), 20 producer. Two MMA-issuing warps split the chunks of a tile
@@ -60,9 +56,22 @@ __device__ __forceinline__ int fold_index(uint32_t warp) {
     return warp == 16 ? 0 : warp == 17 ? 1 : warp == 21 ? 2 : warp == 22 ? 3 : -1;
 }
 // TMEM columns: A buffers [128*i, 128*i+128), then accumulators D[tile parity][MMA warp]
-// (kN columns each), then the (all 1.0) scale factors of A and B
-constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB, kColSF = kColD + 4 * kN;
-static_assert(kColSF + 8 <= kTmemCols, "TMEM budget");
+// (N columns each), then the (all 1.0) scale factors of A and B
+constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB;
+// Per-N configuration. N = kP8 digit columns per cluster: 16 for K <= 2, 32 for K <= 4.
+template <uint32_t NCOL>
+struct TcCfg {
+    static constexpr uint32_t N = NCOL;
+    static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
+    static constexpr uint32_t Stages = NCOL == 16 ? 9 : 3;   // smem ring depth (16 KB each): the larger B
+                                                             // image takes the rest; a multiple of kUW, so
+                                                             // slot g % Stages is unpacked by warp g % kUW
+    static constexpr uint32_t NMW = NCOL == 16 ? 2 : 1;      // MMA-issuing warps (alternate chunks)
+    static constexpr uint32_t ColSF = kColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
+    static_assert(Stages % kUW == 0, "ring slots follow the unpack warps");
+    static_assert(ColSF + 8 <= kTmemCols, "TMEM budget");
+};
+constexpr uint32_t kKB = TcCfg<16>::KB;  // the K <= 2 image (k_finish_tc)
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -74,7 +83,7 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
         "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
 }
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
@@ -90,6 +99,7 @@ __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sy
 #define SEGHDC_KSTEP                                                                                  \
     "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a], b, %3, [%4], [%5], p;\n\t" \
     "add.u64 b, b, %6;\n\tadd.u32 a, a, 8;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+template <uint32_t KB>
 __device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
                                              uint32_t accum) {
     static_assert(kKS == 16, "tc_mma_chunk issues 16 k-steps");
@@ -99,7 +109,7 @@ __device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_
         "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
             SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
                 SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
-        "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(kKB >> 4), "r"(accum)
+        "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(KB >> 4), "r"(accum)
         : "memory");
 }
 #undef SEGHDC_KSTEP
@@ -171,14 +181,16 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t
 #define PRG(code) ((void)0)
 #endif
 
+template <uint32_t NCOL>
 struct TcSmem {
-    static constexpr size_t ring = 0;  // [kStages][128][32] u32, 1024-aligned (128B swizzle)
-    __host__ __device__ static size_t b(uint32_t nks) { return size_t(kStages) * kChunkBytes; }                   // [nks][kKB] B image
-    __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * kKB; }                  // [2][4][32] u32
+    using Cfg = TcCfg<NCOL>;
+    static constexpr size_t ring = 0;  // [Stages][128][32] u32, 1024-aligned (128B swizzle)
+    __host__ __device__ static size_t b(uint32_t nks) { return size_t(Cfg::Stages) * kChunkBytes; }              // [nks][KB] B image
+    __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * Cfg::KB; }             // [2][4][32] u32
     __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + 2 * 4 * 32 * 4; }                   // [2][4] u32
     __host__ __device__ static size_t misc(uint32_t nks) { return listn(nks) + 2 * 4 * 4; }                        // tmem base, skip
     __host__ __device__ static size_t bars(uint32_t nks) { return (misc(nks) + 16 + 7) & ~size_t(7); }
-    static constexpr uint32_t nbars = 2 * kStages + 3 * kAB + 2 + 2 + 2 + 2 + 1;
+    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * kAB + 2 + 2 + 2 + 2 + 1;
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
 
@@ -230,7 +242,7 @@ void read_trace_tc(void* dst) {
 #define TC_CLK(v) ((void)0)
 #endif
 
-template <bool UPD, int H>
+template <bool UPD, int H, uint32_t NCOL>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
@@ -238,6 +250,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine) {
     constexpr uint32_t NRT = kNRW * 32;
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
+    using Cfg = TcCfg<NCOL>;
+    using Smem = TcSmem<NCOL>;
+    constexpr uint32_t kStages = Cfg::Stages, NMW = Cfg::NMW, KC = NCOL / kP8;  // KC: clusters of the layout
+    static_assert(!UPD || NCOL == 16, "the incremental fold is the K == 2 schedule");
     extern __shared__ __align__(1024) uint8_t smem[];
     StateView st = StateView::at(state, K);
 
@@ -245,12 +261,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const uint32_t parity = round & 1;
     uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
     if (warp == 0) TC_TG(0);
-    uint8_t* ring = smem + TcSmem::ring;
-    uint8_t* sB = smem + TcSmem::b(nks);
-    uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + TcSmem::list(nks));
-    uint32_t* s_listn = reinterpret_cast<uint32_t*>(smem + TcSmem::listn(nks));
-    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + TcSmem::misc(nks));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TcSmem::bars(nks));
+    uint8_t* ring = smem + Smem::ring;
+    uint8_t* sB = smem + Smem::b(nks);
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + Smem::list(nks));
+    uint32_t* s_listn = reinterpret_cast<uint32_t*>(smem + Smem::listn(nks));
+    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + Smem::misc(nks));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars(nks));
     uint64_t* slot_full = bars;                 // [kStages] TMA landed
     uint64_t* slot_free = bars + kStages;       // [kStages] unpack warps read the chunk
     // a_full[ab][m]: chunk g (buffer ab = g % kAB) written for MMA warp m = g % 2. One barrier
@@ -287,7 +303,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             mbar_init(&a_free[b], 1);
         }
         for (uint32_t b = 0; b < 2; ++b) {
-            mbar_init(&d_full[b], 2);  // both MMA warps commit
+            mbar_init(&d_full[b], NMW);  // every MMA warp commits
             mbar_init(&d_free[b], 4 * 32);
             mbar_init(&list_ready[b], 4 * 32);
             mbar_init(&list_free[b], NRT);
@@ -308,7 +324,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (warp < 4) {  // scale factors of A and B: every ue8m0 byte 127 (2^0), whatever the layout
         const uint32_t one = 0x7F7F7F7Fu;
         asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                         tbase + ((32 * warp) << 16) + kColSF),
+                         tbase + ((32 * warp) << 16) + Cfg::ColSF),
                      "r"(one)
                      : "memory");
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -376,15 +392,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             PRG(11 * 100000 + g);
             mbar_arrive(&slot_free[s]);
             tc_fence_before();
-            mbar_arrive(&a_full[2 * ab + (g & 1)]);
+            mbar_arrive(&a_full[2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
     } else if (warp < kWEpi + 4) {
         // ---------------------------------------------------------------------- epilogue warps
         const uint32_t qd = warp & 3;
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
-        const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
-        uint32_t changed = 0, cnt1 = 0, total = 0;
+        unsigned long long n2[KC];
+#pragma unroll
+        for (uint32_t c = 0; c < KC; ++c) n2[c] = c < K ? st.norm2[parity * K + c] : 0ull;
+        uint32_t changed = 0, ccount[KC];
+#pragma unroll
+        for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
             const uint64_t px0 = tile_px0(it);
@@ -398,28 +418,44 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             if (qd == 0) TC_ACC(5, c1 - c0);
             tc_fence_after();
             if (qd == 0) TC_TR(4, it);
-            uint32_t c0r[16], c1r[16];  // the two MMA warps' accumulators of this tile
-            tc_ld16(lane_addr + kColD + (2 * db) * kN, c0r);
-            tc_ld16(lane_addr + kColD + (2 * db + 1) * kN, c1r);
+            uint32_t acc[NMW][NCOL];  // the MMA warps' accumulators of this tile
+#pragma unroll
+            for (uint32_t mw = 0; mw < NMW; ++mw)
+#pragma unroll
+                for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16)
+                    tc_ld16(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
             tc_wait_ld();
             tc_fence_before();
             mbar_arrive(&d_free[db]);
             // exact dots: column n = kP8 * c + p holds sum_i y_i d_p(z_c[i]) (an integer in f32);
             // dot_c = sum_p digit_dot_p * 8^p
-            long long d[2] = {0, 0};
+            long long d[KC];
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
+            for (uint32_t c = 0; c < KC; ++c) {
+                d[c] = 0;
 #pragma unroll
-                for (int p = kP8 - 1; p >= 0; --p)
-                    d[c] = d[c] * 8 + (long long)(__float2int_rn(__uint_as_float(c0r[kP8 * c + p])) +
-                                                  __float2int_rn(__uint_as_float(c1r[kP8 * c + p])));
-            const uint32_t best =
-                (K > 1 && strictly_closer((unsigned long long)d[1], n2_1, (unsigned long long)d[0], n2_0)) ? 1u : 0u;
+                for (int p = kP8 - 1; p >= 0; --p) {
+                    int v = 0;
+#pragma unroll
+                    for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][kP8 * c + p]));
+                    d[c] = d[c] * 8 + v;
+                }
+            }
+            // assign_labels (clusterer.cpp:146-158): first strictly closer centroid wins
+            uint32_t best = 0;
+            unsigned long long bd = (unsigned long long)d[0], bn = n2[0];
+#pragma unroll
+            for (uint32_t c = 1; c < KC; ++c)
+                if (c < K && strictly_closer((unsigned long long)d[c], n2[c], bd, bn)) {
+                    best = c;
+                    bd = (unsigned long long)d[c];
+                    bn = n2[c];
+                }
             if (live) {
                 labels[px] = best;
                 changed += old != best;
-                cnt1 += best;
-                ++total;
+#pragma unroll
+                for (uint32_t c = 0; c < KC; ++c) ccount[c] += best == c;
             }
             TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
             if constexpr (UPD) {
@@ -442,21 +478,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         for (int o = 16; o; o >>= 1) {
             changed += __shfl_xor_sync(0xffffffffu, changed, o);
-            cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
-            total += __shfl_xor_sync(0xffffffffu, total, o);
+#pragma unroll
+            for (uint32_t c = 0; c < KC; ++c) ccount[c] += __shfl_xor_sync(0xffffffffu, ccount[c], o);
         }
         if (qd == 0) TC_TG(4);
         if (lane == 0) {
             if (changed) atomicAdd(tail + K, changed);
-            if (total - cnt1) atomicAdd(tail, total - cnt1);
-            if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);
+#pragma unroll
+            for (uint32_t c = 0; c < KC; ++c)
+                if (c < K && ccount[c]) atomicAdd(tail + c, ccount[c]);
         }
-    } else if (warp == kWMma0 || warp == kWMma0 + 1) {
+    } else if (warp >= kWMma0 && warp < kWMma0 + NMW) {
         // ------------------------------------------------------------------------ MMA warps
         // warp m issues the chunks g = m, m+2, ... (global chunk parity) into accumulator
         // D[db][m] of their tile; the whole warp walks the loop (barrier waits are
         // warp-uniform), one elected lane issues inside tc_mma_chunk / tc_commit
-        constexpr uint32_t idesc = idesc_mxf4(kN, kTP);
+        constexpr uint32_t idesc = idesc_mxf4(NCOL, kTP);
         const uint32_t m = warp - kWMma0;
         const uint32_t b0 = smem_u32(sB);
         TCW(5, 0, b_full, 0);
@@ -464,19 +501,21 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         TC_TG(2);
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
-            const uint32_t d_t = tbase + kColD + (2 * db + m) * kN;
+            const uint32_t d_t = tbase + kColD + (NMW * db + m) * NCOL;
             TCW(6, it, &d_free[db], ((it >> 1) & 1) ^ 1);
             __syncwarp();
-            for (uint32_t ch = (it * nch + m) & 1; ch < nch; ch += 2) {  // chunks with g % 2 == m
+            const uint32_t first = (NMW + m - (it * nch) % NMW) % NMW;
+            for (uint32_t ch = first; ch < nch; ch += NMW) {  // chunks with g % NMW == m
                 const uint32_t g = it * nch + ch, ab = g % kAB;
                 TC_CLK(c0);
-                TCW(7, g, &a_full[2 * ab + m], (g / (2 * kAB)) & 1);  // g = x + 6k on this barrier
+                TCW(7, g, &a_full[2 * ab + m], (g / (NMW * kAB)) & 1);  // g = x + NMW kAB t here
                 __syncwarp();  // converge before elect.sync / tcgen05.mma
                 TC_CLK(c1);
                 if (m == 0) TC_ACC(2, c1 - c0);
                 tc_fence_after();
                 PRG(12 * 100000 + g);
-                tc_mma_chunk(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * kKB), idesc, tbase + kColSF, ch >= 2);
+                tc_mma_chunk<Cfg::KB>(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * Cfg::KB), idesc,
+                                      tbase + Cfg::ColSF, ch >= NMW);
                 tc_commit(&a_free[ab]);
                 PRG(13 * 100000 + g);
                 {
@@ -491,7 +530,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     } else if (warp == kWProd) {
         // ----------------------------------------------------------------------- producer warp
         if (lane == 0) {
-            const uint32_t bbytes = nks * kKB;
+            const uint32_t bbytes = nks * Cfg::KB;
             // the grid streams through L2 with evict_first (measured: evict_last on the tiles read
             // last slows every round; evict_first takes round 1 from 98 to 82 us at C1)
             const uint64_t pol_stream = policy_evict_first();
@@ -635,12 +674,12 @@ __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint
     const uint32_t code = (c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u);
     return code | (d < 0 ? 8u : 0u);
 }
-__global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks,
+__global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
                              uint8_t* __restrict__ bimg, const void* state) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
-    const uint32_t total = nks * kKB;
+    const uint32_t total = nks * kb;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t ks = i / kKB, rem = i % kKB;
+        const uint32_t ks = i / kb, rem = i % kb;
         const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
         const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
         bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k) | (b_nibble(Z, K, D, ks, n, k + 1) << 4));
@@ -835,10 +874,10 @@ __global__ void k_tc_stamp(int ev) {
     g_trace_tc[(size_t(blockIdx.x) * 64 + 61) * 8 + ev] = t_;
 }
 #endif
-template <bool UPD, int H>
+template <bool UPD, int H, uint32_t NCOL>
 cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
-    auto kern = k_round_tc<UPD, H>;
-    const size_t smem = tc_smem_bytes(a.W32);
+    auto kern = k_round_tc<UPD, H, NCOL>;
+    const size_t smem = TcSmem<NCOL>::total(tc_ksteps(a.W32));
     cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, dim3(a.ctas), dim3(kWarps * 32), smem, s, *reinterpret_cast<const CUtensorMap*>(a.tmap),
@@ -847,12 +886,16 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
 }
 }  // namespace
 
-bool tc_supported(uint32_t W32) { return W32 > kCW && W32 <= 3 * kNRW * 32; }  // >= 2 chunks: both MMA warps
+// K <= 2: N = 16 digit columns; K <= 4: N = 32 (>= 2 chunks, fold columns <= 3 per thread)
+static uint32_t tc_ncol(uint32_t K) { return K <= 2 ? 16u : 32u; }
+bool tc_supported(uint32_t K, uint32_t W32) { return K >= 1 && K <= 4 && W32 > kCW && W32 <= 3 * kNRW * 32; }
 // largest centroid entry kP8 balanced base-8 digits represent: 3 (8^kP8 - 1) / 7
 uint64_t tc_max_value() { return 3ull * ((1ull << (3 * kP8)) - 1) / 7; }
 uint32_t tc_ksteps(uint32_t W32) { return ((W32 + kCW - 1) / kCW) * kKS; }
-size_t tc_smem_bytes(uint32_t W32) { return TcSmem::total(tc_ksteps(W32)); }
-size_t tc_bimg_bytes(uint32_t W32) { return size_t(tc_ksteps(W32)) * kKB; }
+size_t tc_smem_bytes(uint32_t K, uint32_t W32) {
+    return tc_ncol(K) == 16 ? TcSmem<16>::total(tc_ksteps(W32)) : TcSmem<32>::total(tc_ksteps(W32));
+}
+size_t tc_bimg_bytes(uint32_t K, uint32_t W32) { return size_t(tc_ksteps(W32)) * tc_ncol(K) * 32; }
 uint32_t tc_tile_pixels() { return kTP; }
 
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32) {
@@ -870,9 +913,9 @@ bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S
 
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
                        cudaStream_t s) {
-    const uint32_t nks = tc_ksteps(W32);
-    const uint32_t total = nks * kKB;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, bimg, state);
+    const uint32_t nks = tc_ksteps(W32), kb = tc_ncol(K) * 32;
+    const uint32_t total = nks * kb;
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, bimg, state);
 }
 
 #ifdef SEGHDC_HANGDBG
@@ -889,9 +932,9 @@ void* setup_hang() {
 
 static cudaError_t launch_round_tc_body(const RoundArgs& a, cudaStream_t s) {
     const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + kTP - 1) / kTP * kTP;
-    if (per_cta <= BitCounter<8>::capacity()) return launch_tc_t<true, 8>(a, s);
-    if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12>(a, s);
-    return launch_tc_t<true, 20>(a, s);
+    if (per_cta <= BitCounter<8>::capacity()) return launch_tc_t<true, 8, 16>(a, s);
+    if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12, 16>(a, s);
+    return launch_tc_t<true, 20, 16>(a, s);
 }
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
 #ifdef SEGHDC_TRACE
@@ -905,7 +948,8 @@ cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
     }
     const char* tr = getenv("SEGHDC_TRACE_ROUND");
     if (tr && int(a.round) != atoi(tr)) {  // only the traced round records events and stamps
-        return a.K != 2 ? launch_tc_t<false, 1>(a, s) : launch_round_tc_body(a, s);
+        return a.K == 2 ? launch_round_tc_body(a, s)
+                    : a.K == 1 ? launch_tc_t<false, 1, 16>(a, s) : launch_tc_t<false, 1, 32>(a, s);
     }
     cudaEventRecord(ev[0], s);
     k_tc_stamp<<<148, 1, 0, s>>>(0);
@@ -921,7 +965,8 @@ cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
     } after{s, ev};
     g_tc_events = ev;
 #endif
-    return a.K != 2 ? launch_tc_t<false, 1>(a, s) : launch_round_tc_body(a, s);
+    return a.K == 2 ? launch_round_tc_body(a, s)
+                    : a.K == 1 ? launch_tc_t<false, 1, 16>(a, s) : launch_tc_t<false, 1, 32>(a, s);
 }
 
 }  // namespace seghdc_dev
