@@ -468,10 +468,13 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.tmap = x.tmap;
     a.bimg = x.bimg.p;
     a.nks = tc_ksteps(x.g.W32);
-    // round 1 of the incremental schedule folds every member of cluster 1: a global list and a
-    // whole-GPU fold kernel instead of the per-CTA fold warps (whose load is the nuclei's layout)
+    // round 1 of the incremental schedule folds every member of cluster 1 through a global list
+    // and the whole-GPU k_fold_list instead of the per-CTA fold warps (whose load follows the
+    // nuclei's layout). Later rounds change few pixels and fold in the round kernel.
+    // SEGHDC_FLIST: 0 = fold warps in every round, 1 = list in round 1 (default), 2 = always.
     static const char* fe = getenv("SEGHDC_FLIST");
-    const bool use_flist = do_update && r == 1 && x.incremental() && !(fe && *fe == '0');
+    const int flist_mode = fe ? atoi(fe) : 1;  // measured: lists in every round cost +5 us per round
+    const bool use_flist = do_update && x.incremental() && (flist_mode == 2 || (flist_mode == 1 && r == 1));
     {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;

@@ -799,9 +799,14 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
     extern __shared__ uint32_t s_val[];  // [32][W32]
     const uint32_t nw = (W32 + 31) / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t grp = warp / nw, col = (warp % nw) * 32 + lane, colc = min(col, W32 - 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL) behind the round kernel
     const uint32_t M = *count;
-    const uint32_t r0 = uint32_t(uint64_t(M) * blockIdx.x / gridDim.x);
-    const uint32_t r1 = uint32_t(uint64_t(M) * (blockIdx.x + 1) / gridDim.x);
+    // at least kMinRows rows per CTA: a short list (late rounds) occupies a few CTAs, whose
+    // flush (one atomic per entry of D) dominates, instead of all of them
+    constexpr uint32_t kMinRows = 64;
+    const uint32_t per = max(kMinRows, (M + gridDim.x - 1) / gridDim.x);
+    const uint32_t r0 = min(M, blockIdx.x * per), r1 = min(M, r0 + per);
+    if (r0 >= r1) return;
     for (uint32_t e = threadIdx.x; e < 32 * W32; e += blockDim.x) s_val[e] = 0;
     BitCounter<H> cnt;
     cnt.reset();
@@ -841,13 +846,13 @@ void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     if (per_group <= BitCounter<8>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<8>, smem);
-        k_fold_list<8><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<8>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
     } else if (per_group <= BitCounter<12>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<12>, smem);
-        k_fold_list<12><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<12>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
     } else {
         ensure_dynamic_smem((const void*)k_fold_list<20>, smem);
-        k_fold_list<20><<<ctas, threads, smem, s>>>(list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<20>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
     }
 }
 
