@@ -87,6 +87,7 @@ struct FinishArgs {
     const int32_t* xchg;
     const int32_t* colsum;
     uint32_t* Z;
+    uint32_t* run;  // incremental K > 2: running member sums [2 parities][K][Dp] (row 0 unused); else null
     uint8_t* bfrag;
     void* state;
     uint32_t round;
@@ -123,8 +124,8 @@ struct RoundArgs {
     const void* tmap;     // CUtensorMap of the grid (tc_make_grid_map)
     const uint8_t* bimg;  // centroid B image (launch_build_bimg)
     uint32_t nks;         // k-steps of 64 HV dims (tc_ksteps)
-    uint32_t* flist;        // non-null: append changed pixels here (k_fold_list folds them) instead of folding
-    uint32_t* flist_count;  // entries appended (zeroed before the round)
+    uint32_t* flist;        // non-null: append changed pixels to per-cluster lists (k_fold_list folds them)
+    uint32_t* flist_count;  // entries appended per tracked cluster 1..K-1 (zeroed before the round)
     uint32_t serpentine;     // odd rounds walk the tiles backwards
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
@@ -147,8 +148,11 @@ void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_
 uint64_t tc_max_value();
 // incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of
 // cluster 1's member sums, run1[parity][Dp] the running sums (read p, write p ^ 1)
-void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, const uint32_t* grid,
-                      uint32_t S32, uint32_t W32, int32_t* dst, uint32_t sms, cudaStream_t s);
+// lists: nlists tracked clusters, list l at list + l * max_rows (count[l] entries), folded as
+// signed deltas into dst + l * dst_stride
+void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, uint32_t nlists,
+                      const uint32_t* grid, uint32_t S32, uint32_t W32, int32_t* dst, uint32_t dst_stride,
+                      uint32_t sms, cudaStream_t s);
 void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, const int32_t* colsum, uint32_t* Z,
                       uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
                       cudaStream_t s);  // centroid entries above this need the IMMA kernels

@@ -139,8 +139,9 @@ struct seghdc_ctx {
 
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
     size_t xchg_round_ints() const { return K * g.Dp + K + 1; }
-    // the tcgen05 round kernel re-bundles K == 2 incrementally (deltas of cluster 1)
-    bool incremental() const { return plan.tc && K == 2; }
+    // the tcgen05 round kernel re-bundles incrementally (deltas of clusters 1..K-1): K == 2
+    // with the fused k_finish_tc, K = 3, 4 with k_fold_list every round and k_finish
+    bool incremental() const { return plan.tc && K >= 2 && K <= 4; }
     int32_t* colsum_ptr() { return xchg.p + xchg_round_ints(); }
     void count(uint64_t k = 1) { launches += k; }
     void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
@@ -320,8 +321,8 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     if (x.plan.tc) x.bimg.ensure(tc_bimg_bytes(uint32_t(K), g.W32));
     x.xchg.ensure(x.xchg_round_ints() + g.Dp);
     if (x.incremental()) {
-        x.run1.ensure(2 * size_t(g.Dp));
-        x.flist.ensure(n + 1);
+        x.run1.ensure(2 * K * size_t(g.Dp));  // [2][Dp] (K == 2) or [2][K][Dp]
+        x.flist.ensure((K - 1) * (n + 1));
         x.ticket.ensure(1);
         ck(cudaMemsetAsync(x.ticket.p, 0, 4, x.stream), "clear ticket");
     }
@@ -375,7 +376,7 @@ void select_seeds_dev(seghdc_ctx& x, size_t K) {
 }
 
 void finish(seghdc_ctx& x, int mode, uint32_t round) {
-    if (mode == 0 && x.incremental()) {  // one fused kernel per round
+    if (mode == 0 && x.incremental() && x.K == 2) {  // one fused kernel per round
         launch_finish_tc(x.g.D, x.g.W32, x.g.Dp, x.xchg.p, x.colsum_ptr(), x.Z.p, x.run1.p, x.bimg.p, x.state.p,
                          round, x.early_stop, x.ticket.p, x.stream);
         x.count();
@@ -400,6 +401,7 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.state = x.state.p;
     f.round = round;
     f.early_stop = x.early_stop;
+    f.run = (mode == 0 && x.incremental()) ? x.run1.p : nullptr;
     launch_finish(f, x.stream);
     x.count(2);
     if (x.plan.tc) {
@@ -418,7 +420,7 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     x.early_stop = early_stop;
     ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K)), x.stream), "clear state");
     ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
-    if (x.incremental()) ck(cudaMemsetAsync(x.run1.p, 0, 2 * size_t(x.g.Dp) * 4, x.stream), "clear running sums");
+    if (x.incremental()) ck(cudaMemsetAsync(x.run1.p, 0, 2 * x.K * size_t(x.g.Dp) * 4, x.stream), "clear running sums");
     select_seeds_dev(x, K);
     if (!x.colsum_valid) compute_colsum(x);
     // local column sums into the exchange tail; the init all-reduce makes them global
@@ -474,14 +476,15 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     // SEGHDC_FLIST: 0 = fold warps in every round, 1 = list in round 1 (default), 2 = always.
     static const char* fe = getenv("SEGHDC_FLIST");
     const int flist_mode = fe ? atoi(fe) : 1;  // measured: lists in every round cost +5 us per round
-    const bool use_flist = do_update && x.incremental() && (flist_mode == 2 || (flist_mode == 1 && r == 1));
+    const bool use_flist =
+        do_update && x.incremental() && (x.K > 2 || flist_mode == 2 || (flist_mode == 1 && r == 1));
     {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;
     }
     a.flist = use_flist ? x.flist.p : nullptr;
-    a.flist_count = use_flist ? x.flist.p + x.n_local() : nullptr;
-    if (use_flist) ck(cudaMemsetAsync(a.flist_count, 0, 4, x.stream), "clear fold list");
+    a.flist_count = use_flist ? x.flist.p + (x.K - 1) * x.n_local() : nullptr;
+    if (use_flist) ck(cudaMemsetAsync(a.flist_count, 0, (x.K - 1) * 4, x.stream), "clear fold lists");
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     if (!x.xchg_clean) ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     x.xchg_clean = false;
@@ -500,12 +503,12 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     if (ev_end) ck(cudaEventRecord(ev_end, x.stream), "event");
     x.count();
     if (use_flist) {
-        launch_fold_list(a.flist, a.flist_count, x.n_local(), x.grid.p, x.g.S32, x.g.W32, x.xchg.p + x.g.Dp,
-                         uint32_t(x.sms), x.stream);
+        launch_fold_list(a.flist, a.flist_count, x.n_local(), uint32_t(x.K - 1), x.grid.p, x.g.S32, x.g.W32,
+                         x.xchg.p + x.g.Dp, x.g.Dp, uint32_t(x.sms), x.stream);
         x.count();
         x.check_launch();
     }
-    if (do_update && !x.plan.fused) {  // K >= 3: separate single-read accumulation pass
+    if (do_update && !x.plan.fused && !x.incremental()) {  // K >= 3: separate single-read accumulation pass
         AccumulateArgs u{};
         u.grid = x.grid.p;
         u.S32 = x.g.S32;

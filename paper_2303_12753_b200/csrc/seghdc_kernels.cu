@@ -433,7 +433,7 @@ void launch_accumulate(const AccumulateArgs& a, cudaStream_t s) {
 // =============================================================================================
 __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t W32, uint32_t W32P, uint32_t Dp,
                          const int32_t* __restrict__ xchg, const int32_t* __restrict__ colsum, uint32_t* Z,
-                         uint8_t* bfrag, void* state, uint32_t round, int early_stop) {
+                         uint32_t* __restrict__ run, uint8_t* bfrag, void* state, uint32_t round, int early_stop) {
     StateView st = StateView::at(state, K);
     const uint32_t p = round & 1, np = p ^ 1;  // set produced here is used by round+1
     const uint32_t* counts = reinterpret_cast<const uint32_t*>(xchg) + size_t(K) * Dp;
@@ -453,7 +453,19 @@ __global__ void k_finish(int mode, uint32_t K, uint32_t P, uint32_t D, uint32_t 
         const size_t i = size_t(word) * 32 + lane;
         const bool in = i < D;
         uint32_t z;
-        if (mode == 2) {
+        if (mode == 0 && run) {  // incremental: xchg row c >= 1 holds the round's delta of cluster c
+            // S_c = running sums + delta (written to parity np), S_0 = colsum - sum_{c >= 1} S_c
+            uint32_t sc;
+            if (c != 0) {
+                sc = run[(size_t(p) * K + c) * Dp + i] + uint32_t(xchg[size_t(c) * Dp + i]);
+                run[(size_t(np) * K + c) * Dp + i] = sc;
+            } else {
+                sc = uint32_t(colsum[i]);
+                for (uint32_t o = 1; o < K; ++o)
+                    sc -= run[(size_t(p) * K + o) * Dp + i] + uint32_t(xchg[size_t(o) * Dp + i]);
+            }
+            z = counts[c] != 0 ? sc : (in ? Z[size_t(c) * D + i] : 0u);  // empty clusters keep theirs
+        } else if (mode == 2) {
             z = in ? Z[size_t(c) * D + i] : 0u;
         } else if (mode == 1 || counts[c] != 0) {
             if (int(c) == skip) {
@@ -504,7 +516,8 @@ void launch_finish(const FinishArgs& a, cudaStream_t s) {
     const uint32_t threads = 256;
     const uint64_t total = uint64_t(a.W32) * a.K * 32;
     k_finish<<<uint32_t((total + threads - 1) / threads), threads, 0, s>>>(
-        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.bfrag, a.state, a.round, a.early_stop);
+        a.mode, a.K, a.P, a.D, a.W32, a.W32P, a.Dp, a.xchg, a.colsum, a.Z, a.run, a.bfrag, a.state, a.round,
+        a.early_stop);
 }
 
 // Zero the accumulators of parity np before k_finish accumulates into them.

@@ -458,20 +458,35 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 for (uint32_t c = 0; c < KC; ++c) ccount[c] += best == c;
             }
             TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
+            // incremental re-bundling: pixels whose membership of a tracked cluster c >= 1 changed
+            // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
+            // complement (flag). Global lists (one per tracked cluster, n entries apart) for
+            // k_fold_list, or the tile's shared list for the fold warps (K == 2).
+            if (flist != nullptr && do_update) {
+#pragma unroll
+                for (uint32_t c = 1; c < KC; ++c) {
+                    if (c >= K) break;
+                    const bool enter = live && best == c && old != c, leave = live && old == c && best != c;
+                    const uint32_t m = __ballot_sync(0xffffffffu, enter || leave);
+                    if (!m) continue;
+                    uint32_t base = 0;
+                    if (lane == 0) base = atomicAdd(flist_count + (c - 1), uint32_t(__popc(m)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (enter || leave)
+                        flist[size_t(c - 1) * n + base + __popc(m & ((1u << lane) - 1))] =
+                            uint32_t(px) | (leave ? 0x80000000u : 0u);
+                }
+            }
             if constexpr (UPD) {
-                // membership of cluster 1 changed (old = 0xFFFFFFFF before round 1): entering
-                // pixels add their HV, leaving pixels their complement (flag 0x100)
                 const bool enter = live && best == 1 && old != 1, leave = live && old == 1 && best != 1;
-                const bool take = do_update && (enter || leave);
+                const bool take = folding && (enter || leave);
                 // one compacted list per tile: the four quarters reserve their ranges with an
                 // shared-memory atomic (the fold warps reset the count once they have read it)
                 const uint32_t m = __ballot_sync(0xffffffffu, take);
                 uint32_t base = 0;
-                if (lane == 0 && m) base = atomicAdd(flist ? flist_count : &s_listn[db], uint32_t(__popc(m)));
+                if (lane == 0 && m) base = atomicAdd(&s_listn[db], uint32_t(__popc(m)));
                 base = __shfl_sync(0xffffffffu, base, 0);
-                const uint32_t rank = __popc(m & ((1u << lane) - 1));
-                if (take && flist) flist[base + rank] = uint32_t(px) | (leave ? 0x80000000u : 0u);
-                else if (take) s_list[db * kTP + base + rank] = (32 * qd + lane) | (leave ? 0x100u : 0u);
+                if (take) s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
             mbar_arrive(&list_ready[db]);
             if (qd == 0) TC_TR(5, it);
@@ -794,13 +809,16 @@ void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, cons
 // with one global atomic per entry.
 template <int H>
 __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
-                                                   const uint32_t* __restrict__ grid, uint32_t S32, uint32_t W32,
-                                                   uint32_t* __restrict__ dst) {
+                                                   uint64_t n, const uint32_t* __restrict__ grid, uint32_t S32,
+                                                   uint32_t W32, uint32_t* __restrict__ dst, uint32_t dst_stride) {
     extern __shared__ uint32_t s_val[];  // [32][W32]
     const uint32_t nw = (W32 + 31) / 32, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t grp = warp / nw, col = (warp % nw) * 32 + lane, colc = min(col, W32 - 1);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL) behind the round kernel
-    const uint32_t M = *count;
+    // blockIdx.y = tracked cluster c - 1: its list is n entries after the previous one
+    list += size_t(blockIdx.y) * n;
+    dst += size_t(blockIdx.y) * dst_stride;
+    const uint32_t M = count[blockIdx.y];
     // at least kMinRows rows per CTA: a short list (late rounds) occupies a few CTAs, whose
     // flush (one atomic per entry of D) dominates, instead of all of them
     constexpr uint32_t kMinRows = 64;
@@ -837,22 +855,26 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
     }
 }
 
-void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, const uint32_t* grid,
-                      uint32_t S32, uint32_t W32, int32_t* dst, uint32_t sms, cudaStream_t s) {
-    const uint32_t ctas = sms;
+void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, uint32_t nlists,
+                      const uint32_t* grid, uint32_t S32, uint32_t W32, int32_t* dst, uint32_t dst_stride,
+                      uint32_t sms, cudaStream_t s) {
+    const dim3 ctas(sms, nlists);
     const uint32_t threads = 2 * 32 * ((W32 + 31) / 32);
     const size_t smem = size_t(32) * W32 * 4;
-    const uint64_t per_group = (max_rows + 2 * ctas - 1) / (2 * ctas);  // inputs per counter
+    const uint64_t per_group = (max_rows + 2 * sms - 1) / (2 * sms) + 64;  // inputs per counter
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     if (per_group <= BitCounter<8>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<8>, smem);
-        launch_pdl(k_fold_list<8>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<8>, ctas, dim3(threads), smem, s, list, count, max_rows, grid, S32, W32, d,
+                   dst_stride);
     } else if (per_group <= BitCounter<12>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<12>, smem);
-        launch_pdl(k_fold_list<12>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<12>, ctas, dim3(threads), smem, s, list, count, max_rows, grid, S32, W32, d,
+                   dst_stride);
     } else {
         ensure_dynamic_smem((const void*)k_fold_list<20>, smem);
-        launch_pdl(k_fold_list<20>, dim3(ctas), dim3(threads), smem, s, list, count, grid, S32, W32, d);
+        launch_pdl(k_fold_list<20>, ctas, dim3(threads), smem, s, list, count, max_rows, grid, S32, W32, d,
+                   dst_stride);
     }
 }
 
