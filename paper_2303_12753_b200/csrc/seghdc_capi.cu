@@ -141,7 +141,9 @@ struct seghdc_ctx {
     size_t xchg_round_ints() const { return K * g.Dp + K + 1; }
     // the tcgen05 round kernel re-bundles incrementally (deltas of clusters 1..K-1): K == 2
     // with the fused k_finish_tc, K = 3, 4 with k_fold_list every round and k_finish
-    bool incremental() const { return plan.tc && K >= 2 && K <= 4; }
+    bool incremental() const { return plan.tc && K >= 2 && K <= 8; }
+    // K == 2 on the one-CTA 16-column layout: fold warps in the round kernel + fused k_finish_tc
+    bool fold_warps() const { return plan.tc && K == 2 && seghdc_dev::tc_ncol(2, g.W32) == 16; }
     int32_t* colsum_ptr() { return xchg.p + xchg_round_ints(); }
     void count(uint64_t k = 1) { launches += k; }
     void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
@@ -305,7 +307,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     x.planes = planes;
     if (!plan_round(uint32_t(K), planes, g.W32, g.SS, x.plan, x.smem_optin))
         throw Error(SEGHDC_ERUNTIME, "dim " + std::to_string(g.D) + " does not fit the round kernel's shared memory");
-    if (x.plan.tc && vmax > tc_max_value()) x.plan.tc = false;  // beyond kP8 base-8 digits
+    if (x.plan.tc && vmax > tc_max_value(uint32_t(K), g.W32)) x.plan.tc = false;  // beyond the layout's digits
     x.K = K;
     const uint64_t n = x.n_local();
     if (x.plan.tc && !tc_make_grid_map(x.tmap, x.grid.p, n, g.S32)) x.plan.tc = false;  // no driver entry point
@@ -376,7 +378,7 @@ void select_seeds_dev(seghdc_ctx& x, size_t K) {
 }
 
 void finish(seghdc_ctx& x, int mode, uint32_t round) {
-    if (mode == 0 && x.incremental() && x.K == 2) {  // one fused kernel per round
+    if (mode == 0 && x.fold_warps()) {  // one fused kernel per round
         launch_finish_tc(x.g.D, x.g.W32, x.g.Dp, x.xchg.p, x.colsum_ptr(), x.Z.p, x.run1.p, x.bimg.p, x.state.p,
                          round, x.early_stop, x.ticket.p, x.stream);
         x.count();
@@ -477,7 +479,7 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     static const char* fe = getenv("SEGHDC_FLIST");
     const int flist_mode = fe ? atoi(fe) : 1;  // measured: lists in every round cost +5 us per round
     const bool use_flist =
-        do_update && x.incremental() && (x.K > 2 || flist_mode == 2 || (flist_mode == 1 && r == 1));
+        do_update && x.incremental() && (!x.fold_warps() || flist_mode == 2 || (flist_mode == 1 && r == 1));
     {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;

@@ -32,6 +32,8 @@
 // exactly as in the IMMA kernel (seghdc_kernels.cu), so results are bit-identical.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -42,34 +44,45 @@ constexpr uint32_t kTP = 128;      // pixels per tile (MMA M)
 constexpr uint32_t kCW = 32;       // HV words per chunk (one 128-byte swizzle span per row)
 constexpr uint32_t kKS = kCW / 2;  // k-steps (64 HV dims) per chunk
 constexpr uint32_t kChunkBytes = kTP * kCW * 4;
-constexpr uint32_t kUW = 3;        // unpack warps per TMEM lane quarter (chunk g goes to warp g % kUW)
-constexpr uint32_t kAB = 3;        // A buffers in TMEM (128 columns each)
-static_assert(kAB == kUW, "unpack warp u owns ring slots and A buffers == u mod kUW");
-constexpr uint32_t kP8 = 8;        // balanced base-8 digits per centroid entry
-// warp layout (SM sub-partition = warp % 4): [0, 12) unpack (3 per lane quarter), [12, 16)
-// epilogue (one per lane quarter), 16/17/21/22 fold, 18/19 MMA issue (sub-partitions 2 and 3,
-// away from the producer), 20 producer. Two MMA-issuing warps split the chunks of a tile
-// (even / odd) into two accumulators, halving the issue load on any one sub-partition.
-constexpr uint32_t kWEpi = 4 * kUW, kWMma0 = 18, kWProd = 20, kWarps = 23, kNRW = 4;
-static_assert(kWEpi == 12, "warp layout assumes 12 unpack warps");
+constexpr uint32_t kP8 = 8;        // balanced base-8 digits per centroid entry (K <= 4 layouts)
+// warp layout of the unsplit kernel (SM sub-partition = warp % 4): [0, 12) unpack (3 per lane
+// quarter), [12, 16) epilogue (one per lane quarter), 16/17/21/22 fold, 18/19 MMA issue
+// (sub-partitions 2 and 3, away from the producer), 20 producer. Two MMA-issuing warps split the
+// chunks of a tile (even / odd) into two accumulators, halving the issue load on any one
+// sub-partition. The dimension-split kernel (SPLIT = 4, below) has no fold warps: [0, 8) unpack
+// (2 per lane quarter), [8, 12) epilogue, 12 MMA, 13 producer.
+constexpr uint32_t kNRW = 4;
 __device__ __forceinline__ int fold_index(uint32_t warp) {
     return warp == 16 ? 0 : warp == 17 ? 1 : warp == 21 ? 2 : warp == 22 ? 3 : -1;
 }
 // TMEM columns: A buffers [128*i, 128*i+128), then accumulators D[tile parity][MMA warp]
 // (N columns each), then the (all 1.0) scale factors of A and B
-constexpr uint32_t kTmemCols = 512, kColD = 128 * kAB;
-// Per-N configuration. N = kP8 digit columns per cluster: 16 for K <= 2, 32 for K <= 4.
-template <uint32_t NCOL>
+constexpr uint32_t kTmemCols = 512;
+// Per-layout configuration. N = NDIG digit columns per cluster x KC clusters: 16 (K <= 2) and 32
+// (K <= 4) with 8 digits and the whole B image resident; 72 (K <= 8, 9 digits: entries up to
+// 57.5M, i.e. images of 2^24 pixels) with SPLIT = 4: a cluster of 4 CTAs shares each 128-pixel
+// tile, CTA q owning a quarter of the HV dimensions (and only that quarter of the B image), and
+// the partial dots meet in distributed shared memory.
+template <uint32_t NCOL, uint32_t SPLIT = 1>
 struct TcCfg {
     static constexpr uint32_t N = NCOL;
+    static constexpr uint32_t NDIG = NCOL == 72 ? 9 : kP8;
+    static constexpr uint32_t KC = NCOL / NDIG;              // clusters of the layout
     static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
-    static constexpr uint32_t Stages = NCOL == 16 ? 9 : 3;   // smem ring depth (16 KB each): the larger B
-                                                             // image takes the rest; a multiple of kUW, so
-                                                             // slot g % Stages is unpacked by warp g % kUW
+    static constexpr uint32_t UW = SPLIT > 1 ? 2 : 3;        // unpack warps per TMEM lane quarter
+    static constexpr uint32_t AB = UW;                       // A buffers in TMEM (128 columns each)
+    static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? 4 : 3;  // smem ring depth (16 KB each):
+                                                             // the larger B image takes the rest; a multiple
+                                                             // of UW, so slot g % Stages is unpacked by warp g % UW
     static constexpr uint32_t NMW = NCOL == 16 ? 2 : 1;      // MMA-issuing warps (alternate chunks)
-    static constexpr uint32_t ColSF = kColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
-    static_assert(Stages % kUW == 0, "ring slots follow the unpack warps");
-    static_assert(ColSF + 8 <= kTmemCols, "TMEM budget");
+    static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
+    static constexpr uint32_t WMma0 = SPLIT > 1 ? WEpi + 4 : 18, WProd = SPLIT > 1 ? WEpi + 5 : 20;
+    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 6 : 23;
+    static constexpr uint32_t ColD = 128 * AB;
+    static constexpr uint32_t ColSF = ColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
+    static_assert(Stages % UW == 0, "ring slots follow the unpack warps");
+    static_assert(ColSF + 16 <= kTmemCols, "TMEM budget");
+    static_assert(SPLIT == 1 || WEpi + 4 <= 16, "split layout");
 };
 constexpr uint32_t kKB = TcCfg<16>::KB;  // the K <= 2 image (k_finish_tc)
 
@@ -90,6 +103,12 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* r) {
           "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr)
         : "memory");
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // One chunk (kKS k-steps) of MMAs, issued by an elected lane of the calling warp from a single
@@ -181,18 +200,52 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t
 #define PRG(code) ((void)0)
 #endif
 
-template <uint32_t NCOL>
+template <uint32_t NCOL, uint32_t SPLIT = 1>
 struct TcSmem {
-    using Cfg = TcCfg<NCOL>;
+    using Cfg = TcCfg<NCOL, SPLIT>;
     static constexpr size_t ring = 0;  // [Stages][128][32] u32, 1024-aligned (128B swizzle)
     __host__ __device__ static size_t b(uint32_t nks) { return size_t(Cfg::Stages) * kChunkBytes; }              // [nks][KB] B image
     __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * Cfg::KB; }             // [2][4][32] u32
-    __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + 2 * 4 * 32 * 4; }                   // [2][4] u32
+    __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + (SPLIT > 1 ? 0 : 2 * 4 * 32 * 4); }  // [2][4] u32
     __host__ __device__ static size_t misc(uint32_t nks) { return listn(nks) + 2 * 4 * 4; }                        // tmem base, skip
-    __host__ __device__ static size_t bars(uint32_t nks) { return (misc(nks) + 16 + 7) & ~size_t(7); }
-    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * kAB + 2 + 2 + 2 + 2 + 1;
+    // SPLIT: partial dots of the 4 CTAs for this CTA's lane quarter, [src][32][KC] i64
+    __host__ __device__ static size_t xb(uint32_t nks) { return misc(nks) + 16; }
+    __host__ __device__ static size_t bars(uint32_t nks) {
+        return (xb(nks) + (SPLIT > 1 ? size_t(SPLIT) * 32 * Cfg::KC * 8 : 0) + 7) & ~size_t(7);
+    }
+    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * Cfg::AB + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 1 + SPLIT : 0);
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
+
+// distributed shared memory (SPLIT kernel): the address of the same smem object in CTA `rank`
+// of the cluster, remote stores and cluster-scope mbarrier arrive / wait
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_st_v2(uint32_t addr, unsigned long long a, unsigned long long b) {
+    asm volatile("st.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void cl_arrive(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\nCLW_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra CLW_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 }  // namespace
 
@@ -242,18 +295,20 @@ void read_trace_tc(void* dst) {
 #define TC_CLK(v) ((void)0)
 #endif
 
-template <bool UPD, int H, uint32_t NCOL>
-__global__ void __launch_bounds__(kWarps * 32, 1)
+template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT>
+__global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
                void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp,
                uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine) {
     constexpr uint32_t NRT = kNRW * 32;
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
-    using Cfg = TcCfg<NCOL>;
-    using Smem = TcSmem<NCOL>;
-    constexpr uint32_t kStages = Cfg::Stages, NMW = Cfg::NMW, KC = NCOL / kP8;  // KC: clusters of the layout
-    static_assert(!UPD || NCOL == 16, "the incremental fold is the K == 2 schedule");
+    using Cfg = TcCfg<NCOL, SPLIT>;
+    using Smem = TcSmem<NCOL, SPLIT>;
+    constexpr uint32_t kStages = Cfg::Stages, NMW = Cfg::NMW, KC = Cfg::KC, NDIG = Cfg::NDIG;
+    constexpr uint32_t kUW = Cfg::UW, kAB = Cfg::AB, kWEpi = Cfg::WEpi, kWMma0 = Cfg::WMma0, kWProd = Cfg::WProd;
+    constexpr uint32_t kColD = Cfg::ColD;
+    static_assert(!UPD || (NCOL == 16 && SPLIT == 1), "the incremental fold is the K == 2 schedule");
     extern __shared__ __align__(1024) uint8_t smem[];
     StateView st = StateView::at(state, K);
 
@@ -279,16 +334,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
     uint64_t* list_free = list_ready + 2;       // [2] fold warps done with the list
     uint64_t* b_full = list_free + 2;           // B image landed
+    uint64_t* x_full = b_full + 1;              // SPLIT: the 4 partial dots of this CTA's lane quarter landed
+    uint64_t* x_free = x_full + 1;              // SPLIT: [dest] dest CTA consumed what this CTA's epilogue warp sent
+    const uint32_t qrank = SPLIT > 1 ? cl_rank() : 0u;  // SPLIT: dimension quarter = rank in the cluster
+    const uint32_t cid = blockIdx.x / SPLIT, ncl = gridDim.x / SPLIT;  // tiles go to clusters
 
-    const uint32_t nch = (W32 + kCW - 1) / kCW;  // chunks per tile
+    const uint32_t nch_all = (W32 + kCW - 1) / kCW;  // chunks per tile
+    // SPLIT: this CTA's chunks [ch0, ch0 + nch) of every tile; its B image slice starts at ch0
+    const uint32_t ch0 = qrank * nch_all / SPLIT, nch = (qrank + 1) * nch_all / SPLIT - ch0;
     const uint64_t ntiles = (n + kTP - 1) / kTP;
-    const uint32_t my_tiles = blockIdx.x < ntiles ? uint32_t((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    const uint32_t my_tiles = cid < ntiles ? uint32_t((ntiles - 1 - cid) / ncl + 1) : 0;
     // serpentine traversal: odd rounds walk the tiles from the end of the grid, even rounds from
     // the start, so each round begins with the ~100 MB the previous pass (the encode, or the
     // previous round) left in L2 and only the rest streams from HBM
     const bool reverse = serpentine && (round & 1) != 0;
     auto tile_px0 = [&](uint32_t it) -> uint64_t {
-        const uint64_t t = blockIdx.x + uint64_t(it) * gridDim.x;
+        const uint64_t t = cid + uint64_t(it) * ncl;
         return (reverse ? ntiles - 1 - t : t) * kTP;
     };
 
@@ -309,6 +370,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             mbar_init(&list_free[b], NRT);
         }
         mbar_init(b_full, 1);
+        if (SPLIT > 1) {
+            mbar_init(x_full, SPLIT * 32);
+            for (uint32_t d = 0; d < SPLIT; ++d) mbar_init(&x_free[d], 1);
+        }
         mbar_fence_init();
         s_listn[0] = s_listn[1] = 0;
     }
@@ -319,14 +384,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (SPLIT > 1) cl_sync();  // every CTA's barriers are initialised before any remote arrive
     tc_fence_after();
     const uint32_t tbase = s_misc[0];
     if (warp < 4) {  // scale factors of A and B: every ue8m0 byte 127 (2^0), whatever the layout
-        const uint32_t one = 0x7F7F7F7Fu;
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                         tbase + ((32 * warp) << 16) + Cfg::ColSF),
-                     "r"(one)
-                     : "memory");
+        uint32_t one[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) one[q] = 0x7F7F7F7Fu;
+        tc_st16(tbase + ((32 * warp) << 16) + Cfg::ColSF, one);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     // programmatic dependent launch: everything above (barriers, TMEM, scale factors) overlaps
@@ -399,6 +464,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         // ---------------------------------------------------------------------- epilogue warps
         const uint32_t qd = warp & 3;
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
+        // SPLIT: every epilogue warp sends the partial dots of its lane quarter to CTA qd of the
+        // cluster; the warp with qd == qrank also receives the 4 partials of its quarter and labels
+        const bool fin = SPLIT == 1 || qd == qrank;
+        long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));  // [src][32][KC]
+        uint32_t xdst = 0, xfull_dst = 0;
+        if (SPLIT > 1) {
+            xdst = cl_mapa(smem_u32(xbuf + (qrank * 32 + lane) * KC), qd);
+            xfull_dst = cl_mapa(smem_u32(x_full), qd);
+        }
         unsigned long long n2[KC];
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) n2[c] = c < K ? st.norm2[parity * K + c] : 0ull;
@@ -410,7 +484,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
-            const uint32_t old = live ? labels[px] : 0u;
+            const uint32_t old = (fin && live) ? labels[px] : 0u;
             TC_CLK(c0);
             TCW(3, it, &d_full[db], (it >> 1) & 1);
             __syncwarp();  // converge before the .sync.aligned tcgen05.ld
@@ -422,24 +496,45 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
             for (uint32_t mw = 0; mw < NMW; ++mw)
 #pragma unroll
-                for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16)
+                for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16) {
                     tc_ld16(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
+                    if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // 72 columns: the last 8
+                        tc_ld8(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
+                }
             tc_wait_ld();
             tc_fence_before();
             mbar_arrive(&d_free[db]);
-            // exact dots: column n = kP8 * c + p holds sum_i y_i d_p(z_c[i]) (an integer in f32);
+            // exact dots: column n = NDIG * c + p holds sum_i y_i d_p(z_c[i]) (an integer in f32);
             // dot_c = sum_p digit_dot_p * 8^p
             long long d[KC];
 #pragma unroll
             for (uint32_t c = 0; c < KC; ++c) {
                 d[c] = 0;
 #pragma unroll
-                for (int p = kP8 - 1; p >= 0; --p) {
+                for (int p = NDIG - 1; p >= 0; --p) {
                     int v = 0;
 #pragma unroll
-                    for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][kP8 * c + p]));
+                    for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][NDIG * c + p]));
                     d[c] = d[c] * 8 + v;
                 }
+            }
+            if constexpr (SPLIT > 1) {
+                // partial dots (this CTA's quarter of the dimensions) of lane quarter qd -> CTA qd
+                cl_wait(&x_free[qd], (it & 1) ^ 1);
+#pragma unroll
+                for (uint32_t c = 0; c < KC; c += 2) cl_st_v2(xdst + 8 * c, d[c], d[c + 1]);
+                cl_arrive(xfull_dst);
+                if (!fin) continue;
+                cl_wait(x_full, it & 1);
+#pragma unroll
+                for (uint32_t c = 0; c < KC; ++c) {
+                    long long t = 0;
+#pragma unroll
+                    for (uint32_t src = 0; src < SPLIT; ++src) t += xbuf[(src * 32 + lane) * KC + c];
+                    d[c] = t;
+                }
+                __syncwarp();
+                if (lane < SPLIT) cl_arrive(cl_mapa(smem_u32(&x_free[qrank]), lane));  // slots free again
             }
             // assign_labels (clusterer.cpp:146-158): first strictly closer centroid wins
             uint32_t best = 0;
@@ -457,7 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c) ccount[c] += best == c;
             }
-            TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
+            if (SPLIT == 1) TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
             // incremental re-bundling: pixels whose membership of a tracked cluster c >= 1 changed
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
@@ -488,7 +583,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (take) s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
-            mbar_arrive(&list_ready[db]);
+            if (SPLIT == 1) mbar_arrive(&list_ready[db]);
             if (qd == 0) TC_TR(5, it);
         }
         for (int o = 16; o; o >>= 1) {
@@ -545,12 +640,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     } else if (warp == kWProd) {
         // ----------------------------------------------------------------------- producer warp
         if (lane == 0) {
-            const uint32_t bbytes = nks * Cfg::KB;
+            const uint32_t bbytes = nch * kKS * Cfg::KB;  // this CTA's slice (SPLIT) or the whole image
             // the grid streams through L2 with evict_first (measured: evict_last on the tiles read
             // last slows every round; evict_first takes round 1 from 98 to 82 us at C1)
             const uint64_t pol_stream = policy_evict_first();
             mbar_expect_tx(b_full, bbytes);
-            bulk_g2s(sB, bimg, bbytes, b_full);
+            bulk_g2s(sB, bimg + size_t(ch0) * kKS * Cfg::KB, bbytes, b_full);
             uint32_t g = 0;
             for (uint32_t it = 0; it < my_tiles; ++it) {
                 const int y = int(tile_px0(it));
@@ -562,7 +657,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                     TC_ACC(4, c1 - c0);
                     if (ch == 0) TC_TR(0, it);
                     mbar_expect_tx(&slot_full[s], kChunkBytes);
-                    tma_load_2d_hint(ring + size_t(s) * kChunkBytes, &tmap, int(ch * kCW), y, &slot_full[s],
+                    tma_load_2d_hint(ring + size_t(s) * kChunkBytes, &tmap, int((ch0 + ch) * kCW), y, &slot_full[s],
                                      pol_stream);
                 }
             }
@@ -572,7 +667,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
     // ---------------------------------------------------------------------------- fold warps
     BitCounter<UPD ? H : 1> cnt[CPTMAX];
-    const int fw = fold_index(warp);
+    const int fw = SPLIT == 1 ? fold_index(warp) : -1;
     const uint32_t rt = uint32_t(fw) * 32 + lane;
     const uint32_t cpt = (W32 + NRT - 1) / NRT;
     uint32_t nleave = 0;  // leaving pixels folded by this CTA (same count in every fold thread)
@@ -630,6 +725,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // all roles done: the ring becomes the counters' transpose scratch; free TMEM
     tc_fence_before();
     __syncthreads();
+    if (SPLIT > 1) cl_sync();  // no CTA leaves while a peer may still write its shared memory
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the finish may launch
     if (warp == 0) TC_TG(6);
     if (folding) {  // CTA-uniform: counters -> planes in the ring -> whole-CTA expansion + atomics
@@ -678,10 +774,10 @@ __device__ __forceinline__ int digit8(long long z, uint32_t p) {  // balanced ba
     }
 }
 __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t ks, uint32_t n,
-                                             uint32_t k) {
+                                             uint32_t k, uint32_t ndig) {
     const uint32_t col = k >> 3, j = k & 7, h = col >> 2, c = col & 3;
     const uint32_t dim = 32 * (2 * ks + h) + 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
-    const uint32_t cl = n / kP8, p = n % kP8;
+    const uint32_t cl = n / ndig, p = n % ndig;
     if (cl >= K || dim >= D) return 0;
     const int d = digit8((long long)Z[size_t(cl) * D + dim], p);
     const uint32_t a = uint32_t(d < 0 ? -d : d);
@@ -690,14 +786,14 @@ __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint
     return code | (d < 0 ? 8u : 0u);
 }
 __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
-                             uint8_t* __restrict__ bimg, const void* state) {
+                             uint32_t ndig, uint8_t* __restrict__ bimg, const void* state) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
     const uint32_t total = nks * kb;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t ks = i / kb, rem = i % kb;
         const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
         const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
-        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k) | (b_nibble(Z, K, D, ks, n, k + 1) << 4));
+        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k, ndig) | (b_nibble(Z, K, D, ks, n, k + 1, ndig) << 4));
     }
 }
 
@@ -803,7 +899,7 @@ void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, cons
 }
 
 // Fold of a global list of changed pixels (bit 31: leaving) into xchg row 1, as signed deltas:
-// CTA = 2 row groups x ceil(W32 / 32) warps, thread = word column; each CTA takes a contiguous
+// CTA = 2 row groups (1 when W32 > 384) x ceil(W32 / 32) warps, thread = word column; each CTA takes a contiguous
 // slice of the list, the groups interleave its rows (16 loads in flight per thread), their
 // counts meet in shared memory (u32[32][W32], bit-major: conflict-free both ways) and leave
 // with one global atomic per entry.
@@ -829,11 +925,12 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
     BitCounter<H> cnt;
     cnt.reset();
     uint32_t nleave = 0;
-    for (uint32_t e = r0 + grp; e < r1; e += 32) {  // 16 rows of this group: e, e + 2, ..., e + 30
+    const uint32_t ng = blockDim.x / (32 * nw);  // row groups: 2, or 1 when W32 > 384
+    for (uint32_t e = r0 + grp; e < r1; e += 16 * ng) {  // 16 rows of this group: e, e + ng, ...
         uint32_t x[16];
 #pragma unroll
         for (int v = 0; v < 16; ++v) {
-            const uint32_t i = e + 2 * v;
+            const uint32_t i = e + ng * v;
             const uint32_t en = i < r1 ? list[i] : 0u;
             const uint32_t neg = (en >> 31) ? 0xFFFFFFFFu : 0u;
             const uint32_t word = i < r1 ? __ldg(grid + size_t(en & 0x7FFFFFFFu) * S32 + colc) : 0u;
@@ -859,9 +956,10 @@ void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_
                       const uint32_t* grid, uint32_t S32, uint32_t W32, int32_t* dst, uint32_t dst_stride,
                       uint32_t sms, cudaStream_t s) {
     const dim3 ctas(sms, nlists);
-    const uint32_t threads = 2 * 32 * ((W32 + 31) / 32);
+    const uint32_t ng = W32 > 384 ? 1 : 2;  // row groups per CTA (768 threads at most)
+    const uint32_t threads = ng * 32 * ((W32 + 31) / 32);
     const size_t smem = size_t(32) * W32 * 4;
-    const uint64_t per_group = (max_rows + 2 * sms - 1) / (2 * sms) + 64;  // inputs per counter
+    const uint64_t per_group = (max_rows + ng * sms - 1) / (ng * sms) + 64;  // inputs per counter
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     if (per_group <= BitCounter<8>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<8>, smem);
@@ -901,28 +999,84 @@ __global__ void k_tc_stamp(int ev) {
     g_trace_tc[(size_t(blockIdx.x) * 64 + 61) * 8 + ev] = t_;
 }
 #endif
-template <bool UPD, int H, uint32_t NCOL>
+template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT = 1>
 cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
-    auto kern = k_round_tc<UPD, H, NCOL>;
-    const size_t smem = TcSmem<NCOL>::total(tc_ksteps(a.W32));
+    using Cfg = TcCfg<NCOL, SPLIT>;
+    auto kern = k_round_tc<UPD, H, NCOL, SPLIT>;
+    const uint32_t nch = (a.W32 + kCW - 1) / kCW;
+    const uint32_t nks = SPLIT > 1 ? (nch + SPLIT - 1) / SPLIT * kKS : a.nks;  // B k-steps resident per CTA
+    const size_t smem = TcSmem<NCOL, SPLIT>::total(nks);
     cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(kern, dim3(a.ctas), dim3(kWarps * 32), smem, s, *reinterpret_cast<const CUtensorMap*>(a.tmap),
-                      a.grid, a.n, a.S32, a.W32, a.K, a.bimg, a.nks, a.labels, a.state, a.round, a.do_update,
-                      reinterpret_cast<uint32_t*>(a.xchg), a.Dp, a.flist, a.flist_count, a.serpentine);
+    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(a.tmap);
+    uint32_t* xchg = reinterpret_cast<uint32_t*>(a.xchg);
+    if (SPLIT == 1)
+        return launch_pdl(kern, dim3(a.ctas), dim3(Cfg::Warps * 32), smem, s, tm, a.grid, a.n, a.S32, a.W32, a.K,
+                          a.bimg, nks, a.labels, a.state, a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count,
+                          a.serpentine);
+    // clusters of SPLIT CTAs (one per SM): as many as fit at once, at most one per tile
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(Cfg::Warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = SPLIT;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    static int max_clusters[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && max_clusters[dev] == 0) {
+        cfg.gridDim = dim3(SPLIT * 148);
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, (const void*)kern, &cfg) != cudaSuccess || mc <= 0) {
+            cudaGetLastError();
+            mc = 148 / SPLIT;
+        }
+        max_clusters[dev] = mc;
+    }
+    const uint64_t ntiles = (a.n + kTP - 1) / kTP;
+    const uint64_t ncl = std::max<uint64_t>(1, std::min<uint64_t>(dev < 64 ? max_clusters[dev] : 148 / SPLIT, ntiles));
+    cfg.gridDim = dim3(uint32_t(ncl * SPLIT));
+    return cudaLaunchKernelEx(&cfg, kern, tm, a.grid, a.n, a.S32, a.W32, a.K, a.bimg, nks, a.labels, a.state,
+                              a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine);
 }
 }  // namespace
 
-// K <= 2: N = 16 digit columns; K <= 4: N = 32 (>= 2 chunks, fold columns <= 3 per thread)
-static uint32_t tc_ncol(uint32_t K) { return K <= 2 ? 16u : 32u; }
-bool tc_supported(uint32_t K, uint32_t W32) { return K >= 1 && K <= 4 && W32 > kCW && W32 <= 3 * kNRW * 32; }
-// largest centroid entry kP8 balanced base-8 digits represent: 3 (8^kP8 - 1) / 7
-uint64_t tc_max_value() { return 3ull * ((1ull << (3 * kP8)) - 1) / 7; }
-uint32_t tc_ksteps(uint32_t W32) { return ((W32 + kCW - 1) / kCW) * kKS; }
-size_t tc_smem_bytes(uint32_t K, uint32_t W32) {
-    return tc_ncol(K) == 16 ? TcSmem<16>::total(tc_ksteps(W32)) : TcSmem<32>::total(tc_ksteps(W32));
+// Layout of the tcgen05 kernel for (K, W32): N = 16 digit columns (K <= 2) or 32 (K <= 4) with
+// the whole B image resident in one CTA; N = 72 (K <= 8, 9 digits) split over a cluster of 4
+// CTAs when the whole image does not fit; 0: no tcgen05 layout (IMMA kernels).
+constexpr size_t kSmemOptin = 232448;  // B200: 227 KB of dynamic shared memory per CTA
+static uint32_t tc_nchunks(uint32_t W32) { return (W32 + kCW - 1) / kCW; }
+uint32_t tc_ncol(uint32_t K, uint32_t W32) {
+    const uint32_t nch = tc_nchunks(W32), nks = nch * kKS;
+    if (K < 1 || W32 <= kCW) return 0;
+    if (K <= 2 && W32 <= 3 * kNRW * 32 && TcSmem<16>::total(nks) <= kSmemOptin) return 16;
+    if (K <= 4 && TcSmem<32>::total(nks) <= kSmemOptin) return 32;
+    if (K <= 8 && nch >= 4 && TcSmem<72, 4>::total((nch + 3) / 4 * kKS) <= kSmemOptin) return 72;
+    return 0;
 }
-size_t tc_bimg_bytes(uint32_t K, uint32_t W32) { return size_t(tc_ksteps(W32)) * tc_ncol(K) * 32; }
+bool tc_supported(uint32_t K, uint32_t W32) { return tc_ncol(K, W32) != 0; }
+static uint32_t tc_ndig(uint32_t ncol) { return ncol == 72 ? TcCfg<72, 4>::NDIG : kP8; }
+// largest centroid entry the layout's balanced base-8 digits represent: 3 (8^ndig - 1) / 7
+uint64_t tc_max_value(uint32_t K, uint32_t W32) {
+    const uint32_t nd = tc_ndig(tc_ncol(K, W32));
+    return 3ull * ((1ull << (3 * nd)) - 1) / 7;
+}
+uint32_t tc_ksteps(uint32_t W32) { return tc_nchunks(W32) * kKS; }
+size_t tc_smem_bytes(uint32_t K, uint32_t W32) {
+    const uint32_t nc = tc_ncol(K, W32), nch = tc_nchunks(W32);
+    return nc == 16 ? TcSmem<16>::total(tc_ksteps(W32))
+         : nc == 32 ? TcSmem<32>::total(tc_ksteps(W32))
+         : nc == 72 ? TcSmem<72, 4>::total((nch + 3) / 4 * kKS)
+                    : ~size_t(0);
+}
+size_t tc_bimg_bytes(uint32_t K, uint32_t W32) { return size_t(tc_ksteps(W32)) * tc_ncol(K, W32) * 32; }
 uint32_t tc_tile_pixels() { return kTP; }
 
 bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S32) {
@@ -940,9 +1094,9 @@ bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S
 
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
                        cudaStream_t s) {
-    const uint32_t nks = tc_ksteps(W32), kb = tc_ncol(K) * 32;
+    const uint32_t nc = tc_ncol(K, W32), nks = tc_ksteps(W32), kb = nc * 32;
     const uint32_t total = nks * kb;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, bimg, state);
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), bimg, state);
 }
 
 #ifdef SEGHDC_HANGDBG
@@ -963,6 +1117,14 @@ static cudaError_t launch_round_tc_body(const RoundArgs& a, cudaStream_t s) {
     if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12, 16>(a, s);
     return launch_tc_t<true, 20, 16>(a, s);
 }
+static cudaError_t launch_round_tc_sel(const RoundArgs& a, cudaStream_t s) {
+    switch (tc_ncol(a.K, a.W32)) {
+        case 16: return a.K == 2 ? launch_round_tc_body(a, s) : launch_tc_t<false, 1, 16>(a, s);
+        case 32: return launch_tc_t<false, 1, 32>(a, s);
+        case 72: return launch_tc_t<false, 1, 72, 4>(a, s);
+        default: return cudaErrorInvalidConfiguration;
+    }
+}
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
 #ifdef SEGHDC_TRACE
     // events around [stamp0], [round kernel], [stamp1] separately (read with read_tc_events)
@@ -975,8 +1137,7 @@ cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
     }
     const char* tr = getenv("SEGHDC_TRACE_ROUND");
     if (tr && int(a.round) != atoi(tr)) {  // only the traced round records events and stamps
-        return a.K == 2 ? launch_round_tc_body(a, s)
-                    : a.K == 1 ? launch_tc_t<false, 1, 16>(a, s) : launch_tc_t<false, 1, 32>(a, s);
+        return launch_round_tc_sel(a, s);
     }
     cudaEventRecord(ev[0], s);
     k_tc_stamp<<<148, 1, 0, s>>>(0);
@@ -992,8 +1153,7 @@ cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
     } after{s, ev};
     g_tc_events = ev;
 #endif
-    return a.K == 2 ? launch_round_tc_body(a, s)
-                    : a.K == 1 ? launch_tc_t<false, 1, 16>(a, s) : launch_tc_t<false, 1, 32>(a, s);
+    return launch_round_tc_sel(a, s);
 }
 
 }  // namespace seghdc_dev

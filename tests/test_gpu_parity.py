@@ -155,6 +155,34 @@ def test_cluster_random_vs_oracle(ctx, port, case):
     assert (res2["centroids"] == exp["centroids"]).all()
 
 
+# ------------------------------------------------- K <= 8: 4-CTA dimension-split tcgen05 layout
+@pytest.mark.parametrize("dim,k,h,w,c,its,es", [
+    (3300, 8, 40, 37, 3, 4, False),     # 4 chunks: one per CTA of the cluster
+    (5000, 7, 61, 53, 1, 5, True),      # 5 chunks: 1, 1, 1, 2
+    (10000, 5, 97, 131, 3, 6, False),   # 10 chunks: 2, 3, 2, 3; ~100 tiles
+    (16384, 8, 120, 150, 3, 4, False),  # the C4 shape: 16 chunks, 4 per CTA
+    (16384, 2, 9, 11, 3, 3, True),      # K = 2 too wide for the one-CTA layout; fewer tiles than clusters
+    (16384, 3, 50, 40, 1, 3, False),
+])
+def test_cluster_split_layout_vs_oracle(ctx, port, dim, k, h, w, c, its, es):
+    """The K <= 8 layout (72 digit columns, a cluster of 4 CTAs each owning a quarter of the HV
+    dimensions, partial dots combined in distributed shared memory) against the oracle."""
+    rng = np.random.default_rng(dim + 31 * k + h)
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    img[: h // 2] //= 4
+    cb = S.build_codebooks(dim, h, w, c, 1.0, 3, 1, k)
+    grid = port.encode(img, dim, *cb)
+    got = []
+    res = ctx.cluster(grid, img, dim, k, its, es, on_iteration=lambda r, lab: got.append(lab))
+    assert ctx.round_kernel == "k_round_tc"
+    exp = port.cluster(grid, img, dim, k, its, es, per_round=True)
+    assert res["rounds"] == exp["rounds"]
+    for r in range(exp["rounds"]):
+        assert (got[r] == exp["labels_rounds"][r]).all(), r
+    assert (res["centroids"] == exp["centroids"]).all()
+    assert (res["counts"] == exp["counts"]).all()
+
+
 def test_k1_stops_at_round_two(ctx, port):
     # test_clusterer.cpp:168-174
     img = np.full((2, 2, 1), 10, np.uint8)
