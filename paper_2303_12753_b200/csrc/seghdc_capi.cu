@@ -483,6 +483,10 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;
+        // L2 prefetch distance (chunks) for the layouts whose large B image leaves a shallow
+        // smem ring (N = 32, 72); SEGHDC_PF overrides
+        static const char* pe = getenv("SEGHDC_PF");
+        a.pf = pe ? uint32_t(atoi(pe)) : (x.plan.tc && tc_ncol(uint32_t(x.K), x.g.W32) != 16 ? 8u : 0u);
     }
     a.flist = use_flist ? x.flist.p : nullptr;
     a.flist_count = use_flist ? x.flist.p + (x.K - 1) * x.n_local() : nullptr;

@@ -69,20 +69,22 @@ struct TcCfg {
     static constexpr uint32_t NDIG = NCOL == 72 ? 9 : kP8;
     static constexpr uint32_t KC = NCOL / NDIG;              // clusters of the layout
     static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
-    static constexpr uint32_t UW = SPLIT > 1 ? 2 : 3;        // unpack warps per TMEM lane quarter
-    static constexpr uint32_t AB = UW;                       // A buffers in TMEM (128 columns each)
+    static constexpr uint32_t AB = SPLIT > 1 ? 2 : 3;        // A buffers in TMEM (128 columns each)
+    static constexpr uint32_t UH = SPLIT > 1 ? 2 : 1;        // unpack warps sharing one chunk (halves)
+    static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
     static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? 4 : 3;  // smem ring depth (16 KB each):
                                                              // the larger B image takes the rest; a multiple
-                                                             // of UW, so slot g % Stages is unpacked by warp g % UW
+                                                             // of AB, so slot g % Stages is unpacked by phase g % AB
     static constexpr uint32_t NMW = NCOL == 16 ? 2 : 1;      // MMA-issuing warps (alternate chunks)
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
     static constexpr uint32_t WMma0 = SPLIT > 1 ? WEpi + 4 : 18, WProd = SPLIT > 1 ? WEpi + 5 : 20;
-    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 6 : 23;
+    static constexpr uint32_t WFin = WEpi + 6;               // SPLIT: finalizer warp (labels)
+    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 7 : 23;
     static constexpr uint32_t ColD = 128 * AB;
     static constexpr uint32_t ColSF = ColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
-    static_assert(Stages % UW == 0, "ring slots follow the unpack warps");
+    static_assert(Stages % AB == 0, "ring slots follow the unpack phases");
     static_assert(ColSF + 16 <= kTmemCols, "TMEM budget");
-    static_assert(SPLIT == 1 || WEpi + 4 <= 16, "split layout");
+    static_assert(SPLIT == 1 || Warps == 23, "split layout: 16 unpack, 4 epilogue, MMA, producer, finalizer");
 };
 constexpr uint32_t kKB = TcCfg<16>::KB;  // the K <= 2 image (k_finish_tc)
 
@@ -155,6 +157,11 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// L2 prefetch of a future chunk (no shared memory, no barrier): the ring's TMA load of that chunk
+// then hits L2, so a shallow ring (large B image) still keeps enough bytes in flight
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -208,12 +215,12 @@ struct TcSmem {
     __host__ __device__ static size_t list(uint32_t nks) { return b(nks) + size_t(nks) * Cfg::KB; }             // [2][4][32] u32
     __host__ __device__ static size_t listn(uint32_t nks) { return list(nks) + (SPLIT > 1 ? 0 : 2 * 4 * 32 * 4); }  // [2][4] u32
     __host__ __device__ static size_t misc(uint32_t nks) { return listn(nks) + 2 * 4 * 4; }                        // tmem base, skip
-    // SPLIT: partial dots of the 4 CTAs for this CTA's lane quarter, [src][32][KC] i64
+    // SPLIT: partial dots of the 4 CTAs for this CTA's lane quarter, [2][src][KC][32] i64
     __host__ __device__ static size_t xb(uint32_t nks) { return misc(nks) + 16; }
     __host__ __device__ static size_t bars(uint32_t nks) {
-        return (xb(nks) + (SPLIT > 1 ? size_t(SPLIT) * 32 * Cfg::KC * 8 : 0) + 7) & ~size_t(7);
+        return (xb(nks) + (SPLIT > 1 ? 2 * size_t(SPLIT) * 32 * Cfg::KC * 8 : 0) + 7) & ~size_t(7);
     }
-    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * Cfg::AB + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 1 + SPLIT : 0);
+    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * Cfg::AB + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
 
@@ -229,8 +236,8 @@ __device__ __forceinline__ uint32_t cl_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ void cl_st_v2(uint32_t addr, unsigned long long a, unsigned long long b) {
-    asm volatile("st.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+__device__ __forceinline__ void cl_st_u64(uint32_t addr, unsigned long long a) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(a) : "memory");
 }
 __device__ __forceinline__ void cl_arrive(uint32_t remote_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
@@ -255,7 +262,7 @@ __device__ int g_trace_round;  // 0: trace every launch (the last one wins), r: 
 #define TC_ON (g_trace_round == 0 || int(round) == g_trace_round)
 #define TC_TR(ev, it)                                                                 \
     do {                                                                              \
-        if (lane == 0 && blockIdx.x < 148 && (it) < 64 && TC_ON)                      \
+        if (lane == 0 && blockIdx.x < 148 && (it) < 60 && TC_ON)                      \
             g_trace_tc[(size_t(blockIdx.x) * 64 + (it)) * 8 + (ev)] = clock64();      \
     } while (0)
 static cudaEvent_t* g_tc_events = nullptr;
@@ -300,13 +307,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
                void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp,
-               uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine) {
+               uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine, uint32_t pf) {
     constexpr uint32_t NRT = kNRW * 32;
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
     using Cfg = TcCfg<NCOL, SPLIT>;
     using Smem = TcSmem<NCOL, SPLIT>;
     constexpr uint32_t kStages = Cfg::Stages, NMW = Cfg::NMW, KC = Cfg::KC, NDIG = Cfg::NDIG;
-    constexpr uint32_t kUW = Cfg::UW, kAB = Cfg::AB, kWEpi = Cfg::WEpi, kWMma0 = Cfg::WMma0, kWProd = Cfg::WProd;
+    constexpr uint32_t kAB = Cfg::AB, kUH = Cfg::UH, kWEpi = Cfg::WEpi, kWMma0 = Cfg::WMma0, kWProd = Cfg::WProd;
     constexpr uint32_t kColD = Cfg::ColD;
     static_assert(!UPD || (NCOL == 16 && SPLIT == 1), "the incremental fold is the K == 2 schedule");
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -334,8 +341,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
     uint64_t* list_free = list_ready + 2;       // [2] fold warps done with the list
     uint64_t* b_full = list_free + 2;           // B image landed
-    uint64_t* x_full = b_full + 1;              // SPLIT: the 4 partial dots of this CTA's lane quarter landed
-    uint64_t* x_free = x_full + 1;              // SPLIT: [dest] dest CTA consumed what this CTA's epilogue warp sent
+    uint64_t* x_full = b_full + 1;              // SPLIT: [2] the 4 partial dots of this CTA's lane quarter landed
+    uint64_t* x_free = x_full + 2;              // SPLIT: [2][dest] dest CTA consumed what this CTA's epilogue warp sent
     const uint32_t qrank = SPLIT > 1 ? cl_rank() : 0u;  // SPLIT: dimension quarter = rank in the cluster
     const uint32_t cid = blockIdx.x / SPLIT, ncl = gridDim.x / SPLIT;  // tiles go to clusters
 
@@ -356,11 +363,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     if (tid == 0) {
         for (uint32_t s = 0; s < kStages; ++s) {
             mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_free[s], 4 * 32);
+            mbar_init(&slot_free[s], 4 * 32 * kUH);
         }
         for (uint32_t b = 0; b < kAB; ++b) {
-            mbar_init(&a_full[2 * b], 4 * 32);
-            mbar_init(&a_full[2 * b + 1], 4 * 32);
+            mbar_init(&a_full[2 * b], 4 * 32 * kUH);
+            mbar_init(&a_full[2 * b + 1], 4 * 32 * kUH);
             mbar_init(&a_free[b], 1);
         }
         for (uint32_t b = 0; b < 2; ++b) {
@@ -371,8 +378,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         }
         mbar_init(b_full, 1);
         if (SPLIT > 1) {
-            mbar_init(x_full, SPLIT * 32);
-            for (uint32_t d = 0; d < SPLIT; ++d) mbar_init(&x_free[d], 1);
+            for (uint32_t b = 0; b < 2; ++b) {
+                mbar_init(&x_full[b], SPLIT * 32);
+                for (uint32_t d = 0; d < SPLIT; ++d) mbar_init(&x_free[b * SPLIT + d], 1);
+            }
         }
         mbar_fence_init();
         s_listn[0] = s_listn[1] = 0;
@@ -416,13 +425,15 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     if (warp < kWEpi) {
         // ------------------------------------------------------------------------ unpack warps
         // warp (qd, u) unpacks the 32 rows of lane quarter qd of every chunk g with
-        // g % kUW == u, so kUW chunks are in flight per quarter (each warp's chain of LDS ->
-        // masks -> tcgen05.st -> wait::st is latency-bound)
-        const uint32_t qd = warp & 3, u = warp >> 2;  // lane quarter, chunk phase
+        // g % kAB == u / kUH (words [32 hf / kUH, 32 (hf + 1) / kUH) of the chunk, hf = u % kUH),
+        // so kAB chunks are in flight per quarter (each warp's chain of LDS -> masks ->
+        // tcgen05.st -> wait::st is latency-bound; SPLIT halves it with two warps per chunk)
+        const uint32_t qd = warp & 3, u = warp >> 2;  // lane quarter, chunk phase x half
+        const uint32_t ph = u / kUH, hf = u % kUH;
         const uint32_t r = 32 * qd + lane;            // pixel row of the tile
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
         const uint32_t nchunks = my_tiles * nch;
-        for (uint32_t g = u; g < nchunks; g += kUW) {
+        for (uint32_t g = ph; g < nchunks; g += kAB) {
             const uint32_t s = g % kStages, ab = g % kAB;
             TC_CLK(c0);
             TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
@@ -439,7 +450,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // ALU pipe the four masks per word
             const uint32_t half = opaque(0x80000000u), two = opaque(2u);
 #pragma unroll
-            for (uint32_t c16 = 0; c16 < 8; ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
+            for (uint32_t c16 = hf * (8 / kUH); c16 < (hf + 1) * (8 / kUH); ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
                 const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
                 uint32_t a[16];
@@ -460,17 +471,20 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_arrive(&a_full[2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
-    } else if (warp < kWEpi + 4) {
+    } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp == Cfg::WFin)) {
         // ---------------------------------------------------------------------- epilogue warps
-        const uint32_t qd = warp & 3;
+        // SPLIT: the epilogue warps (one per lane quarter qd) send the partial dots of their 32
+        // pixels (this CTA's quarter of the dimensions) to CTA qd of the cluster; the finalizer
+        // warp receives the 4 partials of this CTA's own lane quarter (qrank) and labels them.
+        // The exchange buffer is double-buffered by tile parity, [2][src][KC][32] i64.
+        const bool finw = SPLIT > 1 && warp == Cfg::WFin;
+        const uint32_t qd = finw ? qrank : (warp & 3);
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
-        // SPLIT: every epilogue warp sends the partial dots of its lane quarter to CTA qd of the
-        // cluster; the warp with qd == qrank also receives the 4 partials of its quarter and labels
-        const bool fin = SPLIT == 1 || qd == qrank;
-        long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));  // [src][32][KC]
+        const bool fin = SPLIT == 1 || finw;  // this warp labels pixels
+        long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));
         uint32_t xdst = 0, xfull_dst = 0;
-        if (SPLIT > 1) {
-            xdst = cl_mapa(smem_u32(xbuf + (qrank * 32 + lane) * KC), qd);
+        if (SPLIT > 1 && !finw) {
+            xdst = cl_mapa(smem_u32(xbuf + (qrank * KC) * 32 + lane), qd);
             xfull_dst = cl_mapa(smem_u32(x_full), qd);
         }
         unsigned long long n2[KC];
@@ -485,56 +499,83 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
             const uint32_t old = (fin && live) ? labels[px] : 0u;
-            TC_CLK(c0);
-            TCW(3, it, &d_full[db], (it >> 1) & 1);
-            __syncwarp();  // converge before the .sync.aligned tcgen05.ld
-            TC_CLK(c1);
-            if (qd == 0) TC_ACC(5, c1 - c0);
-            tc_fence_after();
-            if (qd == 0) TC_TR(4, it);
-            uint32_t acc[NMW][NCOL];  // the MMA warps' accumulators of this tile
-#pragma unroll
-            for (uint32_t mw = 0; mw < NMW; ++mw)
-#pragma unroll
-                for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16) {
-                    tc_ld16(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
-                    if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // 72 columns: the last 8
-                        tc_ld8(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
-                }
-            tc_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&d_free[db]);
-            // exact dots: column n = NDIG * c + p holds sum_i y_i d_p(z_c[i]) (an integer in f32);
-            // dot_c = sum_p digit_dot_p * 8^p
             long long d[KC];
+            if (!finw) {
+                TC_CLK(c0);
+                TCW(3, it, &d_full[db], (it >> 1) & 1);
+                __syncwarp();  // converge before the .sync.aligned tcgen05.ld
+                TC_CLK(c1);
+                if (qd == 0) TC_ACC(5, c1 - c0);
+                tc_fence_after();
+                if (qd == 0) TC_TR(4, it);
+                if constexpr (SPLIT > 1) {
+                    // 72 columns in 3 groups of 24 (registers: 23 warps share the SM): column
+                    // n = NDIG c + p adds digit_dot * 8^p to dot_c
 #pragma unroll
-            for (uint32_t c = 0; c < KC; ++c) {
-                d[c] = 0;
+                    for (uint32_t c = 0; c < KC; ++c) d[c] = 0;
 #pragma unroll
-                for (int p = NDIG - 1; p >= 0; --p) {
-                    int v = 0;
+                    for (uint32_t grp = 0; grp < NCOL / 24; ++grp) {
+                        uint32_t r24[24];
 #pragma unroll
-                    for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][NDIG * c + p]));
-                    d[c] = d[c] * 8 + v;
+                        for (uint32_t q = 0; q < 3; ++q) tc_ld8(lane_addr + kColD + db * NCOL + 24 * grp + 8 * q, r24 + 8 * q);
+                        tc_wait_ld();
+#pragma unroll
+                        for (uint32_t j = 0; j < 24; ++j) {
+                            const uint32_t col = 24 * grp + j, c = col / NDIG, p = col % NDIG;
+                            d[c] += (long long)__float2int_rn(__uint_as_float(r24[j])) * (1ll << (3 * p));
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&d_free[db]);
+                } else {
+                    uint32_t acc[NMW][NCOL];  // the MMA warps' accumulators of this tile
+#pragma unroll
+                    for (uint32_t mw = 0; mw < NMW; ++mw)
+#pragma unroll
+                        for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16) {
+                            tc_ld16(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
+                            if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // 72 columns: the last 8
+                                tc_ld8(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
+                        }
+                    tc_wait_ld();
+                    tc_fence_before();
+                    mbar_arrive(&d_free[db]);
+                    // exact dots: column n = NDIG * c + p holds sum_i y_i d_p(z_c[i]) (an integer in
+                    // f32); dot_c = sum_p digit_dot_p * 8^p
+#pragma unroll
+                    for (uint32_t c = 0; c < KC; ++c) {
+                        d[c] = 0;
+#pragma unroll
+                        for (int p = NDIG - 1; p >= 0; --p) {
+                            int v = 0;
+#pragma unroll
+                            for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][NDIG * c + p]));
+                            d[c] = d[c] * 8 + v;
+                        }
+                    }
                 }
             }
             if constexpr (SPLIT > 1) {
-                // partial dots (this CTA's quarter of the dimensions) of lane quarter qd -> CTA qd
-                cl_wait(&x_free[qd], (it & 1) ^ 1);
+                if (!finw) {  // partial dots of lane quarter qd -> CTA qd, slot [db][qrank]
+                    cl_wait(&x_free[db * SPLIT + qd], ((it >> 1) & 1) ^ 1);
+                    const uint32_t o = db * (SPLIT * KC * 32 * 8);
 #pragma unroll
-                for (uint32_t c = 0; c < KC; c += 2) cl_st_v2(xdst + 8 * c, d[c], d[c + 1]);
-                cl_arrive(xfull_dst);
-                if (!fin) continue;
-                cl_wait(x_full, it & 1);
+                    for (uint32_t c = 0; c < KC; ++c) cl_st_u64(xdst + o + c * 256, (unsigned long long)d[c]);
+                    cl_arrive(xfull_dst + db * 8);
+                    if (qd == 0) TC_TR(5, it);
+                    continue;
+                }
+                cl_wait(&x_full[db], (it >> 1) & 1);
+                const long long* xb = xbuf + db * (SPLIT * KC * 32) + lane;
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c) {
                     long long t = 0;
 #pragma unroll
-                    for (uint32_t src = 0; src < SPLIT; ++src) t += xbuf[(src * 32 + lane) * KC + c];
+                    for (uint32_t src = 0; src < SPLIT; ++src) t += xb[(src * KC + c) * 32];
                     d[c] = t;
                 }
                 __syncwarp();
-                if (lane < SPLIT) cl_arrive(cl_mapa(smem_u32(&x_free[qrank]), lane));  // slots free again
+                if (lane < SPLIT) cl_arrive(cl_mapa(smem_u32(&x_free[db * SPLIT + qrank]), lane));  // slots free again
             }
             // assign_labels (clusterer.cpp:146-158): first strictly closer centroid wins
             uint32_t best = 0;
@@ -647,10 +688,17 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_expect_tx(b_full, bbytes);
             bulk_g2s(sB, bimg + size_t(ch0) * kKS * Cfg::KB, bbytes, b_full);
             uint32_t g = 0;
+            const uint32_t nchunks = my_tiles * nch;
+            for (uint32_t q = 0; q < pf && q < nchunks; ++q)
+                tma_prefetch_2d(&tmap, int((ch0 + q % nch) * kCW), int(tile_px0(q / nch)));
             for (uint32_t it = 0; it < my_tiles; ++it) {
                 const int y = int(tile_px0(it));
                 for (uint32_t ch = 0; ch < nch; ++ch, ++g) {
                     const uint32_t s = g % kStages;
+                    if (pf && g + pf < nchunks) {  // chunk g + pf into L2 now
+                        const uint32_t gp = g + pf;
+                        tma_prefetch_2d(&tmap, int((ch0 + gp % nch) * kCW), int(tile_px0(gp / nch)));
+                    }
                     TC_CLK(c0);
                     TCW(8, g, &slot_free[s], ((g / kStages) & 1) ^ 1);
                     TC_CLK(c1);
@@ -1013,7 +1061,7 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     if (SPLIT == 1)
         return launch_pdl(kern, dim3(a.ctas), dim3(Cfg::Warps * 32), smem, s, tm, a.grid, a.n, a.S32, a.W32, a.K,
                           a.bimg, nks, a.labels, a.state, a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count,
-                          a.serpentine);
+                          a.serpentine, a.pf);
     // clusters of SPLIT CTAs (one per SM): as many as fit at once, at most one per tile
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(Cfg::Warps * 32);
@@ -1044,7 +1092,7 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     const uint64_t ncl = std::max<uint64_t>(1, std::min<uint64_t>(dev < 64 ? max_clusters[dev] : 148 / SPLIT, ntiles));
     cfg.gridDim = dim3(uint32_t(ncl * SPLIT));
     return cudaLaunchKernelEx(&cfg, kern, tm, a.grid, a.n, a.S32, a.W32, a.K, a.bimg, nks, a.labels, a.state,
-                              a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine);
+                              a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine, a.pf);
 }
 }  // namespace
 

@@ -6,7 +6,16 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-constexpr int N = 16;
+#ifndef PN
+#define PN 16
+#endif
+#ifndef BSTEP
+#define BSTEP 512
+#endif
+#ifndef BBYTES
+#define BBYTES 32768
+#endif
+constexpr int N = PN;
 // idesc (block-scaled): a/b format E2M1 (1) at bits 7/10, scale format E8M0 (bit 23), N>>3 at 17, M>>4 at 24
 constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t(N) >> 3) << 17) | ((128u >> 4) << 24);
 __global__ void kcheck(const uint32_t* A, const uint8_t* B, float* D) {
@@ -64,11 +73,11 @@ __global__ void kcheck(const uint32_t* A, const uint8_t* B, float* D) {
 }
 template <int NMW, int STW>
 __global__ void krate(long long* out, int iters) {
-  __shared__ __align__(1024) uint8_t sB[32768];
+  extern __shared__ __align__(1024) uint8_t sB[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < int(sizeof(sB)); i += blockDim.x) sB[i] = uint8_t(i * 7) & 0x77;
+  for (int i = tid; i < BBYTES; i += blockDim.x) sB[i] = uint8_t(i * 7) & 0x77;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -102,7 +111,9 @@ __global__ void krate(long long* out, int iters) {
     const uint64_t bdesc = uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) | (1ull << 46);
     const uint32_t d = tb + 32 * warp;
     long long t0 = clock64();
-#define MX "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a], b, %3, [%4], [%5], p;\n\tadd.u64 b, b, 32;\n\tadd.u32 a, a, 8;\n\t"
+#define STR2(x) #x
+#define STR(x) STR2(x)
+#define MX "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a], b, %3, [%4], [%5], p;\n\tadd.u64 b, b, " STR(BSTEP / 16) ";\n\tadd.u32 a, a, 8;\n\t"
     for (int i0 = 0; i0 < iters; i0 += 16 * NMW) {
       asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
@@ -125,8 +136,9 @@ static float e2m1(unsigned c) {
 template <int NMW, int STW> void rate() {
   long long* d; cudaMalloc(&d, 8 * 148); long long h = 0;
   const int iters = 8192;
-  krate<NMW, STW><<<148, 32 * (4 + STW)>>>(d, iters); cudaDeviceSynchronize();
-  krate<NMW, STW><<<148, 32 * (4 + STW)>>>(d, iters); cudaError_t e = cudaDeviceSynchronize();
+  cudaFuncSetAttribute(krate<NMW, STW>, cudaFuncAttributeMaxDynamicSharedMemorySize, BBYTES);
+  krate<NMW, STW><<<148, 32 * (4 + STW), BBYTES>>>(d, iters); cudaDeviceSynchronize();
+  krate<NMW, STW><<<148, 32 * (4 + STW), BBYTES>>>(d, iters); cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   printf("mxf4 N=%d issuing warps=%d st warps=%2d: %.2f cycles per MMA (%s)\n", N, NMW, STW, double(h) / iters, cudaGetErrorString(e));
 }
