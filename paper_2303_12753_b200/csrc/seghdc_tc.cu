@@ -78,13 +78,13 @@ struct TcCfg {
     static constexpr uint32_t NMW = NCOL == 16 ? 2 : 1;      // MMA-issuing warps (alternate chunks)
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
     static constexpr uint32_t WMma0 = SPLIT > 1 ? WEpi + 4 : 18, WProd = SPLIT > 1 ? WEpi + 5 : 20;
-    static constexpr uint32_t WFin = WEpi + 6;               // SPLIT: finalizer warp (labels)
-    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 7 : 23;
+    static constexpr uint32_t WFin = WEpi + 6;               // SPLIT: 2 finalizer warps (labels), by tile parity
+    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 8 : 23;
     static constexpr uint32_t ColD = 128 * AB;
     static constexpr uint32_t ColSF = ColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
     static_assert(Stages % AB == 0, "ring slots follow the unpack phases");
     static_assert(ColSF + 16 <= kTmemCols, "TMEM budget");
-    static_assert(SPLIT == 1 || Warps == 23, "split layout: 16 unpack, 4 epilogue, MMA, producer, finalizer");
+    static_assert(SPLIT == 1 || Warps == 24, "split layout: 16 unpack, 4 epilogue, MMA, producer, 2 finalizers");
 };
 constexpr uint32_t kKB = TcCfg<16>::KB;  // the K <= 2 image (k_finish_tc)
 
@@ -451,7 +451,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint32_t half = opaque(0x80000000u), two = opaque(2u);
 #pragma unroll
             for (uint32_t c16 = hf * (8 / kUH); c16 < (hf + 1) * (8 / kUH); ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
+#ifndef SEGHDC_EXP_NOLDS  // timing experiment only: no shared-memory reads in the unpack
                 const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
+#else
+                const uint4 v = make_uint4(r, c16, g, lane);
+#endif
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
                 uint32_t a[16];
 #pragma unroll
@@ -471,13 +475,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_arrive(&a_full[2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
-    } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp == Cfg::WFin)) {
+    } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp >= Cfg::WFin)) {
         // ---------------------------------------------------------------------- epilogue warps
         // SPLIT: the epilogue warps (one per lane quarter qd) send the partial dots of their 32
         // pixels (this CTA's quarter of the dimensions) to CTA qd of the cluster; the finalizer
         // warp receives the 4 partials of this CTA's own lane quarter (qrank) and labels them.
         // The exchange buffer is double-buffered by tile parity, [2][src][KC][32] i64.
-        const bool finw = SPLIT > 1 && warp == Cfg::WFin;
+        const bool finw = SPLIT > 1 && warp >= Cfg::WFin;  // finalizer warp f takes the tiles of parity f
         const uint32_t qd = finw ? qrank : (warp & 3);
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
         const bool fin = SPLIT == 1 || finw;  // this warp labels pixels
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
+            if (finw && db != warp - Cfg::WFin) continue;
             const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
@@ -665,8 +670,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 if (m == 0) TC_ACC(2, c1 - c0);
                 tc_fence_after();
                 PRG(12 * 100000 + g);
+#ifndef SEGHDC_EXP_NOMMA  // timing experiment only: the pipeline without the tensor-core work
                 tc_mma_chunk<Cfg::KB>(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * Cfg::KB), idesc,
                                       tbase + Cfg::ColSF, ch >= NMW);
+#endif
                 tc_commit(&a_free[ab]);
                 PRG(13 * 100000 + g);
                 {
