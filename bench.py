@@ -43,6 +43,7 @@ WORKLOAD_TEXT = {
 }
 METRIC = "pixel-HV cluster updates/sec (px·iter/s) at D=10k, K=2; % of roofline"
 BETA, GAMMA, CB_SEED = 26, 1, 0
+C2_IMAGES = 64  # config 2: a batch of 64 independent images (seeds 0..63)
 
 
 def peaks():
@@ -242,7 +243,9 @@ def main():
     ctx.set_stream(stream.cuda_stream)
 
     sharded = world > 1 and args.config in (3, 4)
-    img = S.synth_image(spec["cid"], 0 if sharded else rank)
+    batch = args.config == 2  # C2: 64 independent images, rank r takes images r, r + N, ...
+    img_ids = list(range(rank, C2_IMAGES, world)) if batch else [0 if sharded else rank]
+    img = S.synth_image(spec["cid"], img_ids[0])
     h, w, c = img.shape
     cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], BETA, GAMMA, CB_SEED)
     k, iters, dim = spec["k"], spec["iterations"], spec["dim"]
@@ -257,6 +260,19 @@ def main():
             ctx.encode_async(r0, r1)
             cluster_row_sharded([ctx], k, iters, False, ar)
         n_local = (r1 - r0) * w
+    elif batch:
+        # the rank's images stay resident in HBM; a step loads each one (D2D), encodes and
+        # clusters it (the codebooks are shared: same shape and seed)
+        imgs = [S.synth_image(spec["cid"], i) for i in img_ids]
+        dev_imgs = torch.from_numpy(np.stack(imgs)).to(dev)
+        ptrs = [dev_imgs[j].data_ptr() for j in range(len(imgs))]
+
+        def step():
+            for p in ptrs:
+                ctx.load_image_ptr(p, h, w, c)
+                ctx.encode_async(0, h)
+                ctx.cluster_async(k, iters, False)
+        n_local = h * w * len(imgs)
     else:
         def step():
             ctx.encode_async(0, h)
@@ -286,7 +302,7 @@ def main():
         t = torch.tensor([ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    total_px_iter = (h * w if sharded else h * w * world) * iters * args.steps
+    total_px_iter = (h * w if sharded else C2_IMAGES * h * w if batch else h * w * world) * iters * args.steps
     value = total_px_iter / (ms / 1000.0)
 
     # ---- dominant kernel (round kernel) timed with CUDA events on the same stream
@@ -303,37 +319,39 @@ def main():
         t = json.load(open(tp))
         if t.get("kernel") == kernel_name and args.config == 1:
             traffic = t["dram_bytes_per_launch"]
-    bytes_per_launch = n_local * ((dim + 7) // 8)  # algorithmic: one packed HV read per pixel
+    bytes_per_launch = (n_local // len(img_ids)) * ((dim + 7) // 8)  # algorithmic: one packed HV read per pixel
     achieved = bytes_per_launch / (kern_ms / kern_n / 1000.0) / 1e9
 
     # ---- end to end through the reference-facing C-ABI call with host buffers
     e2e = None
     if not sharded:
-        pin_img = torch.from_numpy(img).pin_memory().numpy()
+        pin_imgs = [torch.from_numpy(S.synth_image(spec["cid"], i)).pin_memory().numpy() for i in img_ids]
         cfg = S.RunConfig(dim=dim, alpha=spec["alpha"], beta=BETA, gamma=GAMMA, clusters=k, iterations=iters,
                           seed=CB_SEED, early_stop=False)
         for _ in range(2):
-            ctx.run_pipeline(pin_img, cfg)
+            ctx.run_pipeline(pin_imgs[0], cfg)
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        e2e_steps = max(3, min(args.steps, 50))
+        e2e_steps = max(3, min(args.steps, 10 if batch else 50))
         for _ in range(e2e_steps):
-            res = ctx.run_pipeline(pin_img, cfg)
+            res = [ctx.run_pipeline(pi, cfg) for pi in pin_imgs]
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
         wph = (dim + 63) // 64
-        h2d = img.nbytes + (2 + c) * wph * 8  # image + the Manhattan codebook bases (tables expand on the device)
-        d2h = h * w * 4
-        e2e = {"value": h * w * iters * world * e2e_steps / dt, "unit": "px·iter/s", "h2d_bytes_per_step": h2d,
+        # per image: the image + the Manhattan codebook bases (tables expand on the device)
+        h2d = len(pin_imgs) * (img.nbytes + (2 + c) * wph * 8)
+        d2h = len(pin_imgs) * h * w * 4
+        e2e = {"value": h * w * len(pin_imgs) * iters * world * e2e_steps / dt, "unit": "px·iter/s",
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "timer": "host wall clock around the synchronous seghdc_run_pipeline "
                                                   "(codebook bases on the host + H2D image/bases + device codebooks + "
                                                   "encode + cluster + D2H labels into page-locked memory)",
                "steps": e2e_steps}
-        labels_sha = hashlib.sha256(res.mask.astype(np.uint32).tobytes()).hexdigest()[:16]
+        labels_sha = hashlib.sha256(b"".join(r.mask.astype(np.uint32).tobytes() for r in res)).hexdigest()[:16]
     else:
         labels_sha = None
 
@@ -349,6 +367,16 @@ def main():
                "sample": f"{args.cpu_sample_rounds} chained assign_labels+update_centroids rounds of the full "
                          f"{spec['name']} image, single thread ({dt:.1f} s)"}
 
+    grid_mb = n_local * (((dim + 31) // 32 + 31) // 32 * 128) / 1e6
+    if batch:
+        l2_note = (f"{len(img_ids)} images per rank, {grid_mb / len(img_ids):.0f} MB grid each ({grid_mb:.0f} MB "
+                   "per step) vs 126 MB L2: a step streams every image's grid from HBM once (encode); "
+                   "one image's later rounds may hit L2 (a property of the 256x256 workload; not flushed)")
+    elif grid_mb > 126:
+        l2_note = f"grid {grid_mb:.0f} MB per rank > 126 MB L2: every round streams from HBM (no flush needed)"
+    else:
+        l2_note = (f"grid {grid_mb:.0f} MB per rank < 126 MB L2: rounds may hit L2 (a property of the small image; "
+                   "not flushed)")
     line = {
         "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -356,11 +384,11 @@ def main():
                                                                    if kernel_name == "k_round_tc" else
                                                                    "u8 x u8 -> s32 IMMA, u64/u128 argmax"),
         "data": "synthetic (seeded generator, SURVEY.md §8d)",
-        "config": {"workload": WORKLOAD_TEXT[args.config], "pixels_per_rank": n_local, "dim": dim, "k": k,
+        "config": {"workload": WORKLOAD_TEXT[args.config], "pixels_per_rank": n_local, "images_per_rank": len(img_ids),
+                   "dim": dim, "k": k,
                    "iterations": iters, "early_stop": False, "parallelism": (f"row-shard x{world}" if sharded else
                                                                             f"replicas x{world}"),
-                   "l2": f"grid {n_local * (((dim + 31) // 32 + 31) // 32 * 128) / 1e6:.0f} MB per rank > 126 MB L2: "
-                         "every round streams from HBM (no flush needed)",
+                   "l2": l2_note,
                    "labels_sha256_16": labels_sha},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name + " (fused assign + re-bundle)",

@@ -174,7 +174,8 @@ void require(bool cond, const std::string& msg) {
 void load_image(seghdc_ctx& x, const uint8_t* px, size_t h, size_t w, size_t c) {
     seghdc_host::validate_image(h, w, c);
     x.img.ensure(h * w * c);
-    ck(cudaMemcpyAsync(x.img.p, px, h * w * c, cudaMemcpyHostToDevice, x.stream), "upload image");
+    // host or device pointer (unified addressing): a batch kept resident in HBM loads D2D
+    ck(cudaMemcpyAsync(x.img.p, px, h * w * c, cudaMemcpyDefault, x.stream), "upload image");
     x.h = h;
     x.w = w;
     x.c = c;
