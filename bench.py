@@ -44,6 +44,7 @@ WORKLOAD_TEXT = {
 METRIC = "pixel-HV cluster updates/sec (px·iter/s) at D=10k, K=2; % of roofline"
 BETA, GAMMA, CB_SEED = 26, 1, 0
 C2_IMAGES = 64  # config 2: a batch of 64 independent images (seeds 0..63)
+C2_GROUPS = int(os.environ.get("SEGHDC_C2_GROUPS", "4"))  # concurrent contexts for the batch
 
 
 def peaks():
@@ -263,15 +264,33 @@ def main():
     elif batch:
         # the rank's images stay resident in HBM; a step loads each one (D2D), encodes and
         # clusters it (the codebooks are shared: same shape and seed)
+        # C2_GROUPS contexts on their own streams, each sized for 1/C2_GROUPS of the SMs, take
+        # the images round-robin: small images run side by side instead of one 148-CTA grid
+        # at a time (each image's 512 tiles would leave the last wave of a full grid half empty)
         imgs = [S.synth_image(spec["cid"], i) for i in img_ids]
         dev_imgs = torch.from_numpy(np.stack(imgs)).to(dev)
         ptrs = [dev_imgs[j].data_ptr() for j in range(len(imgs))]
+        groups = [ctx] + [S.Context(local) for _ in range(C2_GROUPS - 1)]
+        g_streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(C2_GROUPS - 1)]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for gc, gs in zip(groups, g_streams):
+            gc.set_stream(gs.cuda_stream)
+            gc.set_sm_budget(sms // C2_GROUPS)
+            gc.load_image(img)
+            gc.load_codebooks(dim, *cb)
+        fork = torch.cuda.Event()
 
         def step():
-            for p in ptrs:
-                ctx.load_image_ptr(p, h, w, c)
-                ctx.encode_async(0, h)
-                ctx.cluster_async(k, iters, False)
+            fork.record(stream)
+            for gs in g_streams[1:]:
+                gs.wait_event(fork)
+            for j, p in enumerate(ptrs):
+                gc = groups[j % C2_GROUPS]
+                gc.load_image_ptr(p, h, w, c)
+                gc.encode_async(0, h)
+                gc.cluster_async(k, iters, False)
+            for gs in g_streams[1:]:
+                stream.wait_stream(gs)
         n_local = h * w * len(imgs)
     else:
         def step():
@@ -288,7 +307,7 @@ def main():
         step()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.kernel_launches
+    launches0 = sum(g.kernel_launches for g in groups) if batch else ctx.kernel_launches
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
@@ -296,7 +315,7 @@ def main():
             step()
         e1.record(stream)
         barrier()
-    launches = ctx.kernel_launches - launches0
+    launches = sum(g.kernel_launches for g in groups) - launches0 if batch else ctx.kernel_launches - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -306,11 +325,16 @@ def main():
     value = total_px_iter / (ms / 1000.0)
 
     # ---- dominant kernel (round kernel) timed with CUDA events on the same stream
-    ctx.profile_rounds(True)
+    profs = groups if batch else [ctx]
+    for g in profs:
+        g.profile_rounds(True)
     for _ in range(args.steps):
         step()
-    kern_ms, kern_n = ctx.profile_read()
-    ctx.profile_rounds(False)
+    kern_ms = kern_n = 0
+    for g in profs:
+        a_ms, a_n = g.profile_read()
+        kern_ms, kern_n = kern_ms + a_ms, kern_n + a_n
+        g.profile_rounds(False)
     peak, peak_src = peaks()
     kernel_name = ctx.round_kernel
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
@@ -321,6 +345,8 @@ def main():
             traffic = t["dram_bytes_per_launch"]
     bytes_per_launch = (n_local // len(img_ids)) * ((dim + 7) // 8)  # algorithmic: one packed HV read per pixel
     achieved = bytes_per_launch / (kern_ms / kern_n / 1000.0) / 1e9
+    if batch:  # C2_GROUPS launches run side by side, each on 1/C2_GROUPS of the SMs
+        achieved *= len(profs)
 
     # ---- end to end through the reference-facing C-ABI call with host buffers
     e2e = None
@@ -332,10 +358,19 @@ def main():
             ctx.run_pipeline(pin_imgs[0], cfg)
         if world > 1:
             torch.distributed.barrier()
-        t0 = time.perf_counter()
         e2e_steps = max(3, min(args.steps, 10 if batch else 50))
+        if batch:  # one host thread per context: the synchronous calls of the groups overlap
+            from concurrent.futures import ThreadPoolExecutor
+            pool = ThreadPoolExecutor(len(groups))
+
+            def run_group(j):
+                return [(i, groups[j].run_pipeline(pin_imgs[i], cfg)) for i in range(j, len(pin_imgs), len(groups))]
+        t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            res = [ctx.run_pipeline(pi, cfg) for pi in pin_imgs]
+            if batch:
+                res = [r for _, r in sorted(x for part in pool.map(run_group, range(len(groups))) for x in part)]
+            else:
+                res = [ctx.run_pipeline(pi, cfg) for pi in pin_imgs]
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device=dev)
@@ -393,7 +428,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name + " (fused assign + re-bundle)",
                      "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": kern_ms / kern_n,
-                     "launches_timed": kern_n, "kernel_share_of_step": kern_ms / ms,
+                     "launches_timed": kern_n, "kernel_share_of_step": kern_ms / len(profs) / ms,
+                     "concurrent_launches": len(profs),
                      "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -49,6 +49,10 @@ void seghdc_destroy(seghdc_ctx* ctx);
 const char* seghdc_last_error(const seghdc_ctx* ctx);
 /* Order all further work of ctx on an external cudaStream_t (NULL: the context's own). */
 int seghdc_set_stream(seghdc_ctx* ctx, void* cuda_stream);
+/* Size this context's kernel grids for `sms` SMs (0: the whole device), so several contexts on
+   separate streams share the GPU (batches of small images run side by side). No reference
+   counterpart: a scheduling hint that leaves every result unchanged. */
+int seghdc_set_sm_budget(seghdc_ctx* ctx, int sms);
 int seghdc_synchronize(seghdc_ctx* ctx);
 /* Number of device kernels this context has launched so far (for launch accounting). */
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx);

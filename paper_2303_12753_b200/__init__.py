@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+import threading
 import weakref
 from typing import Callable, Optional
 
@@ -47,6 +48,7 @@ SIGNATURES = {
     "seghdc_destroy": ([C.c_void_p], None),
     "seghdc_last_error": ([C.c_void_p], C.c_char_p),
     "seghdc_set_stream": ([C.c_void_p, C.c_void_p], C.c_int),
+    "seghdc_set_sm_budget": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_synchronize": ([C.c_void_p], C.c_int),
     "seghdc_kernel_launches": ([C.c_void_p], C.c_uint64),
     "seghdc_round_kernel": ([C.c_void_p], C.c_char_p),
@@ -146,10 +148,12 @@ def build_codebooks(dim: int, h: int, w: int, channels: int, alpha: float = 0.2,
 
 
 _pinned_free: dict = {}  # nbytes -> [pointers]: page-locked buffers returned by dead arrays
+_pinned_lock = threading.Lock()
 
 
 def _return_pinned(nbytes: int, ptr: int) -> None:
-    _pinned_free.setdefault(nbytes, []).append(ptr)
+    with _pinned_lock:
+        _pinned_free.setdefault(nbytes, []).append(ptr)
 
 
 def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
@@ -157,10 +161,12 @@ def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
     through a process-wide pool once every view of it is gone."""
     dtype = np.dtype(dtype)
     nbytes = int(np.prod(shape)) * dtype.itemsize
-    free = _pinned_free.get(nbytes)
-    if free:
-        ptr = free.pop()
-    else:
+    ptr = None
+    with _pinned_lock:  # callers on several host threads (one per context)
+        free = _pinned_free.get(nbytes)
+        if free:
+            ptr = free.pop()
+    if ptr is None:
         p = C.c_void_p()
         _check(lib().seghdc_pinned_alloc(nbytes, C.byref(p)))
         ptr = p.value
@@ -212,6 +218,11 @@ class Context:
 
     def set_stream(self, stream_handle: int) -> None:
         self.check(lib().seghdc_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    def set_sm_budget(self, sms: int) -> None:
+        """Size this context's grids for ``sms`` SMs (0 = all): contexts on separate streams then
+        run side by side (batches of small images). Results do not depend on it."""
+        self.check(lib().seghdc_set_sm_budget(self.h, sms))
 
     def synchronize(self) -> None:
         self.check(lib().seghdc_synchronize(self.h))

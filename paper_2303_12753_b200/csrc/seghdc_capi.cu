@@ -629,6 +629,15 @@ void seghdc_destroy(seghdc_ctx* ctx) {
 
 const char* seghdc_last_error(const seghdc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
 
+int seghdc_set_sm_budget(seghdc_ctx* ctx, int sms) {
+    return guarded(ctx, [&] {
+        require(sms >= 0, "SM budget must be >= 0");
+        int dev_sms = 0;
+        ck(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device), "attr");
+        ctx->sms = (sms == 0 || sms > dev_sms) ? dev_sms : sms;
+    });
+}
+
 int seghdc_set_stream(seghdc_ctx* ctx, void* stream) {
     return guarded(ctx, [&] {
         ck(cudaStreamSynchronize(ctx->stream), "sync");

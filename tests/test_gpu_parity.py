@@ -183,6 +183,37 @@ def test_cluster_split_layout_vs_oracle(ctx, port, dim, k, h, w, c, its, es):
     assert (res["counts"] == exp["counts"]).all()
 
 
+@pytest.mark.parametrize("k,dim", [(2, 10000), (8, 16384)])
+def test_sm_budget_and_concurrent_contexts(port, k, dim):
+    """Contexts with an SM budget on separate streams (bench --config 2) give the oracle's results."""
+    import torch
+    rng = np.random.default_rng(k)
+    imgs = [rng.integers(0, 256, (48, 57, 3), dtype=np.uint8) for _ in range(3)]
+    cb = S.build_codebooks(dim, 48, 57, 3, 1.0, 2, 1, 0)
+    ctxs, streams = [], []
+    for j in range(3):
+        c = S.Context(0)
+        st = torch.cuda.Stream()
+        c.set_stream(st.cuda_stream)
+        c.set_sm_budget(13 + 20 * j)
+        c.load_image(imgs[j])
+        c.load_codebooks(dim, *cb)
+        ctxs.append(c)
+        streams.append(st)
+    for c, im in zip(ctxs, imgs):
+        c.encode_async(0, 48)
+        c.cluster_async(k, 4, False)
+    for c, im in zip(ctxs, imgs):
+        res = c.fetch_results(48 * 57, k, dim)
+        exp = port.cluster(port.encode(im, dim, *cb), im, dim, k, 4, False)
+        assert (res["labels"] == exp["labels"]).all()
+        assert (res["centroids"] == exp["centroids"]).all()
+    with pytest.raises(S.ConfigError):
+        ctxs[0].set_sm_budget(-1)
+    for c in ctxs:
+        c.close()
+
+
 def test_k1_stops_at_round_two(ctx, port):
     # test_clusterer.cpp:168-174
     img = np.full((2, 2, 1), 10, np.uint8)
