@@ -338,10 +338,11 @@ def main():
     peak, peak_src = peaks()
     kernel_name = ctx.round_kernel
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-    tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "round1_traffic.json" if args.config == 1 else
+                      f"round1_traffic_c{args.config}.json")
     if os.path.exists(tp):
         t = json.load(open(tp))
-        if t.get("kernel") == kernel_name and args.config == 1:
+        if t.get("kernel") == kernel_name:
             traffic = t["dram_bytes_per_launch"]
     bytes_per_launch = (n_local // len(img_ids)) * ((dim + 7) // 8)  # algorithmic: one packed HV read per pixel
     achieved = bytes_per_launch / (kern_ms / kern_n / 1000.0) / 1e9
@@ -397,10 +398,15 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        dt, pxr, kind = cpu_reference_rounds(spec, img, args.cpu_sample_rounds, 1)
+        # bounded sample (~5-20 s of CPU work): the whole image up to 400k pixels, else its
+        # first rows (C3/C4: ~200k pixels, a crop clustered as an image of its own)
+        rows = h if h * w <= 400_000 else max(1, 200_000 // w)
+        crop = np.ascontiguousarray(img[:rows])
+        dt, pxr, kind = cpu_reference_rounds(spec, crop, args.cpu_sample_rounds, 1)
+        what = f"the full {spec['name']} image" if rows == h else f"the first {rows} rows ({rows * w} px) of the {spec['name']} image"
         cpu = {"value": pxr / dt, "unit": "px·iter/s", "cores": 1, "kind": kind,
-               "sample": f"{args.cpu_sample_rounds} chained assign_labels+update_centroids rounds of the full "
-                         f"{spec['name']} image, single thread ({dt:.1f} s)"}
+               "sample": f"{args.cpu_sample_rounds} chained assign_labels+update_centroids rounds of {what}, "
+                         f"single thread ({dt:.1f} s)"}
 
     grid_mb = n_local * (((dim + 31) // 32 + 31) // 32 * 128) / 1e6
     if batch:

@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #ifndef SEGHDC_EXP_NOLDS  // timing experiment only: no shared-memory reads in the unpack
                 const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
 #else
-                const uint4 v = make_uint4(r, c16, g, lane);
+                const uint4 v = make_uint4(0u, 0u, 0u, 0u);  // all-zero A: every dot 0, labels settle at 0
 #endif
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
                 uint32_t a[16];
@@ -465,7 +465,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     a[4 * i + 2] = (w4[i] * two) & 0x22222222u;
                     a[4 * i + 3] = __umulhi(w4[i], half) & 0x44444444u;
                 }
+#ifndef SEGHDC_EXP_NOSTTM  // timing experiment only: no A stores into TMEM
                 tc_st16(lane_addr + ab * 128 + c16 * 16, a);  // k-steps 2*c16, 2*c16+1: 8 columns each
+#else
+                if (a[0] == 0x12345678u) tc_st16(lane_addr + ab * 128 + c16 * 16, a);
+#endif
             }
             PRG(10 * 100000 + g);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -562,7 +566,12 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             }
             if constexpr (SPLIT > 1) {
                 if (!finw) {  // partial dots of lane quarter qd -> CTA qd, slot [db][qrank]
+                    TC_CLK(cx0);
                     cl_wait(&x_free[db * SPLIT + qd], ((it >> 1) & 1) ^ 1);
+                    {
+                        TC_CLK(cx1);
+                        if (qd == 0) TC_ACC(7, cx1 - cx0);
+                    }
                     const uint32_t o = db * (SPLIT * KC * 32 * 8);
 #pragma unroll
                     for (uint32_t c = 0; c < KC; ++c) cl_st_u64(xdst + o + c * 256, (unsigned long long)d[c]);
@@ -603,7 +612,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
             // k_fold_list, or the tile's shared list for the fold warps (K == 2).
+#if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM)
+            if (false) {  // timing experiments: results are meaningless, keep the lists out of it
+#else
             if (flist != nullptr && do_update) {
+#endif
 #pragma unroll
                 for (uint32_t c = 1; c < KC; ++c) {
                     if (c >= K) break;
@@ -658,8 +671,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;
             const uint32_t d_t = tbase + kColD + (NMW * db + m) * NCOL;
+            TC_CLK(cf0);
             TCW(6, it, &d_free[db], ((it >> 1) & 1) ^ 1);
             __syncwarp();
+            {
+                TC_CLK(cf1);
+                if (m == 0) TC_ACC(6, cf1 - cf0);
+            }
             const uint32_t first = (NMW + m - (it * nch) % NMW) % NMW;
             for (uint32_t ch = first; ch < nch; ch += NMW) {  // chunks with g % NMW == m
                 const uint32_t g = it * nch + ch, ab = g % kAB;

@@ -32,7 +32,7 @@ acc = t[:, 62, :].copy()
 # with SEGHDC_TRACE_ROUND=r the accumulators cover round r of the 3 runs above
 nchunk = 3 * ((tiles + 32) // 33) * ((dim // 32 + 31) // 32 // 4)
 print("cycles per chunk (median over CTAs):", ", ".join(f"{n}={np.median(acc[:, i]) / nchunk:.0f}" for i, n in enumerate(
-    ["unp_slotfull", "unp_afree", "mma_afull", "mma_issue", "prod_slotfree", "epi_dfull"])))
+    ["unp_slotfull", "unp_afree", "mma_afull", "mma_issue", "prod_slotfree", "epi_dfull", "mma_dfree", "epi_xfree"])))
 t[:, 60:, :] = t[:, 59:60, :]
 t = t - t[:, :1, 0:1]
 names = ["prod_issue", "unpack_beg", "unpack_end", "mma_commit", "epi_D", "epi_list"]
