@@ -313,7 +313,13 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
     const uint64_t n = x.n_local();
     if (x.plan.tc && !tc_make_grid_map(x.tmap, x.grid.p, n, g.S32)) x.plan.tc = false;  // no driver entry point
     const uint64_t tp = x.plan.tc ? tc_tile_pixels() : 16ull * x.plan.mt;
-    x.round_ctas = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(x.sms, (n + tp - 1) / tp)));
+    // balanced waves: as few CTAs as give every CTA the same number of tiles as with x.sms
+    // (C0: 512 tiles -> 128 CTAs x 4 instead of 148 CTAs with 3 or 4)
+    {
+        const uint64_t tiles = std::max<uint64_t>(1, (n + tp - 1) / tp);
+        const uint64_t per = (tiles + x.sms - 1) / x.sms;
+        x.round_ctas = uint32_t(std::max<uint64_t>(1, (tiles + per - 1) / per));
+    }
     const uint32_t NT = x.plan.nt;
     x.state.ensure(StateView::bytes(uint32_t(K)));
     x.labels.ensure(n + 4);  // +4: the fused kernel's TMA of a tile's labels rounds up to 16 B

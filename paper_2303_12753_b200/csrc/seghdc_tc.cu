@@ -1114,7 +1114,10 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
         max_clusters[dev] = mc;
     }
     const uint64_t ntiles = (a.n + kTP - 1) / kTP;
-    const uint64_t ncl = std::max<uint64_t>(1, std::min<uint64_t>(dev < 64 ? max_clusters[dev] : 148 / SPLIT, ntiles));
+    const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(dev < 64 ? max_clusters[dev] : 148 / SPLIT,
+                                                                  a.ctas / SPLIT));
+    const uint64_t per = (ntiles + cap - 1) / cap;  // balanced waves, as for the one-CTA layouts
+    const uint64_t ncl = std::max<uint64_t>(1, (ntiles + per - 1) / per);
     cfg.gridDim = dim3(uint32_t(ncl * SPLIT));
     return cudaLaunchKernelEx(&cfg, kern, tm, a.grid, a.n, a.S32, a.W32, a.K, a.bimg, nks, a.labels, a.state,
                               a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine, a.pf);
