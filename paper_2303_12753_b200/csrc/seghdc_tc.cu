@@ -682,7 +682,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             for (uint32_t ch = first; ch < nch; ch += NMW) {  // chunks with g % NMW == m
                 const uint32_t g = it * nch + ch, ab = g % kAB;
                 TC_CLK(c0);
-                TCW(7, g, &a_full[2 * ab + m], (g / (NMW * kAB)) & 1);  // g = x + NMW kAB t here
+                // a_full[2 ab + m] carries chunks g = x + lcm(NMW, kAB) t
+                constexpr uint32_t kLcm = (kAB % NMW == 0) ? kAB : NMW * kAB;
+                TCW(7, g, &a_full[2 * ab + m], (g / kLcm) & 1);
                 __syncwarp();  // converge before elect.sync / tcgen05.mma
                 TC_CLK(c1);
                 if (m == 0) TC_ACC(2, c1 - c0);

@@ -135,7 +135,7 @@ static float e2m1(unsigned c) {
 }
 template <int NMW, int STW> void rate() {
   long long* d; cudaMalloc(&d, 8 * 148); long long h = 0;
-  const int iters = 8192;
+  const int iters = getenv("PITERS") ? atoi(getenv("PITERS")) : 8192;
   cudaFuncSetAttribute(krate<NMW, STW>, cudaFuncAttributeMaxDynamicSharedMemorySize, BBYTES);
   krate<NMW, STW><<<148, 32 * (4 + STW), BBYTES>>>(d, iters); cudaDeviceSynchronize();
   krate<NMW, STW><<<148, 32 * (4 + STW), BBYTES>>>(d, iters); cudaError_t e = cudaDeviceSynchronize();

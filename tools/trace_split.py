@@ -7,8 +7,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2303_12753_b200 as S
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
-dim, k = 16384, 8
-img = S.synth_image(4, 0)[:side, :side].copy()
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 4  # 4: D = 16384, K = 8 (split layout); 3: D = 10000, K = 4
+dim, k = (16384, 8) if cfg == 4 else (10000, 4)
+img = S.synth_image(cfg, 0)[:side, :side].copy()
 h, w, c = img.shape
 ctx = S.Context(0)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st); ctx.set_stream(st.cuda_stream)
@@ -30,7 +31,8 @@ S.lib().seghdc_debug_trace_tc(buf.ctypes.data_as(ctypes.c_void_p))
 t = buf.reshape(148, 64, 8).astype(np.int64)
 acc = t[:, 62, :].copy()
 # with SEGHDC_TRACE_ROUND=r the accumulators cover round r of the 3 runs above
-nchunk = 3 * ((tiles + 32) // 33) * ((dim // 32 + 31) // 32 // 4)
+ncta = 33 if cfg == 4 else 148
+nchunk = 3 * ((tiles + ncta - 1) // ncta) * (((dim + 31) // 32 + 31) // 32 // (4 if cfg == 4 else 1))
 print("cycles per chunk (median over CTAs):", ", ".join(f"{n}={np.median(acc[:, i]) / nchunk:.0f}" for i, n in enumerate(
     ["unp_slotfull", "unp_afree", "mma_afull", "mma_issue", "prod_slotfree", "epi_dfull", "mma_dfree", "epi_xfree"])))
 t[:, 60:, :] = t[:, 59:60, :]
