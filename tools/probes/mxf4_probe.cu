@@ -77,7 +77,14 @@ __global__ void krate(long long* out, int iters) {
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < BBYTES; i += blockDim.x) sB[i] = uint8_t(i * 7) & 0x77;
+  for (int i = tid; i < BBYTES; i += blockDim.x) {
+#ifdef RANDB  // random e2m1 digit codes of both signs, as balanced base-8 centroid digits give
+    uint32_t x = uint32_t(i) * 2246822519u; x ^= x >> 13; x *= 3266489917u; x ^= x >> 16;
+    sB[i] = uint8_t(x);
+#else
+    sB[i] = uint8_t(i * 7) & 0x77;
+#endif
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -88,6 +95,17 @@ __global__ void krate(long long* out, int iters) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tb = tmem_base;
+#ifdef RANDA  // the A operand (TMEM columns 256..383): random HV bits as the round kernel's nibbles
+  if (warp < 4) {
+    for (int c = 0; c < 128; ++c) {
+      uint32_t x = (tid * 2654435761u) ^ (c * 40503u) ^ 0x9E3779B9u;
+      x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+      const uint32_t v = x & ((c & 1) ? 0x44444444u : 0x22222222u);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tb + ((32 * warp) << 16) + 256 + c), "r"(v));
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+#endif
   if (warp < 4) {
     const uint32_t s = 0x7F7F7F7Fu;
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tb + ((32 * warp) << 16) + 500), "r"(s), "r"(s), "r"(s), "r"(s));
