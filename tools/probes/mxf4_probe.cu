@@ -133,6 +133,13 @@ __global__ void krate(long long* out, int iters) {
 #define STR(x) STR2(x)
 #define MX "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [a], b, %3, [%4], [%5], p;\n\tadd.u64 b, b, " STR(BSTEP / 16) ";\n\tadd.u32 a, a, 8;\n\t"
     for (int i0 = 0; i0 < iters; i0 += 16 * NMW) {
+#ifdef FENCE  // as the round kernel: mbarrier wait + fence::after_thread_sync before every 16 MMAs
+      asm volatile("{\n\t.reg .pred p;\n\tWF: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 1;\n\t@!p bra WF;\n\t}" ::"r"(smem_u32(&bar[warp])));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#endif
+#ifdef COMMIT  // and a commit to an mbarrier after every 16 MMAs (the A buffer release)
+      if (i0) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar[warp ^ 1])));
+#endif
       asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
         MX MX MX MX MX MX MX MX MX MX MX MX MX MX MX MX "}"
