@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(kEncWarps * 32, 3)
             const uint32_t rv = s_row[rr * 32 + lane];
             const uint8_t* px = s_img + rr * kEncCols * C;
             uint32_t* o = grid + (size_t(rb + rr - row_begin) * w + c0) * S32 + w0 + lane;
-            for (uint32_t c16 = 0; c16 < nc; c16 += 16) {
-                const uint32_t lim = nc - c16;  // >= 16 except in the last group of a ragged tile
+            uint32_t c16 = 0;
+            for (; c16 + 16 <= nc; c16 += 16) {  // full groups of 16 pixels: no bounds per word
                 uint32_t x[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
@@ -148,14 +148,33 @@ __global__ void __launch_bounds__(kEncWarps * 32, 3)
                     uint32_t v = rv ^ s_col_l[cc * 32];
 #pragma unroll
                     for (int ch = 0; ch < C; ++ch) v ^= s_wid_l[(ch * 256 + px[cc * C + ch]) * 32];
-                    x[u] = uint32_t(u) < lim ? v : 0u;
+                    x[u] = v;
                 }
                 if (st) {
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        if (uint32_t(u) < lim) *o = x[u];
-                        o += S32;
+                    for (int u = 0; u < 16; ++u) o[size_t(u) * S32] = x[u];
+                }
+                o += size_t(16) * S32;
+                cnt.add16(x);
+            }
+            if (c16 < nc) {  // the ragged last group of a tile
+                const uint32_t lim = nc - c16;
+                uint32_t x[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const uint32_t cc = c16 + u;
+                    uint32_t v = 0;
+                    if (uint32_t(u) < lim) {
+                        v = rv ^ s_col_l[cc * 32];
+#pragma unroll
+                        for (int ch = 0; ch < C; ++ch) v ^= s_wid_l[(ch * 256 + px[cc * C + ch]) * 32];
                     }
+                    x[u] = v;
+                }
+                if (st) {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        if (uint32_t(u) < lim) o[size_t(u) * S32] = x[u];
                 }
                 cnt.add16(x);
             }
