@@ -72,16 +72,25 @@ struct TcCfg {
     static constexpr uint32_t AB = SPLIT > 1 ? 2 : 3;        // A buffers in TMEM (128 columns each)
     static constexpr uint32_t UH = SPLIT > 1 ? 2 : 1;        // unpack warps sharing one chunk (halves)
     static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
+#ifndef SEGHDC_C3_NMW2
+    static constexpr uint32_t DB = 2;                        // accumulator sets (by tile parity)
+#else
+    static constexpr uint32_t DB = (NCOL == 32 && SPLIT == 1) ? 1 : 2;
+#endif
     static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? 4 : 3;  // smem ring depth (16 KB each):
                                                              // the larger B image takes the rest; a multiple
                                                              // of AB, so slot g % Stages is unpacked by phase g % AB
+#ifndef SEGHDC_C3_NMW2
     static constexpr uint32_t NMW = NCOL == 16 ? 2 : 1;      // MMA-issuing warps (alternate chunks)
+#else
+    static constexpr uint32_t NMW = (NCOL == 16 || (NCOL == 32 && SPLIT == 1)) ? 2 : 1;
+#endif
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
     static constexpr uint32_t WMma0 = SPLIT > 1 ? WEpi + 4 : 18, WProd = SPLIT > 1 ? WEpi + 5 : 20;
     static constexpr uint32_t WFin = WEpi + 6;               // SPLIT: 2 finalizer warps (labels), by tile parity
     static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 8 : 23;
     static constexpr uint32_t ColD = 128 * AB;
-    static constexpr uint32_t ColSF = ColD + 2 * NMW * NCOL;  // after D[2 tile parities][NMW]
+    static constexpr uint32_t ColSF = ColD + DB * NMW * NCOL;  // after D[DB tile parities][NMW]
     static_assert(Stages % AB == 0, "ring slots follow the unpack phases");
     static_assert(ColSF + 16 <= kTmemCols, "TMEM budget");
     static_assert(SPLIT == 1 || Warps == 24, "split layout: 16 unpack, 4 epilogue, MMA, producer, 2 finalizers");
@@ -502,8 +511,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
-            const uint32_t db = it & 1;
+            const uint32_t db = it & 1;  // exchange slot / finalizer
             if (finw && db != warp - Cfg::WFin) continue;
+            const uint32_t dd = it % Cfg::DB, dpar = (it / Cfg::DB) & 1;  // accumulator set, its phase
             const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
@@ -511,7 +521,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             long long d[KC];
             if (!finw) {
                 TC_CLK(c0);
-                TCW(3, it, &d_full[db], (it >> 1) & 1);
+                TCW(3, it, &d_full[dd], dpar);
                 __syncwarp();  // converge before the .sync.aligned tcgen05.ld
                 TC_CLK(c1);
                 if (qd == 0) TC_ACC(5, c1 - c0);
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     for (uint32_t grp = 0; grp < NCOL / 24; ++grp) {
                         uint32_t r24[24];
 #pragma unroll
-                        for (uint32_t q = 0; q < 3; ++q) tc_ld8(lane_addr + kColD + db * NCOL + 24 * grp + 8 * q, r24 + 8 * q);
+                        for (uint32_t q = 0; q < 3; ++q) tc_ld8(lane_addr + kColD + dd * NCOL + 24 * grp + 8 * q, r24 + 8 * q);
                         tc_wait_ld();
 #pragma unroll
                         for (uint32_t j = 0; j < 24; ++j) {
@@ -535,20 +545,20 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                         }
                     }
                     tc_fence_before();
-                    mbar_arrive(&d_free[db]);
+                    mbar_arrive(&d_free[dd]);
                 } else {
                     uint32_t acc[NMW][NCOL];  // the MMA warps' accumulators of this tile
 #pragma unroll
                     for (uint32_t mw = 0; mw < NMW; ++mw)
 #pragma unroll
                         for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16) {
-                            tc_ld16(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
+                            tc_ld16(lane_addr + kColD + (NMW * dd + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
                             if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // 72 columns: the last 8
-                                tc_ld8(lane_addr + kColD + (NMW * db + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
+                                tc_ld8(lane_addr + kColD + (NMW * dd + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
                         }
                     tc_wait_ld();
                     tc_fence_before();
-                    mbar_arrive(&d_free[db]);
+                    mbar_arrive(&d_free[dd]);
                     // exact dots: column n = NDIG * c + p holds sum_i y_i d_p(z_c[i]) (an integer in
                     // f32); dot_c = sum_p digit_dot_p * 8^p
 #pragma unroll
@@ -669,10 +679,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         __syncwarp();
         TC_TG(2);
         for (uint32_t it = 0; it < my_tiles; ++it) {
-            const uint32_t db = it & 1;
+            const uint32_t db = it % Cfg::DB;  // accumulator set
             const uint32_t d_t = tbase + kColD + (NMW * db + m) * NCOL;
             TC_CLK(cf0);
-            TCW(6, it, &d_free[db], ((it >> 1) & 1) ^ 1);
+            TCW(6, it, &d_free[db], ((it / Cfg::DB) & 1) ^ 1);
             __syncwarp();
             {
                 TC_CLK(cf1);
