@@ -324,6 +324,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     constexpr uint32_t kStages = Cfg::Stages, NMW = Cfg::NMW, KC = Cfg::KC, NDIG = Cfg::NDIG;
     constexpr uint32_t kAB = Cfg::AB, kUH = Cfg::UH, kWEpi = Cfg::WEpi, kWMma0 = Cfg::WMma0, kWProd = Cfg::WProd;
     constexpr uint32_t kColD = Cfg::ColD;
+#ifdef SEGHDC_SPLIT_LDG
+    constexpr bool kLdg = SPLIT > 1;  // experiment: the unpack warps load A rows from global memory
+#else
+    constexpr bool kLdg = false;
+#endif
     static_assert(!UPD || (NCOL == 16 && SPLIT == 1), "the incremental fold is the K == 2 schedule");
     extern __shared__ __align__(1024) uint8_t smem[];
     StateView st = StateView::at(state, K);
@@ -442,10 +447,32 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         const uint32_t r = 32 * qd + lane;            // pixel row of the tile
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
         const uint32_t nchunks = my_tiles * nch;
+        // kLdg: the warp's 64 bytes of each chunk row come from global memory, one chunk ahead
+        uint4 nv[4];
+        auto ld_row = [&](uint32_t gg, uint4 (&o)[4]) {
+            const uint64_t pr = tile_px0(gg / nch) + r;
+            if (pr < n) {
+                const uint4* p4 = reinterpret_cast<const uint4*>(grid + pr * S32 + (ch0 + gg % nch) * kCW + hf * 16);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[j] = __ldg(p4 + j);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[j] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        };
+        if constexpr (kLdg) {
+            if (ph < nchunks) ld_row(ph, nv);
+        }
         for (uint32_t g = ph; g < nchunks; g += kAB) {
             const uint32_t s = g % kStages, ab = g % kAB;
+            uint4 cv[4];
+            if constexpr (kLdg) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cv[j] = nv[j];
+                if (g + kAB < nchunks) ld_row(g + kAB, nv);
+            }
             TC_CLK(c0);
-            TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
+            if (!kLdg) TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
             TC_CLK(c1);
             if (warp == 0 && g == 0) TC_TG(3);
             TCW(2, g, &a_free[ab], ((g / kAB) & 1) ^ 1);
@@ -461,7 +488,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #pragma unroll
             for (uint32_t c16 = hf * (8 / kUH); c16 < (hf + 1) * (8 / kUH); ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
 #ifndef SEGHDC_EXP_NOLDS  // timing experiment only: no shared-memory reads in the unpack
-                const uint4 v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
+                uint4 v;
+                if constexpr (kLdg) v = cv[(c16 - hf * (8 / kUH)) & 3];
+                else v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
 #else
                 const uint4 v = make_uint4(0u, 0u, 0u, 0u);  // all-zero A: every dot 0, labels settle at 0
 #endif
@@ -483,7 +512,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             PRG(10 * 100000 + g);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             PRG(11 * 100000 + g);
-            mbar_arrive(&slot_free[s]);
+            if (!kLdg) mbar_arrive(&slot_free[s]);
             tc_fence_before();
             mbar_arrive(&a_full[2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
@@ -725,10 +754,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_expect_tx(b_full, bbytes);
             bulk_g2s(sB, bimg + size_t(ch0) * kKS * Cfg::KB, bbytes, b_full);
             uint32_t g = 0;
-            const uint32_t nchunks = my_tiles * nch;
+            const uint32_t nchunks = kLdg ? 0u : my_tiles * nch;  // kLdg: the unpack warps load A
             for (uint32_t q = 0; q < pf && q < nchunks; ++q)
                 tma_prefetch_2d(&tmap, int((ch0 + q % nch) * kCW), int(tile_px0(q / nch)));
-            for (uint32_t it = 0; it < my_tiles; ++it) {
+            for (uint32_t it = 0; it < (kLdg ? 0u : my_tiles); ++it) {
                 const int y = int(tile_px0(it));
                 for (uint32_t ch = 0; ch < nch; ++ch, ++g) {
                     const uint32_t s = g % kStages;
