@@ -79,10 +79,14 @@ void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_
 // row, lane = word: coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane;
 // the CTA folds them in shared memory and adds 1024 column sums to the global array.
 // =============================================================================================
-constexpr uint32_t kEncRows = 32, kEncCols = 64, kEncWarps = 8;
+constexpr uint32_t kEncRows = 32, kEncCols = 64;
+// warps per CTA: 8 with one channel (~46 KB of smem, 3 CTAs per SM); with three channels the
+// 96 KB of colour tables leave room for one CTA per SM, so that CTA runs 24 warps
+template <int C>
+constexpr uint32_t enc_warps() { return C == 1 ? 8 : 24; }
 
 template <int C>
-__global__ void __launch_bounds__(kEncWarps * 32, 3)
+__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? 3 : 1)
     k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
              uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t* __restrict__ colsum, uint32_t W32) {
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, 3)
             s_img[rr * kEncCols * C + k] = __ldg(img + (size_t(rb + rr) * w + c0) * C + k);
         }
         __syncthreads();
-        for (uint32_t rr = warp; rr < nrb; rr += kEncWarps) {  // warp = one image row
+        for (uint32_t rr = warp; rr < nrb; rr += enc_warps<C>()) {  // warp = one image row
             const uint32_t rv = s_row[rr * 32 + lane];
             const uint8_t* px = s_img + rr * kEncCols * C;
             uint32_t* o = grid + (size_t(rb + rr - row_begin) * w + c0) * S32 + w0 + lane;
@@ -199,7 +203,7 @@ template <int C>
 static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
     const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
     ensure_dynamic_smem((const void*)k_encode<C>, smem);
-    k_encode<C><<<g, kEncWarps * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref, a.S32,
+    k_encode<C><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref, a.S32,
                                                 a.grid, a.colsum, a.W32);
 }
 
