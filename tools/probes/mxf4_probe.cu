@@ -75,7 +75,7 @@ template <int NMW, int STW>
 __global__ void krate(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t sB[];
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[4];
   const int tid = threadIdx.x, warp = tid >> 5;
   for (int i = tid; i < BBYTES; i += blockDim.x) {
 #ifdef RANDB  // random e2m1 digit codes of both signs, as balanced base-8 centroid digits give
@@ -89,7 +89,7 @@ __global__ void krate(long long* out, int iters) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 0) { for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i]))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+  if (tid == 0) { for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i]))); asm volatile("fence.mbarrier_init.release.cluster;"); }
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -138,7 +138,7 @@ __global__ void krate(long long* out, int iters) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #endif
 #ifdef COMMIT  // and a commit to an mbarrier after every 16 MMAs (the A buffer release)
-      if (i0) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar[warp ^ 1])));
+      if (i0) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar[2 + warp])));
 #endif
       asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, 1, 0;\n\tmov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
