@@ -111,6 +111,18 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
                         seghdc_round_cb on_round, void* user, uint32_t* labels_out,
                         size_t* rounds_out, double* timings_ms_out);
 
+/* ---- closed-form Manhattan variant (SURVEY.md §7 hard part 4, §8f rank 1) ------------ */
+/* run_pipeline (pipeline.cpp:40-75) + cluster (clusterer.cpp:190-218) for the Manhattan
+ * encoder without materialising the pixel HVs: each HV is B ^ (2 + C runs of ones), so
+ * dot_words is 10 prefix-table lookups per cluster and update_centroids a difference array.
+ * Same labels, centroids (k x dim u32, the set used by the final assignment), member counts
+ * and rounds as the packed path; k <= 32. */
+int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w,
+                               size_t c, size_t dim, double alpha, size_t beta, size_t gamma,
+                               size_t k, size_t iterations, uint64_t seed, int early_stop,
+                               uint32_t* labels_out, uint32_t* centroids_out,
+                               uint64_t* counts_out, size_t* rounds_out);
+
 /* ---- device-resident staging (no reference analogue: keeps HVs in HBM) --------------- */
 /* Image: full image on every rank. Codebooks: tables as produced by seghdc_build_codebooks.
  * Pointers are host pointers unless the *_device variant is used. */

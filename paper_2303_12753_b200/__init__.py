@@ -63,6 +63,8 @@ SIGNATURES = {
                         _u32p, C.c_void_p, C.c_void_p, C.POINTER(_sz)], C.c_int),
     "seghdc_run_pipeline": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64, C.c_int,
                              C.c_int, ROUND_CB, C.c_void_p, _u32p, C.POINTER(_sz), C.c_void_p], C.c_int),
+    "seghdc_run_pipeline_closed": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64,
+                                    C.c_int, _u32p, _u32p, _u64p, C.POINTER(_sz)], C.c_int),
     "seghdc_load_image": ([C.c_void_p, C.c_void_p, _sz, _sz, _sz], C.c_int),
     "seghdc_load_codebooks": ([C.c_void_p, _sz, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "seghdc_encode_async": ([C.c_void_p, _sz, _sz], C.c_int),
@@ -338,6 +340,24 @@ class Context:
                                              C.byref(rounds), C.cast(timings, C.c_void_p)))
         names = ("encode_position", "encode_color", "produce_pixels", "cluster", "total")
         return PipelineResult(labels.reshape(h, w), rounds.value, dict(zip(names, list(timings))))
+
+    def run_pipeline_closed(self, img: np.ndarray, config: "RunConfig") -> dict:
+        """Closed-form Manhattan variant of run_pipeline (SURVEY.md §7 hard part 4): the pixel
+        HVs are never materialised. Returns labels (h*w), centroids (k x dim, the set used by
+        the final assignment), counts and rounds, like cluster()."""
+        if config.encoder != "manhattan":
+            raise ConfigError("closed-form variant: Manhattan codebooks only")
+        img = _img3(img)
+        h, w, c = img.shape
+        labels = np.empty(h * w, np.uint32)
+        cents = np.empty((config.clusters, config.dim), np.uint32)
+        counts = np.empty(config.clusters, np.uint64)
+        rounds = _sz(0)
+        self.check(lib().seghdc_run_pipeline_closed(self.h, img, h, w, c, config.dim, float(config.alpha), config.beta,
+                                                    config.gamma, config.clusters, config.iterations, config.seed,
+                                                    int(config.early_stop), labels, cents.reshape(-1), counts,
+                                                    C.byref(rounds)))
+        return {"labels": labels, "centroids": cents, "counts": counts, "rounds": rounds.value}
 
     # ---- device-resident staging (bench / sharding) ----------------------------------------
     def load_image(self, img: np.ndarray) -> None:

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/seghdc_cuda.h"
+#include "closed.h"
 #include "host_internal.h"
 #include "kernels.cuh"
 #include "launch.h"
@@ -855,6 +856,101 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
             timings[3] = clu_ms;
             timings[4] = ms(t_total);
         }
+    });
+}
+
+int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c, size_t dim,
+                               double alpha, size_t beta, size_t gamma, size_t k, size_t iterations, uint64_t seed,
+                               int early_stop, uint32_t* labels_out, uint32_t* centroids_out, uint64_t* counts_out,
+                               size_t* rounds_out) {
+    return guarded(ctx, [&] {
+        // RunConfig::validate before any work (pipeline.cpp:25-30, 42)
+        seghdc_host::validate_image(h, w, c);
+        seghdc_host::validate_position(dim, h, w, alpha, beta);
+        seghdc_host::validate_color(dim, c, gamma);
+        seghdc_host::validate_cluster(k, iterations, h * w);
+        require(k <= 32, "closed-form variant: k = " + std::to_string(k) + " > 32");
+        const size_t wph = (dim + 63) / 64;
+        std::mt19937_64 rng(seed);  // pipeline.cpp:43-59, Manhattan codebooks only
+        std::vector<uint64_t> bases((2 + c) * wph);
+        const auto mp = seghdc_host::manhattan_bases(dim, h, w, c, alpha, beta, gamma, rng, bases.data());
+        std::vector<uint8_t> bflag(dim);  // B = XOR of the bases: every run empty (row 0, col 0, value 0)
+        for (size_t i = 0; i < dim; ++i) {
+            uint64_t x = 0;
+            for (size_t b = 0; b < 2 + c; ++b) x ^= bases[b * wph + (i >> 6)];
+            bflag[i] = uint8_t((x >> (i & 63)) & 1);
+        }
+        load_image(*ctx, pixels, h, w, c);
+        ctx->K = k;  // select_initial_centroids on the device, as seghdc_select_seeds
+        ctx->state.ensure(StateView::bytes(uint32_t(k)));
+        ctx->seeds.ensure(k);
+        ctx->slots.ensure(2 + k);
+        ctx->min_dist.ensure(h * w);
+        select_seeds_dev(*ctx, k);
+
+        const size_t n = h * w, stride = dim + 1;
+        DevBuf<long long> Q;
+        DevBuf<unsigned long long> P, n2, cnt, counts, changed;
+        DevBuf<uint32_t> Z, labels;
+        DevBuf<int32_t> diff;
+        DevBuf<uint8_t> bf;
+        Q.ensure(k * stride);
+        P.ensure(k);
+        n2.ensure(k);
+        cnt.ensure(k);
+        counts.ensure(k);
+        changed.ensure(1);
+        Z.ensure(k * dim);
+        labels.ensure(n);
+        diff.ensure(k * stride);
+        bf.ensure(dim);
+        ck(cudaMemcpyAsync(bf.p, bflag.data(), dim, cudaMemcpyHostToDevice, ctx->stream), "upload B");
+        ck(cudaMemsetAsync(diff.p, 0, k * stride * 4, ctx->stream), "clear diff");
+        ck(cudaMemsetAsync(cnt.p, 0, k * 8, ctx->stream), "clear counts");
+        ck(cudaMemsetAsync(labels.p, 0xFF, n * 4, ctx->stream), "clear labels");
+        ClosedArgs a{};
+        a.img = ctx->img.p;
+        a.n = n;
+        a.w = uint32_t(w);
+        a.c = uint32_t(c);
+        a.dim = uint32_t(dim);
+        a.beta = mp.beta;
+        a.x_row = mp.x_row;
+        a.x_col = mp.x_col;
+        a.K = uint32_t(k);
+        for (int i = 0; i < 3; ++i) a.off[i] = mp.off[i], a.unit[i] = mp.unit[i];
+        ClosedState st{Q.p, P.p, n2.p, Z.p, diff.p, cnt.p, counts.p, bf.p, labels.p, changed.p};
+        launch_closed_seed(a, ctx->seeds.p, st, ctx->stream);
+        launch_closed_finish(a, st, ctx->stream);
+        ctx->count(2);
+        ctx->check_launch();
+        size_t rounds = 0;
+        for (size_t r = 1; r <= iterations; ++r) {  // clusterer.cpp:208-216
+            ck(cudaMemsetAsync(changed.p, 0, 8, ctx->stream), "clear changed");
+            launch_closed_assign(a, st, ctx->sms, ctx->stream);
+            ctx->count();
+            ctx->check_launch();
+            rounds = r;
+            if (early_stop && r > 1) {
+                unsigned long long ch = 0;
+                ck(cudaMemcpyAsync(&ch, changed.p, 8, cudaMemcpyDeviceToHost, ctx->stream), "download changed");
+                ck(cudaStreamSynchronize(ctx->stream), "sync");
+                if (ch == 0) break;
+            }
+            if (r < iterations) {
+                launch_closed_accumulate(a, st, ctx->sms, ctx->stream);
+                launch_closed_finish(a, st, ctx->stream);
+                ctx->count(2);
+                ctx->check_launch();
+            }
+        }
+        ck(cudaMemcpyAsync(labels_out, labels.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream), "download labels");
+        if (centroids_out)
+            ck(cudaMemcpyAsync(centroids_out, Z.p, k * dim * 4, cudaMemcpyDeviceToHost, ctx->stream), "download Z");
+        if (counts_out)
+            ck(cudaMemcpyAsync(counts_out, counts.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream), "download counts");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        if (rounds_out) *rounds_out = rounds;
     });
 }
 

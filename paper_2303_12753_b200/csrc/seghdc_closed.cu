@@ -1,0 +1,228 @@
+// Closed-form Manhattan variant of the clustering loop (SURVEY.md §7 hard part 4, §8f rank 1).
+//
+// A Manhattan pixel HV is y = B ^ F, B the XOR of the 2 + C codebook bases and F the XOR of
+// 2 + C runs of ones (closed.h). Sorting the 2(2 + C) run endpoints e_0 <= ... <= e_9 turns F
+// into the disjoint runs [e_0, e_1), [e_2, e_3), ... (XOR = coverage parity). With
+//   P_k = sum_i B_i z_k[i],   Q_k[t] = sum_{i < t} (1 - 2 B_i) z_k[i]
+// the reference's dot_words(y, z_k) (hypervector.cpp:138-151) is P_k + sum_m Q_k[e_2m+1] - Q_k[e_2m],
+// and update_centroids' add_words (hypervector.cpp:112-121) sums to z_k[i] = B_i n_k + (1 - 2 B_i) c_k[i],
+// c_k = prefix sum of a +1/-1 difference array on the members' sorted endpoints. No D-sized
+// work per pixel: 10 table lookups per cluster to assign, 10 shared-memory atomics to update.
+// The dots and norms are exact integers, so the labels equal the packed-bit path's
+// (strictly_closer in 128 bits, clusterer.cpp:41-50).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+
+#include "closed.h"
+#include "launch.h"
+
+namespace seghdc_dev {
+
+namespace {
+
+constexpr int kRuns = 10;  // 2 + C <= 5 runs
+
+// Sorted run endpoints of pixel p; unused slots are dim (empty runs [dim, dim)).
+__device__ __forceinline__ void closed_runs(const ClosedArgs& a, uint64_t p, uint32_t (&e)[kRuns]) {
+    const uint32_t i = uint32_t(p / a.w), j = uint32_t(p % a.w);
+    e[0] = 0;
+    e[1] = (i / a.beta) * a.x_row;
+    e[2] = a.dim / 2;
+    e[3] = a.dim / 2 + (j / a.beta) * a.x_col;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        if (uint32_t(ch) < a.c) {
+            const uint32_t v = a.img[p * a.c + ch];
+            e[4 + 2 * ch] = a.off[ch];
+            e[5 + 2 * ch] = a.off[ch] + v * a.unit[ch];
+        } else {
+            e[4 + 2 * ch] = e[5 + 2 * ch] = a.dim;
+        }
+    }
+    // odd-even transposition sort, fully unrolled (registers only)
+#pragma unroll
+    for (int r = 0; r < kRuns; ++r) {
+#pragma unroll
+        for (int q = (r & 1); q + 1 < kRuns; q += 2) {
+            const uint32_t lo = min(e[q], e[q + 1]), hi = max(e[q], e[q + 1]);
+            e[q] = lo;
+            e[q + 1] = hi;
+        }
+    }
+}
+
+// clusterer.cpp:41-50, mod 2^128 like the reference's unsigned __int128
+__device__ __forceinline__ bool strictly_closer_dev(unsigned long long dc, unsigned long long nc,
+                                                    unsigned long long db, unsigned long long nb) {
+    if (nc == 0) return false;
+    if (nb == 0) return dc > 0;
+    const unsigned __int128 lhs = (unsigned __int128)dc * dc * nb;
+    const unsigned __int128 rhs = (unsigned __int128)db * db * nc;
+    return lhs > rhs;
+}
+
+__global__ void k_closed_seed(ClosedArgs a, const uint64_t* __restrict__ seeds, ClosedState s) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= a.K) return;
+    uint32_t e[kRuns];
+    closed_runs(a, seeds[k], e);
+    int32_t* d = s.diff + size_t(k) * (a.dim + 1);
+#pragma unroll
+    for (int m = 0; m < kRuns; m += 2) {
+        if (e[m] == e[m + 1]) continue;
+        atomicAdd(d + e[m], 1);
+        atomicAdd(d + e[m + 1], -1);
+    }
+    s.cnt[k] = 1;
+}
+
+constexpr int kMaxK = 32;
+
+__global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState s) {
+    __shared__ unsigned long long sP[kMaxK], sN[kMaxK];
+    for (uint32_t k = threadIdx.x; k < a.K; k += blockDim.x) sP[k] = s.P[k], sN[k] = s.norm2[k];
+    __syncthreads();
+    const size_t stride = size_t(a.dim) + 1;
+    unsigned long long changed = 0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t e[kRuns];
+        closed_runs(a, p, e);
+        uint32_t best = 0;
+        unsigned long long best_dot = 0, best_n2 = 0;
+        for (uint32_t k = 0; k < a.K; ++k) {
+            const long long* q = s.Q + k * stride;
+            long long d = (long long)sP[k];
+#pragma unroll
+            for (int m = 0; m < kRuns; m += 2) d += __ldg(q + e[m + 1]) - __ldg(q + e[m]);
+            const unsigned long long dot = (unsigned long long)d, n2 = sN[k];
+            if (k == 0) {
+                best_dot = dot, best_n2 = n2;
+            } else if (strictly_closer_dev(dot, n2, best_dot, best_n2)) {
+                best = k, best_dot = dot, best_n2 = n2;
+            }
+        }
+        changed += (s.labels[p] != best);
+        s.labels[p] = best;
+    }
+    // one atomic per warp
+#pragma unroll
+    for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
+}
+
+// grid = (blocks, cluster groups); group y owns clusters [y*G, y*G + G), one difference array
+// of dim + 1 ints each in shared memory. Only the run endpoints are ever touched, so the flush
+// skips zero entries.
+__global__ void __launch_bounds__(512) k_closed_accumulate(ClosedArgs a, ClosedState s, uint32_t G) {
+    extern __shared__ int32_t sd[];
+    const uint32_t stride = a.dim + 1, k0 = blockIdx.y * G, kn = min(G, a.K - k0);
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(sd + size_t(G) * stride);
+    for (uint32_t t = threadIdx.x; t < kn * stride; t += blockDim.x) sd[t] = 0;
+    for (uint32_t t = threadIdx.x; t < kn; t += blockDim.x) scnt[t] = 0;
+    __syncthreads();
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t l = s.labels[p] - k0;
+        if (l >= kn) continue;
+        uint32_t e[kRuns];
+        closed_runs(a, p, e);
+        int32_t* d = sd + size_t(l) * stride;
+#pragma unroll
+        for (int m = 0; m < kRuns; m += 2) {
+            if (e[m] == e[m + 1]) continue;
+            atomicAdd(d + e[m], 1);
+            atomicAdd(d + e[m + 1], -1);
+        }
+        atomicAdd(scnt + l, 1u);
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < kn * stride; t += blockDim.x)
+        if (sd[t]) atomicAdd(s.diff + size_t(k0) * stride + t, sd[t]);
+    for (uint32_t t = threadIdx.x; t < kn; t += blockDim.x)
+        if (scnt[t]) atomicAdd(s.cnt + k0 + t, (unsigned long long)scnt[t]);
+}
+
+constexpr int kFinT = 1024;
+
+// One CTA per cluster: c = prefix(diff), z = B ? n - c : c, then norm2, P and the prefix Q of
+// (1 - 2B) z. An empty cluster keeps its previous state (clusterer.cpp:183-185), count 0.
+__global__ void __launch_bounds__(kFinT) k_closed_finish(ClosedArgs a, ClosedState s) {
+    using ScanI = cub::BlockScan<long long, kFinT>;
+    using RedU = cub::BlockReduce<unsigned long long, kFinT>;
+    __shared__ union {
+        typename ScanI::TempStorage scan;
+        typename RedU::TempStorage red;
+    } tmp;
+    const uint32_t k = blockIdx.x, stride = a.dim + 1;
+    const unsigned long long n = s.cnt[k];
+    __syncthreads();
+    if (threadIdx.x == 0) s.counts[k] = n, s.cnt[k] = 0;
+    if (n == 0) return;  // block-uniform
+    int32_t* d = s.diff + size_t(k) * stride;
+    uint32_t* z = s.Z + size_t(k) * a.dim;
+    long long* q = s.Q + size_t(k) * stride;
+    const uint32_t chunk = (a.dim + kFinT - 1) / kFinT;
+    const uint32_t i0 = min(a.dim, threadIdx.x * chunk), i1 = min(a.dim, i0 + chunk);
+    long long part = 0;
+    for (uint32_t i = i0; i < i1; ++i) part += d[i];
+    long long c;
+    ScanI(tmp.scan).ExclusiveSum(part, c);
+    __syncthreads();
+    unsigned long long n2 = 0, pb = 0;
+    long long sp = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+        c += d[i];
+        d[i] = 0;
+        const bool b = s.bflag[i];
+        const unsigned long long zi = b ? n - (unsigned long long)c : (unsigned long long)c;
+        z[i] = uint32_t(zi);
+        n2 += zi * zi;
+        if (b) pb += zi, sp -= (long long)zi;
+        else sp += (long long)zi;
+    }
+    if (threadIdx.x == 0) d[a.dim] = 0;
+    long long qb;
+    ScanI(tmp.scan).ExclusiveSum(sp, qb);
+    __syncthreads();
+    n2 = RedU(tmp.red).Sum(n2);
+    __syncthreads();
+    pb = RedU(tmp.red).Sum(pb);
+    if (threadIdx.x == 0) {
+        s.norm2[k] = n2;
+        s.P[k] = pb;
+        q[0] = 0;
+    }
+    for (uint32_t i = i0; i < i1; ++i) {
+        const long long zi = z[i];
+        qb += s.bflag[i] ? -zi : zi;
+        q[i + 1] = qb;
+    }
+}
+
+}  // namespace
+
+void launch_closed_seed(const ClosedArgs& a, const uint64_t* seeds, ClosedState s, cudaStream_t st) {
+    k_closed_seed<<<(a.K + 63) / 64, 64, 0, st>>>(a, seeds, s);
+}
+
+void launch_closed_assign(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
+    const uint64_t blocks = std::min<uint64_t>((a.n + 255) / 256, uint64_t(sms) * 8);
+    k_closed_assign<<<uint32_t(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(a, s);
+}
+
+void launch_closed_accumulate(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
+    const size_t per = size_t(a.dim + 1) * 4;
+    const uint32_t G = uint32_t(std::max<size_t>(1, std::min<size_t>(a.K, (200u << 10) / per)));
+    const uint32_t groups = (a.K + G - 1) / G;
+    const size_t smem = G * per + G * 4;
+    ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_accumulate), smem);
+    const uint64_t blocks = std::min<uint64_t>((a.n + 511) / 512, uint64_t(sms));
+    k_closed_accumulate<<<dim3(uint32_t(std::max<uint64_t>(blocks, 1)), groups), 512, smem, st>>>(a, s, G);
+}
+
+void launch_closed_finish(const ClosedArgs& a, ClosedState s, cudaStream_t st) {
+    k_closed_finish<<<a.K, kFinT, 0, st>>>(a, s);
+}
+
+}  // namespace seghdc_dev
