@@ -16,6 +16,9 @@ struct ClosedArgs {
     uint64_t n;          // pixels
     uint32_t w, c, dim, beta, x_row, x_col, K;
     uint32_t off[3], unit[3];
+    // compressed endpoint tables: every run endpoint is one of L = nr + nc + 256 C + 1 positions
+    // (row ends b * x_row, column ends dim/2 + b * x_col, colour ends off_ch + v * unit_ch, dim)
+    uint32_t nr, nc, L;
 };
 
 // Per-cluster state on the device (int64 prefix tables, see seghdc_closed.cu):
@@ -33,6 +36,7 @@ struct ClosedState {
     const uint8_t* bflag;
     uint32_t* labels;
     unsigned long long* changed;
+    int32_t* diffc;  // [K][L] difference counts on compressed endpoint indices (k_closed_accumulate_c)
 };
 
 // centroids from the seed pixels (clusterer.cpp:197-205): runs of seed k into diff[k], cnt[k] = 1

@@ -132,6 +132,14 @@ struct seghdc_ctx {
     DevBuf<uint64_t> seeds;
     DevBuf<unsigned long long> slots;
     DevBuf<uint16_t> min_dist;
+    // closed-form Manhattan variant (seghdc_run_pipeline_closed), grow-only
+    struct {
+        DevBuf<long long> Q;
+        DevBuf<unsigned long long> P, n2, cnt, counts, changed;
+        DevBuf<uint32_t> Z, labels;
+        DevBuf<int32_t> diff, diffc;
+        DevBuf<uint8_t> bf;
+    } cf;
     int exchange_phase = 0;  // 0: rounds, 1: init (includes colsums)
     // optional CUDA-event timing of every round kernel (bench.py's roofline)
     bool profiling = false;
@@ -889,11 +897,12 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         select_seeds_dev(*ctx, k);
 
         const size_t n = h * w, stride = dim + 1;
-        DevBuf<long long> Q;
-        DevBuf<unsigned long long> P, n2, cnt, counts, changed;
-        DevBuf<uint32_t> Z, labels;
-        DevBuf<int32_t> diff;
-        DevBuf<uint8_t> bf;
+        require(n < (size_t(1) << 32), "closed-form variant: more than 2^32 pixels");
+        auto& Q = ctx->cf.Q;
+        auto &P = ctx->cf.P, &n2 = ctx->cf.n2, &cnt = ctx->cf.cnt, &counts = ctx->cf.counts, &changed = ctx->cf.changed;
+        auto &Z = ctx->cf.Z, &labels = ctx->cf.labels;
+        auto& diff = ctx->cf.diff;
+        auto& bf = ctx->cf.bf;
         Q.ensure(k * stride);
         P.ensure(k);
         n2.ensure(k);
@@ -919,7 +928,19 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         a.x_col = mp.x_col;
         a.K = uint32_t(k);
         for (int i = 0; i < 3; ++i) a.off[i] = mp.off[i], a.unit[i] = mp.unit[i];
-        ClosedState st{Q.p, P.p, n2.p, Z.p, diff.p, cnt.p, counts.p, bf.p, labels.p, changed.p};
+        a.nr = uint32_t((h - 1) / beta + 1);
+        a.nc = uint32_t((w - 1) / beta + 1);
+        a.L = a.nr + a.nc + 256 * uint32_t(c) + 1;
+        // compressed endpoint indices when they fit (keys pos << 15 | index, [K][L] tables in smem)
+        const bool compressed = a.L < (1u << 15) && dim < (1u << 17) && size_t(a.L) * k * 8 <= (160u << 10) &&
+                                !getenv("SEGHDC_CLOSED_POSITIONS");
+        auto& diffc = ctx->cf.diffc;
+        if (compressed) {
+            diffc.ensure(k * a.L);
+            ck(cudaMemsetAsync(diffc.p, 0, k * a.L * 4, ctx->stream), "clear diffc");
+        }
+        ClosedState st{Q.p, P.p, n2.p, Z.p, diff.p, cnt.p, counts.p, bf.p, labels.p, changed.p,
+                       compressed ? diffc.p : nullptr};
         launch_closed_seed(a, ctx->seeds.p, st, ctx->stream);
         launch_closed_finish(a, st, ctx->stream);
         ctx->count(2);

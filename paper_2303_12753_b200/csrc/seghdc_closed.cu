@@ -26,7 +26,7 @@ constexpr int kRuns = 10;  // 2 + C <= 5 runs
 
 // Sorted run endpoints of pixel p; unused slots are dim (empty runs [dim, dim)).
 __device__ __forceinline__ void closed_runs(const ClosedArgs& a, uint64_t p, uint32_t (&e)[kRuns]) {
-    const uint32_t i = uint32_t(p / a.w), j = uint32_t(p % a.w);
+    const uint32_t i = uint32_t(p) / a.w, j = uint32_t(p) % a.w;  // n < 2^32 (checked by the host)
     e[0] = 0;
     e[1] = (i / a.beta) * a.x_row;
     e[2] = a.dim / 2;
@@ -51,6 +51,47 @@ __device__ __forceinline__ void closed_runs(const ClosedArgs& a, uint64_t p, uin
             e[q + 1] = hi;
         }
     }
+}
+
+// Position of compressed endpoint index t (ClosedArgs::L layout).
+__device__ __forceinline__ uint32_t closed_pos(const ClosedArgs& a, uint32_t t) {
+    if (t < a.nr) return t * a.x_row;
+    t -= a.nr;
+    if (t < a.nc) return a.dim / 2 + t * a.x_col;
+    t -= a.nc;
+    if (t < 256 * a.c) return a.off[t >> 8] + (t & 255) * a.unit[t >> 8];
+    return a.dim;
+}
+
+// Sorted run endpoints of pixel p as compressed indices (sort key: position << 15 | index).
+__device__ __forceinline__ void closed_runs_idx(const ClosedArgs& a, uint64_t p, uint32_t (&e)[kRuns]) {
+    const uint32_t i = uint32_t(p) / a.w, j = uint32_t(p) % a.w;
+    const uint32_t bi = i / a.beta, bj = j / a.beta;
+    e[0] = 0u;  // row run start: row entry 0, position 0
+    e[1] = ((bi * a.x_row) << 15) | bi;
+    e[2] = ((a.dim / 2) << 15) | a.nr;
+    e[3] = ((a.dim / 2 + bj * a.x_col) << 15) | (a.nr + bj);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        if (uint32_t(ch) < a.c) {
+            const uint32_t v = a.img[p * a.c + ch], base = a.nr + a.nc + 256u * ch;
+            e[4 + 2 * ch] = (a.off[ch] << 15) | base;
+            e[5 + 2 * ch] = ((a.off[ch] + v * a.unit[ch]) << 15) | (base + v);
+        } else {
+            e[4 + 2 * ch] = e[5 + 2 * ch] = (a.dim << 15) | (a.L - 1);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kRuns; ++r) {
+#pragma unroll
+        for (int q = (r & 1); q + 1 < kRuns; q += 2) {
+            const uint32_t lo = min(e[q], e[q + 1]), hi = max(e[q], e[q + 1]);
+            e[q] = lo;
+            e[q + 1] = hi;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kRuns; ++q) e[q] &= 0x7FFFu;
 }
 
 // clusterer.cpp:41-50, mod 2^128 like the reference's unsigned __int128
@@ -112,6 +153,44 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
     if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
 }
 
+// assign_labels with the K prefix tables restricted to the L endpoint positions, staged once per
+// CTA in shared memory ([L][K] int64): 10 shared-memory loads per pixel and cluster.
+__global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, ClosedState s) {
+    extern __shared__ long long sq[];
+    __shared__ unsigned long long sP[kMaxK], sN[kMaxK];
+    const uint32_t K = a.K;
+    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) sP[k] = s.P[k], sN[k] = s.norm2[k];
+    const size_t stride = size_t(a.dim) + 1;
+    for (uint32_t t = threadIdx.x; t < a.L * K; t += blockDim.x) {
+        const uint32_t idx = t / K, k = t % K;
+        sq[t] = s.Q[k * stride + closed_pos(a, idx)];
+    }
+    __syncthreads();
+    unsigned long long changed = 0;
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t e[kRuns];
+        closed_runs_idx(a, p, e);
+        uint32_t best = 0;
+        unsigned long long best_dot = 0, best_n2 = 0;
+        for (uint32_t k = 0; k < K; ++k) {
+            long long d = (long long)sP[k];
+#pragma unroll
+            for (int m = 0; m < kRuns; m += 2) d += sq[e[m + 1] * K + k] - sq[e[m] * K + k];
+            const unsigned long long dot = (unsigned long long)d, n2 = sN[k];
+            if (k == 0) {
+                best_dot = dot, best_n2 = n2;
+            } else if (strictly_closer_dev(dot, n2, best_dot, best_n2)) {
+                best = k, best_dot = dot, best_n2 = n2;
+            }
+        }
+        changed += (s.labels[p] != best);
+        s.labels[p] = best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
+}
+
 // grid = (blocks, cluster groups); group y owns clusters [y*G, y*G + G), one difference array
 // of dim + 1 ints each in shared memory. Only the run endpoints are ever touched, so the flush
 // skips zero entries.
@@ -143,6 +222,35 @@ __global__ void __launch_bounds__(512) k_closed_accumulate(ClosedArgs a, ClosedS
         if (scnt[t]) atomicAdd(s.cnt + k0 + t, (unsigned long long)scnt[t]);
 }
 
+// update_centroids' accumulation on compressed endpoint indices: every cluster's [L] difference
+// counts in shared memory at once (one pass over the labels), flushed into diffc; k_closed_finish
+// scatters them to positions.
+__global__ void __launch_bounds__(512) k_closed_accumulate_c(ClosedArgs a, ClosedState s) {
+    extern __shared__ int32_t sc[];
+    const uint32_t K = a.K, L = a.L;
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(sc + K * L);
+    for (uint32_t t = threadIdx.x; t < K * L + K; t += blockDim.x) sc[t] = 0;
+    __syncthreads();
+    for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t l = s.labels[p];
+        uint32_t e[kRuns];
+        closed_runs_idx(a, p, e);
+        int32_t* d = sc + l * L;
+#pragma unroll
+        for (int m = 0; m < kRuns; m += 2) {
+            if (e[m] == e[m + 1]) continue;
+            atomicAdd(d + e[m], 1);
+            atomicAdd(d + e[m + 1], -1);
+        }
+        atomicAdd(scnt + l, 1u);
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < K * L; t += blockDim.x)
+        if (sc[t]) atomicAdd(s.diffc + t, sc[t]);
+    for (uint32_t t = threadIdx.x; t < K; t += blockDim.x)
+        if (scnt[t]) atomicAdd(s.cnt + t, (unsigned long long)scnt[t]);
+}
+
 constexpr int kFinT = 1024;
 
 // One CTA per cluster: c = prefix(diff), z = B ? n - c : c, then norm2, P and the prefix Q of
@@ -160,6 +268,14 @@ __global__ void __launch_bounds__(kFinT) k_closed_finish(ClosedArgs a, ClosedSta
     if (threadIdx.x == 0) s.counts[k] = n, s.cnt[k] = 0;
     if (n == 0) return;  // block-uniform
     int32_t* d = s.diff + size_t(k) * stride;
+    if (s.diffc) {  // compressed counts -> positions (block-visible after the barrier)
+        int32_t* dc = s.diffc + size_t(k) * a.L;
+        for (uint32_t t = threadIdx.x; t < a.L; t += blockDim.x) {
+            const int32_t v = dc[t];
+            if (v) atomicAdd(d + closed_pos(a, t), v), dc[t] = 0;
+        }
+        __syncthreads();
+    }
     uint32_t* z = s.Z + size_t(k) * a.dim;
     long long* q = s.Q + size_t(k) * stride;
     const uint32_t chunk = (a.dim + kFinT - 1) / kFinT;
@@ -207,11 +323,25 @@ void launch_closed_seed(const ClosedArgs& a, const uint64_t* seeds, ClosedState 
 }
 
 void launch_closed_assign(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
+    const size_t smem = size_t(a.L) * a.K * 8;
+    if (s.diffc) {  // compressed indices fit (seghdc_run_pipeline_closed decides)
+        ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_assign_smem), smem);
+        const uint64_t blocks = std::min<uint64_t>((a.n + 511) / 512, uint64_t(sms) * (smem <= (100u << 10) ? 2 : 1));
+        k_closed_assign_smem<<<uint32_t(std::max<uint64_t>(blocks, 1)), 512, smem, st>>>(a, s);
+        return;
+    }
     const uint64_t blocks = std::min<uint64_t>((a.n + 255) / 256, uint64_t(sms) * 8);
     k_closed_assign<<<uint32_t(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(a, s);
 }
 
 void launch_closed_accumulate(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
+    if (s.diffc) {
+        const size_t smem = (size_t(a.L) + 1) * a.K * 4;
+        ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_accumulate_c), smem);
+        const uint64_t blocks = std::min<uint64_t>((a.n + 511) / 512, uint64_t(sms) * (smem <= (100u << 10) ? 2 : 1));
+        k_closed_accumulate_c<<<uint32_t(std::max<uint64_t>(blocks, 1)), 512, smem, st>>>(a, s);
+        return;
+    }
     const size_t per = size_t(a.dim + 1) * 4;
     const uint32_t G = uint32_t(std::max<size_t>(1, std::min<size_t>(a.K, (200u << 10) / per)));
     const uint32_t groups = (a.K + G - 1) / G;

@@ -97,3 +97,11 @@ def test_closed_validation(ctx):
         ctx.run_pipeline_closed(img, S.RunConfig(dim=1000, alpha=1.0, clusters=2, iterations=2, encoder="rpos"))
     with pytest.raises(S.ConfigError):  # x_row = 0 (position_encoder.cpp:29-38)
         ctx.run_pipeline_closed(np.zeros((4096, 1, 1), np.uint8), S.RunConfig(dim=1000, alpha=0.2, clusters=2))
+
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[5], CASES[8]])
+def test_closed_position_tables_match(ctx, port, case, monkeypatch):
+    """The full-position tables (SEGHDC_CLOSED_POSITIONS, used when the compressed endpoint
+    tables do not fit shared memory) give the same results."""
+    monkeypatch.setenv("SEGHDC_CLOSED_POSITIONS", "1")
+    test_closed_matches_oracle(ctx, port, case)
