@@ -154,20 +154,23 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
 }
 
 // assign_labels with the K prefix tables restricted to the L endpoint positions, staged once per
-// CTA in shared memory ([L][K] int64): 10 shared-memory loads per pixel and cluster.
+// CTA in shared memory ([K][L] int64): 10 shared-memory loads per pixel and cluster.
 __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, ClosedState s) {
     extern __shared__ long long sq[];
     __shared__ unsigned long long sP[kMaxK], sN[kMaxK];
     const uint32_t K = a.K;
     for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) sP[k] = s.P[k], sN[k] = s.norm2[k];
     const size_t stride = size_t(a.dim) + 1;
+    // [K][L]: lanes with random colour values spread over all 16 bank pairs (an [L][K] layout
+    // puts every entry of one cluster on 32 / K of them: 16-way conflicts at K = 8)
     for (uint32_t t = threadIdx.x; t < a.L * K; t += blockDim.x) {
-        const uint32_t idx = t / K, k = t % K;
+        const uint32_t k = t / a.L, idx = t % a.L;
         sq[t] = s.Q[k * stride + closed_pos(a, idx)];
     }
     __syncthreads();
     unsigned long long changed = 0;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t old = s.labels[p];  // issued with the image loads, not after the argmax
         uint32_t e[kRuns];
         closed_runs_idx(a, p, e);
         uint32_t best = 0;
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
         for (uint32_t k = 0; k < K; ++k) {
             long long d = (long long)sP[k];
 #pragma unroll
-            for (int m = 0; m < kRuns; m += 2) d += sq[e[m + 1] * K + k] - sq[e[m] * K + k];
+            for (int m = 0; m < kRuns; m += 2) d += sq[k * a.L + e[m + 1]] - sq[k * a.L + e[m]];
             const unsigned long long dot = (unsigned long long)d, n2 = sN[k];
             if (k == 0) {
                 best_dot = dot, best_n2 = n2;
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
                 best = k, best_dot = dot, best_n2 = n2;
             }
         }
-        changed += (s.labels[p] != best);
+        changed += (old != best);
         s.labels[p] = best;
     }
 #pragma unroll
