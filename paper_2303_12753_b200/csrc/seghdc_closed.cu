@@ -14,6 +14,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "closed.h"
 #include "launch.h"
@@ -319,6 +320,104 @@ __global__ void __launch_bounds__(kFinT) k_closed_finish(ClosedArgs a, ClosedSta
     }
 }
 
+// Skewed shared-memory index: each thread walks a contiguous chunk of `chunk` words, so word
+// i + i/32 puts the 32 lanes of a warp on 32 distinct banks for every chunk length.
+__host__ __device__ __forceinline__ uint32_t fin_skew(uint32_t i) { return i + (i >> 5); }
+
+// k_closed_finish with the counts and B flags staged in shared memory: the diff row and the flags
+// are read once, coalesced; the compressed counts scatter into shared memory; the three serial
+// per-thread passes (c, z, Q) run on shared memory instead of chains of dependent global loads.
+// Global Z and Q are store-only. Same arithmetic and order as k_closed_finish (bit-identical).
+__global__ void __launch_bounds__(kFinT) k_closed_finish_smem(ClosedArgs a, ClosedState s) {
+    using ScanI = cub::BlockScan<long long, kFinT>;
+    using RedU = cub::BlockReduce<unsigned long long, kFinT>;
+    __shared__ union {
+        typename ScanI::TempStorage scan;
+        typename RedU::TempStorage red;
+    } tmp;
+    extern __shared__ int32_t fin_sm[];
+    const uint32_t k = blockIdx.x, stride = a.dim + 1;
+    int32_t* sd = fin_sm;                               // [skew(dim) + 1] counts, then z
+    int32_t* sb = fin_sm + fin_skew(a.dim) + 1;         // [skew(dim - 1) + 1] B flags
+    const unsigned long long n = s.cnt[k];
+    __syncthreads();
+    if (threadIdx.x == 0) s.counts[k] = n, s.cnt[k] = 0;
+    if (n == 0) return;  // block-uniform
+    int32_t* d = s.diff + size_t(k) * stride;
+    // batches of 8 per thread: all 16 loads in flight before the first store (the zeroing store
+    // to d would otherwise serialise one load latency per element)
+    constexpr int kB = 8;
+    for (uint32_t t0 = threadIdx.x; t0 <= a.dim; t0 += kB * blockDim.x) {
+        int32_t v[kB];
+        uint8_t bf[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const uint32_t t = t0 + j * blockDim.x;
+            v[j] = t <= a.dim ? __ldcg(d + t) : 0;
+            bf[j] = t < a.dim ? __ldg(s.bflag + t) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const uint32_t t = t0 + j * blockDim.x;
+            if (t <= a.dim) {
+                sd[fin_skew(t)] = v[j];
+                d[t] = 0;
+                if (t < a.dim) sb[fin_skew(t)] = bf[j];
+            }
+        }
+    }
+    __syncthreads();
+    if (s.diffc) {
+        int32_t* dc = s.diffc + size_t(k) * a.L;
+        for (uint32_t t = threadIdx.x; t < a.L; t += blockDim.x) {
+            const int32_t v = dc[t];
+            if (v) atomicAdd(sd + fin_skew(closed_pos(a, t)), v), dc[t] = 0;
+        }
+        __syncthreads();
+    }
+    uint32_t* z = s.Z + size_t(k) * a.dim;
+    long long* q = s.Q + size_t(k) * stride;
+    const uint32_t chunk = (a.dim + kFinT - 1) / kFinT;
+    const uint32_t i0 = min(a.dim, threadIdx.x * chunk), i1 = min(a.dim, i0 + chunk);
+    long long part = 0;
+    for (uint32_t i = i0; i < i1; ++i) part += sd[fin_skew(i)];
+    long long c;
+    ScanI(tmp.scan).ExclusiveSum(part, c);
+    __syncthreads();
+    unsigned long long n2 = 0, pb = 0;
+    long long sp = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint32_t si = fin_skew(i);
+        c += sd[si];
+        const bool b = sb[si];
+        const unsigned long long zi = b ? n - (unsigned long long)c : (unsigned long long)c;
+        z[i] = uint32_t(zi);
+        sd[si] = int32_t(uint32_t(zi));
+        n2 += zi * zi;
+        if (b) pb += zi, sp -= (long long)zi;
+        else sp += (long long)zi;
+    }
+    long long qb;
+    ScanI(tmp.scan).ExclusiveSum(sp, qb);
+    __syncthreads();
+    n2 = RedU(tmp.red).Sum(n2);
+    __syncthreads();
+    pb = RedU(tmp.red).Sum(pb);
+    if (threadIdx.x == 0) {
+        s.norm2[k] = n2;
+        s.P[k] = pb;
+        q[0] = 0;
+    }
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint32_t si = fin_skew(i);
+        const long long zi = uint32_t(sd[si]);
+        qb += sb[si] ? -zi : zi;
+        q[i + 1] = qb;
+    }
+}
+
+size_t fin_smem_bytes(uint32_t dim) { return (size_t(fin_skew(dim)) + 1 + fin_skew(dim)) * 4; }
+
 }  // namespace
 
 void launch_closed_seed(const ClosedArgs& a, const uint64_t* seeds, ClosedState s, cudaStream_t st) {
@@ -355,6 +454,12 @@ void launch_closed_accumulate(const ClosedArgs& a, ClosedState s, int sms, cudaS
 }
 
 void launch_closed_finish(const ClosedArgs& a, ClosedState s, cudaStream_t st) {
+    const size_t smem = fin_smem_bytes(a.dim);
+    if (!getenv("SEGHDC_CLOSED_FIN_GLOBAL") && smem <= (200u << 10) &&
+        ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_finish_smem), smem) == cudaSuccess) {
+        k_closed_finish_smem<<<a.K, kFinT, smem, st>>>(a, s);
+        return;
+    }
     k_closed_finish<<<a.K, kFinT, 0, st>>>(a, s);
 }
 
