@@ -27,23 +27,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {  # BASELINE.json configs (C3/C4 alpha 1.0: 0.2 fails the reference's validation)
-    0: dict(name="C0", cid=0, dim=10000, k=2, iterations=10, alpha=0.2),
-    1: dict(name="C1", cid=1, dim=10000, k=2, iterations=10, alpha=0.2),
-    2: dict(name="C2", cid=2, dim=10000, k=2, iterations=10, alpha=0.2),
-    3: dict(name="C3", cid=3, dim=10000, k=4, iterations=20, alpha=1.0),
-    4: dict(name="C4", cid=4, dim=16384, k=8, iterations=20, alpha=1.0),
-}
-WORKLOAD_TEXT = {
-    0: "C0: 256x256x3 synthetic nuclei (20 ellipses), D=10000, K=2, 10 iterations",
-    1: "C1: 520x696x1 synthetic nuclei (60 ellipses, blur 1.5), D=10000, K=2, 10 iterations",
-    2: "C2: 64 x 256x256x3 synthetic nuclei images, D=10000, K=2, 10 iterations each",
-    3: "C3: 2048x2048x3 synthetic nuclei (1500 ellipses, 3 classes), D=10000, K=4, 20 iterations",
-    4: "C4: 4096x4096x3 synthetic nuclei (6000 ellipses, 7 classes), D=16384, K=8, 20 iterations",
-}
+from workloads import C2_IMAGES, CB_SEED, CONFIGS, GAMMA, BETA, WORKLOAD_TEXT, synth_image  # noqa: E402
+
 METRIC = "pixel-HV cluster updates/sec (px·iter/s) at D=10k, K=2; % of roofline"
-BETA, GAMMA, CB_SEED = 26, 1, 0
-C2_IMAGES = 64  # config 2: a batch of 64 independent images (seeds 0..63)
 C2_GROUPS = int(os.environ.get("SEGHDC_C2_GROUPS", "4"))  # concurrent contexts for the batch
 
 
@@ -111,104 +97,141 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------- CPU baselines
-def cpu_reference_rounds(spec, img, rounds: int, nthreads: int, rows=None):
-    """The reference's own assign_labels + update_centroids (oracle/_ref: the /root/reference
-    sources compiled unmodified) chained for `rounds` rounds over image rows `rows`, split into
-    one row-block per thread. Returns (seconds, pixel-rounds, kind)."""
+def host_cpu():
+    """CPU model and logical core count of the box (state both)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+def reference_setup(spec, img):
+    """Inputs of the reference's loop, built by the reference itself where it was compiled
+    (oracle/_ref: run_pipeline's codebook order, its own encode_image and
+    select_initial_centroids), else by the C restatement. Nothing from the product library."""
     import oracle
 
     h, w, c = img.shape
-    r0, r1 = rows or (0, h)
-    P = oracle.Port()
-    import paper_2303_12753_b200 as S
-    cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], BETA, GAMMA, CB_SEED)
-    grid = P.encode(img, spec["dim"], *cb)
-    seeds = P.select_seeds(img, spec["k"])
-    nw = grid.shape[1]
-    z = np.zeros((spec["k"], spec["dim"]), np.uint32)
-    for s, p in enumerate(seeds):  # seed centroids (clusterer.cpp:197-205)
-        bits = np.unpackbits(grid[int(p)].view(np.uint8), bitorder="little")[: spec["dim"]]
-        z[s] = bits
-    counts = np.ones(spec["k"], np.uint64)
     if oracle.have_ref():
         R = oracle.Ref()
-        hnd = R.par_create(grid, h, w, spec["dim"], r0, r1, nthreads)
-        t = time.perf_counter()
-        for _ in range(rounds):
-            z, counts = R.par_round(hnd, z, counts)
-        dt = time.perf_counter() - t
-        R.par_destroy(hnd)
+        grid = R.encode(img, spec["dim"], spec["alpha"], BETA, GAMMA, CB_SEED)
+        seeds = R.select_seeds(img, spec["k"])
         kind = "reference"
-    else:  # the C restatement, if the reference could not be compiled
-        P.set_threads(nthreads)
-        sub = grid[r0 * w: r1 * w]
-        t = time.perf_counter()
-        for _ in range(rounds):
-            lab = P.assign(sub, spec["dim"], z)
-            z, counts = P.update(sub, spec["dim"], lab, z)
-        dt = time.perf_counter() - t
+    else:
+        R = oracle.Port()
+        cb = R.build_codebooks(spec["dim"], h, w, c, spec["alpha"], BETA, GAMMA, CB_SEED)
+        grid = R.encode(img, spec["dim"], *cb)
+        seeds = R.select_seeds(img, spec["k"])
         kind = "port"
-    del nw
-    return dt, (r1 - r0) * w * rounds, kind
+    z = np.zeros((spec["k"], spec["dim"]), np.uint32)
+    for s, p in enumerate(seeds):  # seed centroids = the seed pixels' HVs (clusterer.cpp:197-205)
+        z[s] = np.unpackbits(grid[int(p)].view(np.uint8), bitorder="little")[: spec["dim"]]
+    return grid, z, np.ones(spec["k"], np.uint64), kind
+
+
+def reference_round_fn(spec, grid, h, w, nthreads, kind):
+    """One chained assign_labels + update_centroids round over `grid`, rows split into one
+    block per thread: the reference's own functions (ref_par_round) or the restatement."""
+    import oracle
+
+    if kind == "reference":
+        R = oracle.Ref()
+        hnd = R.par_create(grid, h, w, spec["dim"], 0, h, nthreads)
+        return (lambda z, cn: R.par_round(hnd, z, cn)), (lambda: R.par_destroy(hnd))
+    P = oracle.Port()
+    P.set_threads(nthreads)
+
+    def step(z, cn):
+        lab = P.assign(grid, spec["dim"], z)
+        return P.update(grid, spec["dim"], lab, z)
+    return step, (lambda: None)
+
+
+def cpu_sample_image(spec, img):
+    """Bounded CPU sample (~5-20 s of single-thread work): the whole image up to 400k pixels,
+    else its first rows (C3/C4: ~200k pixels, a crop clustered as an image of its own)."""
+    h, w = img.shape[:2]
+    rows = h if h * w <= 400_000 else max(1, 200_000 // w)
+    return np.ascontiguousarray(img[:rows]), rows
+
+
+def cpu_reference_rounds(spec, img, rounds: int, nthreads: int):
+    """Seconds for `rounds` chained reference rounds over img on nthreads threads."""
+    h, w = img.shape[:2]
+    grid, z, counts, kind = reference_setup(spec, img)
+    step, done = reference_round_fn(spec, grid, h, w, nthreads, kind)
+    t = time.perf_counter()
+    for _ in range(rounds):
+        z, counts = step(z, counts)
+    dt = time.perf_counter() - t
+    done()
+    return dt, h * w * rounds, kind
+
+
+def workload_layout(config: int, world: int, rank: int, h: int, w: int):
+    """How the workload splits over ranks (same answer for both arms): C3/C4 row-shard one image
+    (N > 1), C2 deals its 64 images round-robin, C0/C1 run one image per rank (replicas)."""
+    sharded = world > 1 and config in (3, 4)
+    batch = config == 2
+    img_ids = list(range(rank, C2_IMAGES, world)) if batch else [0 if sharded else rank]
+    if sharded:
+        r0, r1 = h * rank // world, h * (rank + 1) // world
+        n_local = (r1 - r0) * w
+        par = f"row-shard x{world}"
+    else:
+        n_local = h * w * len(img_ids)
+        par = f"image-shard x{world}" if batch else f"replicas x{world}"
+    return sharded, batch, img_ids, n_local, par
+
+
+def bench_config(args, spec, n_local, n_images, parallelism):
+    """The `config` object shared by both arms (same keys, same values for the same workload)."""
+    return {"workload": WORKLOAD_TEXT[args.config], "pixels_per_rank": n_local, "images_per_rank": n_images,
+            "dim": spec["dim"], "k": spec["k"], "iterations": spec["iterations"], "early_stop": False,
+            "parallelism": parallelism}
 
 
 def run_reference_arm(args, spec):
-    """--impl reference: the reference's CPU implementation on all host threads."""
+    """--impl reference: the reference's CPU implementation of the path (oracle/_ref: the
+    unmodified /root/reference sources) on all host threads. Imports nothing from the product
+    package; inputs come from `workloads` (the same bytes the GPU arm reads)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_2303_12753_b200 as S
-
-    img = S.synth_image(spec["cid"], 0)
+    img = synth_image(spec["cid"], 0)
     h, w, c = img.shape
     full_px = h * w
-    if h * w > 2_000_000:  # C3/C4: a bounded sample (the first rows, clustered as an image of its own)
-        img = np.ascontiguousarray(img[: max(1, 1_000_000 // w)])
-        h = img.shape[0]
+    sample, rows = cpu_sample_image(spec, img) if h * w > 2_000_000 else (img, h)
+    sh = sample.shape[0]
     threads = os.cpu_count() or 1
-    # one step = one assign+update round over the whole image, chained like the real loop;
-    # setup (encode, shard copies) stays outside the timed region
-    times = []
-    import oracle
-    P = oracle.Port()
-    cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], BETA, GAMMA, CB_SEED)
-    grid = P.encode(img, spec["dim"], *cb)
-    seeds = P.select_seeds(img, spec["k"])
-    z = np.zeros((spec["k"], spec["dim"]), np.uint32)
-    for s, p in enumerate(seeds):
-        z[s] = np.unpackbits(grid[int(p)].view(np.uint8), bitorder="little")[: spec["dim"]]
-    counts = np.ones(spec["k"], np.uint64)
-    if oracle.have_ref():
-        R = oracle.Ref()
-        hnd = R.par_create(grid, h, w, spec["dim"], 0, h, threads)
-        step = lambda z, cn: R.par_round(hnd, z, cn)  # noqa: E731
-        kind = "reference"
-    else:
-        P.set_threads(threads)
-        kind = "port"
-
-        def step(z, cn):
-            lab = P.assign(grid, spec["dim"], z)
-            return P.update(grid, spec["dim"], lab, z)
+    grid, z, counts, kind = reference_setup(spec, sample)
+    step, done = reference_round_fn(spec, grid, sh, w, threads, kind)
     for _ in range(args.warmup):
         z, counts = step(z, counts)
-    for _ in range(args.steps):
+    times = []
+    for _ in range(args.steps):  # one step = one chained assign+update round (setup untimed)
         t = time.perf_counter()
         z, counts = step(z, counts)
         times.append(time.perf_counter() - t)
+    done()
     total = sum(times)
-    value = h * w * args.steps / total
+    value = sh * w * args.steps / total
+    what = ("the whole image" if sh == h else f"the first {sh} rows ({sh * w} of {full_px} px)")
+    _, _, img_ids, n_local, par = workload_layout(args.config, world, 0, h, w)
+    cfg = bench_config(args, spec, n_local, len(img_ids), par)
+    cfg["sample"] = f"one assign_labels+update_centroids round of {what} per step"
     line = {
-        "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32/u64 (reference integer dot)", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD_TEXT[args.config], "pixels": h * w, "dim": spec["dim"], "k": spec["k"],
-                   "step": ("one assign_labels+update_centroids round over the whole image" if h * w == full_px else
-                            f"one assign_labels+update_centroids round over the first {h} rows ({h * w} of "
-                            f"{full_px} px)")},
-        "cpu_baseline": {"value": value, "unit": "px·iter/s", "cores": threads, "kind": kind,
-                         "sample": f"{args.steps} chained rounds of {spec['name']} "
-                                   f"({'full image' if h * w == full_px else f'first {h} rows'}), one row-block per "
+        "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 (reference integer dot)", "data": "synthetic",
+        "impl": "reference", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "px·iter/s", "cores": threads, "kind": kind, "host": host_cpu(),
+                         "sample": f"{args.steps} chained rounds of {spec['name']} ({what}), one row-block per "
                                    f"thread, reference assign_labels/update_centroids"},
         "e2e": {"value": value, "unit": "px·iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -221,12 +244,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE.json config 0..4 (default: C1 on one GPU; C2, the 64-image batch sharded "
+                         "across ranks, under torchrun)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rounds", type=int, default=2)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config is None:
+        args.config = 2 if dist_env()[0] > 1 else 1
     spec = CONFIGS[args.config]
 
     if args.impl == "reference":
@@ -250,11 +277,10 @@ def main():
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
-    sharded = world > 1 and args.config in (3, 4)
-    batch = args.config == 2  # C2: 64 independent images, rank r takes images r, r + N, ...
-    img_ids = list(range(rank, C2_IMAGES, world)) if batch else [0 if sharded else rank]
-    img = S.synth_image(spec["cid"], img_ids[0])
-    h, w, c = img.shape
+    h, w, c = synth_image(spec["cid"], 0).shape
+    # C2: 64 independent images, rank r takes images r, r + N, ...; C3/C4 row-shard one image
+    sharded, batch, img_ids, _, parallelism = workload_layout(args.config, world, rank, h, w)
+    img = synth_image(spec["cid"], img_ids[0])
     cb = S.build_codebooks(spec["dim"], h, w, c, spec["alpha"], BETA, GAMMA, CB_SEED)
     k, iters, dim = spec["k"], spec["iterations"], spec["dim"]
     ctx.load_image(img)
@@ -274,7 +300,7 @@ def main():
         # C2_GROUPS contexts on their own streams, each sized for 1/C2_GROUPS of the SMs, take
         # the images round-robin: small images run side by side instead of one 148-CTA grid
         # at a time (each image's 512 tiles would leave the last wave of a full grid half empty)
-        imgs = [S.synth_image(spec["cid"], i) for i in img_ids]
+        imgs = [synth_image(spec["cid"], i) for i in img_ids]
         dev_imgs = torch.from_numpy(np.stack(imgs)).to(dev)
         ptrs = [dev_imgs[j].data_ptr() for j in range(len(imgs))]
         groups = [ctx] + [S.Context(local) for _ in range(C2_GROUPS - 1)]
@@ -359,7 +385,7 @@ def main():
     # ---- end to end through the reference-facing C-ABI call with host buffers
     e2e = None
     if not sharded:
-        pin_imgs = [torch.from_numpy(S.synth_image(spec["cid"], i)).pin_memory().numpy() for i in img_ids]
+        pin_imgs = [torch.from_numpy(synth_image(spec["cid"], i)).pin_memory().numpy() for i in img_ids]
         cfg = S.RunConfig(dim=dim, alpha=spec["alpha"], beta=BETA, gamma=GAMMA, clusters=k, iterations=iters,
                           seed=CB_SEED, early_stop=False)
         for _ in range(2):
@@ -405,13 +431,10 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        # bounded sample (~5-20 s of CPU work): the whole image up to 400k pixels, else its
-        # first rows (C3/C4: ~200k pixels, a crop clustered as an image of its own)
-        rows = h if h * w <= 400_000 else max(1, 200_000 // w)
-        crop = np.ascontiguousarray(img[:rows])
+        crop, rows = cpu_sample_image(spec, img)
         dt, pxr, kind = cpu_reference_rounds(spec, crop, args.cpu_sample_rounds, 1)
         what = f"the full {spec['name']} image" if rows == h else f"the first {rows} rows ({rows * w} px) of the {spec['name']} image"
-        cpu = {"value": pxr / dt, "unit": "px·iter/s", "cores": 1, "kind": kind,
+        cpu = {"value": pxr / dt, "unit": "px·iter/s", "cores": 1, "kind": kind, "host": host_cpu(),
                "sample": f"{args.cpu_sample_rounds} chained assign_labels+update_centroids rounds of {what}, "
                          f"single thread ({dt:.1f} s)"}
 
@@ -432,12 +455,8 @@ def main():
                                                                    if kernel_name == "k_round_tc" else
                                                                    "u8 x u8 -> s32 IMMA, u64/u128 argmax"),
         "data": "synthetic (seeded generator, SURVEY.md §8d)",
-        "config": {"workload": WORKLOAD_TEXT[args.config], "pixels_per_rank": n_local, "images_per_rank": len(img_ids),
-                   "dim": dim, "k": k,
-                   "iterations": iters, "early_stop": False, "parallelism": (f"row-shard x{world}" if sharded else
-                                                                            f"replicas x{world}"),
-                   "l2": l2_note,
-                   "labels_sha256_16": labels_sha},
+        "config": dict(bench_config(args, spec, n_local, len(img_ids), parallelism), l2=l2_note,
+                       labels_sha256_16=labels_sha),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": kernel_name + " (fused assign + re-bundle)",
                      "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": kern_ms / kern_n,

@@ -60,6 +60,13 @@ uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx);
  * "k_round"; "" before any plan). */
 const char* seghdc_round_kernel(const seghdc_ctx* ctx);
 
+/* Diagnostic (no reference counterpart): per-round number of strictly_closer comparisons
+ * (clusterer.cpp:41-50) whose unsigned __int128 products exceeded 2^128 in the last clustering
+ * run of ctx (seghdc_cluster / _async / run_pipeline / run_pipeline_closed / assign; a shard
+ * counts its own pixels). The result is still the reference's wrapped comparison; this only
+ * reports how often it happened. Copies min(rounds, cap) counts; rounds_out = rounds run. */
+int seghdc_round_wraps(seghdc_ctx* ctx, uint64_t* out, size_t cap, size_t* rounds_out);
+
 /* ---- host-side codebooks (stay on the host: mt19937_64 is sequential and cheap) -------- */
 /* run_pipeline's codebook stage (pipeline.cpp:43-59): one Rng(seed), position codebook
  * (position_encoder.hpp:45, or build_random_position_codebook pixel_pipeline.hpp:79 for
@@ -174,16 +181,10 @@ int seghdc_profile_read(seghdc_ctx* ctx, double* total_ms, uint64_t* count);
 /* as profile_read, plus the first `cap` per-launch times (in launch order) into each_ms */
 int seghdc_profile_read_each(seghdc_ctx* ctx, double* total_ms, uint64_t* count, double* each_ms, size_t cap);
 
-/* ---- synthetic inputs (bench/test workloads) --------------------------- */
-/* config_id 0..4 = BASELINE.json configs; config 2 is config 0's construction (use seed
- * 0..63 per image). Writes h*w*c bytes. Returns the shape through h/w/c when out is NULL. */
 /* Page-locked host memory (cudaHostAlloc, portable) for result buffers: device->host copies
  * of labels into it run at full PCIe rate instead of through the driver's pageable staging. */
 int seghdc_pinned_alloc(size_t bytes, void** out);
 int seghdc_pinned_free(void* p);
-
-int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w,
-                       size_t* c);
 
 #ifdef __cplusplus
 }

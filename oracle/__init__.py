@@ -93,6 +93,16 @@ class Port(_Lib):
     def __init__(self, path: str = PORT_SO):
         super().__init__(path)
 
+    def last_wraps(self) -> list:
+        """Per-round count of 128-bit-wrapping strictly_closer comparisons of the last
+        assign / cluster / cluster_stream call (so_last_wraps; diagnostic, not reference API)."""
+        out = np.zeros(4096, np.uint64)
+        f = self.lib.so_last_wraps
+        f.argtypes = [_u64p, _sz]
+        f.restype = _sz
+        n = f(out, out.size)
+        return [int(x) for x in out[:n]]
+
     def set_threads(self, n: int) -> None:
         self.lib.so_set_threads(C.c_int(n))
 
@@ -260,6 +270,46 @@ class Ref(_Lib):
         self._check(f(handle, np.ascontiguousarray(z).ravel(), np.ascontiguousarray(counts, np.uint64), k,
                       nz.ravel(), nc))
         return nz, nc
+
+    # reference-pure full-length loop whose shard grids come from the reference's own
+    # encode_image (ref_pare_*: peak host memory one grid; C4 = 34.4 GB)
+    def cluster_encoded(self, img, dim, k, iterations, alpha=0.2, beta=26, gamma=1, seed=0, nthreads=None,
+                        on_round=None):
+        """cluster() (clusterer.cpp:190-218, early stop off) on the reference's own encode_image,
+        rows split over threads. Returns labels per round (via on_round(r, labels) if given),
+        the final labels, the centroid set used by the final assignment and its counts."""
+        h, w, c = img.shape
+        n = h * w
+        nthreads = nthreads or os.cpu_count() or 1
+        f = self.lib.ref_pare_create
+        f.argtypes = [_u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, C.c_uint64, C.c_int, C.c_int]
+        f.restype = C.c_void_p
+        hnd = f(np.ascontiguousarray(img), h, w, c, dim, alpha, beta, gamma, seed, 0, nthreads)
+        if not hnd:
+            raise OracleError(2, self._err().decode())
+        try:
+            seeds = self.select_seeds(img, k)
+            z = np.zeros((k, dim), np.uint32)
+            fs = self.lib.ref_pare_seed
+            fs.argtypes = [C.c_void_p, _u64p, _sz, _u32p]
+            self._check(fs(hnd, seeds, k, z.ravel()))
+            counts = np.ones(k, np.uint64)
+            fr = self.lib.ref_pare_round
+            fr.argtypes = [C.c_void_p, _u32p, _u64p, _sz, C.c_int, _u32p, _u32p, _u64p]
+            labels = np.zeros(n, np.uint32)
+            for r in range(1, iterations + 1):
+                upd = r < iterations
+                nz = np.zeros_like(z)
+                nc = np.zeros(k, np.uint64)
+                self._check(fr(hnd, z.ravel(), counts, k, int(upd), labels, nz.ravel(), nc))
+                if on_round:
+                    on_round(r, labels)
+                if upd:
+                    z, counts = nz, nc
+            return {"labels": labels, "centroids": z, "counts": counts, "rounds": iterations, "seeds": seeds}
+        finally:
+            self.lib.ref_pare_destroy.argtypes = [C.c_void_p]
+            self.lib.ref_pare_destroy(hnd)
 
     def par_destroy(self, handle):
         self.lib.ref_par_destroy.argtypes = [C.c_void_p]

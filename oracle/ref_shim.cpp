@@ -13,6 +13,7 @@
 //    does not return its centroids (clusterer.hpp:68-71);
 //  * widening of colour table entries to full D (mirrors the file-static
 //    widen_color_tables, reference src/pixel_pipeline.cpp:70-88) for table export.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -291,5 +292,106 @@ int ref_par_round(void* handle, const std::uint32_t* centroids, const std::uint6
 }
 
 void ref_par_destroy(void* handle) { delete static_cast<RefPar*>(handle); }
+
+// ---- reference-pure full-length loop for images whose grid is too large to copy ---------
+// Same row-block shards as RefPar, but every shard grid is produced by the reference's OWN
+// encode_image (src/pixel_pipeline.cpp:92-126) on the shard's rows, with the position
+// codebook's row table sliced to those rows (the codebook is built once for the full image
+// in run_pipeline's RNG order, pipeline.cpp:43-59). Peak host memory is one grid (C4:
+// 34.4 GB) instead of two. The loop is cluster()'s (src/clusterer.cpp:190-218): seed
+// centroids from the seed pixels' HVs (:197-205), assign_labels every round, update_centroids
+// between rounds; assign/update run per shard in parallel and the integer sums are combined
+// exactly (empty everywhere -> previous centroid, :184-186).
+struct RefParEnc {
+    std::vector<PixelHvGrid> shards;
+    std::vector<std::size_t> row0;
+    std::size_t h = 0, w = 0, dim = 0;
+};
+
+void* ref_pare_create(const std::uint8_t* px, std::size_t h, std::size_t w, std::size_t c,
+                      std::size_t dim, double alpha, std::size_t beta, std::size_t gamma,
+                      std::uint64_t seed, int encoder, int nthreads) {
+    auto* p = new RefParEnc;
+    const int rc = guard([&] {
+        p->h = h;
+        p->w = w;
+        p->dim = dim;
+        const Codebooks cb = build_codebooks(dim, h, w, c, alpha, beta, gamma, seed, encoder);
+        const std::size_t t = std::max<std::size_t>(1, std::min<std::size_t>(nthreads, h));
+        p->shards.resize(t);
+        std::vector<std::thread> threads;
+        for (std::size_t s = 0; s < t; ++s) {
+            const std::size_t r0 = h * s / t, r1 = h * (s + 1) / t;
+            p->row0.push_back(r0);
+            threads.emplace_back([&, s, r0, r1] {
+                const ImageBuffer sub = make_image(px + r0 * w * c, r1 - r0, w, c);
+                PositionCodebook pos = cb.pos;  // row table sliced to this shard's rows
+                pos.config.n_rows = r1 - r0;
+                pos.row_hvs.assign(cb.pos.row_hvs.begin() + r0, cb.pos.row_hvs.begin() + r1);
+                p->shards[s] = encode_image(sub, pos, cb.color);
+            });
+        }
+        for (auto& th : threads) th.join();
+        p->row0.push_back(h);
+    });
+    if (rc) {
+        delete p;
+        return nullptr;
+    }
+    return p;
+}
+
+// seed centroids (clusterer.cpp:197-205) for row-major seed indices
+int ref_pare_seed(void* handle, const std::uint64_t* seeds, std::size_t k, std::uint32_t* z_out) {
+    auto* p = static_cast<RefParEnc*>(handle);
+    return guard([&] {
+        for (std::size_t s = 0; s < k; ++s) {
+            const std::size_t row = seeds[s] / p->w, col = seeds[s] % p->w;
+            std::size_t sh = 0;
+            while (p->row0[sh + 1] <= row) ++sh;
+            IntVector v(p->dim);
+            v.add_words(p->shards[sh].hv_words(row - p->row0[sh], col));
+            const auto vals = v.values();
+            std::memcpy(z_out + s * p->dim, vals.data(), p->dim * 4);
+        }
+    });
+}
+
+// one round: assign_labels on every shard (labels_out[h*w], nullable); if do_update, the
+// combined update_centroids into next_out / next_counts.
+int ref_pare_round(void* handle, const std::uint32_t* centroids, const std::uint64_t* counts,
+                   std::size_t k, int do_update, std::uint32_t* labels_out, std::uint32_t* next_out,
+                   std::uint64_t* next_counts) {
+    auto* p = static_cast<RefParEnc*>(handle);
+    return guard([&] {
+        const CentroidSet cs = make_centroids(centroids, counts, k, p->dim);
+        std::vector<CentroidSet> parts(p->shards.size());
+        std::vector<std::thread> threads;
+        for (std::size_t s = 0; s < p->shards.size(); ++s) {
+            threads.emplace_back([&, s] {
+                const auto mask = assign_labels(p->shards[s], cs);
+                if (labels_out)
+                    std::memcpy(labels_out + p->row0[s] * p->w, mask.labels.data(), mask.labels.size() * 4);
+                if (do_update) parts[s] = update_centroids(p->shards[s], mask, cs);
+            });
+        }
+        for (auto& th : threads) th.join();
+        if (!do_update) return;
+        for (std::size_t c = 0; c < k; ++c) {
+            std::uint64_t total = 0;
+            std::vector<std::uint32_t> sum(p->dim, 0);
+            for (const auto& part : parts) {
+                if (part.member_counts[c] == 0) continue;
+                total += part.member_counts[c];
+                const auto vals = part.centroids[c].values();
+                for (std::size_t i = 0; i < p->dim; ++i) sum[i] += vals[i];
+            }
+            std::memcpy(next_out + c * p->dim, total ? sum.data() : centroids + c * p->dim, p->dim * 4);
+            next_counts[c] = total;
+        }
+    });
+}
+
+void ref_pare_destroy(void* handle) { delete static_cast<RefParEnc*>(handle); }
 
 }  // extern "C"

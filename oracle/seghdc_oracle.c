@@ -295,6 +295,33 @@ static int strictly_closer(uint64_t dc, uint64_t n2c, uint64_t db, uint64_t n2b)
     return lhs > rhs;
 }
 
+/* Diagnostic (not in the reference): does d*d*n2 exceed 2^128, i.e. did the reference's
+ * unsigned __int128 product in strictly_closer wrap? A comparison "wraps" when either side
+ * does (both norms non-zero, so both products are evaluated). Counted per round by
+ * so_assign / so_cluster / so_cluster_stream and read back with so_last_wraps. */
+static int prod_wraps(uint64_t d, uint64_t n2) {
+    const unsigned __int128 sq = (unsigned __int128)d * d;
+    const unsigned __int128 lo = (unsigned __int128)(uint64_t)sq * n2;
+    const unsigned __int128 hi = (unsigned __int128)(uint64_t)(sq >> 64) * n2 + (lo >> 64);
+    return (hi >> 64) != 0;
+}
+static int compare_wraps(uint64_t dc, uint64_t n2c, uint64_t db, uint64_t n2b) {
+    if (n2c == 0 || n2b == 0) return 0;
+    return prod_wraps(dc, n2b) | prod_wraps(db, n2c);
+}
+#define SO_MAX_WRAP_ROUNDS 4096
+static uint64_t g_wraps[SO_MAX_WRAP_ROUNDS];
+static size_t g_wrap_rounds;
+size_t so_last_wraps(uint64_t* out, size_t cap) {
+    for (size_t r = 0; r < g_wrap_rounds && r < cap; r++) out[r] = g_wraps[r];
+    return g_wrap_rounds;
+}
+static void record_wraps(size_t round, uint64_t wraps) { /* round is 1-based */
+    if (round == 1) g_wrap_rounds = 0;
+    if (round <= SO_MAX_WRAP_ROUNDS) g_wraps[round - 1] = wraps;
+    g_wrap_rounds = round;
+}
+
 /* assign_labels, clusterer.cpp:132-162. */
 int so_assign(const uint64_t* grid, size_t n, size_t dim, const uint32_t* z, size_t k, uint32_t* labels_out) {
     if (k == 0) return fail(1, "assign_labels: empty centroid set");
@@ -303,13 +330,15 @@ int so_assign(const uint64_t* grid, size_t n, size_t dim, const uint32_t* z, siz
     for (size_t c = 0; c < k; c++) /* IntVector::norm_squared, hypervector.cpp:123-127 */
         for (size_t i = 0; i < dim; i++) norm2[c] += (uint64_t)z[c * dim + i] * z[c * dim + i];
     /* dot_words indexes z[(wi<<6)+b] for set bits only; tail bits are zero so b < dim. */
-#pragma omp parallel for schedule(dynamic, 256) num_threads(nthreads())
+    uint64_t wraps = 0;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(nthreads()) reduction(+ : wraps)
     for (size_t p = 0; p < n; p++) {
         const uint64_t* y = grid + p * nw;
         uint32_t best = 0;
         uint64_t best_dot = dot_words(y, nw, z);
         for (size_t c = 1; c < k; c++) {
             const uint64_t d = dot_words(y, nw, z + c * dim);
+            wraps += (uint64_t)compare_wraps(d, norm2[c], best_dot, norm2[best]);
             if (strictly_closer(d, norm2[c], best_dot, norm2[best])) {
                 best = (uint32_t)c;
                 best_dot = d;
@@ -318,6 +347,7 @@ int so_assign(const uint64_t* grid, size_t n, size_t dim, const uint32_t* z, siz
         labels_out[p] = best;
     }
     free(norm2);
+    record_wraps(1, wraps);
     return 0;
 }
 
@@ -391,9 +421,11 @@ int so_cluster(const uint64_t* grid, const uint8_t* px, size_t h, size_t w, size
         counts[s] = 1;
     }
     uint32_t* prev = malloc(n * 4);
+    uint64_t* wr_hist = calloc(SO_MAX_WRAP_ROUNDS, 8);
     size_t rounds = 0;
     for (size_t r = 1; r <= iterations; r++) { /* :209-216 */
         so_assign(grid, n, dim, z, k, labels_final);
+        if (r <= SO_MAX_WRAP_ROUNDS) wr_hist[r - 1] = g_wraps[0];
         rounds = r;
         if (labels_rounds) memcpy(labels_rounds + (r - 1) * n, labels_final, n * 4);
         if (early_stop && r > 1 && memcmp(labels_final, prev, n * 4) == 0) break;
@@ -408,6 +440,8 @@ int so_cluster(const uint64_t* grid, const uint8_t* px, size_t h, size_t w, size
     if (centroids_out) memcpy(centroids_out, z, k * dim * 4);
     if (counts_out) memcpy(counts_out, counts, k * 8);
     *rounds_out = rounds;
+    for (size_t r = 1; r <= rounds && r <= SO_MAX_WRAP_ROUNDS; r++) record_wraps(r, wr_hist[r - 1]);
+    free(wr_hist);
     free(prev);
     free(seeds);
     free(z);
@@ -464,7 +498,8 @@ int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t di
         }
         memset(part, 0, (size_t)T * k * dim * 4);
         memset(cnt, 0, (size_t)T * k * 8);
-#pragma omp parallel num_threads(T)
+        uint64_t wraps = 0;
+#pragma omp parallel num_threads(T) reduction(+ : wraps)
         {
             const int t = omp_get_thread_num();
             uint32_t* acc = part + (size_t)t * k * dim;
@@ -490,8 +525,10 @@ int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t di
                     }
                 }
                 uint32_t best = 0; /* assign_labels, clusterer.cpp:132-162 */
-                for (size_t cc = 1; cc < k; cc++)
+                for (size_t cc = 1; cc < k; cc++) {
+                    wraps += (uint64_t)compare_wraps(d[cc], norm2[cc], d[best], norm2[best]);
                     if (strictly_closer(d[cc], norm2[cc], d[best], norm2[best])) best = (uint32_t)cc;
+                }
                 labels_final[p] = best;
                 if (do_update) { /* IntVector::add_words into this thread's partial sums */
                     uint32_t* zc = acc + (size_t)best * dim;
@@ -507,6 +544,7 @@ int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t di
             }
             free(yy);
         }
+        record_wraps(r, wraps);
         rounds = r;
         if (labels_rounds) memcpy(labels_rounds + (r - 1) * n, labels_final, n * 4);
         if (early_stop && r > 1 && memcmp(labels_final, prev, n * 4) == 0) break;

@@ -60,6 +60,11 @@ int so_cluster_stream(const uint8_t* px, size_t h, size_t w, size_t c, size_t di
                       uint32_t* labels_rounds, uint32_t* labels_final, uint32_t* centroids_out,
                       uint64_t* counts_out, size_t* rounds_out);
 
+/* Per-round count of strictly_closer comparisons whose 128-bit products wrapped (either side
+ * >= 2^128) in the last so_assign (1 round) / so_cluster / so_cluster_stream call; returns
+ * the number of rounds recorded, copies up to cap. Diagnostic, not reference API. */
+size_t so_last_wraps(uint64_t* out, size_t cap);
+
 /* threads used by the OpenMP loops (0 = OpenMP default). */
 void so_set_threads(int n);
 int so_get_threads(void);

@@ -80,12 +80,12 @@ SIGNATURES = {
     "seghdc_shard_assign": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_round_needs_exchange": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_finish": ([C.c_void_p, _sz], C.c_int),
+    "seghdc_round_wraps": ([C.c_void_p, C.c_void_p, _sz, C.POINTER(_sz)], C.c_int),
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
     "seghdc_profile_read_each": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_void_p, _sz], C.c_int),
     "seghdc_pinned_alloc": ([_sz, C.POINTER(C.c_void_p)], C.c_int),
     "seghdc_pinned_free": ([C.c_void_p], C.c_int),
-    "seghdc_synth_image": ([C.c_int, C.c_uint64, C.c_void_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -178,12 +178,11 @@ def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
 
 
 def synth_image(config_id: int, seed: int = 0) -> np.ndarray:
-    """Seeded synthetic nuclei image of BASELINE.json config ``config_id``."""
-    h, w, c = _sz(), _sz(), _sz()
-    _check(lib().seghdc_synth_image(config_id, seed, None, C.byref(h), C.byref(w), C.byref(c)))
-    out = np.zeros((h.value, w.value, c.value), np.uint8)
-    _check(lib().seghdc_synth_image(config_id, seed, out.ctypes.data, C.byref(h), C.byref(w), C.byref(c)))
-    return out
+    """Seeded synthetic nuclei image of BASELINE.json config ``config_id``; the
+    generator lives in the repo's ``workloads`` package, outside the product library."""
+    import workloads
+
+    return workloads.synth_image(config_id, seed)
 
 
 # ------------------------------------------------------------------------------------------
@@ -237,6 +236,14 @@ class Context:
     def round_kernel(self) -> str:
         """Round kernel of the current clustering plan (k_round_tc / k_round_fused / k_round)."""
         return lib().seghdc_round_kernel(self.h).decode()
+
+    def round_wraps(self) -> list:
+        """Per-round count of 128-bit-wrapping strictly_closer comparisons in the last clustering
+        run (seghdc_round_wraps; diagnostic, compared with the oracle's so_last_wraps)."""
+        out = np.zeros(4096, np.uint64)
+        n = _sz()
+        self.check(lib().seghdc_round_wraps(self.h, out.ctypes.data, out.size, C.byref(n)))
+        return [int(x) for x in out[:min(n.value, out.size)]]
 
     def profile_rounds(self, enable: bool) -> None:
         self.check(lib().seghdc_profile_rounds(self.h, int(enable)))

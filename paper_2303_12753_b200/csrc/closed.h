@@ -37,6 +37,7 @@ struct ClosedState {
     uint32_t* labels;
     unsigned long long* changed;
     int32_t* diffc;  // [K][L] difference counts on compressed endpoint indices (k_closed_accumulate_c)
+    unsigned long long* wraps;  // this round's count of 128-bit-wrapping comparisons (diagnostic)
 };
 
 // centroids from the seed pixels (clusterer.cpp:197-205): runs of seed k into diff[k], cnt[k] = 1

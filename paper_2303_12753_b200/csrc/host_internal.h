@@ -35,6 +35,4 @@ struct ManhattanParams {
 ManhattanParams manhattan_bases(size_t dim, size_t h, size_t w, size_t c, double alpha, size_t beta, size_t gamma,
                                 std::mt19937_64& rng, uint64_t* bases);
 
-void synth_image(int id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c);
-
 }  // namespace seghdc_host

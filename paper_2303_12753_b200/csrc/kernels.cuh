@@ -39,20 +39,24 @@ struct RoundState {
 // Followed in memory by (K = number of clusters):
 //   u32 cur[2][K]        member counts of the centroid set used by the round's assignment
 //   u64 norm2[2][K]      IntVector::norm_squared of that set (hypervector.cpp:123-127)
+//   u64 wraps[iterations] per-round count of 128-bit-wrapping comparisons (diagnostic)
 struct StateView {
     RoundState* hdr;
     uint32_t* cur;
     unsigned long long* norm2;
+    unsigned long long* wraps;
     uint32_t K;
     __host__ __device__ static size_t norm2_offset(uint32_t K) {
         return (sizeof(RoundState) + 2 * size_t(K) * 4 + 7) & ~size_t(7);
     }
     __host__ __device__ static size_t bytes(uint32_t K) { return norm2_offset(K) + 2 * size_t(K) * 8; }
+    __host__ __device__ static size_t bytes(uint32_t K, size_t iterations) { return bytes(K) + 8 * (iterations + 1); }
     __host__ __device__ static StateView at(void* base, uint32_t K) {
         StateView v;
         v.hdr = reinterpret_cast<RoundState*>(base);
         v.cur = reinterpret_cast<uint32_t*>(v.hdr + 1);
         v.norm2 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + norm2_offset(K));
+        v.wraps = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + bytes(K));
         v.K = K;
         return v;
     }
@@ -76,6 +80,22 @@ __device__ __forceinline__ bool strictly_closer(unsigned long long dc, unsigned 
     const unsigned __int128 lhs = (unsigned __int128)dc * dc * n2b;
     const unsigned __int128 rhs = (unsigned __int128)db * db * n2c;
     return lhs > rhs;
+}
+
+// Diagnostic, not reference behaviour: did strictly_closer's unsigned __int128 product
+// d*d*n2 exceed 2^128 (so the reference compared wrapped values)? A comparison wraps when
+// either side does (both norms non-zero). Fast reject on bit lengths, exact 192-bit check
+// otherwise; counted per round so the oracle's per-round counts can be matched.
+__device__ __forceinline__ bool prod_wraps(unsigned long long d, unsigned long long n2) {
+    if (2 * (64 - __clzll(d)) + (64 - __clzll(n2)) <= 128) return false;
+    const unsigned long long sl = d * d, sh = __umul64hi(d, d);
+    const unsigned long long a1 = __umul64hi(sl, n2), b0 = sh * n2, b1 = __umul64hi(sh, n2);
+    return b1 != 0 || b0 + a1 < b0;
+}
+__device__ __forceinline__ uint32_t compare_wraps(unsigned long long dc, unsigned long long n2c,
+                                                  unsigned long long db, unsigned long long n2b) {
+    if (n2c == 0 || n2b == 0) return 0u;
+    return (prod_wraps(dc, n2b) || prod_wraps(db, n2c)) ? 1u : 0u;
 }
 
 // ------------------------------------------------------------------------------------------

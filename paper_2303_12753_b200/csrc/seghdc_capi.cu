@@ -141,6 +141,11 @@ struct seghdc_ctx {
         DevBuf<uint8_t> bf;
     } cf;
     int exchange_phase = 0;  // 0: rounds, 1: init (includes colsums)
+    // per-round counts of 128-bit-wrapping comparisons of the last clustering run (diagnostic):
+    // the packed path keeps them behind its round state, the closed-form variant in wraps_hist
+    DevBuf<unsigned long long> wraps_hist;
+    const unsigned long long* wraps_src = nullptr;
+    size_t wraps_rounds = 0;
     // optional CUDA-event timing of every round kernel (bench.py's roofline)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -330,7 +335,7 @@ void alloc_cluster(seghdc_ctx& x, size_t K, uint64_t vmax = 0) {
         x.round_ctas = uint32_t(std::max<uint64_t>(1, (tiles + per - 1) / per));
     }
     const uint32_t NT = x.plan.nt;
-    x.state.ensure(StateView::bytes(uint32_t(K)));
+    x.state.ensure(StateView::bytes(uint32_t(K), x.iterations));
     x.labels.ensure(n + 4);  // +4: the fused kernel's TMA of a tile's labels rounds up to 16 B
     x.Z.ensure(K * g.D);
     // B fragments: entries of words >= W32 must stay zero -> clear on every (re)plan
@@ -433,10 +438,12 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
 void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     require(x.h > 0 && x.w == x.g_w && x.h == x.g_h, "image and grid shapes differ");
     seghdc_host::validate_cluster(K, iterations, x.h * x.w);
-    alloc_cluster(x, K);
     x.iterations = iterations;
+    alloc_cluster(x, K);
     x.early_stop = early_stop;
-    ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K)), x.stream), "clear state");
+    ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K), iterations), x.stream), "clear state");
+    x.wraps_src = StateView::at(x.state.p, uint32_t(K)).wraps;
+    x.wraps_rounds = 0;
     ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
     if (x.incremental()) ck(cudaMemsetAsync(x.run1.p, 0, 2 * x.K * size_t(x.g.Dp) * 4, x.stream), "clear running sums");
     select_seeds_dev(x, K);
@@ -673,6 +680,19 @@ int seghdc_synchronize(seghdc_ctx* ctx) {
 
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int seghdc_round_wraps(seghdc_ctx* ctx, uint64_t* out, size_t cap, size_t* rounds_out) {
+    return guarded(ctx, [&] {
+        require(ctx->wraps_src != nullptr, "no clustering run on this context yet");
+        size_t rounds = ctx->wraps_rounds;
+        const bool packed = ctx->K && ctx->state.p && ctx->wraps_src == StateView::at(ctx->state.p, uint32_t(ctx->K)).wraps;
+        if (packed) rounds = read_state(*ctx).hdr.rounds_run;  // synchronises
+        const size_t nc = std::min(rounds, cap);
+        if (nc) ck(cudaMemcpyAsync(out, ctx->wraps_src, nc * 8, cudaMemcpyDeviceToHost, ctx->stream), "download wraps");
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        if (rounds_out) *rounds_out = rounds;
+    });
+}
+
 const char* seghdc_round_kernel(const seghdc_ctx* ctx) {
     if (!ctx || ctx->K == 0) return "";
     return ctx->plan.tc ? "k_round_tc" : ctx->plan.fused ? "k_round_fused" : "k_round";
@@ -737,13 +757,14 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         // caller centroids may hold any u32 (the reference's IntVector): up to 6 planes
         uint32_t zmax = 0;
         for (size_t i = 0; i < k * dim; ++i) zmax = std::max(zmax, centroids[i]);
-        alloc_cluster(*ctx, k, std::max<uint64_t>(zmax, 1));
-        ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
-        ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k)), ctx->stream), "clear state");
-        ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");
-        finish(*ctx, 2, 0);  // norm2 + B fragments of the given set (parity 1)
         ctx->iterations = 1;
         ctx->early_stop = 0;
+        alloc_cluster(*ctx, k, std::max<uint64_t>(zmax, 1));
+        ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
+        ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k), 1), ctx->stream), "clear state");
+        ctx->wraps_src = StateView::at(ctx->state.p, uint32_t(k)).wraps;
+        ck(cudaMemsetAsync(ctx->labels.p, 0xFF, ctx->n_local() * 4, ctx->stream), "clear labels");
+        finish(*ctx, 2, 0);  // norm2 + B fragments of the given set (parity 1)
         round_assign(*ctx, 1);
         ck(cudaMemcpyAsync(labels_out, ctx->labels.p, ctx->n_local() * 4, cudaMemcpyDeviceToHost, ctx->stream),
            "download labels");
@@ -897,7 +918,8 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         select_seeds_dev(*ctx, k);
 
         const size_t n = h * w, stride = dim + 1;
-        require(n < (size_t(1) << 32), "closed-form variant: more than 2^32 pixels");
+        // per-position member counts (diff, diffc) are int32
+        require(n < (size_t(1) << 31), "closed-form variant: 2^31 pixels or more");
         auto& Q = ctx->cf.Q;
         auto &P = ctx->cf.P, &n2 = ctx->cf.n2, &cnt = ctx->cf.cnt, &counts = ctx->cf.counts, &changed = ctx->cf.changed;
         auto &Z = ctx->cf.Z, &labels = ctx->cf.labels;
@@ -934,13 +956,20 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         // compressed endpoint indices when they fit (keys pos << 15 | index, [K][L] tables in smem)
         const bool compressed = a.L < (1u << 15) && dim < (1u << 17) && size_t(a.L) * k * 8 <= (160u << 10) &&
                                 !getenv("SEGHDC_CLOSED_POSITIONS");
+        // the position-table accumulate keeps one [dim + 1] int32 difference row per cluster
+        // group in shared memory (k_closed_accumulate, at least one cluster per group)
+        require(compressed || (dim + 1) * 4 + 4 <= ctx->smem_optin,
+                "closed-form variant: dim = " + std::to_string(dim) +
+                    " needs the position tables, whose difference row exceeds shared memory");
         auto& diffc = ctx->cf.diffc;
         if (compressed) {
             diffc.ensure(k * a.L);
             ck(cudaMemsetAsync(diffc.p, 0, k * a.L * 4, ctx->stream), "clear diffc");
         }
         ClosedState st{Q.p, P.p, n2.p, Z.p, diff.p, cnt.p, counts.p, bf.p, labels.p, changed.p,
-                       compressed ? diffc.p : nullptr};
+                       compressed ? diffc.p : nullptr, nullptr};
+        ctx->wraps_hist.ensure(iterations + 1);
+        ck(cudaMemsetAsync(ctx->wraps_hist.p, 0, (iterations + 1) * 8, ctx->stream), "clear wraps");
         launch_closed_seed(a, ctx->seeds.p, st, ctx->stream);
         launch_closed_finish(a, st, ctx->stream);
         ctx->count(2);
@@ -948,6 +977,7 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         size_t rounds = 0;
         for (size_t r = 1; r <= iterations; ++r) {  // clusterer.cpp:208-216
             ck(cudaMemsetAsync(changed.p, 0, 8, ctx->stream), "clear changed");
+            st.wraps = ctx->wraps_hist.p + (r - 1);
             launch_closed_assign(a, st, ctx->sms, ctx->stream);
             ctx->count();
             ctx->check_launch();
@@ -972,6 +1002,8 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
             ck(cudaMemcpyAsync(counts_out, counts.p, k * 8, cudaMemcpyDeviceToHost, ctx->stream), "download counts");
         ck(cudaStreamSynchronize(ctx->stream), "sync");
         if (rounds_out) *rounds_out = rounds;
+        ctx->wraps_src = ctx->wraps_hist.p;
+        ctx->wraps_rounds = rounds;
     });
 }
 
@@ -1097,10 +1129,6 @@ int seghdc_pinned_alloc(size_t bytes, void** out) {
 
 int seghdc_pinned_free(void* p) {
     return guarded(nullptr, [&] { ck(cudaFreeHost(p), "cudaFreeHost"); });
-}
-
-int seghdc_synth_image(int config_id, uint64_t seed, uint8_t* out, size_t* h, size_t* w, size_t* c) {
-    return guarded(nullptr, [&] { seghdc_host::synth_image(config_id, seed, out, h, w, c); });
 }
 
 }  // extern "C"

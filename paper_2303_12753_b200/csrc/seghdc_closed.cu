@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "closed.h"
+#include "kernels.cuh"
 #include "launch.h"
 
 namespace seghdc_dev {
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
     __syncthreads();
     const size_t stride = size_t(a.dim) + 1;
     unsigned long long changed = 0;
+    uint32_t nwrap = 0;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
         uint32_t e[kRuns];
         closed_runs(a, p, e);
@@ -141,8 +143,9 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
             const unsigned long long dot = (unsigned long long)d, n2 = sN[k];
             if (k == 0) {
                 best_dot = dot, best_n2 = n2;
-            } else if (strictly_closer_dev(dot, n2, best_dot, best_n2)) {
-                best = k, best_dot = dot, best_n2 = n2;
+            } else {
+                nwrap += compare_wraps(dot, n2, best_dot, best_n2);
+                if (strictly_closer_dev(dot, n2, best_dot, best_n2)) best = k, best_dot = dot, best_n2 = n2;
             }
         }
         changed += (s.labels[p] != best);
@@ -150,8 +153,12 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
     }
     // one atomic per warp
 #pragma unroll
-    for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+    for (int o = 16; o; o >>= 1) {
+        changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+        nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
+    }
     if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
+    if ((threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
 }
 
 // assign_labels with the K prefix tables restricted to the L endpoint positions, staged once per
@@ -170,6 +177,7 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
     }
     __syncthreads();
     unsigned long long changed = 0;
+    uint32_t nwrap = 0;
     for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.n; p += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t old = s.labels[p];  // issued with the image loads, not after the argmax
         uint32_t e[kRuns];
@@ -183,16 +191,21 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
             const unsigned long long dot = (unsigned long long)d, n2 = sN[k];
             if (k == 0) {
                 best_dot = dot, best_n2 = n2;
-            } else if (strictly_closer_dev(dot, n2, best_dot, best_n2)) {
-                best = k, best_dot = dot, best_n2 = n2;
+            } else {
+                nwrap += compare_wraps(dot, n2, best_dot, best_n2);
+                if (strictly_closer_dev(dot, n2, best_dot, best_n2)) best = k, best_dot = dot, best_n2 = n2;
             }
         }
         changed += (old != best);
         s.labels[p] = best;
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+    for (int o = 16; o; o >>= 1) {
+        changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
+        nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
+    }
     if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
+    if ((threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
 }
 
 // grid = (blocks, cluster groups); group y owns clusters [y*G, y*G + G), one difference array

@@ -704,12 +704,13 @@ __global__ void __launch_bounds__(TB, 1)
         }
         if (tid < npx) {
             const uint32_t* rr = red + tid * NCT;
-            uint32_t best = 0;
+            uint32_t best = 0, nwrap = 0;
             unsigned long long bdot = 0, bn2 = 0;
             for (uint32_t c = 0; c < K; ++c) {
                 unsigned long long d = 0;
                 for (uint32_t pl = 0; pl < P; ++pl) d += (unsigned long long)rr[P * c + pl] << (kPlaneBits * pl);
                 const unsigned long long n2 = s_n2[c];
+                if (c > 0) nwrap += compare_wraps(d, n2, bdot, bn2);
                 if (c == 0 || strictly_closer(d, n2, bdot, bn2)) {
                     best = c;
                     bdot = d;
@@ -717,6 +718,7 @@ __global__ void __launch_bounds__(TB, 1)
                 }
             }
             labels[px0 + tid] = best;
+            if (nwrap) atomicAdd(st.wraps + (round - 1), (unsigned long long)nwrap);
             if (old != best) atomicAdd(&s_misc[0], 1u);
             atomicAdd(&s_misc[2 + best], 1u);
         }
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__((NMW + NRW + 2) * 32, 1)
     if (warp == NMW + NRW) {
         // ----------------------------------------------------------------------- epilogue warp
         const unsigned long long n2_0 = st.norm2[parity * K], n2_1 = K > 1 ? st.norm2[parity * K + 1] : 0ull;
-        uint32_t changed = 0, cnt1 = 0, total = 0;
+        uint32_t changed = 0, cnt1 = 0, total = 0, nwrap = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t pb = it & 1, b = it % NB;
             const uint64_t px0 = (blockIdx.x + uint64_t(it) * gridDim.x) * TP;
@@ -898,6 +900,7 @@ __global__ void __launch_bounds__((NMW + NRW + 2) * 32, 1)
                                           ((unsigned long long)uint32_t(col[7]) << (3 * kPlaneBits));
             const uint32_t best = (K > 1 && strictly_closer(d1, n2_1, d0, n2_0)) ? 1u : 0u;
             const bool live = lane < npx;
+            if (K > 1 && live) nwrap += compare_wraps(d1, n2_1, d0, n2_0);
             const uint32_t old = s_old[b * TP + lane];
             if (live) {
                 labels[px0 + lane] = best;
@@ -917,8 +920,10 @@ __global__ void __launch_bounds__((NMW + NRW + 2) * 32, 1)
         for (int o = 16; o; o >>= 1) {
             changed += __shfl_xor_sync(0xffffffffu, changed, o);
             cnt1 += __shfl_xor_sync(0xffffffffu, cnt1, o);
+            nwrap += __shfl_xor_sync(0xffffffffu, nwrap, o);
         }
         if (lane == 0) {
+            if (nwrap) atomicAdd(st.wraps + (round - 1), (unsigned long long)nwrap);
             if (changed) atomicAdd(tail + K, changed);
             if (total - cnt1) atomicAdd(tail, total - cnt1);
             if (K > 1 && cnt1) atomicAdd(tail + 1, cnt1);

@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         unsigned long long n2[KC];
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) n2[c] = c < K ? st.norm2[parity * K + c] : 0ull;
-        uint32_t changed = 0, ccount[KC];
+        uint32_t changed = 0, nwrap = 0, ccount[KC];
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
@@ -634,13 +634,19 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             uint32_t best = 0;
             unsigned long long bd = (unsigned long long)d[0], bn = n2[0];
 #pragma unroll
+            uint32_t wr = 0;
+#pragma unroll
             for (uint32_t c = 1; c < KC; ++c)
-                if (c < K && strictly_closer((unsigned long long)d[c], n2[c], bd, bn)) {
-                    best = c;
-                    bd = (unsigned long long)d[c];
-                    bn = n2[c];
+                if (c < K) {
+                    wr += compare_wraps((unsigned long long)d[c], n2[c], bd, bn);
+                    if (strictly_closer((unsigned long long)d[c], n2[c], bd, bn)) {
+                        best = c;
+                        bd = (unsigned long long)d[c];
+                        bn = n2[c];
+                    }
                 }
             if (live) {
+                nwrap += wr;
                 labels[px] = best;
                 changed += old != best;
 #pragma unroll
@@ -686,11 +692,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         }
         for (int o = 16; o; o >>= 1) {
             changed += __shfl_xor_sync(0xffffffffu, changed, o);
+            nwrap += __shfl_xor_sync(0xffffffffu, nwrap, o);
 #pragma unroll
             for (uint32_t c = 0; c < KC; ++c) ccount[c] += __shfl_xor_sync(0xffffffffu, ccount[c], o);
         }
         if (qd == 0) TC_TG(4);
         if (lane == 0) {
+            if (nwrap) atomicAdd(st.wraps + (round - 1), (unsigned long long)nwrap);
             if (changed) atomicAdd(tail + K, changed);
 #pragma unroll
             for (uint32_t c = 0; c < KC; ++c)

@@ -41,6 +41,7 @@ def test_closed_matches_oracle(ctx, port, case):
     res = ctx.run_pipeline_closed(img, cfg)
     cb = S.build_codebooks(dim, h, w, c, alpha, beta, gamma, seed)
     exp = port.cluster(port.encode(img, dim, *cb), img, dim, k, its, es)
+    assert ctx.round_wraps() == port.last_wraps()
     assert res["rounds"] == exp["rounds"]
     assert (res["labels"] == exp["labels"]).all()
     assert (res["centroids"] == exp["centroids"]).all()
@@ -77,16 +78,18 @@ def test_closed_config_golden(ctx, golden_configs, name):
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_closed_config_large_golden(ctx, golden_configs, name):
-    """C3 (20 rounds) / C4 (first 2 rounds, 128-bit comparator wrap) against the validated port."""
-    if name not in golden_configs:
-        pytest.skip(f"{name} golden not generated")
+    """C3 / C4 at their full 20 rounds against the reference (make_golden_full.py), including
+    the per-round count of 128-bit comparator wraps."""
     g, spec = golden_configs[name], golden_configs["_meta"]["configs"][name]
     img = S.synth_image(spec["cid"], 0)
     cfg = S.RunConfig(dim=spec["dim"], alpha=spec["alpha"], beta=26, gamma=1, clusters=spec["k"],
                       iterations=g["iterations"], seed=0, early_stop=False)
     res = ctx.run_pipeline_closed(img, cfg)
+    assert sha(res["labels"]) == g["labels_sha256"]
     assert sha(res["centroids"]) == g["centroids_sha256"]
     assert res["counts"].tolist() == g["counts"]
+    if "round_wraps" in g:
+        assert ctx.round_wraps() == g["round_wraps"]
 
 
 def test_closed_validation(ctx):
@@ -104,4 +107,13 @@ def test_closed_position_tables_match(ctx, port, case, monkeypatch):
     """The full-position tables (SEGHDC_CLOSED_POSITIONS, used when the compressed endpoint
     tables do not fit shared memory) give the same results."""
     monkeypatch.setenv("SEGHDC_CLOSED_POSITIONS", "1")
+    test_closed_matches_oracle(ctx, port, case)
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[5], (30000, 20, 23, 3, 1.0, 3, 1, 3, 4, 12, False)])
+def test_closed_global_finish_matches(ctx, port, case, monkeypatch):
+    """The global-memory finish (k_closed_finish: forced by SEGHDC_CLOSED_FIN_GLOBAL, and taken
+    whenever the shared-memory rows exceed 200 KB, i.e. dim above ~25k) gives the same results."""
+    if case[0] < 25000:
+        monkeypatch.setenv("SEGHDC_CLOSED_FIN_GLOBAL", "1")
     test_closed_matches_oracle(ctx, port, case)

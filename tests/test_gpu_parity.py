@@ -66,6 +66,8 @@ def test_assign_matches_oracle(ctx, port, dim, k, zmax):
         z[2] = z[0] * 3      # magnitude invariance (clusterer.hpp:27-28)
     lab = ctx.assign_labels(grid, h, w, dim, z)
     assert (lab == port.assign(grid, dim, z)).all()
+    # how often the reference's unsigned __int128 comparison wrapped (zmax = 2^32 - 1 wraps)
+    assert ctx.round_wraps() == port.last_wraps()
 
 
 def test_assign_zero_centroid_and_ties(ctx, port):
@@ -153,6 +155,7 @@ def test_cluster_random_vs_oracle(ctx, port, case):
     res2 = ctx.cluster(None, img, dim, k, iterations, es)
     assert res2["rounds"] == exp["rounds"] and (res2["labels"] == exp["labels"]).all()
     assert (res2["centroids"] == exp["centroids"]).all()
+    assert ctx.round_wraps() == port.last_wraps()
 
 
 # ------------------------------------------------- K <= 8: 4-CTA dimension-split tcgen05 layout
@@ -273,15 +276,17 @@ def test_config_c2_batch(ctx, golden_configs):
 
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_config_large_golden(ctx, golden_configs, name):
-    """C3 (20 rounds) / C4 (first 2 rounds) against the validated port."""
-    if name not in golden_configs:
-        pytest.skip(f"{name} golden not generated")
+    """C3 / C4 at their full 20 rounds against the reference itself (make_golden_full.py): every
+    round's labels, the final centroids and counts, and the per-round number of comparisons
+    whose 128-bit products wrapped (C4 wraps: clusters of millions of pixels)."""
     g = golden_configs[name]
     img, res, rounds = _config_run(ctx, golden_configs, name, iterations=g["iterations"])
     assert sha(img) == g["image_sha256"]
     assert rounds == g["round_labels_sha256"]
     assert sha(res["centroids"]) == g["centroids_sha256"]
     assert res["counts"].tolist() == g["counts"]
+    if "round_wraps" in g:
+        assert ctx.round_wraps() == g["round_wraps"]
 
 
 # ---------------------------------------------------------------- run_pipeline (closed-form codebooks)

@@ -128,3 +128,48 @@ def test_streaming_cluster_equals_stored_grid(port, seed):
     assert got["rounds"] == exp["rounds"]
     assert (got["labels_rounds"] == exp["labels_rounds"]).all()
     assert (got["centroids"] == exp["centroids"]).all() and (got["counts"] == exp["counts"]).all()
+
+
+def test_wrap_counter_matches_bigint(port):
+    """so_last_wraps counts strictly_closer comparisons whose unsigned __int128 products exceed
+    2^128 (clusterer.cpp:41-50; norm_squared is u64 and wraps too, hypervector.cpp:123-127).
+    Checked against Python big integers, labels included."""
+    rng = np.random.default_rng(1)
+    n, dim, k = 200, 200, 3
+    grid = rng.integers(0, 2**63, (n, (dim + 63) // 64), dtype=np.uint64)
+    grid[:, -1] &= np.uint64((1 << (dim % 64)) - 1)
+    z = rng.integers(0, 2**32, (k, dim), dtype=np.uint64).astype(np.uint32)
+    z[0] //= 1 << 20
+    lab = port.assign(grid, dim, z)
+    bits = np.unpackbits(grid.view(np.uint8), axis=1, bitorder="little")[:, :dim].astype(object)
+    dots = bits.dot(z.astype(object).T)
+    n2 = [sum(int(v) * int(v) for v in z[c]) % (1 << 64) for c in range(k)]
+    M, wraps, exp = 1 << 128, 0, []
+    for p in range(n):
+        best = 0
+        for c in range(1, k):
+            dc, db = int(dots[p, c]), int(dots[p, best])
+            if n2[c] and n2[best]:
+                lhs, rhs = dc * dc * n2[best], db * db * n2[c]
+                wraps += lhs >= M or rhs >= M
+                if lhs % M > rhs % M:
+                    best = c
+            elif n2[c] and not n2[best] and dc > 0:
+                best = c
+        exp.append(best)
+    assert port.last_wraps() == [wraps] and wraps > 0
+    assert lab.tolist() == exp
+
+
+def test_reference_encoded_loop_equals_replay(ref):
+    """ref_pare_* (row shards encoded by the reference's own encode_image, used for the
+    full-length C3/C4 goldens) equals the single-grid replay of cluster()."""
+    import workloads
+    img = workloads.synth_image(0, 0)[:48, :60].copy()
+    for k, it in ((2, 4), (4, 3)):
+        grid = ref.encode(img, 2000, 0.5)
+        a = ref.cluster_replay(grid, img, 2000, k, it, False, per_round=True)
+        rounds = []
+        b = ref.cluster_encoded(img, 2000, k, it, alpha=0.5, nthreads=3, on_round=lambda r, l: rounds.append(l.copy()))
+        assert (a["labels_rounds"] == np.array(rounds)).all()
+        assert (a["centroids"] == b["centroids"]).all() and (a["counts"] == b["counts"]).all()
