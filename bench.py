@@ -286,13 +286,16 @@ def main():
     ctx.load_image(img)
     ctx.load_codebooks(dim, *cb)
     if sharded:
-        from paper_2303_12753_b200.sharded import cluster_row_sharded, nccl_allreduce, row_ranges
-        r0, r1 = row_ranges(h, world)[rank]
-        ar = nccl_allreduce()
+        # the library's own sharded loop: one ncclAllReduce per round inside the C-ABI, on the
+        # context's stream (rank 0's NCCL unique id reaches the others through torch.distributed)
+        uid = [S.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], rank, world)
+        r0, r1 = S.shard_rows(h, rank, world)
 
         def step():
             ctx.encode_async(r0, r1)
-            cluster_row_sharded([ctx], k, iters, False, ar)
+            ctx.cluster_sharded_async(k, iters, False)
         n_local = (r1 - r0) * w
     elif batch:
         # the rank's images stay resident in HBM; a step loads each one (D2D), encodes and
@@ -383,46 +386,52 @@ def main():
         achieved *= len(profs)
 
     # ---- end to end through the reference-facing C-ABI call with host buffers
-    e2e = None
-    if not sharded:
-        pin_imgs = [torch.from_numpy(synth_image(spec["cid"], i)).pin_memory().numpy() for i in img_ids]
-        cfg = S.RunConfig(dim=dim, alpha=spec["alpha"], beta=BETA, gamma=GAMMA, clusters=k, iterations=iters,
-                          seed=CB_SEED, early_stop=False)
-        for _ in range(2):
-            ctx.run_pipeline(pin_imgs[0], cfg)
-        if world > 1:
-            torch.distributed.barrier()
-        e2e_steps = max(3, min(args.steps, 10 if batch else 50))
-        if batch:  # one host thread per context: the synchronous calls of the groups overlap
-            from concurrent.futures import ThreadPoolExecutor
-            pool = ThreadPoolExecutor(len(groups))
+    # (pageable numpy images, as a C++ caller's std::vector: the library stages them through its
+    # own page-locked buffers; codebook bases on the host, H2D, device work, D2H labels)
+    host_imgs = [synth_image(spec["cid"], i) for i in img_ids]
+    cfg = S.RunConfig(dim=dim, alpha=spec["alpha"], beta=BETA, gamma=GAMMA, clusters=k, iterations=iters,
+                      seed=CB_SEED, early_stop=False)
+    call = (lambda im: ctx.run_pipeline_sharded(im, cfg)) if sharded else (lambda im: ctx.run_pipeline(im, cfg))
+    for _ in range(3):  # eager run, CUDA-graph capture, replay
+        call(host_imgs[0])
+    if batch:  # one host thread per context: the synchronous calls of the groups overlap
+        from concurrent.futures import ThreadPoolExecutor
+        pool = ThreadPoolExecutor(len(groups))
 
-            def run_group(j):
-                return [(i, groups[j].run_pipeline(pin_imgs[i], cfg)) for i in range(j, len(pin_imgs), len(groups))]
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            if batch:
-                res = [r for _, r in sorted(x for part in pool.map(run_group, range(len(groups))) for x in part)]
-            else:
-                res = [ctx.run_pipeline(pi, cfg) for pi in pin_imgs]
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dt = float(t.item())
-        wph = (dim + 63) // 64
-        # per image: the image + the Manhattan codebook bases (tables expand on the device)
-        h2d = len(pin_imgs) * (img.nbytes + (2 + c) * wph * 8)
-        d2h = len(pin_imgs) * h * w * 4
-        e2e = {"value": h * w * len(pin_imgs) * iters * world * e2e_steps / dt, "unit": "px·iter/s",
-               "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "timer": "host wall clock around the synchronous seghdc_run_pipeline "
-                                                  "(codebook bases on the host + H2D image/bases + device codebooks + "
-                                                  "encode + cluster + D2H labels into page-locked memory)",
-               "steps": e2e_steps}
-        labels_sha = hashlib.sha256(b"".join(r.mask.astype(np.uint32).tobytes() for r in res)).hexdigest()[:16]
-    else:
+        def run_group(j):
+            return [(i, groups[j].run_pipeline(host_imgs[i], cfg)) for i in range(j, len(host_imgs), len(groups))]
+        for _ in range(2):
+            pool.map(run_group, range(len(groups)))
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_steps = max(3, min(args.steps, 10 if batch else 50))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if batch:
+            res = [r for _, r in sorted(x for part in pool.map(run_group, range(len(groups))) for x in part)]
+        else:
+            res = [call(im) for im in host_imgs]
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    wph = (dim + 63) // 64
+    # per image: the image + the Manhattan codebook bases (tables expand on the device); back:
+    # this rank's labels (+ the centroids for the sharded call)
+    h2d = len(host_imgs) * (img.nbytes + (2 + c) * wph * 8)
+    d2h = len(host_imgs) * n_local // len(img_ids) * 4 + (k * dim * 4 if sharded else 0)
+    px_e2e = h * w if sharded else h * w * len(host_imgs) * world
+    e2e = {"value": px_e2e * iters * e2e_steps / dt, "unit": "px·iter/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h,
+           "timer": "host wall clock around the synchronous seghdc_run_pipeline%s (pageable host image; codebook "
+                    "bases on the host + H2D image/bases + one CUDA graph: device codebooks, encode, seeds, rounds%s "
+                    "+ D2H labels)" % ("_sharded" if sharded else "", ", ncclAllReduce per round" if sharded else ""),
+           "steps": e2e_steps}
+    if sharded:
         labels_sha = None
+    else:
+        labels_sha = hashlib.sha256(b"".join(r.mask.astype(np.uint32).tobytes() for r in res)).hexdigest()[:16]
 
     if rank != 0:
         if world > 1:

@@ -172,6 +172,41 @@ int seghdc_shard_assign(seghdc_ctx* ctx, size_t round);
 int seghdc_shard_round_needs_exchange(const seghdc_ctx* ctx, size_t round);
 int seghdc_shard_finish(seghdc_ctx* ctx, size_t round);
 
+/* ---- multi-GPU with the collective inside the library (one process per GPU) ----------- */
+/* Row-block sharding of one image: rank r of n owns the contiguous pixel rows
+ * seghdc_shard_rows(h, r, n) and the full image; seeds are selected redundantly on every rank;
+ * the only collective is one SUM all-reduce (int32) per round of the exchange buffer. Integer
+ * sums are order independent: every rank ends with bit-identical centroids and its rows'
+ * labels equal the single-GPU run's. The reference is single-threaded (clusterer.cpp:190-218
+ * is the loop being sharded); these calls have no reference counterpart.
+ *
+ * Collective, one of:
+ *  - NCCL (NVLink / NVSwitch): rank 0 calls seghdc_nccl_get_unique_id, ships the 128 bytes to
+ *    the other ranks out of band, every rank calls seghdc_nccl_init. libnccl.so.2 is loaded
+ *    at run time (no link-time dependency).
+ *  - any other (MPI, gloo, host-staged): seghdc_set_allreduce with a callback that leaves
+ *    device_buf[0..n) equal to the SUM over ranks, ordered on (or synchronising) cuda_stream;
+ *    it returns 0 on success. */
+#define SEGHDC_NCCL_UNIQUE_ID_BYTES 128
+typedef int (*seghdc_allreduce_fn)(void* user, int32_t* device_buf, size_t n_int32, void* cuda_stream);
+int seghdc_nccl_get_unique_id(void* id_out /* SEGHDC_NCCL_UNIQUE_ID_BYTES */);
+int seghdc_nccl_init(seghdc_ctx* ctx, const void* unique_id, int rank, int nranks);
+int seghdc_set_allreduce(seghdc_ctx* ctx, seghdc_allreduce_fn fn, void* user, int rank, int nranks);
+/* rows [row_begin, row_end) of rank `rank`: contiguous blocks differing by at most one row */
+int seghdc_shard_rows(size_t h, int rank, int nranks, size_t* row_begin, size_t* row_end);
+/* cluster() over this rank's resident rows (seghdc_load_image + seghdc_load_codebooks +
+ * seghdc_encode_async(row_begin, row_end) first); no host synchronisation; results through
+ * seghdc_fetch_results (labels of this rank's rows). */
+int seghdc_cluster_sharded_async(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop);
+/* run_pipeline (pipeline.cpp:40-75) sharded: every rank passes the full image; labels_out
+ * receives this rank's rows (seghdc_shard_rows), centroids_out / counts_out (nullable) the
+ * final centroid set, identical on every rank. */
+int seghdc_run_pipeline_sharded(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c,
+                                size_t dim, double alpha, size_t beta, size_t gamma, size_t k,
+                                size_t iterations, uint64_t seed, int encoder, int early_stop,
+                                uint32_t* labels_out, uint32_t* centroids_out, uint64_t* counts_out,
+                                size_t* rounds_out, double* timings_ms_out);
+
 /* ---- measurement -------------------------------------------------------------------- */
 /* Bracket every round kernel (the dominant kernel) with CUDA events on the context's stream;
  * profile_read synchronises and returns the summed kernel time and launch count since the

@@ -80,6 +80,14 @@ SIGNATURES = {
     "seghdc_shard_assign": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_round_needs_exchange": ([C.c_void_p, _sz], C.c_int),
     "seghdc_shard_finish": ([C.c_void_p, _sz], C.c_int),
+    "seghdc_nccl_get_unique_id": ([C.c_void_p], C.c_int),
+    "seghdc_nccl_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "seghdc_set_allreduce": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "seghdc_shard_rows": ([_sz, C.c_int, C.c_int, C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
+    "seghdc_cluster_sharded_async": ([C.c_void_p, _sz, _sz, C.c_int], C.c_int),
+    "seghdc_run_pipeline_sharded": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64,
+                                     C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz), C.c_void_p],
+                                    C.c_int),
     "seghdc_round_wraps": ([C.c_void_p, C.c_void_p, _sz, C.POINTER(_sz)], C.c_int),
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
@@ -175,6 +183,24 @@ def pinned_empty(shape, dtype=np.uint32) -> np.ndarray:
     raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(max(nbytes, 1),))
     weakref.finalize(raw.base, _return_pinned, nbytes, ptr)
     return raw[:nbytes].view(dtype).reshape(shape)
+
+
+# (user, device int32 buffer, n, cudaStream_t) -> 0 on success: seghdc_allreduce_fn
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, _sz, C.c_void_p)
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0), to be shipped to the other ranks out of band."""
+    buf = C.create_string_buffer(128)
+    _check(lib().seghdc_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def shard_rows(h: int, rank: int, nranks: int) -> tuple[int, int]:
+    """Rows [r0, r1) of rank ``rank``: contiguous blocks differing by at most one row."""
+    r0, r1 = _sz(), _sz()
+    _check(lib().seghdc_shard_rows(h, rank, nranks, C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
 
 
 def synth_image(config_id: int, seed: int = 0) -> np.ndarray:
@@ -403,6 +429,55 @@ class Context:
                                               None if z is None else z.ctypes.data, counts.ctypes.data,
                                               C.byref(rounds)))
         return {"labels": lab, "centroids": z, "counts": counts, "rounds": rounds.value}
+
+    # ---- row-block sharding with the collective inside the library -------------------------
+    def nccl_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        """NCCL communicator for this rank (seghdc_nccl_init); the sharded calls then all-reduce
+        the exchange buffer with ncclAllReduce on the context's stream."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self.check(lib().seghdc_nccl_init(self.h, buf, rank, nranks))
+        self.rank, self.nranks = rank, nranks
+
+    def set_allreduce(self, fn: Optional[Callable[[int, int, int], None]], rank: int, nranks: int) -> None:
+        """Any other collective: ``fn(device_ptr, n_int32, cuda_stream)`` must leave the int32
+        buffer equal to the SUM over ranks (seghdc_set_allreduce). ``fn=None`` clears it."""
+        if fn is None:
+            self._ar_cb = None
+            self.check(lib().seghdc_set_allreduce(self.h, None, None, rank, nranks))
+        else:
+            def _cb(_user, ptr, n, stream):
+                try:
+                    fn(int(ptr), int(n), int(stream or 0))
+                    return 0
+                except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            self._ar_cb = ALLREDUCE_FN(_cb)  # keep alive while the context may call it
+            self.check(lib().seghdc_set_allreduce(self.h, C.cast(self._ar_cb, C.c_void_p), None, rank, nranks))
+        self.rank, self.nranks = rank, nranks
+
+    def cluster_sharded_async(self, k: int, iterations: int, early_stop: bool = False) -> None:
+        self.check(lib().seghdc_cluster_sharded_async(self.h, k, iterations, int(early_stop)))
+
+    def run_pipeline_sharded(self, img: np.ndarray, config: "RunConfig") -> dict:
+        """run_pipeline over this rank's rows (seghdc_run_pipeline_sharded): labels of rows
+        shard_rows(h, rank, nranks), and the final centroids/counts (identical on every rank)."""
+        img = _img3(img)
+        h, w, c = img.shape
+        r0, r1 = shard_rows(h, getattr(self, "rank", 0), getattr(self, "nranks", 1))
+        labels = np.empty((r1 - r0) * w, np.uint32)
+        cents = np.empty((config.clusters, config.dim), np.uint32)
+        counts = np.empty(config.clusters, np.uint64)
+        rounds = _sz(0)
+        timings = (C.c_double * 5)()
+        self.check(lib().seghdc_run_pipeline_sharded(
+            self.h, img, h, w, c, config.dim, float(config.alpha), config.beta, config.gamma, config.clusters,
+            config.iterations, config.seed, ENCODERS[config.encoder], int(config.early_stop), labels.ctypes.data,
+            cents.ctypes.data, counts.ctypes.data, C.byref(rounds), C.cast(timings, C.c_void_p)))
+        names = ("encode_position", "encode_color", "produce_pixels", "cluster", "total")
+        return {"labels": labels, "rows": (r0, r1), "centroids": cents, "counts": counts, "rounds": rounds.value,
+                "timings": dict(zip(names, list(timings)))}
 
     # ---- row-block sharding: the caller all-reduces exchange_buffer() -------------------
     def shard_begin(self, k: int, iterations: int, early_stop: bool = False) -> None:

@@ -1,8 +1,11 @@
 // C-ABI of the SegHDC B200 hot path (include/seghdc_cuda.h): device context, resident buffers,
 // the round schedule and the reference-API entry points. No exception crosses the boundary.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the symbols are resolved at run time (nccl_api below)
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -46,6 +49,10 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error(SEGHDC_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// bumped whenever any device buffer is (re)allocated: a captured CUDA graph bakes in device
+// pointers, so a graph recorded under an older epoch is re-captured (seghdc_run_pipeline)
+std::atomic<uint64_t> g_realloc_epoch{0};
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -64,11 +71,83 @@ struct DevBuf {
             n = 0;
             ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
             n = count;
+            g_realloc_epoch.fetch_add(1);
             if (zero) ck(cudaMemset(p, 0, count * sizeof(T)), "cudaMemset");
         }
     }
     size_t bytes() const { return n * sizeof(T); }
 };
+
+// NCCL, resolved with dlopen("libnccl.so.2") on first use: the library has no link-time NCCL
+// dependency, and a process that already loaded one (torch's bundled NCCL) shares that copy.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    std::string err;
+};
+
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            a.err = std::string("cannot load libnccl.so.2: ") + (e ? e : "unknown error");
+            return a;
+        }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!a.get_unique_id || !a.comm_init_rank || !a.all_reduce || !a.comm_destroy || !a.error_string)
+            a.err = "libnccl.so.2 lacks ncclGetUniqueId / ncclCommInitRank / ncclAllReduce / ncclCommDestroy";
+        return a;
+    }();
+    if (!api.err.empty()) throw Error(SEGHDC_ERUNTIME, api.err);
+    return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(SEGHDC_ERUNTIME, std::string(what) + ": " + nccl_api().error_string(r));
+}
+
+// page-locked host staging (grow-only): pageable caller buffers pass through it, so every
+// host<->device copy of the pipeline runs as a true async DMA at PCIe rate
+struct PinnedBuf {
+    uint8_t* p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    uint8_t* ensure(size_t bytes) {
+        if (bytes > n) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            n = 0;
+            ck(cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocPortable), "cudaHostAlloc");
+            n = bytes;
+        }
+        return p;
+    }
+};
+
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
 
 struct Geometry {
     uint32_t D = 0, W32 = 0, S32 = 0, SS = 0, nwarp_words = 0, W32P = 0, Dp = 0;
@@ -141,11 +220,29 @@ struct seghdc_ctx {
         DevBuf<uint8_t> bf;
     } cf;
     int exchange_phase = 0;  // 0: rounds, 1: init (includes colsums)
+    // row-block sharding across ranks (seghdc_nccl_init / seghdc_set_allreduce): this rank's
+    // collective for the per-round SUM all-reduce of the exchange buffer
+    int rank = 0, nranks = 1;
+    ncclComm_t nccl_comm = nullptr;
+    seghdc_allreduce_fn ar_fn = nullptr;
+    void* ar_user = nullptr;
     // per-round counts of 128-bit-wrapping comparisons of the last clustering run (diagnostic):
     // the packed path keeps them behind its round state, the closed-form variant in wraps_hist
     DevBuf<unsigned long long> wraps_hist;
     const unsigned long long* wraps_src = nullptr;
     size_t wraps_rounds = 0;
+    // run_pipeline: staging buffers, stage events (created once) and the CUDA graph of the
+    // device part (codebook expansion, encode, seeds, every round) for the last signature
+    PinnedBuf stage_in, stage_out;
+    cudaEvent_t stage_ev[3] = {nullptr, nullptr, nullptr};
+    struct Graph {
+        std::vector<uint64_t> sig;
+        uint64_t epoch = 0;
+        int seen = 0;  // eager runs with this signature (capture on the second)
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;
+        bool failed = false;
+    } graph;
     // optional CUDA-event timing of every round kernel (bench.py's roofline)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -212,13 +309,21 @@ void load_codebooks(seghdc_ctx& x, size_t dim, size_t h, size_t w, size_t c, con
 
 // Manhattan codebooks from their bases: only (2 + C) HVs cross PCIe, the tables are expanded
 // on the device (k_expand_codebooks); same tables as load_codebooks of the host-built ones.
-void load_codebooks_closed(seghdc_ctx& x, const seghdc_host::ManhattanParams& p, const uint64_t* bases) {
+void upload_bases(seghdc_ctx& x, const seghdc_host::ManhattanParams& p, const uint64_t* bases) {
     const size_t wph = (p.dim + 63) / 64, wref = 2 * wph;
     x.row.ensure(size_t(p.h) * wref);
     x.col.ensure(size_t(p.w) * wref);
     x.wid.ensure(size_t(p.c) * 256 * wref);
     x.cb_bases.ensure((2 + p.c) * wph);
     ck(cudaMemcpyAsync(x.cb_bases.p, bases, (2 + p.c) * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload bases");
+    x.cb_dim = p.dim;
+    x.cb_h = p.h;
+    x.cb_w = p.w;
+    x.cb_c = p.c;
+}
+
+void expand_codebooks(seghdc_ctx& x, const seghdc_host::ManhattanParams& p) {
+    const size_t wph = (p.dim + 63) / 64, wref = 2 * wph;
     ExpandArgs a{};
     a.dim = p.dim;
     a.h = p.h;
@@ -235,10 +340,6 @@ void load_codebooks_closed(seghdc_ctx& x, const seghdc_host::ManhattanParams& p,
     launch_expand_codebooks(reinterpret_cast<const uint32_t*>(x.cb_bases.p), a, x.row.p, x.col.p, x.wid.p, x.stream);
     x.count();
     x.check_launch();
-    x.cb_dim = p.dim;
-    x.cb_h = p.h;
-    x.cb_w = p.w;
-    x.cb_c = p.c;
 }
 
 void set_grid_shape(seghdc_ctx& x, size_t h, size_t w, size_t dim, size_t r0, size_t r1) {
@@ -603,10 +704,228 @@ void fetch(seghdc_ctx& x, uint32_t* labels, uint32_t* centroids, uint64_t* count
         for (size_t c = 0; c < x.K; ++c) counts[c] = h.cur[h.hdr.rounds_run & 1][c];
 }
 
+// ---- row-block sharding with the collective inside the library ---------------------------------
+// rank r of n owns rows [r0, r1): contiguous blocks, sizes differing by at most one row
+void shard_rows(size_t h, int rank, int nranks, size_t& r0, size_t& r1) {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "shard: rank out of range");
+    require(size_t(nranks) <= h, "shard: more ranks than image rows");
+    const size_t base = h / size_t(nranks), extra = h % size_t(nranks), r = size_t(rank);
+    r0 = r * base + std::min(r, extra);
+    r1 = r0 + base + (r < extra ? 1 : 0);
+}
+
+// SUM all-reduce of the current exchange buffer ([K*Dp sums | K counts | changed], plus the
+// column sums at init) over the ranks, ordered on the context's stream
+void allreduce_exchange(seghdc_ctx& x) {
+    const size_t n = x.xchg_round_ints() + (x.exchange_phase == 1 ? x.g.Dp : 0);
+    if (x.nccl_comm) {
+        nck(nccl_api().all_reduce(x.xchg.p, x.xchg.p, n, ncclInt32, ncclSum, x.nccl_comm, x.stream), "ncclAllReduce");
+    } else if (x.ar_fn) {
+        if (x.ar_fn(x.ar_user, x.xchg.p, n, x.stream) != 0) throw Error(SEGHDC_ERUNTIME, "all-reduce callback failed");
+    } else {
+        require(x.nranks == 1, "sharded clustering needs a collective (seghdc_nccl_init or seghdc_set_allreduce)");
+    }
+}
+
+// cluster() (clusterer.cpp:190-218) over this rank's rows: the seeds come from the full image
+// on every rank (no communication), the only exchange is one all-reduce per round. Integer
+// sums are order independent, so every rank finalises bit-identical centroids and the labels
+// equal the single-GPU run's. No host synchronisation.
+void cluster_sharded(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
+    size_t r0, r1;
+    shard_rows(x.h, x.rank, x.nranks, r0, r1);
+    require(x.grid_valid && x.row_begin == r0 && x.row_end == r1 && x.g_h == x.h,
+            "sharded cluster: the resident grid must hold exactly this rank's rows (seghdc_shard_rows)");
+    cluster_begin(x, K, iterations, early_stop);
+    allreduce_exchange(x);
+    init_finish(x);
+    for (uint32_t r = 1; r <= iterations; ++r) {
+        round_assign(x, r);
+        if (r < iterations) {
+            allreduce_exchange(x);
+            finish(x, 0, r);
+        }
+    }
+}
+
 void cluster_full(seghdc_ctx& x, size_t K, size_t iterations, int early_stop, seghdc_round_cb cb, void* user) {
     cluster_begin(x, K, iterations, early_stop);
     init_finish(x);
     run_rounds(x, cb, user);
+}
+
+// ---- run_pipeline (pipeline.cpp:40-75) ---------------------------------------------------------
+struct PipelineCall {
+    const uint8_t* pixels;
+    size_t h, w, c, dim;
+    double alpha;
+    size_t beta, gamma, k, iterations;
+    uint64_t seed;
+    int encoder, early_stop;
+};
+
+// The device part of the pipeline, everything between the input upload and the result
+// download: codebook expansion (Manhattan), encode of rows [r0, r1), seeds, every round.
+// capturing: the stage events become event-record nodes of the graph (cudaEventRecordExternal)
+void pipeline_device(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::ManhattanParams* mp, size_t r0,
+                     size_t r1, bool sharded, seghdc_round_cb cb, void* user, bool capturing) {
+    auto stamp = [&](int i) {
+        ck(capturing ? cudaEventRecordWithFlags(x.stage_ev[i], x.stream, cudaEventRecordExternal)
+                     : cudaEventRecord(x.stage_ev[i], x.stream),
+           "event");
+    };
+    if (mp) expand_codebooks(x, *mp);
+    stamp(0);
+    encode_rows(x, r0, r1);
+    stamp(1);
+    if (sharded)
+        cluster_sharded(x, pc.k, pc.iterations, pc.early_stop);
+    else
+        cluster_full(x, pc.k, pc.iterations, pc.early_stop, cb, user);
+    stamp(2);
+}
+
+// run_pipeline: validation and codebooks on the host (one Rng, position then colour), then the
+// device part. Without a per-round callback the device part is one CUDA graph per call
+// signature (captured on the second call with the same shapes, replayed afterwards); inputs
+// and labels cross PCIe through page-locked staging when the caller's buffers are pageable.
+void run_pipeline_impl(seghdc_ctx& x, const PipelineCall& pc, seghdc_round_cb cb, void* user, uint32_t* labels_out,
+                       uint32_t* centroids_out, uint64_t* counts_out, size_t* rounds_out, double* timings,
+                       bool sharded) {
+    using Clock = std::chrono::steady_clock;
+    auto ms = [](Clock::time_point t0) { return std::chrono::duration<double, std::milli>(Clock::now() - t0).count(); };
+    const size_t h = pc.h, w = pc.w, c = pc.c, dim = pc.dim;
+    // RunConfig::validate before any work (pipeline.cpp:25-30, 42)
+    seghdc_host::validate_image(h, w, c);
+    seghdc_host::validate_position(dim, h, w, pc.alpha, pc.beta);
+    seghdc_host::validate_color(dim, c, pc.gamma);
+    seghdc_host::validate_cluster(pc.k, pc.iterations, h * w);
+    size_t r0 = 0, r1 = h;
+    if (sharded) shard_rows(h, x.rank, x.nranks, r0, r1);
+    const auto t_total = Clock::now();
+    const size_t wph = (dim + 63) / 64, img_bytes = h * w * c;
+    const bool manhattan = pc.encoder == SEGHDC_ENCODER_MANHATTAN;
+    for (auto& e : x.stage_ev)
+        if (!e) ck(cudaEventCreate(&e), "event");
+    std::mt19937_64 rng(pc.seed);  // one stream: position codebook, then colour (pipeline.cpp:43-59)
+    double t_pos = 0, t_col = 0;
+    // inputs: the image (and the Manhattan bases) staged together, one H2D each
+    const size_t nb = manhattan ? (2 + c) * wph : 0;
+    const bool px_pinned = is_pinned(pc.pixels);
+    uint8_t* stage = x.stage_in.ensure((px_pinned ? 0 : (img_bytes + 7) / 8 * 8) + nb * 8);
+    uint64_t* bases = reinterpret_cast<uint64_t*>(stage + (px_pinned ? 0 : (img_bytes + 7) / 8 * 8));
+    ck(cudaStreamSynchronize(x.stream), "sync");  // the staging buffer is free (previous call's copies done)
+    seghdc_host::ManhattanParams mp{};
+    if (manhattan) {  // closed form: bases on the host, tables expanded on the device
+        auto t = Clock::now();
+        mp = seghdc_host::manhattan_bases(dim, h, w, c, pc.alpha, pc.beta, pc.gamma, rng, bases);
+        t_pos = ms(t);
+    }
+    const uint8_t* src = pc.pixels;
+    if (!px_pinned) {
+        std::memcpy(stage, pc.pixels, img_bytes);
+        src = stage;
+    }
+    load_image(x, src, h, w, c);
+    if (manhattan) {
+        upload_bases(x, mp, bases);
+    } else {
+        std::vector<uint64_t> row(h * wph), col(w * wph), wid(c * 256 * wph);
+        auto t = Clock::now();
+        seghdc_host::build_position(dim, h, w, pc.alpha, pc.beta, pc.encoder, rng, row.data(), col.data());
+        t_pos = ms(t);
+        t = Clock::now();
+        seghdc_host::build_color(dim, c, pc.gamma, pc.encoder, rng, wid.data());
+        t_col = ms(t);
+        load_codebooks(x, dim, h, w, c, row.data(), col.data(), wid.data());
+        ck(cudaStreamSynchronize(x.stream), "sync");  // the host tables go out of scope
+    }
+    // the device part: eager, or one graph launch
+    static const char* ge = getenv("SEGHDC_GRAPH");
+    // (a host-staged all-reduce callback synchronises, so it cannot live inside a graph)
+    const bool graphs = !cb && !x.ar_fn && !(ge && *ge == '0');
+    std::vector<uint64_t> sig = {h, w, c, dim, pc.k, pc.iterations, uint64_t(pc.encoder), uint64_t(pc.early_stop),
+                                 r0, r1, uint64_t(sharded), uint64_t(x.sms), uint64_t(x.nranks),
+                                 reinterpret_cast<uint64_t>(x.nccl_comm), reinterpret_cast<uint64_t>(x.ar_fn)};
+    if (manhattan)
+        for (uint64_t v : {uint64_t(mp.beta), uint64_t(mp.x_row), uint64_t(mp.x_col), uint64_t(mp.off[1]),
+                           uint64_t(mp.off[2]), uint64_t(mp.unit[0]), uint64_t(mp.unit[1]), uint64_t(mp.unit[2])})
+            sig.push_back(v);
+    auto& G = x.graph;
+    const bool same = G.sig == sig && G.epoch == g_realloc_epoch.load();
+    if (!same) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        G = {};
+        G.sig = sig;
+        G.epoch = g_realloc_epoch.load();
+    }
+    bool ran = false;
+    if (graphs && G.exec) {
+        ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
+        x.count(G.launches);
+        ran = true;
+    } else if (graphs && G.seen >= 1 && !G.failed) {
+        // capture the device part (every buffer is already allocated by the eager run)
+        const uint64_t l0 = x.launches;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamBeginCapture(x.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                pipeline_device(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, nullptr, nullptr, true);
+            } catch (const Error&) {
+                ok = false;
+            }
+            ok = (cudaStreamEndCapture(x.stream, &graph) == cudaSuccess) && ok && graph;
+        }
+        if (ok && g_realloc_epoch.load() == G.epoch &&
+            cudaGraphInstantiateWithFlags(&G.exec, graph, 0) == cudaSuccess) {
+            G.launches = x.launches - l0;
+            x.launches = l0;
+        } else {
+            G.exec = nullptr;
+            G.failed = true;
+            x.launches = l0;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();  // a failed capture leaves a sticky-free error; clear it
+        if (G.exec) {
+            ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
+            x.count(G.launches);
+            ran = true;
+        }
+    }
+    if (!ran) {
+        pipeline_device(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, cb, user, false);
+        G.seen++;
+    }
+    // results: labels (this rank's rows) + round state, through the staging buffer unless the
+    // caller's label buffer is page-locked
+    const size_t n_loc = (r1 - r0) * w, sbytes = StateView::bytes(uint32_t(pc.k));
+    const bool lab_pinned = labels_out && is_pinned(labels_out);
+    uint8_t* out = x.stage_out.ensure(sbytes + (lab_pinned || !labels_out ? 0 : n_loc * 4));
+    if (labels_out)
+        ck(cudaMemcpyAsync(lab_pinned ? static_cast<void*>(labels_out) : static_cast<void*>(out + sbytes), x.labels.p,
+                           n_loc * 4, cudaMemcpyDeviceToHost, x.stream),
+           "download labels");
+    ck(cudaMemcpyAsync(out, x.state.p, sbytes, cudaMemcpyDeviceToHost, x.stream), "read state");
+    if (centroids_out)
+        ck(cudaMemcpyAsync(centroids_out, x.Z.p, pc.k * dim * 4, cudaMemcpyDeviceToHost, x.stream), "download centroids");
+    ck(cudaStreamSynchronize(x.stream), "sync");
+    if (labels_out && !lab_pinned) std::memcpy(labels_out, out + sbytes, n_loc * 4);
+    const StateView v = StateView::at(out, uint32_t(pc.k));
+    if (rounds_out) *rounds_out = v.hdr->rounds_run;
+    if (counts_out)
+        for (size_t q = 0; q < pc.k; ++q) counts_out[q] = v.cur[size_t(v.hdr->rounds_run & 1) * pc.k + q];
+    if (timings) {
+        float enc_ms = 0, clu_ms = 0;
+        cudaEventElapsedTime(&enc_ms, x.stage_ev[0], x.stage_ev[1]);
+        cudaEventElapsedTime(&clu_ms, x.stage_ev[1], x.stage_ev[2]);
+        timings[0] = t_pos;
+        timings[1] = t_col;
+        timings[2] = enc_ms;
+        timings[3] = clu_ms;
+        timings[4] = ms(t_total);
+    }
 }
 
 }  // namespace
@@ -642,6 +961,10 @@ void seghdc_destroy(seghdc_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->nccl_comm) nccl_api().comm_destroy(ctx->nccl_comm);
+    if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
+    for (auto& e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ctx->prof_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -831,60 +1154,66 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
                         int early_stop, seghdc_round_cb on_round, void* user, uint32_t* labels_out, size_t* rounds_out,
                         double* timings) {
     return guarded(ctx, [&] {
-        using Clock = std::chrono::steady_clock;
-        auto ms = [](Clock::time_point t0) {
-            return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
-        };
-        // RunConfig::validate before any work (pipeline.cpp:25-30, 42)
-        seghdc_host::validate_image(h, w, c);
-        seghdc_host::validate_position(dim, h, w, alpha, beta);
-        seghdc_host::validate_color(dim, c, gamma);
-        seghdc_host::validate_cluster(k, iterations, h * w);
-        const auto t_total = Clock::now();
-        const size_t wph = (dim + 63) / 64;
-        std::mt19937_64 rng(seed);  // one stream: position codebook, then colour (pipeline.cpp:43-59)
-        double t_pos = 0, t_col = 0;
-        cudaEvent_t e0, e1, e2;
-        ck(cudaEventCreate(&e0), "event");
-        ck(cudaEventCreate(&e1), "event");
-        ck(cudaEventCreate(&e2), "event");
-        load_image(*ctx, pixels, h, w, c);
-        if (encoder == SEGHDC_ENCODER_MANHATTAN) {  // closed form: bases on the host, tables on the device
-            std::vector<uint64_t> bases((2 + c) * wph);
-            auto t = Clock::now();
-            const auto p = seghdc_host::manhattan_bases(dim, h, w, c, alpha, beta, gamma, rng, bases.data());
-            t_pos = ms(t);
-            load_codebooks_closed(*ctx, p, bases.data());
-        } else {
-            std::vector<uint64_t> row(h * wph), col(w * wph), wid(c * 256 * wph);
-            auto t = Clock::now();
-            seghdc_host::build_position(dim, h, w, alpha, beta, encoder, rng, row.data(), col.data());
-            t_pos = ms(t);
-            t = Clock::now();
-            seghdc_host::build_color(dim, c, gamma, encoder, rng, wid.data());
-            t_col = ms(t);
-            load_codebooks(*ctx, dim, h, w, c, row.data(), col.data(), wid.data());
-            ck(cudaStreamSynchronize(ctx->stream), "sync");  // the host tables go out of scope
+        PipelineCall pc{pixels, h, w, c, dim, alpha, beta, gamma, k, iterations, seed, encoder, early_stop};
+        run_pipeline_impl(*ctx, pc, on_round, user, labels_out, nullptr, nullptr, rounds_out, timings, false);
+    });
+}
+
+int seghdc_nccl_get_unique_id(void* id_out) {
+    return guarded(nullptr, [&] {
+        require(id_out != nullptr, "nccl_get_unique_id: null output");
+        nck(nccl_api().get_unique_id(static_cast<ncclUniqueId*>(id_out)), "ncclGetUniqueId");
+    });
+}
+
+int seghdc_nccl_init(seghdc_ctx* ctx, const void* unique_id, int rank, int nranks) {
+    return guarded(ctx, [&] {
+        require(unique_id != nullptr, "nccl_init: null unique id");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "nccl_init: rank out of range");
+        if (ctx->nccl_comm) {
+            nccl_api().comm_destroy(ctx->nccl_comm);
+            ctx->nccl_comm = nullptr;
         }
-        ck(cudaEventRecord(e0, ctx->stream), "event");
-        encode_rows(*ctx, 0, h);
-        ck(cudaEventRecord(e1, ctx->stream), "event");
-        cluster_full(*ctx, k, iterations, early_stop, on_round, user);
-        ck(cudaEventRecord(e2, ctx->stream), "event");
-        fetch(*ctx, labels_out, nullptr, nullptr, rounds_out);
-        float enc_ms = 0, clu_ms = 0;
-        cudaEventElapsedTime(&enc_ms, e0, e1);
-        cudaEventElapsedTime(&clu_ms, e1, e2);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaEventDestroy(e2);
-        if (timings) {
-            timings[0] = t_pos;
-            timings[1] = t_col;
-            timings[2] = enc_ms;
-            timings[3] = clu_ms;
-            timings[4] = ms(t_total);
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        nck(nccl_api().comm_init_rank(&ctx->nccl_comm, nranks, id, rank), "ncclCommInitRank");
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        ctx->ar_fn = nullptr;
+        ctx->ar_user = nullptr;
+    });
+}
+
+int seghdc_set_allreduce(seghdc_ctx* ctx, seghdc_allreduce_fn fn, void* user, int rank, int nranks) {
+    return guarded(ctx, [&] {
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "set_allreduce: rank out of range");
+        if (ctx->nccl_comm) {
+            nccl_api().comm_destroy(ctx->nccl_comm);
+            ctx->nccl_comm = nullptr;
         }
+        ctx->ar_fn = fn;
+        ctx->ar_user = user;
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+    });
+}
+
+int seghdc_shard_rows(size_t h, int rank, int nranks, size_t* row_begin, size_t* row_end) {
+    return guarded(nullptr, [&] { shard_rows(h, rank, nranks, *row_begin, *row_end); });
+}
+
+int seghdc_cluster_sharded_async(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop) {
+    return guarded(ctx, [&] { cluster_sharded(*ctx, k, iterations, early_stop); });
+}
+
+int seghdc_run_pipeline_sharded(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t w, size_t c, size_t dim,
+                                double alpha, size_t beta, size_t gamma, size_t k, size_t iterations, uint64_t seed,
+                                int encoder, int early_stop, uint32_t* labels_out, uint32_t* centroids_out,
+                                uint64_t* counts_out, size_t* rounds_out, double* timings_ms_out) {
+    return guarded(ctx, [&] {
+        PipelineCall pc{pixels, h, w, c, dim, alpha, beta, gamma, k, iterations, seed, encoder, early_stop};
+        run_pipeline_impl(*ctx, pc, nullptr, nullptr, labels_out, centroids_out, counts_out, rounds_out, timings_ms_out,
+                          true);
     });
 }
 

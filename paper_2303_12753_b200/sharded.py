@@ -72,30 +72,69 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False), "version": 3}
 
 
+def _sum_local(ctxs: Sequence[Context]) -> np.ndarray:
+    """Exchange buffers of this process's shards, summed on the host (int32 wraps exactly like
+    the device's u32 arithmetic)."""
+    total = None
+    for c in ctxs:
+        buf = c.exchange_download()
+        total = buf.copy() if total is None else (total + buf).astype(np.int32)
+    return total
+
+
 def nccl_allreduce(group=None) -> Callable[[Sequence[Context]], None]:
-    """torch.distributed all-reduce (SUM) of the exchange buffer, on the context's stream
-    (set it to torch's current stream with Context.set_stream first)."""
+    """torch.distributed all-reduce (SUM) of the exchange buffer. One shard per process (the
+    normal case): zero-copy on the context's buffer, on its stream (set it to torch's current
+    stream with Context.set_stream first). Several shards in one process: their buffers are
+    summed locally first, all-reduced once, and the total written back to every shard, so the
+    result is the SUM over all shards of all ranks."""
     import torch
     import torch.distributed as dist
 
     def _ar(ctxs: Sequence[Context]) -> None:
-        for c in ctxs:
+        if len(ctxs) == 1:
+            c = ctxs[0]
             ptr, n = c.exchange_buffer()
             t = torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{c.device}")
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            return
+        total = torch.from_numpy(_sum_local(ctxs)).to(f"cuda:{ctxs[0].device}")
+        dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+        host = total.cpu().numpy()
+        for c in ctxs:
+            c.exchange_upload(host)
 
     return _ar
 
 
 def gloo_allreduce(group=None) -> Callable[[Sequence[Context]], None]:
-    """Host-staged all-reduce over a CPU process group (gloo)."""
+    """Host-staged all-reduce over a CPU process group (gloo); local shards summed first."""
     import torch
     import torch.distributed as dist
 
     def _ar(ctxs: Sequence[Context]) -> None:
+        buf = torch.from_numpy(_sum_local(ctxs))
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         for c in ctxs:
-            buf = torch.from_numpy(c.exchange_download())
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
             c.exchange_upload(buf.numpy())
 
     return _ar
+
+
+def gloo_collective(group=None) -> Callable[[int, int, int], None]:
+    """A seghdc_allreduce_fn for Context.set_allreduce: the library's own sharded loop
+    (seghdc_run_pipeline_sharded / seghdc_cluster_sharded_async) with a host-staged gloo
+    all-reduce — device buffer to host, SUM over the CPU process group, back to the device."""
+    import torch
+    import torch.distributed as dist
+
+    def _fn(ptr: int, n: int, stream: int) -> None:
+        dev = torch.cuda.current_device()
+        t = torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{dev}")
+        torch.cuda.synchronize(dev)  # the context's stream produced the buffer
+        host = t.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(host)
+        torch.cuda.synchronize(dev)
+
+    return _fn
