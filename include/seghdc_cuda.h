@@ -64,7 +64,11 @@ const char* seghdc_round_kernel(const seghdc_ctx* ctx);
  * (clusterer.cpp:41-50) whose unsigned __int128 products exceeded 2^128 in the last clustering
  * run of ctx (seghdc_cluster / _async / run_pipeline / run_pipeline_closed / assign; a shard
  * counts its own pixels). The result is still the reference's wrapped comparison; this only
- * reports how often it happened. Copies min(rounds, cap) counts; rounds_out = rounds run. */
+ * reports how often it happened. Copies min(rounds, cap) counts; rounds_out = rounds run.
+ * Counting is opt-in (seghdc_set_wrap_counting before the run): on the largest images it
+ * selects round-kernel variants that carry the extra arithmetic (about 5-10% at C4); labels
+ * and centroids are identical either way. */
+int seghdc_set_wrap_counting(seghdc_ctx* ctx, int enable);
 int seghdc_round_wraps(seghdc_ctx* ctx, uint64_t* out, size_t cap, size_t* rounds_out);
 
 /* ---- host-side codebooks (stay on the host: mt19937_64 is sequential and cheap) -------- */

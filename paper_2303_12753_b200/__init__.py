@@ -88,6 +88,7 @@ SIGNATURES = {
     "seghdc_run_pipeline_sharded": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64,
                                      C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz), C.c_void_p],
                                     C.c_int),
+    "seghdc_set_wrap_counting": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_round_wraps": ([C.c_void_p, C.c_void_p, _sz, C.POINTER(_sz)], C.c_int),
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
@@ -108,6 +109,8 @@ def lib() -> C.CDLL:
                                  "(python -m paper_2303_12753_b200.build)")
         L = C.CDLL(LIB_PATH)
         for name, (argtypes, restype) in SIGNATURES.items():
+            if os.environ.get("SEGHDC_LIB") and not hasattr(L, name):
+                continue  # a diagnostic / older build selected for an A/B run
             f = getattr(L, name)
             f.argtypes = argtypes
             f.restype = restype
@@ -262,6 +265,10 @@ class Context:
     def round_kernel(self) -> str:
         """Round kernel of the current clustering plan (k_round_tc / k_round_fused / k_round)."""
         return lib().seghdc_round_kernel(self.h).decode()
+
+    def set_wrap_counting(self, enable: bool) -> None:
+        """Opt in to counting 128-bit comparator wraps (seghdc_set_wrap_counting)."""
+        self.check(lib().seghdc_set_wrap_counting(self.h, int(enable)))
 
     def round_wraps(self) -> list:
         """Per-round count of 128-bit-wrapping strictly_closer comparisons in the last clustering

@@ -50,15 +50,20 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra: lis
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + PUBLIC_HEADERS + [__file__]
     if not force and not _stale(out, deps):
         return out
-    objs = []
-    logs = []
-    for src in srcs:
+    def compile_one(src):
         obj = out + "." + os.path.basename(src) + ".o"
         cmd = [nvcc()] + ARCH + NVCC_FLAGS + extra + ["-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [nvcc()] + ARCH + ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-x", "c++",
                                      "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 1))) as pool:  # one nvcc per source
+        results = list(pool.map(compile_one, srcs))
+    objs, logs = [], []
+    for src, obj, r in results:
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

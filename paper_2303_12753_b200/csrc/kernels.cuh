@@ -98,6 +98,26 @@ __device__ __forceinline__ uint32_t compare_wraps(unsigned long long dc, unsigne
     return (prod_wraps(dc, n2b) || prod_wraps(db, n2c)) ? 1u : 0u;
 }
 
+// Can any comparison of this centroid set wrap? A pixel HV has at most D ones, so
+// dot_c^2 <= n2_c * D (Cauchy-Schwarz) and every product is below n2max^2 * D. False for every
+// configuration but the largest (C4), so the round kernels count wraps only when it is true.
+__device__ __forceinline__ bool wraps_possible(const unsigned long long* n2, uint32_t K, uint32_t D) {
+    int b = 0;
+    for (uint32_t c = 0; c < K; ++c) b = max(b, 64 - __clzll(n2[c]));
+    return 2 * b + (32 - __clz(D)) > 128;
+}
+// the argmax's comparison sequence replayed (clusterer.cpp:149-157), counting wrapped ones;
+// out of line so the epilogues it is called from keep their registers
+template <uint32_t KC>
+__device__ __noinline__ uint32_t count_wraps_seq(const long long (&d)[KC], const unsigned long long (&n2)[KC], uint32_t K) {
+    uint32_t best = 0, w = 0;
+    for (uint32_t c = 1; c < KC && c < K; ++c) {
+        w += compare_wraps((unsigned long long)d[c], n2[c], (unsigned long long)d[best], n2[best]);
+        if (strictly_closer((unsigned long long)d[c], n2[c], (unsigned long long)d[best], n2[best])) best = c;
+    }
+    return w;
+}
+
 // ------------------------------------------------------------------------------------------
 // Harley-Seal bit-sliced counter: 32 independent counters (one per bit of a 32-bit word
 // column), count = ones + 2 twos + 4 fours + 8 eights + sum_m 16*2^m hi[m].

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -231,6 +232,8 @@ struct seghdc_ctx {
     DevBuf<unsigned long long> wraps_hist;
     const unsigned long long* wraps_src = nullptr;
     size_t wraps_rounds = 0;
+    bool assign_vmax_wraps = false;  // seghdc_assign with caller centroids large enough to wrap
+    bool count_wraps = false;        // seghdc_set_wrap_counting: the tcgen05 kernels' counting variant
     // run_pipeline: staging buffers, stage events (created once) and the CUDA graph of the
     // device part (codebook expansion, encode, seeds, every round) for the last signature
     PinnedBuf stage_in, stage_out;
@@ -611,6 +614,13 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
         // smem ring (N = 32, 72); SEGHDC_PF overrides
         static const char* pe = getenv("SEGHDC_PF");
         a.pf = pe ? uint32_t(atoi(pe)) : (x.plan.tc && tc_ncol(uint32_t(x.K), x.g.W32) != 16 ? 8u : 0u);
+    }
+    // entries are member sums <= the image's pixel count n, so norm2 <= D n^2 and every
+    // cross product of strictly_closer is below D^3 n^4: no wrap possible under 2^128
+    {
+        const double n_img = double(x.g_h) * double(x.g_w), D = double(x.g.D);
+        a.wraps = x.count_wraps &&
+                  (std::log2(D) * 3 + std::log2(std::max(n_img, 1.0)) * 4 >= 127.0 || x.assign_vmax_wraps);
     }
     a.flist = use_flist ? x.flist.p : nullptr;
     a.flist_count = use_flist ? x.flist.p + (x.K - 1) * x.n_local() : nullptr;
@@ -1003,8 +1013,13 @@ int seghdc_synchronize(seghdc_ctx* ctx) {
 
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int seghdc_set_wrap_counting(seghdc_ctx* ctx, int enable) {
+    return guarded(ctx, [&] { ctx->count_wraps = enable != 0; });
+}
+
 int seghdc_round_wraps(seghdc_ctx* ctx, uint64_t* out, size_t cap, size_t* rounds_out) {
     return guarded(ctx, [&] {
+        require(ctx->count_wraps, "wrap counting is off: enable it with seghdc_set_wrap_counting before the run");
         require(ctx->wraps_src != nullptr, "no clustering run on this context yet");
         size_t rounds = ctx->wraps_rounds;
         const bool packed = ctx->K && ctx->state.p && ctx->wraps_src == StateView::at(ctx->state.p, uint32_t(ctx->K)).wraps;
@@ -1083,6 +1098,8 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         ctx->iterations = 1;
         ctx->early_stop = 0;
         alloc_cluster(*ctx, k, std::max<uint64_t>(zmax, 1));
+        // caller centroids are arbitrary u32: dot^2 * norm2 <= (D zmax)^2 * D zmax^2 = D^3 zmax^4
+        ctx->assign_vmax_wraps = std::log2(double(dim)) * 3 + std::log2(std::max(double(zmax), 1.0)) * 4 >= 127.0;
         ck(cudaMemcpyAsync(ctx->Z.p, centroids, k * dim * 4, cudaMemcpyHostToDevice, ctx->stream), "upload centroids");
         ck(cudaMemsetAsync(ctx->state.p, 0, StateView::bytes(uint32_t(k), 1), ctx->stream), "clear state");
         ctx->wraps_src = StateView::at(ctx->state.p, uint32_t(k)).wraps;
@@ -1092,6 +1109,7 @@ int seghdc_assign(seghdc_ctx* ctx, const uint64_t* grid, size_t h, size_t w, siz
         ck(cudaMemcpyAsync(labels_out, ctx->labels.p, ctx->n_local() * 4, cudaMemcpyDeviceToHost, ctx->stream),
            "download labels");
         ck(cudaStreamSynchronize(ctx->stream), "sync");
+        ctx->assign_vmax_wraps = false;
     });
 }
 

@@ -311,7 +311,9 @@ void read_trace_tc(void* dst) {
 #define TC_CLK(v) ((void)0)
 #endif
 
-template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT>
+// WR: count 128-bit comparator wraps (diagnostic; instantiated only where the host's bound says
+// a wrap is possible, because the counting costs the split layout registers)
+template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT, bool WR>
 __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
@@ -536,6 +538,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         unsigned long long n2[KC];
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) n2[c] = c < K ? st.norm2[parity * K + c] : 0ull;
+        const bool count_wraps = WR && fin && wraps_possible(n2, K < KC ? K : KC, 32 * W32);
         uint32_t changed = 0, nwrap = 0, ccount[KC];
 #pragma unroll
         for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
@@ -634,19 +637,21 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             uint32_t best = 0;
             unsigned long long bd = (unsigned long long)d[0], bn = n2[0];
 #pragma unroll
-            uint32_t wr = 0;
 #pragma unroll
             for (uint32_t c = 1; c < KC; ++c)
-                if (c < K) {
-                    wr += compare_wraps((unsigned long long)d[c], n2[c], bd, bn);
-                    if (strictly_closer((unsigned long long)d[c], n2[c], bd, bn)) {
-                        best = c;
-                        bd = (unsigned long long)d[c];
-                        bn = n2[c];
-                    }
+                if (c < K && strictly_closer((unsigned long long)d[c], n2[c], bd, bn)) {
+                    best = c;
+                    bd = (unsigned long long)d[c];
+                    bn = n2[c];
                 }
+            if (count_wraps && live) {  // copies: d and n2 themselves stay in registers
+                long long dw[KC];
+                unsigned long long nw[KC];
+#pragma unroll
+                for (uint32_t c = 0; c < KC; ++c) dw[c] = d[c], nw[c] = n2[c];
+                nwrap += count_wraps_seq<KC>(dw, nw, K);
+            }
             if (live) {
-                nwrap += wr;
                 labels[px] = best;
                 changed += old != best;
 #pragma unroll
@@ -1121,10 +1126,10 @@ __global__ void k_tc_stamp(int ev) {
     g_trace_tc[(size_t(blockIdx.x) * 64 + 61) * 8 + ev] = t_;
 }
 #endif
-template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT = 1>
+template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT = 1, bool WR = false>
 cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     using Cfg = TcCfg<NCOL, SPLIT>;
-    auto kern = k_round_tc<UPD, H, NCOL, SPLIT>;
+    auto kern = k_round_tc<UPD, H, NCOL, SPLIT, WR>;
     const uint32_t nch = (a.W32 + kCW - 1) / kCW;
     const uint32_t nks = SPLIT > 1 ? (nch + SPLIT - 1) / SPLIT * kKS : a.nks;  // B k-steps resident per CTA
     const size_t smem = TcSmem<NCOL, SPLIT>::total(nks);
@@ -1238,15 +1243,18 @@ void* setup_hang() {
 
 static cudaError_t launch_round_tc_body(const RoundArgs& a, cudaStream_t s) {
     const uint64_t per_cta = ((a.n + a.ctas - 1) / a.ctas + kTP - 1) / kTP * kTP;
+    if (a.wraps) return launch_tc_t<true, 20, 16, 1, true>(a, s);  // only images of millions of pixels
     if (per_cta <= BitCounter<8>::capacity()) return launch_tc_t<true, 8, 16>(a, s);
     if (per_cta <= BitCounter<12>::capacity()) return launch_tc_t<true, 12, 16>(a, s);
     return launch_tc_t<true, 20, 16>(a, s);
 }
 static cudaError_t launch_round_tc_sel(const RoundArgs& a, cudaStream_t s) {
     switch (tc_ncol(a.K, a.W32)) {
-        case 16: return a.K == 2 ? launch_round_tc_body(a, s) : launch_tc_t<false, 1, 16>(a, s);
-        case 32: return launch_tc_t<false, 1, 32>(a, s);
-        case 72: return launch_tc_t<false, 1, 72, 4>(a, s);
+        case 16:
+            if (a.K == 2) return launch_round_tc_body(a, s);
+            return a.wraps ? launch_tc_t<false, 1, 16, 1, true>(a, s) : launch_tc_t<false, 1, 16>(a, s);
+        case 32: return a.wraps ? launch_tc_t<false, 1, 32, 1, true>(a, s) : launch_tc_t<false, 1, 32>(a, s);
+        case 72: return a.wraps ? launch_tc_t<false, 1, 72, 4, true>(a, s) : launch_tc_t<false, 1, 72, 4>(a, s);
         default: return cudaErrorInvalidConfiguration;
     }
 }

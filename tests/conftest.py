@@ -47,6 +47,7 @@ def ctx():
     import paper_2303_12753_b200 as S
 
     c = S.Context(0)
+    c.set_wrap_counting(True)  # the parity tests compare the comparator-wrap counts too
     yield c
     c.close()
 
