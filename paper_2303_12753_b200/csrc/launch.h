@@ -148,7 +148,7 @@ struct ExpandArgs {  // closed-form Manhattan codebooks (seghdc_host::manhattan_
 void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_t* row, uint32_t* col, uint32_t* wid,
                              cudaStream_t s);
 uint64_t tc_max_value(uint32_t K, uint32_t W32);
-uint32_t tc_ncol(uint32_t K, uint32_t W32);  // 16 / 32 (one CTA), 72 (4-CTA dimension split), 0
+uint32_t tc_ncol(uint32_t K, uint32_t W32);  // 16 / 32 (one CTA), 64 (4-CTA dimension split), 0
 // incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of
 // cluster 1's member sums, run1[parity][Dp] the running sums (read p, write p ^ 1)
 // lists: nlists tracked clusters, list l at list + l * max_rows (count[l] entries), folded as

@@ -611,7 +611,7 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;
         // L2 prefetch distance (chunks) for the layouts whose large B image leaves a shallow
-        // smem ring (N = 32, 72); SEGHDC_PF overrides
+        // smem ring (N = 32, 64); SEGHDC_PF overrides
         static const char* pe = getenv("SEGHDC_PF");
         a.pf = pe ? uint32_t(atoi(pe)) : (x.plan.tc && tc_ncol(uint32_t(x.K), x.g.W32) != 16 ? 8u : 0u);
     }

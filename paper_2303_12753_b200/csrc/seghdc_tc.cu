@@ -59,14 +59,18 @@ __device__ __forceinline__ int fold_index(uint32_t warp) {
 // (N columns each), then the (all 1.0) scale factors of A and B
 constexpr uint32_t kTmemCols = 512;
 // Per-layout configuration. N = NDIG digit columns per cluster x KC clusters: 16 (K <= 2) and 32
-// (K <= 4) with 8 digits and the whole B image resident; 72 (K <= 8, 9 digits: entries up to
-// 57.5M, i.e. images of 2^24 pixels) with SPLIT = 4: a cluster of 4 CTAs shares each 128-pixel
+// (K <= 4) with 8 digits and the whole B image resident; 64 (K <= 8, 8 base-9 digits: entries up to
+// 21.5M, i.e. images of 2^24 pixels) with SPLIT = 4: a cluster of 4 CTAs shares each 128-pixel
 // tile, CTA q owning a quarter of the HV dimensions (and only that quarter of the B image), and
 // the partial dots meet in distributed shared memory.
 template <uint32_t NCOL, uint32_t SPLIT = 1>
 struct TcCfg {
     static constexpr uint32_t N = NCOL;
-    static constexpr uint32_t NDIG = NCOL == 72 ? 9 : kP8;
+    // the split layout uses balanced base 9 (digits -4..4: each digit and half-digit is still an
+    // e2m1 value), so 8 digits cover entries up to 4 (9^8 - 1) / 8 = 21.5M (images of 2^24
+    // pixels) with N = 8 x 8 = 64 columns instead of 9 base-8 digits (N = 72)
+    static constexpr uint32_t BASE = SPLIT > 1 ? 9 : 8;
+    static constexpr uint32_t NDIG = kP8;
     static constexpr uint32_t KC = NCOL / NDIG;              // clusters of the layout
     static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
     static constexpr uint32_t AB = SPLIT > 1 ? 2 : 3;        // A buffers in TMEM (128 columns each)
@@ -560,20 +564,22 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 tc_fence_after();
                 if (qd == 0) TC_TR(4, it);
                 if constexpr (SPLIT > 1) {
-                    // 72 columns in 3 groups of 24 (registers: 23 warps share the SM): column
-                    // n = NDIG c + p adds digit_dot * 8^p to dot_c
+                    // 64 columns in 4 groups of 16 (registers: 24 warps share the SM): column
+                    // n = NDIG c + p adds digit_dot * BASE^p to dot_c
 #pragma unroll
                     for (uint32_t c = 0; c < KC; ++c) d[c] = 0;
 #pragma unroll
-                    for (uint32_t grp = 0; grp < NCOL / 24; ++grp) {
-                        uint32_t r24[24];
-#pragma unroll
-                        for (uint32_t q = 0; q < 3; ++q) tc_ld8(lane_addr + kColD + dd * NCOL + 24 * grp + 8 * q, r24 + 8 * q);
+                    for (uint32_t grp = 0; grp < NCOL / 16; ++grp) {
+                        uint32_t r16[16];
+                        tc_ld16(lane_addr + kColD + dd * NCOL + 16 * grp, r16);
                         tc_wait_ld();
 #pragma unroll
-                        for (uint32_t j = 0; j < 24; ++j) {
-                            const uint32_t col = 24 * grp + j, c = col / NDIG, p = col % NDIG;
-                            d[c] += (long long)__float2int_rn(__uint_as_float(r24[j])) * (1ll << (3 * p));
+                        for (uint32_t j = 0; j < 16; ++j) {
+                            const uint32_t col = 16 * grp + j, c = col / NDIG, p = col % NDIG;
+                            long long pw = 1;
+#pragma unroll
+                            for (uint32_t q = 0; q < p; ++q) pw *= Cfg::BASE;
+                            d[c] += (long long)__float2int_rn(__uint_as_float(r16[j])) * pw;
                         }
                     }
                     tc_fence_before();
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #pragma unroll
                         for (uint32_t c16 = 0; c16 < NCOL / 16; ++c16) {
                             tc_ld16(lane_addr + kColD + (NMW * dd + mw) * NCOL + 16 * c16, acc[mw] + 16 * c16);
-                            if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // 72 columns: the last 8
+                            if (NCOL % 16 != 0 && c16 == NCOL / 16 - 1)  // N % 16 == 8: the last 8 columns
                                 tc_ld8(lane_addr + kColD + (NMW * dd + mw) * NCOL + 16 * (c16 + 1), acc[mw] + 16 * (c16 + 1));
                         }
                     tc_wait_ld();
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                             int v = 0;
 #pragma unroll
                             for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][NDIG * c + p]));
-                            d[c] = d[c] * 8 + v;
+                            d[c] = d[c] * Cfg::BASE + v;
                         }
                     }
                 }
@@ -892,35 +898,36 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 // column col = k / 8 = 4h + c, i.e. class c of HV word 2ks + h (header): c = 0 / 2 carry bits
 // 4j+1 / 4j as 1.0, c = 1 / 3 carry bits 4j+2 / 4j+3 as 2.0. Row n = kP8 * cluster + p holds
 // digit p of the centroid entry (weight 1) or half of it (weight 2), so every product is bit * d.
-__device__ __forceinline__ int digit8(long long z, uint32_t p) {  // balanced base 8: [-4, 3]
+// balanced base 8 (digits [-4, 3]) or base 9 (digits [-4, 4])
+__device__ __forceinline__ int digit_b(long long z, uint32_t p, uint32_t base) {
     for (uint32_t q = 0;; ++q) {
-        int r = int(z & 7);
-        if (r >= 4) r -= 8;
+        int r = int(z % base);
+        if (r >= int(base) - 4) r -= int(base);
         if (q == p) return r;
-        z = (z - r) >> 3;
+        z = (z - r) / base;
     }
 }
 __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t ks, uint32_t n,
-                                             uint32_t k, uint32_t ndig) {
+                                             uint32_t k, uint32_t ndig, uint32_t base) {
     const uint32_t col = k >> 3, j = k & 7, h = col >> 2, c = col & 3;
     const uint32_t dim = 32 * (2 * ks + h) + 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
     const uint32_t cl = n / ndig, p = n % ndig;
     if (cl >= K || dim >= D) return 0;
-    const int d = digit8((long long)Z[size_t(cl) * D + dim], p);
+    const int d = digit_b((long long)Z[size_t(cl) * D + dim], p, base);
     const uint32_t a = uint32_t(d < 0 ? -d : d);
     // weight 1: |d| in 0..4 -> e2m1 {0, 1, 2, 3, 4}; weight 2: |d|/2 in {0, .5, 1, 1.5, 2}
     const uint32_t code = (c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u);
     return code | (d < 0 ? 8u : 0u);
 }
 __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
-                             uint32_t ndig, uint8_t* __restrict__ bimg, const void* state) {
+                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
     const uint32_t total = nks * kb;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t ks = i / kb, rem = i % kb;
         const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
         const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
-        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k, ndig) | (b_nibble(Z, K, D, ks, n, k + 1, ndig) << 4));
+        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k, ndig, base) | (b_nibble(Z, K, D, ks, n, k + 1, ndig, base) << 4));
     }
 }
 
@@ -1179,7 +1186,7 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
 }  // namespace
 
 // Layout of the tcgen05 kernel for (K, W32): N = 16 digit columns (K <= 2) or 32 (K <= 4) with
-// the whole B image resident in one CTA; N = 72 (K <= 8, 9 digits) split over a cluster of 4
+// the whole B image resident in one CTA; N = 64 (K <= 8, 8 base-9 digits) split over a cluster of 4
 // CTAs when the whole image does not fit; 0: no tcgen05 layout (IMMA kernels).
 constexpr size_t kSmemOptin = 232448;  // B200: 227 KB of dynamic shared memory per CTA
 static uint32_t tc_nchunks(uint32_t W32) { return (W32 + kCW - 1) / kCW; }
@@ -1188,22 +1195,26 @@ uint32_t tc_ncol(uint32_t K, uint32_t W32) {
     if (K < 1 || W32 <= kCW) return 0;
     if (K <= 2 && W32 <= 3 * kNRW * 32 && TcSmem<16>::total(nks) <= kSmemOptin) return 16;
     if (K <= 4 && TcSmem<32>::total(nks) <= kSmemOptin) return 32;
-    if (K <= 8 && nch >= 4 && TcSmem<72, 4>::total((nch + 3) / 4 * kKS) <= kSmemOptin) return 72;
+    if (K <= 8 && nch >= 4 && TcSmem<64, 4>::total((nch + 3) / 4 * kKS) <= kSmemOptin) return 64;
     return 0;
 }
 bool tc_supported(uint32_t K, uint32_t W32) { return tc_ncol(K, W32) != 0; }
-static uint32_t tc_ndig(uint32_t ncol) { return ncol == 72 ? TcCfg<72, 4>::NDIG : kP8; }
-// largest centroid entry the layout's balanced base-8 digits represent: 3 (8^ndig - 1) / 7
+static uint32_t tc_ndig(uint32_t ncol) { return ncol == 64 ? TcCfg<64, 4>::NDIG : kP8; }
+static uint32_t tc_base(uint32_t ncol) { return ncol == 64 ? TcCfg<64, 4>::BASE : 8u; }
+// largest centroid entry the layout's balanced digits represent: 3 (8^ndig - 1) / 7 in base 8,
+// 4 (9^ndig - 1) / 8 in base 9
 uint64_t tc_max_value(uint32_t K, uint32_t W32) {
-    const uint32_t nd = tc_ndig(tc_ncol(K, W32));
-    return 3ull * ((1ull << (3 * nd)) - 1) / 7;
+    const uint32_t nc = tc_ncol(K, W32), nd = tc_ndig(nc), b = tc_base(nc);
+    uint64_t pw = 1;
+    for (uint32_t q = 0; q < nd; ++q) pw *= b;
+    return (b / 2 - (b % 2 == 0 ? 1 : 0)) * (pw - 1) / (b - 1);
 }
 uint32_t tc_ksteps(uint32_t W32) { return tc_nchunks(W32) * kKS; }
 size_t tc_smem_bytes(uint32_t K, uint32_t W32) {
     const uint32_t nc = tc_ncol(K, W32), nch = tc_nchunks(W32);
     return nc == 16 ? TcSmem<16>::total(tc_ksteps(W32))
          : nc == 32 ? TcSmem<32>::total(tc_ksteps(W32))
-         : nc == 72 ? TcSmem<72, 4>::total((nch + 3) / 4 * kKS)
+         : nc == 64 ? TcSmem<64, 4>::total((nch + 3) / 4 * kKS)
                     : ~size_t(0);
 }
 size_t tc_bimg_bytes(uint32_t K, uint32_t W32) { return size_t(tc_ksteps(W32)) * tc_ncol(K, W32) * 32; }
@@ -1226,7 +1237,7 @@ void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, 
                        cudaStream_t s) {
     const uint32_t nc = tc_ncol(K, W32), nks = tc_ksteps(W32), kb = nc * 32;
     const uint32_t total = nks * kb;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), bimg, state);
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state);
 }
 
 #ifdef SEGHDC_HANGDBG
@@ -1254,7 +1265,7 @@ static cudaError_t launch_round_tc_sel(const RoundArgs& a, cudaStream_t s) {
             if (a.K == 2) return launch_round_tc_body(a, s);
             return a.wraps ? launch_tc_t<false, 1, 16, 1, true>(a, s) : launch_tc_t<false, 1, 16>(a, s);
         case 32: return a.wraps ? launch_tc_t<false, 1, 32, 1, true>(a, s) : launch_tc_t<false, 1, 32>(a, s);
-        case 72: return a.wraps ? launch_tc_t<false, 1, 72, 4, true>(a, s) : launch_tc_t<false, 1, 72, 4>(a, s);
+        case 64: return a.wraps ? launch_tc_t<false, 1, 64, 4, true>(a, s) : launch_tc_t<false, 1, 64, 4>(a, s);
         default: return cudaErrorInvalidConfiguration;
     }
 }
