@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstddef>
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <map>
@@ -250,5 +251,23 @@ struct ClusterResultWithCentroids {
 };
 ClusterResultWithCentroids cluster_with_centroids(const PixelHvGrid& grid, const ImageBuffer& img,
                                                   const ClusterConfig& config, const IterationCallback& on_iteration = {});
+
+// Multi-GPU: row-block sharding of one image, one process (or host thread) per GPU. Rank 0
+// calls nccl_unique_id() and ships the bytes to the other ranks out of band (MPI_Bcast, a
+// file, a socket); every rank calls init_sharding(...) once and then run_pipeline_sharded()
+// with the FULL image. Each rank gets its rows' labels; the centroids are bit-identical on
+// every rank, and the rows of all ranks together equal run_pipeline()'s mask (the only
+// exchange is one NCCL all-reduce per round, clusterer.cpp:190-218 sharded).
+using NcclUniqueId = std::array<std::uint8_t, 128>;
+NcclUniqueId nccl_unique_id();
+void init_sharding(const NcclUniqueId& id, int rank, int nranks);
+struct ShardedPipelineResult {
+    std::size_t row_begin = 0, row_end = 0;  // this rank's rows of the image
+    SegmentationMask rows;                   // (row_end - row_begin) x width labels
+    CentroidSet centroids;                   // the centroid set of the final assignment
+    std::size_t iterations_run = 0;
+    StageTimings timings;
+};
+ShardedPipelineResult run_pipeline_sharded(const ImageBuffer& img, const RunConfig& config);
 
 }  // namespace seghdc

@@ -198,6 +198,8 @@ int seghdc_nccl_init(seghdc_ctx* ctx, const void* unique_id, int rank, int nrank
 int seghdc_set_allreduce(seghdc_ctx* ctx, seghdc_allreduce_fn fn, void* user, int rank, int nranks);
 /* rows [row_begin, row_end) of rank `rank`: contiguous blocks differing by at most one row */
 int seghdc_shard_rows(size_t h, int rank, int nranks, size_t* row_begin, size_t* row_end);
+/* the same for this context's rank (seghdc_nccl_init / seghdc_set_allreduce; 0 of 1 before) */
+int seghdc_shard_row_range(const seghdc_ctx* ctx, size_t h, size_t* row_begin, size_t* row_end);
 /* cluster() over this rank's resident rows (seghdc_load_image + seghdc_load_codebooks +
  * seghdc_encode_async(row_begin, row_end) first); no host synchronisation; results through
  * seghdc_fetch_results (labels of this rank's rows). */

@@ -84,6 +84,7 @@ SIGNATURES = {
     "seghdc_nccl_init": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
     "seghdc_set_allreduce": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
     "seghdc_shard_rows": ([_sz, C.c_int, C.c_int, C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
+    "seghdc_shard_row_range": ([C.c_void_p, _sz, C.POINTER(_sz), C.POINTER(_sz)], C.c_int),
     "seghdc_cluster_sharded_async": ([C.c_void_p, _sz, _sz, C.c_int], C.c_int),
     "seghdc_run_pipeline_sharded": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64,
                                      C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz), C.c_void_p],

@@ -1220,6 +1220,13 @@ int seghdc_shard_rows(size_t h, int rank, int nranks, size_t* row_begin, size_t*
     return guarded(nullptr, [&] { shard_rows(h, rank, nranks, *row_begin, *row_end); });
 }
 
+int seghdc_shard_row_range(const seghdc_ctx* ctx, size_t h, size_t* row_begin, size_t* row_end) {
+    return guarded(nullptr, [&] {
+        require(ctx != nullptr, "shard_row_range: null context");
+        shard_rows(h, ctx->rank, ctx->nranks, *row_begin, *row_end);
+    });
+}
+
 int seghdc_cluster_sharded_async(seghdc_ctx* ctx, size_t k, size_t iterations, int early_stop) {
     return guarded(ctx, [&] { cluster_sharded(*ctx, k, iterations, early_stop); });
 }

@@ -550,4 +550,35 @@ PipelineResult run_pipeline(const ImageBuffer& img, const RunConfig& config, con
     return r;
 }
 
+NcclUniqueId nccl_unique_id() {
+    NcclUniqueId id{};
+    check(seghdc_nccl_get_unique_id(id.data()), nullptr);
+    return id;
+}
+
+void init_sharding(const NcclUniqueId& id, int rank, int nranks) {
+    seghdc_ctx* c = ctx();
+    check(seghdc_nccl_init(c, id.data(), rank, nranks), c);
+}
+
+ShardedPipelineResult run_pipeline_sharded(const ImageBuffer& img, const RunConfig& config) {
+    config.validate(img);
+    seghdc_ctx* c = ctx();
+    ShardedPipelineResult r;
+    const std::size_t k = config.clusters, d = config.dim;
+    std::vector<std::uint32_t> labels(img.pixel_count()), z(k * d);
+    std::vector<std::uint64_t> counts(k);
+    double t[5] = {0, 0, 0, 0, 0};
+    check(seghdc_run_pipeline_sharded(c, img.pixels.data(), img.height, img.width, img.channels, d, config.alpha,
+                                      config.beta, config.gamma, k, config.iterations, config.seed, int(config.encoder),
+                                      config.early_stop, labels.data(), z.data(), counts.data(), &r.iterations_run, t),
+          c);
+    check(seghdc_shard_row_range(c, img.height, &r.row_begin, &r.row_end), c);
+    labels.resize((r.row_end - r.row_begin) * img.width);
+    r.rows = {r.row_end - r.row_begin, img.width, std::move(labels)};
+    r.centroids = unflatten(z, counts, k, d);
+    r.timings = {t[0], t[1], t[2], t[3], t[4]};
+    return r;
+}
+
 }  // namespace seghdc

@@ -1080,9 +1080,9 @@ bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p,
     p.nt = (K * P + 7) / 8;
     p.fused = false;
     p.tc = false;
-    const char* tcenv = getenv("SEGHDC_TC");
-    if (!(tcenv && *tcenv == '0') && tc_supported(K, W32) && tc_smem_bytes(K, W32) <= smem_limit) {
-        // tcgen05 kernel; the IMMA plan below stays valid as the fallback (bfrag layout)
+    if (tc_supported(K, W32) && tc_smem_bytes(K, W32) <= smem_limit) {
+        // tcgen05 kernel. The IMMA plan below is still computed: it serves only the shapes no
+        // tcgen05 layout covers (D <= 1024, K > 8, centroid entries beyond the layout's digits)
         p.tc = true;
     }
     if (p.nt == 1) {

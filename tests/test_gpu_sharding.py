@@ -200,3 +200,19 @@ def test_two_processes_gloo(port, tmp_path):
     for p in parts:
         assert (p["centroids"] == exp["centroids"]).all() and (p["counts"] == exp["counts"]).all()
         assert int(p["rounds"]) == exp["rounds"]
+
+
+def test_cpp_dropin_sharded_pipeline(tmp_path):
+    """A C++ caller of the drop-in's run_pipeline_sharded (NCCL, one rank) against run_pipeline."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2303_12753_b200", "lib")
+    exe = tmp_path / "sharded_pipeline"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "sharded_pipeline.cpp"), "-o", str(exe), "-L", lib,
+                    "-lseghdc_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
+                    "-Wl,-rpath,/usr/local/cuda/lib64"], check=True)
+    out = subprocess.run([str(exe), "96", "130", "3", "3", "5"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
