@@ -122,6 +122,16 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
                         seghdc_round_cb on_round, void* user, uint32_t* labels_out,
                         size_t* rounds_out, double* timings_ms_out);
 
+/* ---- a batch of same-shape images (the reference CLI's `batch`, seghdc_main.cpp:180-225) */
+/* run_pipeline for each of n_images images of one shape and config (one codebook set):
+ * labels_out[i] (h*w u32) and rounds_out[i] (nullable) per image; results identical to n
+ * separate seghdc_run_pipeline calls. Images run side by side on child streams, each with a
+ * share of the SMs (SEGHDC_BATCH_GROUPS, default 4). */
+int seghdc_run_pipeline_batch(seghdc_ctx* ctx, const uint8_t* const* pixels, size_t n_images, size_t h,
+                              size_t w, size_t c, size_t dim, double alpha, size_t beta, size_t gamma,
+                              size_t k, size_t iterations, uint64_t seed, int encoder, int early_stop,
+                              uint32_t* const* labels_out, size_t* rounds_out);
+
 /* ---- closed-form Manhattan variant (SURVEY.md §7 hard part 4, §8f rank 1) ------------ */
 /* run_pipeline (pipeline.cpp:40-75) + cluster (clusterer.cpp:190-218) for the Manhattan
  * encoder without materialising the pixel HVs: each HV is B ^ (2 + C runs of ones), so
@@ -212,6 +222,14 @@ int seghdc_run_pipeline_sharded(seghdc_ctx* ctx, const uint8_t* pixels, size_t h
                                 size_t iterations, uint64_t seed, int encoder, int early_stop,
                                 uint32_t* labels_out, uint32_t* centroids_out, uint64_t* counts_out,
                                 size_t* rounds_out, double* timings_ms_out);
+
+/* ---- scoring (metrics.hpp:22-36, metrics.cpp:42-101; off the throughput path) -------- */
+/* best_foreground_iou: the highest IoU of any non-empty proper subset of the k <= 4 cluster
+ * labels (k = 1: the whole image) against gt_bits (h*w, nonzero = foreground); ties to the
+ * smallest, then lexicographically smallest subset, returned as a bit mask of labels.
+ * SEGHDC_ECONFIG for k = 0 or k > 4 or a label >= k, like the reference's ConfigError. */
+int seghdc_best_foreground_iou(const uint32_t* labels, const uint8_t* gt_bits, size_t h, size_t w, size_t k,
+                               double* iou_out, uint32_t* subset_mask_out);
 
 /* ---- measurement -------------------------------------------------------------------- */
 /* Bracket every round kernel (the dominant kernel) with CUDA events on the context's stream;

@@ -63,6 +63,8 @@ SIGNATURES = {
                         _u32p, C.c_void_p, C.c_void_p, C.POINTER(_sz)], C.c_int),
     "seghdc_run_pipeline": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64, C.c_int,
                              C.c_int, ROUND_CB, C.c_void_p, _u32p, C.POINTER(_sz), C.c_void_p], C.c_int),
+    "seghdc_run_pipeline_batch": ([C.c_void_p, C.c_void_p, _sz, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz,
+                                   C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "seghdc_run_pipeline_closed": ([C.c_void_p, _u8p, _sz, _sz, _sz, _sz, C.c_double, _sz, _sz, _sz, _sz, C.c_uint64,
                                     C.c_int, _u32p, _u32p, _u64p, C.POINTER(_sz)], C.c_int),
     "seghdc_load_image": ([C.c_void_p, C.c_void_p, _sz, _sz, _sz], C.c_int),
@@ -91,6 +93,8 @@ SIGNATURES = {
                                     C.c_int),
     "seghdc_set_wrap_counting": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_round_wraps": ([C.c_void_p, C.c_void_p, _sz, C.POINTER(_sz)], C.c_int),
+    "seghdc_best_foreground_iou": ([_u32p, _u8p, _sz, _sz, _sz, C.POINTER(C.c_double), C.POINTER(C.c_uint32)],
+                                   C.c_int),
     "seghdc_profile_rounds": ([C.c_void_p, C.c_int], C.c_int),
     "seghdc_profile_read": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)], C.c_int),
     "seghdc_profile_read_each": ([C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_void_p, _sz], C.c_int),
@@ -205,6 +209,21 @@ def shard_rows(h: int, rank: int, nranks: int) -> tuple[int, int]:
     r0, r1 = _sz(), _sz()
     _check(lib().seghdc_shard_rows(h, rank, nranks, C.byref(r0), C.byref(r1)))
     return r0.value, r1.value
+
+
+def best_foreground_iou(labels: np.ndarray, gt: np.ndarray, k: int):
+    """best_foreground_iou (metrics.hpp:33-36): (iou, subset of labels) for a mask of cluster
+    labels and a ground truth (nonzero = foreground) of the same shape; k <= 4."""
+    lab = np.ascontiguousarray(labels, np.uint32).ravel()
+    g = (np.ascontiguousarray(gt).reshape(lab.shape[0], -1) != 0).any(axis=1).astype(np.uint8)
+    if g.size != lab.size:
+        raise ConfigError("best_foreground_iou: mask shapes differ")
+    v, m = C.c_double(), C.c_uint32()
+    rc = lib().seghdc_best_foreground_iou(lab, g, 1, lab.size, k, C.byref(v), C.byref(m))
+    if rc == SEGHDC_ECONFIG:
+        raise ConfigError(f"best_foreground_iou: k = {k} must be 1..4 and every label < k")
+    _check(rc)
+    return v.value, [c for c in range(k) if m.value >> c & 1]
 
 
 def synth_image(config_id: int, seed: int = 0) -> np.ndarray:
@@ -381,6 +400,24 @@ class Context:
                                              C.byref(rounds), C.cast(timings, C.c_void_p)))
         names = ("encode_position", "encode_color", "produce_pixels", "cluster", "total")
         return PipelineResult(labels.reshape(h, w), rounds.value, dict(zip(names, list(timings))))
+
+    def run_pipeline_batch(self, imgs, config: "RunConfig"):
+        """run_pipeline over a list of same-shape images in one call (seghdc_run_pipeline_batch):
+        returns (labels[n, h, w], rounds[n])."""
+        imgs = [_img3(i) for i in imgs]
+        h, w, c = imgs[0].shape
+        if any(i.shape != (h, w, c) for i in imgs):
+            raise ConfigError("run_pipeline_batch: images must share one shape")
+        n = len(imgs)
+        labels = pinned_empty((n, h, w), np.uint32)
+        rounds = np.zeros(n, np.uint64)
+        px = (C.c_void_p * n)(*[i.ctypes.data for i in imgs])
+        outs = (C.c_void_p * n)(*[labels[j].ctypes.data for j in range(n)])
+        self.check(lib().seghdc_run_pipeline_batch(self.h, px, n, h, w, c, config.dim, float(config.alpha),
+                                                   config.beta, config.gamma, config.clusters, config.iterations,
+                                                   config.seed, ENCODERS[config.encoder], int(config.early_stop),
+                                                   outs, rounds.ctypes.data))
+        return labels, rounds
 
     def run_pipeline_closed(self, img: np.ndarray, config: "RunConfig") -> dict:
         """Closed-form Manhattan variant of run_pipeline (SURVEY.md §7 hard part 4): the pixel

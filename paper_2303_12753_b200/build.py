@@ -17,10 +17,12 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libseghdc_b200.so")
 
-SOURCES = ["seghdc_kernels.cu", "seghdc_tc.cu", "seghdc_closed.cu", "seghdc_capi.cu", "seghdc_host.cpp", "seghdc_dropin.cpp"]
+SOURCES = ["seghdc_kernels.cu", "seghdc_tc.cu", "seghdc_closed.cu", "seghdc_capi.cu", "seghdc_host.cpp", "seghdc_dropin.cpp",
+           "seghdc_metrics.cpp"]
 HEADERS = ["kernels.cuh", "launch.h", "host_internal.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "seghdc_cuda.h"),
-                  os.path.join(ROOT, "include", "seghdc", "seghdc.hpp")]
+                  os.path.join(ROOT, "include", "seghdc", "seghdc.hpp"),
+                  os.path.join(ROOT, "include", "seghdc", "metrics.hpp")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",

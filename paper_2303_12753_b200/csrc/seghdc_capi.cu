@@ -246,6 +246,8 @@ struct seghdc_ctx {
         uint64_t launches = 0;
         bool failed = false;
     } graph;
+    // seghdc_run_pipeline_batch: child contexts, each on its own stream with a share of the SMs
+    std::vector<seghdc_ctx*> batch;
     // optional CUDA-event timing of every round kernel (bench.py's roofline)
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -795,6 +797,75 @@ void pipeline_device(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::M
     stamp(2);
 }
 
+// The device part of one pipeline call on x's stream: eager on the first call with a given
+// signature, captured into a CUDA graph on the second, replayed from then on.
+void run_device_part(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::ManhattanParams* mpp, size_t r0,
+                     size_t r1, bool sharded, seghdc_round_cb cb, void* user) {
+    const size_t h = pc.h, w = pc.w, c = pc.c, dim = pc.dim;
+    const bool manhattan = mpp != nullptr;
+    const seghdc_host::ManhattanParams mp = mpp ? *mpp : seghdc_host::ManhattanParams{};
+    for (auto& e : x.stage_ev)
+        if (!e) ck(cudaEventCreate(&e), "event");
+    // the device part: eager, or one graph launch
+    static const char* ge = getenv("SEGHDC_GRAPH");
+    // (a host-staged all-reduce callback synchronises, so it cannot live inside a graph)
+    const bool graphs = !cb && !x.ar_fn && !(ge && *ge == '0');
+    std::vector<uint64_t> sig = {h, w, c, dim, pc.k, pc.iterations, uint64_t(pc.encoder), uint64_t(pc.early_stop),
+                                 r0, r1, uint64_t(sharded), uint64_t(x.sms), uint64_t(x.nranks),
+                                 reinterpret_cast<uint64_t>(x.nccl_comm), reinterpret_cast<uint64_t>(x.ar_fn)};
+    if (manhattan)
+        for (uint64_t v : {uint64_t(mp.beta), uint64_t(mp.x_row), uint64_t(mp.x_col), uint64_t(mp.off[1]),
+                           uint64_t(mp.off[2]), uint64_t(mp.unit[0]), uint64_t(mp.unit[1]), uint64_t(mp.unit[2])})
+            sig.push_back(v);
+    auto& G = x.graph;
+    const bool same = G.sig == sig && G.epoch == g_realloc_epoch.load();
+    if (!same) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        G = {};
+        G.sig = sig;
+        G.epoch = g_realloc_epoch.load();
+    }
+    bool ran = false;
+    if (graphs && G.exec) {
+        ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
+        x.count(G.launches);
+        ran = true;
+    } else if (graphs && G.seen >= 1 && !G.failed) {
+        // capture the device part (every buffer is already allocated by the eager run)
+        const uint64_t l0 = x.launches;
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamBeginCapture(x.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                pipeline_device(x, pc, mpp, r0, r1, sharded, nullptr, nullptr, true);
+            } catch (const Error&) {
+                ok = false;
+            }
+            ok = (cudaStreamEndCapture(x.stream, &graph) == cudaSuccess) && ok && graph;
+        }
+        if (ok && g_realloc_epoch.load() == G.epoch &&
+            cudaGraphInstantiateWithFlags(&G.exec, graph, 0) == cudaSuccess) {
+            G.launches = x.launches - l0;
+            x.launches = l0;
+        } else {
+            G.exec = nullptr;
+            G.failed = true;
+            x.launches = l0;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();  // a failed capture leaves a sticky-free error; clear it
+        if (G.exec) {
+            ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
+            x.count(G.launches);
+            ran = true;
+        }
+    }
+    if (!ran) {
+        pipeline_device(x, pc, mpp, r0, r1, sharded, cb, user, false);
+        G.seen++;
+    }
+}
+
 // run_pipeline: validation and codebooks on the host (one Rng, position then colour), then the
 // device part. Without a per-round callback the device part is one CUDA graph per call
 // signature (captured on the second call with the same shapes, replayed afterwards); inputs
@@ -850,64 +921,7 @@ void run_pipeline_impl(seghdc_ctx& x, const PipelineCall& pc, seghdc_round_cb cb
         load_codebooks(x, dim, h, w, c, row.data(), col.data(), wid.data());
         ck(cudaStreamSynchronize(x.stream), "sync");  // the host tables go out of scope
     }
-    // the device part: eager, or one graph launch
-    static const char* ge = getenv("SEGHDC_GRAPH");
-    // (a host-staged all-reduce callback synchronises, so it cannot live inside a graph)
-    const bool graphs = !cb && !x.ar_fn && !(ge && *ge == '0');
-    std::vector<uint64_t> sig = {h, w, c, dim, pc.k, pc.iterations, uint64_t(pc.encoder), uint64_t(pc.early_stop),
-                                 r0, r1, uint64_t(sharded), uint64_t(x.sms), uint64_t(x.nranks),
-                                 reinterpret_cast<uint64_t>(x.nccl_comm), reinterpret_cast<uint64_t>(x.ar_fn)};
-    if (manhattan)
-        for (uint64_t v : {uint64_t(mp.beta), uint64_t(mp.x_row), uint64_t(mp.x_col), uint64_t(mp.off[1]),
-                           uint64_t(mp.off[2]), uint64_t(mp.unit[0]), uint64_t(mp.unit[1]), uint64_t(mp.unit[2])})
-            sig.push_back(v);
-    auto& G = x.graph;
-    const bool same = G.sig == sig && G.epoch == g_realloc_epoch.load();
-    if (!same) {
-        if (G.exec) cudaGraphExecDestroy(G.exec);
-        G = {};
-        G.sig = sig;
-        G.epoch = g_realloc_epoch.load();
-    }
-    bool ran = false;
-    if (graphs && G.exec) {
-        ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
-        x.count(G.launches);
-        ran = true;
-    } else if (graphs && G.seen >= 1 && !G.failed) {
-        // capture the device part (every buffer is already allocated by the eager run)
-        const uint64_t l0 = x.launches;
-        cudaGraph_t graph = nullptr;
-        bool ok = cudaStreamBeginCapture(x.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-        if (ok) {
-            try {
-                pipeline_device(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, nullptr, nullptr, true);
-            } catch (const Error&) {
-                ok = false;
-            }
-            ok = (cudaStreamEndCapture(x.stream, &graph) == cudaSuccess) && ok && graph;
-        }
-        if (ok && g_realloc_epoch.load() == G.epoch &&
-            cudaGraphInstantiateWithFlags(&G.exec, graph, 0) == cudaSuccess) {
-            G.launches = x.launches - l0;
-            x.launches = l0;
-        } else {
-            G.exec = nullptr;
-            G.failed = true;
-            x.launches = l0;
-        }
-        if (graph) cudaGraphDestroy(graph);
-        cudaGetLastError();  // a failed capture leaves a sticky-free error; clear it
-        if (G.exec) {
-            ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
-            x.count(G.launches);
-            ran = true;
-        }
-    }
-    if (!ran) {
-        pipeline_device(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, cb, user, false);
-        G.seen++;
-    }
+    run_device_part(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, cb, user);
     // results: labels (this rank's rows) + round state, through the staging buffer unless the
     // caller's label buffer is page-locked
     const size_t n_loc = (r1 - r0) * w, sbytes = StateView::bytes(uint32_t(pc.k));
@@ -935,6 +949,86 @@ void run_pipeline_impl(seghdc_ctx& x, const PipelineCall& pc, seghdc_round_cb cb
         timings[2] = enc_ms;
         timings[3] = clu_ms;
         timings[4] = ms(t_total);
+    }
+}
+
+// ---- a batch of same-shape images (the reference CLI's `batch`, seghdc_main.cpp:180-225) -------
+// One call runs every image's run_pipeline. The images are dealt round-robin to G child
+// contexts, each on its own stream with 1/G of the SMs, so small images run side by side
+// (a 256 x 256 image has 512 tiles: one full-GPU grid per image would leave the last wave of
+// every round half empty). Each child replays one CUDA graph per image; inputs and labels move
+// through page-locked staging; the host synchronises once, at the end.
+void run_pipeline_batch(seghdc_ctx& x, const uint8_t* const* pixels, size_t n_img, const PipelineCall& pc,
+                        uint32_t* const* labels_out, size_t* rounds_out) {
+    const size_t h = pc.h, w = pc.w, c = pc.c, dim = pc.dim;
+    require(n_img >= 1, "run_pipeline_batch: no images");
+    seghdc_host::validate_image(h, w, c);
+    seghdc_host::validate_position(dim, h, w, pc.alpha, pc.beta);
+    seghdc_host::validate_color(dim, c, pc.gamma);
+    seghdc_host::validate_cluster(pc.k, pc.iterations, h * w);
+    static const char* ge = getenv("SEGHDC_BATCH_GROUPS");
+    const size_t G = std::min<size_t>(n_img, ge ? std::max(1, atoi(ge)) : 4);
+    while (x.batch.size() < G) {
+        seghdc_ctx* child = nullptr;
+        if (seghdc_create(x.device, &child) != SEGHDC_OK) throw Error(SEGHDC_ERUNTIME, seghdc_last_error(nullptr));
+        x.batch.push_back(child);
+    }
+    for (size_t g = 0; g < G; ++g) {
+        x.batch[g]->sms = std::max(1, x.sms / int(G));
+        x.batch[g]->count_wraps = x.count_wraps;
+    }
+    const size_t wph = (dim + 63) / 64, img_bytes = h * w * c, img_slot = (img_bytes + 15) / 16 * 16;
+    const bool manhattan = pc.encoder == SEGHDC_ENCODER_MANHATTAN;
+    const size_t nb = manhattan ? (2 + c) * wph : 0;
+    const size_t n = h * w, sbytes = (StateView::bytes(uint32_t(pc.k)) + 15) / 16 * 16, out_slot = n * 4 + sbytes;
+    for (size_t g = 0; g < G; ++g) ck(cudaStreamSynchronize(x.batch[g]->stream), "sync");  // staging free
+    uint8_t* in = x.stage_in.ensure(n_img * img_slot + nb * 8);
+    uint8_t* out = x.stage_out.ensure(n_img * out_slot);
+    uint64_t* bases = reinterpret_cast<uint64_t*>(in + n_img * img_slot);
+    std::mt19937_64 rng(pc.seed);  // same shape and seed: one codebook set for every image
+    seghdc_host::ManhattanParams mp{};
+    std::vector<uint64_t> row, col, wid;
+    if (manhattan) {
+        mp = seghdc_host::manhattan_bases(dim, h, w, c, pc.alpha, pc.beta, pc.gamma, rng, bases);
+    } else {
+        row.resize(h * wph);
+        col.resize(w * wph);
+        wid.resize(c * 256 * wph);
+        seghdc_host::build_position(dim, h, w, pc.alpha, pc.beta, pc.encoder, rng, row.data(), col.data());
+        seghdc_host::build_color(dim, c, pc.gamma, pc.encoder, rng, wid.data());
+    }
+    for (size_t g = 0; g < G; ++g) {
+        seghdc_ctx& ch = *x.batch[g];
+        ch.use();
+        if (manhattan) {
+            upload_bases(ch, mp, bases);
+        } else {
+            ch.h = h, ch.w = w, ch.c = c;
+            load_codebooks(ch, dim, h, w, c, row.data(), col.data(), wid.data());
+        }
+    }
+    for (size_t i = 0; i < n_img; ++i) {
+        seghdc_ctx& ch = *x.batch[i % G];
+        ch.use();
+        std::memcpy(in + i * img_slot, pixels[i], img_bytes);  // host copy overlaps earlier images' device work
+        load_image(ch, in + i * img_slot, h, w, c);
+        run_device_part(ch, pc, manhattan ? &mp : nullptr, 0, h, false, nullptr, nullptr);
+        uint8_t* o = out + i * out_slot;
+        ck(cudaMemcpyAsync(o, ch.labels.p, n * 4, cudaMemcpyDeviceToHost, ch.stream), "download labels");
+        ck(cudaMemcpyAsync(o + n * 4, ch.state.p, StateView::bytes(uint32_t(pc.k)), cudaMemcpyDeviceToHost, ch.stream),
+           "read state");
+    }
+    for (size_t g = 0; g < G; ++g) {
+        x.batch[g]->use();
+        ck(cudaStreamSynchronize(x.batch[g]->stream), "sync");
+        x.launches += x.batch[g]->launches;
+        x.batch[g]->launches = 0;
+    }
+    x.use();
+    for (size_t i = 0; i < n_img; ++i) {
+        const uint8_t* o = out + i * out_slot;
+        if (labels_out && labels_out[i]) std::memcpy(labels_out[i], o, n * 4);
+        if (rounds_out) rounds_out[i] = StateView::at(const_cast<uint8_t*>(o + n * 4), uint32_t(pc.k)).hdr->rounds_run;
     }
 }
 
@@ -972,6 +1066,7 @@ void seghdc_destroy(seghdc_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     if (ctx->nccl_comm) nccl_api().comm_destroy(ctx->nccl_comm);
+    for (seghdc_ctx* child : ctx->batch) seghdc_destroy(child);
     if (ctx->graph.exec) cudaGraphExecDestroy(ctx->graph.exec);
     for (auto& e : ctx->stage_ev)
         if (e) cudaEventDestroy(e);
@@ -1174,6 +1269,16 @@ int seghdc_run_pipeline(seghdc_ctx* ctx, const uint8_t* pixels, size_t h, size_t
     return guarded(ctx, [&] {
         PipelineCall pc{pixels, h, w, c, dim, alpha, beta, gamma, k, iterations, seed, encoder, early_stop};
         run_pipeline_impl(*ctx, pc, on_round, user, labels_out, nullptr, nullptr, rounds_out, timings, false);
+    });
+}
+
+int seghdc_run_pipeline_batch(seghdc_ctx* ctx, const uint8_t* const* pixels, size_t n_images, size_t h, size_t w,
+                              size_t c, size_t dim, double alpha, size_t beta, size_t gamma, size_t k, size_t iterations,
+                              uint64_t seed, int encoder, int early_stop, uint32_t* const* labels_out,
+                              size_t* rounds_out) {
+    return guarded(ctx, [&] {
+        PipelineCall pc{nullptr, h, w, c, dim, alpha, beta, gamma, k, iterations, seed, encoder, early_stop};
+        run_pipeline_batch(*ctx, pixels, n_images, pc, labels_out, rounds_out);
     });
 }
 

@@ -92,3 +92,33 @@ def test_row_ranges():
     assert row_ranges(4096, 8)[-1] == (3584, 4096)
     with pytest.raises(ValueError):
         row_ranges(2, 3)
+
+
+def test_best_foreground_iou_matches_reference_rules():
+    """best_foreground_iou (metrics.cpp:42-101) through the C-ABI, host-only: the reference
+    suite's cases plus a brute-force comparison with the per-subset definition."""
+    lab = np.array([0, 1, 2, 0, 1, 2], np.uint32)
+    assert S.best_foreground_iou(lab, np.array([0, 1, 1, 0, 1, 1]), 3) == (1.0, [1, 2])
+    v, sub = S.best_foreground_iou(np.array([0, 1], np.uint32), np.array([1, 1]), 2)
+    assert sub == [0] and abs(v - 0.5) < 1e-12  # tie -> smaller label
+    with pytest.raises(S.ConfigError):
+        S.best_foreground_iou(lab, np.ones(6), 5)
+    with pytest.raises(S.ConfigError):
+        S.best_foreground_iou(lab, np.ones(6), 2)  # label 2 out of range
+    rng = np.random.default_rng(0)
+    for t in range(50):
+        k = int(rng.integers(1, 5))
+        n = int(rng.integers(1, 40))
+        l = rng.integers(0, k, n).astype(np.uint32)
+        g = rng.integers(0, 2, n)
+        best = None
+        for s in range(1, 1 << k):
+            if k > 1 and s == (1 << k) - 1:
+                continue
+            p = (s >> l) & 1
+            inter, uni = int((p & g).sum()), int((p | g).sum())
+            score = 1.0 if uni == 0 else inter / uni
+            labs = [c for c in range(k) if s >> c & 1]
+            if best is None or score > best[0] or (score == best[0] and (len(labs), labs) < (len(best[1]), best[1])):
+                best = (score, labs)
+        assert S.best_foreground_iou(l, g, k) == best, (t, k)

@@ -323,3 +323,19 @@ def test_run_pipeline_c1_golden(ctx, golden_configs):
     res = ctx.run_pipeline(img, cfg)
     assert sha(res.mask.astype(np.uint32).reshape(-1)) == g["early_stop_labels_sha256"]
     assert res.iterations_run == g["early_stop_rounds"]
+
+
+@pytest.mark.parametrize("enc,n", [("manhattan", 11), ("rpos", 3)])
+def test_run_pipeline_batch_equals_single_calls(ctx, golden_configs, enc, n):
+    """seghdc_run_pipeline_batch (images side by side on child streams, one host sync) gives
+    every image the labels and rounds of its own run_pipeline call; C2 images 0-3 also match
+    the reference's goldens."""
+    imgs = [S.synth_image(2, s) for s in range(n)]
+    cfg = S.RunConfig(dim=10000, alpha=0.2, clusters=2, iterations=10, early_stop=False, encoder=enc)
+    for _ in range(2):  # second call: every child context replays its CUDA graph
+        labels, rounds = ctx.run_pipeline_batch(imgs, cfg)
+        for j, im in enumerate(imgs):
+            one = ctx.run_pipeline(im, cfg)
+            assert (labels[j] == one.mask).all() and rounds[j] == one.iterations_run, j
+            if enc == "manhattan" and j < 4:
+                assert sha(labels[j].astype(np.uint32).reshape(-1)) == golden_configs["C2"]["images"][j]["labels_sha256"]

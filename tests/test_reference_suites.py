@@ -11,7 +11,7 @@ import subprocess
 import pytest
 
 SUITES_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "suites")
-HOST_ONLY = ["test_hypervector", "test_position_encoder", "test_color_encoder"]
+HOST_ONLY = ["test_hypervector", "test_position_encoder", "test_color_encoder", "test_metrics"]
 DEVICE = ["test_pixel_pipeline", "test_clusterer"]
 
 
