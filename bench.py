@@ -391,26 +391,21 @@ def main():
     host_imgs = [synth_image(spec["cid"], i) for i in img_ids]
     cfg = S.RunConfig(dim=dim, alpha=spec["alpha"], beta=BETA, gamma=GAMMA, clusters=k, iterations=iters,
                       seed=CB_SEED, early_stop=False)
-    call = (lambda im: ctx.run_pipeline_sharded(im, cfg)) if sharded else (lambda im: ctx.run_pipeline(im, cfg))
+    if batch:  # the whole batch in one seghdc_run_pipeline_batch call (a context with every SM)
+        bctx = S.Context(local)
+        call = lambda im: bctx.run_pipeline_batch(host_imgs, cfg)  # noqa: E731
+    elif sharded:
+        call = lambda im: ctx.run_pipeline_sharded(im, cfg)  # noqa: E731
+    else:
+        call = lambda im: ctx.run_pipeline(im, cfg)  # noqa: E731
     for _ in range(3):  # eager run, CUDA-graph capture, replay
         call(host_imgs[0])
-    if batch:  # one host thread per context: the synchronous calls of the groups overlap
-        from concurrent.futures import ThreadPoolExecutor
-        pool = ThreadPoolExecutor(len(groups))
-
-        def run_group(j):
-            return [(i, groups[j].run_pipeline(host_imgs[i], cfg)) for i in range(j, len(host_imgs), len(groups))]
-        for _ in range(2):
-            pool.map(run_group, range(len(groups)))
     if world > 1:
         torch.distributed.barrier()
     e2e_steps = max(3, min(args.steps, 10 if batch else 50))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        if batch:
-            res = [r for _, r in sorted(x for part in pool.map(run_group, range(len(groups))) for x in part)]
-        else:
-            res = [call(im) for im in host_imgs]
+        res = [call(None)] if batch else [call(im) for im in host_imgs]
     dt = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([dt], device=dev)
@@ -424,14 +419,17 @@ def main():
     px_e2e = h * w if sharded else h * w * len(host_imgs) * world
     e2e = {"value": px_e2e * iters * e2e_steps / dt, "unit": "px·iter/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h,
-           "timer": "host wall clock around the synchronous seghdc_run_pipeline%s (pageable host image; codebook "
+           "timer": "host wall clock around the synchronous seghdc_run_pipeline%s (pageable host image%s; codebook "
                     "bases on the host + H2D image/bases + one CUDA graph: device codebooks, encode, seeds, rounds%s "
-                    "+ D2H labels)" % ("_sharded" if sharded else "", ", ncclAllReduce per round" if sharded else ""),
+                    "+ D2H labels)" % ("_sharded" if sharded else "_batch" if batch else "",
+                                       "s, one call per batch" if batch else "",
+                                       ", ncclAllReduce per round" if sharded else ""),
            "steps": e2e_steps}
     if sharded:
         labels_sha = None
     else:
-        labels_sha = hashlib.sha256(b"".join(r.mask.astype(np.uint32).tobytes() for r in res)).hexdigest()[:16]
+        masks = res[0][0] if batch else [r.mask for r in res]
+        labels_sha = hashlib.sha256(b"".join(m.astype(np.uint32).tobytes() for m in masks)).hexdigest()[:16]
 
     if rank != 0:
         if world > 1:

@@ -215,4 +215,4 @@ def test_cpp_dropin_sharded_pipeline(tmp_path):
                     "-lseghdc_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}",
                     "-Wl,-rpath,/usr/local/cuda/lib64"], check=True)
     out = subprocess.run([str(exe), "96", "130", "3", "3", "5"], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
+    assert out.returncode == 0 and out.stdout.strip().splitlines()[-1] == "ok", out.stdout + out.stderr  # NCCL may print a banner
