@@ -26,6 +26,27 @@
 
 namespace seghdc_dev {
 
+// Checked build (-DSEGHDC_CHECKED; compute-sanitizer is not available on the GPU pool): index
+// invariants of the hot kernels are tested at run time; the first violated check's line
+// number lands in g_check_line (read with seghdc_debug_check), and the kernel goes on.
+#ifdef SEGHDC_CHECKED
+static __device__ unsigned int g_check_line;  // one per translation unit (no -rdc)
+#define SG_CHECK(cond)                                                              \
+    do {                                                                            \
+        if (!(cond)) atomicCAS(&::seghdc_dev::g_check_line, 0u, unsigned(__LINE__)); \
+    } while (0)
+// this translation unit's first violated line (0: none), reset afterwards
+static inline unsigned int take_check_line() {
+    unsigned int v = 0;
+    const unsigned int zero = 0;
+    cudaMemcpyFromSymbol(&v, g_check_line, sizeof(v));
+    cudaMemcpyToSymbol(g_check_line, &zero, sizeof(zero));
+    return v;
+}
+#else
+#define SG_CHECK(cond) ((void)0)
+#endif
+
 // ------------------------------------------------------------------------------------------
 // Device-side round state. Index [p] is the round parity (round r uses p = r & 1); the
 // double buffering lets round r's consumer and round r+1's producer run back to back

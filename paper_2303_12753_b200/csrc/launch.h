@@ -162,5 +162,10 @@ void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, cons
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
                        cudaStream_t s);
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s);
+#ifdef SEGHDC_CHECKED
+unsigned int check_line_tc();       // first violated SG_CHECK line per translation unit (0: none)
+unsigned int check_line_kernels();
+unsigned int check_line_closed();
+#endif
 
 }  // namespace seghdc_dev

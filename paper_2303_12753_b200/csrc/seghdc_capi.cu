@@ -1108,6 +1108,20 @@ int seghdc_synchronize(seghdc_ctx* ctx) {
 
 uint64_t seghdc_kernel_launches(const seghdc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+#ifdef SEGHDC_CHECKED
+// checked build only: source line of the first violated device-side index check (0: none),
+// then reset
+extern "C" int seghdc_debug_check(unsigned int* line_out) {
+    return guarded(nullptr, [&] {
+        ck(cudaDeviceSynchronize(), "sync");
+        unsigned int v = seghdc_dev::check_line_tc();
+        if (!v) v = seghdc_dev::check_line_kernels();
+        if (!v) v = seghdc_dev::check_line_closed();
+        *line_out = v;
+    });
+}
+#endif
+
 int seghdc_set_wrap_counting(seghdc_ctx* ctx, int enable) {
     return guarded(ctx, [&] { ctx->count_wraps = enable != 0; });
 }

@@ -252,9 +252,11 @@ __global__ void __launch_bounds__(512) k_closed_accumulate_c(ClosedArgs a, Close
         const uint32_t l = s.labels[p];
         uint32_t e[kRuns];
         closed_runs_idx(a, p, e);
+        SG_CHECK(l < K);
         int32_t* d = sc + l * L;
 #pragma unroll
         for (int m = 0; m < kRuns; m += 2) {
+            SG_CHECK(e[m] < L && e[m + 1] < L);
             if (e[m] == e[m + 1]) continue;
             atomicAdd(d + e[m], 1);
             atomicAdd(d + e[m + 1], -1);
@@ -475,5 +477,9 @@ void launch_closed_finish(const ClosedArgs& a, ClosedState s, cudaStream_t st) {
     }
     k_closed_finish<<<a.K, kFinT, 0, st>>>(a, s);
 }
+
+#ifdef SEGHDC_CHECKED
+unsigned int check_line_closed() { return take_check_line(); }
+#endif
 
 }  // namespace seghdc_dev

@@ -1149,4 +1149,8 @@ cudaError_t launch_round(const RoundArgs& a, const RoundPlan& p, cudaStream_t s)
 #ifdef SEGHDC_TRACE
 void read_trace(void* dst) { cudaMemcpyFromSymbol(dst, g_trace, sizeof(g_trace)); }
 #endif
+#ifdef SEGHDC_CHECKED
+unsigned int check_line_kernels() { return take_check_line(); }
+#endif
+
 }  // namespace seghdc_dev

@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
+            SG_CHECK(!(fin && live) || px < n);
             const uint32_t old = (fin && live) ? labels[px] : 0u;
             long long d[KC];
             if (!finw) {
@@ -628,6 +629,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     continue;
                 }
                 cl_wait(&x_full[db], (it >> 1) & 1);
+                SG_CHECK(Smem::xb(nks) + (size_t(db + 1) * SPLIT * KC * 32) * 8 <= Smem::bars(nks));
                 const long long* xb = xbuf + db * (SPLIT * KC * 32) + lane;
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c) {
@@ -682,6 +684,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     uint32_t base = 0;
                     if (lane == 0) base = atomicAdd(flist_count + (c - 1), uint32_t(__popc(m)));
                     base = __shfl_sync(0xffffffffu, base, 0);
+                    SG_CHECK(!(enter || leave) || base + __popc(m & ((1u << lane) - 1)) < n);
                     if (enter || leave)
                         flist[size_t(c - 1) * n + base + __popc(m & ((1u << lane) - 1))] =
                             uint32_t(px) | (leave ? 0x80000000u : 0u);
@@ -696,6 +699,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 uint32_t base = 0;
                 if (lane == 0 && m) base = atomicAdd(&s_listn[db], uint32_t(__popc(m)));
                 base = __shfl_sync(0xffffffffu, base, 0);
+                SG_CHECK(!take || base + __popc(m & ((1u << lane) - 1)) < kTP);
                 if (take) s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
             if (SPLIT == 1) mbar_arrive(&list_ready[db]);
@@ -1049,6 +1053,7 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
     list += size_t(blockIdx.y) * n;
     dst += size_t(blockIdx.y) * dst_stride;
     const uint32_t M = count[blockIdx.y];
+    SG_CHECK(M <= n);
     // at least kMinRows rows per CTA: a short list (late rounds) occupies a few CTAs, whose
     // flush (one atomic per entry of D) dominates, instead of all of them
     constexpr uint32_t kMinRows = 64;
@@ -1066,6 +1071,7 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
         for (int v = 0; v < 16; ++v) {
             const uint32_t i = e + ng * v;
             const uint32_t en = i < r1 ? list[i] : 0u;
+            SG_CHECK(i >= r1 || (en & 0x7FFFFFFFu) < n);
             const uint32_t neg = (en >> 31) ? 0xFFFFFFFFu : 0u;
             const uint32_t word = i < r1 ? __ldg(grid + size_t(en & 0x7FFFFFFFu) * S32 + colc) : 0u;
             x[v] = (word ^ neg) & (i < r1 ? 0xFFFFFFFFu : 0u);
@@ -1299,5 +1305,9 @@ cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s) {
 #endif
     return launch_round_tc_sel(a, s);
 }
+
+#ifdef SEGHDC_CHECKED
+unsigned int check_line_tc() { return take_check_line(); }
+#endif
 
 }  // namespace seghdc_dev

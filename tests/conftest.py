@@ -56,3 +56,20 @@ def instance_arrays(inst):
     img = np.array(inst["image"], np.uint8).reshape(inst["h"], inst["w"], inst["channels"])
     grid = np.array([int(x, 16) for x in inst["grid"]], np.uint64).reshape(inst["h"] * inst["w"], -1)
     return img, grid
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _checked_build_guard():
+    """With a checked build selected (SEGHDC_LIB=.../libseghdc_b200_checked.so, built with
+    -DSEGHDC_CHECKED), fail the session if any device-side index check was violated."""
+    yield
+    if not os.environ.get("SEGHDC_LIB"):
+        return
+    import ctypes
+    import paper_2303_12753_b200 as S
+
+    L = S.lib()
+    if hasattr(L, "seghdc_debug_check"):
+        line = ctypes.c_uint(0)
+        assert L.seghdc_debug_check(ctypes.byref(line)) == 0
+        assert line.value == 0, f"device-side index check failed at source line {line.value}"

@@ -1,4 +1,6 @@
-"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): every
+"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck / initcheck) and for the
+checked build (-DSEGHDC_CHECKED, SEGHDC_LIB=...; compute-sanitizer is closed on the GPU pool),
+each case re-run 5 times (a race shows up as run-to-run differences): every
 round-kernel layout (tcgen05 one-CTA K <= 2 and K <= 4, the 4-CTA dimension split for K <= 8,
 the IMMA kernels), encode, seeds, fold lists, finish, and the closed-form variant. Each case
 is checked against the oracle so a sanitizer run also proves the results did not change."""
@@ -27,6 +29,9 @@ for dim, h, w, c, k, its, kern in cases:
     cb = S.build_codebooks(dim, h, w, c, 1.0, 3, 1, 1)
     grid = ctx.encode_image(img, dim, *cb)
     res = ctx.cluster(None, img, dim, k, its, False)
+    for _ in range(5):  # determinism: identical labels and centroids on every re-run
+        again = ctx.cluster(None, img, dim, k, its, False)
+        assert (again["labels"] == res["labels"]).all() and (again["centroids"] == res["centroids"]).all()
     exp = port.cluster(grid, img, dim, k, its, False)
     assert (grid == port.encode(img, dim, *cb)).all()
     assert (res["labels"] == exp["labels"]).all() and (res["centroids"] == exp["centroids"]).all(), (dim, k)
@@ -36,4 +41,11 @@ for dim, h, w, c, k, its, kern in cases:
     ex = port.cluster(port.encode(img, dim, *S.build_codebooks(dim, h, w, c, 1.0, 3, 1, 1)), img, dim, min(k, 8), its, False)
     assert (cl["labels"] == ex["labels"]).all() and (cl["centroids"] == ex["centroids"]).all()
     print(f"closed dim={dim} k={min(k, 8)} ok", flush=True)
+L = S.lib()
+if hasattr(L, "seghdc_debug_check"):
+    import ctypes
+    line = ctypes.c_uint(0)
+    assert L.seghdc_debug_check(ctypes.byref(line)) == 0
+    print("checked build: first violated device-side check at line", line.value, "(0 = none)")
+    assert line.value == 0
 print("sanitize cases ok")
