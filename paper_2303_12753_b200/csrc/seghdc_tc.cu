@@ -440,7 +440,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     // flist != nullptr (round 1: every member of cluster 1 enters): the changed pixels are
     // appended to a global list that k_fold_list folds with the whole GPU after this kernel,
     // instead of the fold warps reading them back tile by tile
+#ifdef SEGHDC_EXP_NOGRID
+    const bool folding = false;  // timing experiment: labels are meaningless, nothing to fold
+#else
     const bool folding = UPD && do_update && flist == nullptr;
+#endif
 
     if (warp < kWEpi) {
         // ------------------------------------------------------------------------ unpack warps
@@ -493,7 +497,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint32_t half = opaque(0x80000000u), two = opaque(2u);
 #pragma unroll
             for (uint32_t c16 = hf * (8 / kUH); c16 < (hf + 1) * (8 / kUH); ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
-#ifndef SEGHDC_EXP_NOLDS  // timing experiment only: no shared-memory reads in the unpack
+#if defined(SEGHDC_EXP_NOGRID)  // timing experiment: no grid at all (no TMA, no smem), words from a hash
+                const uint32_t hq = uint32_t(tile_px0(g / nch) + r) * 2654435761u ^ ((g % nch) * 8 + c16) * 40503u;
+                const uint4 v = make_uint4(hq, hq * 3u, hq ^ 0x9E3779B9u, hq + 0x7F4A7C15u);
+#elif !defined(SEGHDC_EXP_NOLDS)  // timing experiment only: no shared-memory reads in the unpack
                 uint4 v;
                 if constexpr (kLdg) v = cv[(c16 - hf * (8 / kUH)) & 3];
                 else v = *reinterpret_cast<const uint4*>(row + ((c16 ^ (r & 7)) << 4));
@@ -670,7 +677,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
             // k_fold_list, or the tile's shared list for the fold warps (K == 2).
-#if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM)
+#if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM) || defined(SEGHDC_EXP_NOGRID)
             if (false) {  // timing experiments: results are meaningless, keep the lists out of it
 #else
             if (flist != nullptr && do_update) {
@@ -793,9 +800,14 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     TC_CLK(c1);
                     TC_ACC(4, c1 - c0);
                     if (ch == 0) TC_TR(0, it);
+#ifdef SEGHDC_EXP_NOGRID  // timing experiment: the slot is "full" without any data
+                    (void)y;
+                    mbar_arrive(&slot_full[s]);
+#else
                     mbar_expect_tx(&slot_full[s], kChunkBytes);
                     tma_load_2d_hint(ring + size_t(s) * kChunkBytes, &tmap, int((ch0 + ch) * kCW), y, &slot_full[s],
                                      pol_stream);
+#endif
                 }
             }
         }
