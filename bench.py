@@ -374,12 +374,15 @@ def main():
     peak, peak_src = peaks()
     kernel_name = ctx.round_kernel
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-    tp = os.path.join(ROOT, "profiles", "round1_traffic.json" if args.config == 1 else
-                      f"round1_traffic_c{args.config}.json")
+    tp = os.path.join(ROOT, "profiles", f"round2_traffic_c{args.config}.json")
     if os.path.exists(tp):
         t = json.load(open(tp))
         if t.get("kernel") == kernel_name:
             traffic = t["dram_bytes_per_launch"]
+    # the round kernel's tensor work: exact FP4 digit products, M = pixels, K = HV dims padded to
+    # whole 1024-dim chunks, N = digit columns of the layout (16 / 32 / 64; 0: IMMA kernels)
+    ncols = (16 if k <= 2 and (dim + 31) // 32 <= 384 else 32 if k <= 4 else 64) if kernel_name == "k_round_tc" else 0
+    fp4_ops = 2.0 * (n_local // len(img_ids)) * (((dim + 31) // 32 + 31) // 32 * 1024) * ncols
     bytes_per_launch = (n_local // len(img_ids)) * ((dim + 7) // 8)  # algorithmic: one packed HV read per pixel
     achieved = bytes_per_launch / (kern_ms / kern_n / 1000.0) / 1e9
     if batch:  # C2_GROUPS launches run side by side, each on 1/C2_GROUPS of the SMs
@@ -469,7 +472,13 @@ def main():
                      "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": kern_ms / kern_n,
                      "launches_timed": kern_n, "kernel_share_of_step": kern_ms / len(profs) / ms,
                      "concurrent_launches": len(profs),
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     # the same launch against the tensor pipe (secondary bound): exact FP4 products
+                     "tensor_fp4": None if not ncols else {
+                         "achieved": fp4_ops / (kern_ms / kern_n / 1000.0) / 1e12 * (len(profs) if batch else 1),
+                         "peak": 9000.0, "unit": "TFLOP/s", "columns": ncols,
+                         "frac": fp4_ops / (kern_ms / kern_n / 1000.0) / 1e12 * (len(profs) if batch else 1) / 9000.0,
+                         "ops_per_launch": fp4_ops, "peak_source": "nominal dense FP4 (B200_PROFILING.md)"}},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -612,10 +612,10 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     {
         static const char* se = getenv("SEGHDC_SERPENTINE");
         a.serpentine = (se && *se == '0') ? 0u : 1u;
-        // L2 prefetch distance (chunks) for the layouts whose large B image leaves a shallow
-        // smem ring (N = 32, 64); SEGHDC_PF overrides
+        // L2 prefetch distance (chunks) of the producer, SEGHDC_PF; default off: measured slower
+        // for every layout (round 2: C3 1050 vs 1100 us per round at 8, C4 12.2 vs 12.6 ms)
         static const char* pe = getenv("SEGHDC_PF");
-        a.pf = pe ? uint32_t(atoi(pe)) : (x.plan.tc && tc_ncol(uint32_t(x.K), x.g.W32) != 16 ? 8u : 0u);
+        a.pf = pe ? uint32_t(atoi(pe)) : 0u;
     }
     // entries are member sums <= the image's pixel count n, so norm2 <= D n^2 and every
     // cross product of strictly_closer is below D^3 n^4: no wrap possible under 2^128

@@ -677,10 +677,12 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
             // k_fold_list, or the tile's shared list for the fold warps (K == 2).
-#if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM) || defined(SEGHDC_EXP_NOGRID)
+#if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM) || defined(SEGHDC_EXP_NOGRID) || \
+    defined(SEGHDC_EXP_NOFLIST)
             if (false) {  // timing experiments: results are meaningless, keep the lists out of it
 #else
-            if (flist != nullptr && do_update) {
+            // one ballot first: after the first rounds almost no warp holds a changed pixel
+            if (flist != nullptr && do_update && __ballot_sync(0xffffffffu, live && old != best)) {
 #endif
 #pragma unroll
                 for (uint32_t c = 1; c < KC; ++c) {

@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py launches <launches.csv> <out.md>    # per-kernel device-time share
   python tools/ncu_summary.py kernel   <report.ncu-rep> <out.md>  # key --set full metrics of one kernel
+  python tools/ncu_summary.py traffic  <report.ncu-rep> <out.json> <config>  # + DRAM bytes per launch
 """
 import collections
 import csv
@@ -17,7 +18,10 @@ KEYS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
-    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "IMMA pipe %"),
+    ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "IMMA pipe % (legacy mma.sync)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active % (tcgen05)"),
+    ("sm__ops_path_tensor_src_fp4_dst_fp32.sum", "FP4 tensor ops (2 x MAC)"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "TMEM active %"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__block_size", "block size"),
@@ -77,7 +81,19 @@ def kernel(path, out):
         f.write("\n## Warp stall samples\n\n| reason | share |\n|---|---|\n")
         for s, n in sorted(stalls, reverse=True)[:10]:
             f.write(f"| {n} | {100 * s / tot:.1f} % |\n")
+    return d
+
+
+def traffic(path, out_json, config):
+    """DRAM read + write per launch of the captured kernel -> bench.py's roofline `traffic`."""
+    import json
+    d = kernel(path, out_json.replace(".json", ".md"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    b = sum(float(d[k][1].replace(",", "")) * scale[d[k][0]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    name = d.get("Kernel Name", ("", "?"))[1]
+    json.dump({"kernel": name.split("<")[0].replace("void ", "").split("::")[-1], "kernel_full": name,
+               "dram_bytes_per_launch": b, "config": int(config), "source": path}, open(out_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    {"launches": launches, "kernel": kernel}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "kernel": kernel, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
