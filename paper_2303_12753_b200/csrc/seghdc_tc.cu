@@ -677,15 +677,23 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
             // k_fold_list, or the tile's shared list for the fold warps (K == 2).
+            // the warp's touched clusters >= 1 in one reduction: after the first rounds almost no
+            // warp holds a changed pixel, and a changed one touches one or two clusters
+            uint32_t touched = 0;
 #if defined(SEGHDC_EXP_NOMMA) || defined(SEGHDC_EXP_NOLDS) || defined(SEGHDC_EXP_NOSTTM) || defined(SEGHDC_EXP_NOGRID) || \
     defined(SEGHDC_EXP_NOFLIST)
             if (false) {  // timing experiments: results are meaningless, keep the lists out of it
 #else
-            // one ballot first: after the first rounds almost no warp holds a changed pixel
             if (flist != nullptr && do_update && __ballot_sync(0xffffffffu, live && old != best)) {
+                const uint32_t mine =
+                    (live && old != best) ? ((1u << best) | (old < KC ? (1u << old) : 0u)) : 0u;
+                touched = __reduce_or_sync(0xffffffffu, mine) & ~1u;
+            }
+            if (touched) {
 #endif
-#pragma unroll
-                for (uint32_t c = 1; c < KC; ++c) {
+                while (touched) {
+                    const uint32_t c = __ffs(touched) - 1;
+                    touched &= touched - 1;
                     if (c >= K) break;
                     const bool enter = live && best == c && old != c, leave = live && old == c && best != c;
                     const uint32_t m = __ballot_sync(0xffffffffu, enter || leave);
