@@ -73,15 +73,21 @@ struct TcCfg {
     static constexpr uint32_t NDIG = kP8;
     static constexpr uint32_t KC = NCOL / NDIG;              // clusters of the layout
     static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
+#ifndef SEGHDC_SPLIT_AB3
     static constexpr uint32_t AB = SPLIT > 1 ? 2 : 3;        // A buffers in TMEM (128 columns each)
+#else  // experiment: 3 A buffers and one accumulator set in the split layout (32 warps)
+    static constexpr uint32_t AB = 3;
+#endif
     static constexpr uint32_t UH = SPLIT > 1 ? 2 : 1;        // unpack warps sharing one chunk (halves)
     static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
-#ifndef SEGHDC_C3_NMW2
+#if defined(SEGHDC_SPLIT_AB3)
+    static constexpr uint32_t DB = SPLIT > 1 ? 1 : 2;
+#elif !defined(SEGHDC_C3_NMW2)
     static constexpr uint32_t DB = 2;                        // accumulator sets (by tile parity)
 #else
     static constexpr uint32_t DB = (NCOL == 32 && SPLIT == 1) ? 1 : 2;
 #endif
-    static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? 4 : 3;  // smem ring depth (16 KB each):
+    static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? (AB == 3 ? 3 : 4) : 3;  // smem ring depth (16 KB each):
                                                              // the larger B image takes the rest; a multiple
                                                              // of AB, so slot g % Stages is unpacked by phase g % AB
 #ifndef SEGHDC_C3_NMW2
@@ -97,7 +103,7 @@ struct TcCfg {
     static constexpr uint32_t ColSF = ColD + DB * NMW * NCOL;  // after D[DB tile parities][NMW]
     static_assert(Stages % AB == 0, "ring slots follow the unpack phases");
     static_assert(ColSF + 16 <= kTmemCols, "TMEM budget");
-    static_assert(SPLIT == 1 || Warps == 24, "split layout: 16 unpack, 4 epilogue, MMA, producer, 2 finalizers");
+    static_assert(SPLIT == 1 || Warps == 4 * UW + 8, "split layout: unpack, 4 epilogue, MMA, producer, 2 finalizers");
 };
 constexpr uint32_t kKB = TcCfg<16>::KB;  // the K <= 2 image (k_finish_tc)
 
