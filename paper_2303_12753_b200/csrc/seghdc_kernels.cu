@@ -85,7 +85,9 @@ constexpr uint32_t kEncRows = 32, kEncCols = 64;
 template <int C>
 constexpr uint32_t enc_warps() { return C == 1 ? 8 : 24; }
 
-template <int C>
+// H: weight-16 planes of the column-sum counters, the fewest that hold the pixels one warp
+// encodes (its ripple is 2 LOP3 per plane per 16 pixels on the ALU-bound path)
+template <int C, int H>
 __global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? 3 : 1)
     k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? 3 : 1)
     }
     for (uint32_t e = tid; e < 1024; e += blockDim.x) s_sum[e] = 0;
 
-    BitCounter<12> cnt;  // <= rows_per / warps * 64 pixels per warp
+    BitCounter<H> cnt;  // <= ceil(rows_per / kEncRows) * ceil(kEncRows / warps) * kEncCols pixels per warp
     cnt.reset();
     const bool st = w0 + lane < S32;
     // staged tables hold 0 for words >= wref, so lanes past the HV need no masking below
@@ -199,12 +201,22 @@ __global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? 3 : 1)
     }
 }
 
+template <int C, int H>
+static void launch_encode_ch(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
+    const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
+    ensure_dynamic_smem((const void*)k_encode<C, H>, smem);
+    k_encode<C, H><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
+                                                       a.S32, a.grid, a.colsum, a.W32);
+}
 template <int C>
 static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
-    const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
-    ensure_dynamic_smem((const void*)k_encode<C>, smem);
-    k_encode<C><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref, a.S32,
-                                                a.grid, a.colsum, a.W32);
+    const uint64_t rows_per = (uint64_t(row_end - row_begin) + g.z - 1) / g.z;
+    const uint64_t per_warp = (rows_per + kEncRows - 1) / kEncRows * ((kEncRows + enc_warps<C>() - 1) / enc_warps<C>()) *
+                              kEncCols;
+    if (per_warp <= BitCounter<6>::capacity()) return launch_encode_ch<C, 6>(a, g, row_begin, row_end, s);
+    if (per_warp <= BitCounter<8>::capacity()) return launch_encode_ch<C, 8>(a, g, row_begin, row_end, s);
+    if (per_warp <= BitCounter<10>::capacity()) return launch_encode_ch<C, 10>(a, g, row_begin, row_end, s);
+    launch_encode_ch<C, 12>(a, g, row_begin, row_end, s);
 }
 
 void launch_encode(const EncodeArgs& a, cudaStream_t s) {
