@@ -129,6 +129,8 @@ struct RoundArgs {
     uint32_t serpentine;     // odd rounds walk the tiles backwards
     uint32_t pf;             // L2 prefetch distance of the producer, in chunks (0: none)
     bool wraps;              // a 128-bit comparator wrap is possible: use the wrap-counting kernels
+    const unsigned long long* labels_host_slot;  // tcgen05, last round: device slot holding a mapped host
+                                                 // label pointer (0: none) that also receives the labels
 };
 size_t round_smem_bytes(uint32_t MT, uint32_t NTG, uint32_t SS, uint32_t nwarps, uint32_t K, uint32_t NT);
 bool plan_round(uint32_t K, uint32_t P, uint32_t W32, uint32_t SS, RoundPlan& p, size_t smem_limit);

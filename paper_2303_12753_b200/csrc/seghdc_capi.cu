@@ -234,6 +234,10 @@ struct seghdc_ctx {
     size_t wraps_rounds = 0;
     bool assign_vmax_wraps = false;  // seghdc_assign with caller centroids large enough to wrap
     bool count_wraps = false;        // seghdc_set_wrap_counting: the tcgen05 kernels' counting variant
+    // run_pipeline: device slot with the caller's mapped label pointer for the last round
+    DevBuf<unsigned long long> zc_slot;
+    unsigned long long zc_host = 0;
+    bool in_pipeline = false;  // launches belong to run_pipeline's device part (may arm zc_slot)
     // run_pipeline: staging buffers, stage events (created once) and the CUDA graph of the
     // device part (codebook expansion, encode, seeds, every round) for the last signature
     PinnedBuf stage_in, stage_out;
@@ -624,6 +628,7 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
         a.wraps = x.count_wraps &&
                   (std::log2(D) * 3 + std::log2(std::max(n_img, 1.0)) * 4 >= 127.0 || x.assign_vmax_wraps);
     }
+    a.labels_host_slot = (x.in_pipeline && r == x.iterations) ? x.zc_slot.p : nullptr;
     a.flist = use_flist ? x.flist.p : nullptr;
     a.flist_count = use_flist ? x.flist.p + (x.K - 1) * x.n_local() : nullptr;
     if (use_flist) ck(cudaMemsetAsync(a.flist_count, 0, (x.K - 1) * 4, x.stream), "clear fold lists");
@@ -799,8 +804,10 @@ void pipeline_device(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::M
 
 // The device part of one pipeline call on x's stream: eager on the first call with a given
 // signature, captured into a CUDA graph on the second, replayed from then on.
-void run_device_part(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::ManhattanParams* mpp, size_t r0,
-                     size_t r1, bool sharded, seghdc_round_cb cb, void* user) {
+// zc_labels (nullable): device-mapped caller label buffer; returns whether the last round was
+// armed to write it (tcgen05 plan of this same signature, early stop off, no callback)
+bool run_device_part(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::ManhattanParams* mpp, size_t r0,
+                     size_t r1, bool sharded, seghdc_round_cb cb, void* user, void* zc_labels = nullptr) {
     const size_t h = pc.h, w = pc.w, c = pc.c, dim = pc.dim;
     const bool manhattan = mpp != nullptr;
     const seghdc_host::ManhattanParams mp = mpp ? *mpp : seghdc_host::ManhattanParams{};
@@ -825,6 +832,16 @@ void run_device_part(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::M
         G.sig = sig;
         G.epoch = g_realloc_epoch.load();
     }
+    // a plan for this signature exists once it ran eagerly; only tcgen05 plans write host labels
+    const bool zc = zc_labels && !cb && !pc.early_stop && G.seen > 0 && x.plan.tc;
+    x.zc_slot.ensure(1);
+    x.zc_host = zc ? reinterpret_cast<unsigned long long>(zc_labels) : 0ull;
+    ck(cudaMemcpyAsync(x.zc_slot.p, &x.zc_host, 8, cudaMemcpyHostToDevice, x.stream), "label slot");
+    x.in_pipeline = true;
+    struct Reset {
+        seghdc_ctx& x;
+        ~Reset() { x.in_pipeline = false; }
+    } reset{x};
     bool ran = false;
     if (graphs && G.exec) {
         ck(cudaGraphLaunch(G.exec, x.stream), "cudaGraphLaunch");
@@ -864,6 +881,7 @@ void run_device_part(seghdc_ctx& x, const PipelineCall& pc, const seghdc_host::M
         pipeline_device(x, pc, mpp, r0, r1, sharded, cb, user, false);
         G.seen++;
     }
+    return zc;
 }
 
 // run_pipeline: validation and codebooks on the host (one Rng, position then colour), then the
@@ -921,13 +939,19 @@ void run_pipeline_impl(seghdc_ctx& x, const PipelineCall& pc, seghdc_round_cb cb
         load_codebooks(x, dim, h, w, c, row.data(), col.data(), wid.data());
         ck(cudaStreamSynchronize(x.stream), "sync");  // the host tables go out of scope
     }
-    run_device_part(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, cb, user);
+    // zero-copy labels: a page-locked caller buffer can be written by the last round kernel
+    // itself (armed inside run_device_part once this signature's plan is known)
+    void* lab_dev = nullptr;
+    if (labels_out && !cb && !pc.early_stop && cudaHostGetDevicePointer(&lab_dev, labels_out, 0) != cudaSuccess)
+        lab_dev = nullptr;
+    cudaGetLastError();
+    const bool zc = run_device_part(x, pc, manhattan ? &mp : nullptr, r0, r1, sharded, cb, user, lab_dev);
     // results: labels (this rank's rows) + round state, through the staging buffer unless the
     // caller's label buffer is page-locked
     const size_t n_loc = (r1 - r0) * w, sbytes = StateView::bytes(uint32_t(pc.k));
     const bool lab_pinned = labels_out && is_pinned(labels_out);
     uint8_t* out = x.stage_out.ensure(sbytes + (lab_pinned || !labels_out ? 0 : n_loc * 4));
-    if (labels_out)
+    if (labels_out && !zc)
         ck(cudaMemcpyAsync(lab_pinned ? static_cast<void*>(labels_out) : static_cast<void*>(out + sbytes), x.labels.p,
                            n_loc * 4, cudaMemcpyDeviceToHost, x.stream),
            "download labels");

@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     k_round_tc(const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grid, uint64_t n, uint32_t S32,
                uint32_t W32, uint32_t K, const uint8_t* __restrict__ bimg, uint32_t nks, uint32_t* labels,
                void* state, uint32_t round, int do_update, uint32_t* __restrict__ xchg, uint32_t Dp,
-               uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine, uint32_t pf) {
+               uint32_t* __restrict__ flist, uint32_t* __restrict__ flist_count, uint32_t serpentine, uint32_t pf,
+               const unsigned long long* __restrict__ lh_slot) {
     constexpr uint32_t NRT = kNRW * 32;
     constexpr int CPTMAX = 3;  // fold columns per thread: W32 <= 3 * NRW * 32 (tc_supported)
     using Cfg = TcCfg<NCOL, SPLIT>;
@@ -433,6 +434,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     // the previous kernel; state, B image, labels and the exchange buffer are read after it
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool done = *reinterpret_cast<volatile uint32_t*>(&st.hdr->done) != 0;
+    // last round of a run_pipeline call: the labels also go straight into the caller's
+    // page-locked buffer (a device-mapped host pointer, written before the graph launch), so the
+    // download overlaps the round instead of following it
+    uint32_t* const labels_host = lh_slot ? reinterpret_cast<uint32_t*>(*lh_slot) : nullptr;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -674,6 +679,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             }
             if (live) {
                 labels[px] = best;
+                if (labels_host) labels_host[px] = best;
                 changed += old != best;
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c) ccount[c] += best == c;
@@ -1181,7 +1187,7 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     if (SPLIT == 1)
         return launch_pdl(kern, dim3(a.ctas), dim3(Cfg::Warps * 32), smem, s, tm, a.grid, a.n, a.S32, a.W32, a.K,
                           a.bimg, nks, a.labels, a.state, a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count,
-                          a.serpentine, a.pf);
+                          a.serpentine, a.pf, a.labels_host_slot);
     // clusters of SPLIT CTAs (one per SM): as many as fit at once, at most one per tile
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(Cfg::Warps * 32);
@@ -1215,7 +1221,8 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     const uint64_t ncl = std::max<uint64_t>(1, (ntiles + per - 1) / per);
     cfg.gridDim = dim3(uint32_t(ncl * SPLIT));
     return cudaLaunchKernelEx(&cfg, kern, tm, a.grid, a.n, a.S32, a.W32, a.K, a.bimg, nks, a.labels, a.state,
-                              a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine, a.pf);
+                              a.round, a.do_update, xchg, a.Dp, a.flist, a.flist_count, a.serpentine, a.pf,
+                              a.labels_host_slot);
 }
 }  // namespace
 

@@ -339,3 +339,17 @@ def test_run_pipeline_batch_equals_single_calls(ctx, golden_configs, enc, n):
             assert (labels[j] == one.mask).all() and rounds[j] == one.iterations_run, j
             if enc == "manhattan" and j < 4:
                 assert sha(labels[j].astype(np.uint32).reshape(-1)) == golden_configs["C2"]["images"][j]["labels_sha256"]
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_run_pipeline_large_golden(ctx, golden_configs, name):
+    """The end-to-end call (run_pipeline: device codebooks, encode, seeds, 20 rounds as one CUDA
+    graph from the second call on) at BASELINE sizes against the reference's goldens."""
+    g, spec = golden_configs[name], golden_configs["_meta"]["configs"][name]
+    img = S.synth_image(spec["cid"], 0)
+    cfg = S.RunConfig(dim=spec["dim"], alpha=spec["alpha"], beta=26, gamma=1, clusters=spec["k"],
+                      iterations=spec["iterations"], seed=0, early_stop=False)
+    for _ in range(2):  # eager, then captured
+        res = ctx.run_pipeline(img, cfg)
+        assert sha(res.mask.astype(np.uint32).reshape(-1)) == g["labels_sha256"]
+        assert res.iterations_run == g["rounds"]

@@ -216,3 +216,52 @@ def test_cpp_dropin_sharded_pipeline(tmp_path):
                     "-Wl,-rpath,/usr/local/cuda/lib64"], check=True)
     out = subprocess.run([str(exe), "96", "130", "3", "3", "5"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip().splitlines()[-1] == "ok", out.stdout + out.stderr  # NCCL may print a banner
+
+
+def test_c3_row_sharded_library_loop_matches_reference_golden(golden_configs):
+    """BASELINE config C3 at full size (2048^2 x 3, D = 10000, K = 4, 20 rounds) row-sharded over
+    3 callers of seghdc_run_pipeline_sharded (host-staged callback collective): the row blocks
+    together and every rank's centroids equal the reference's golden."""
+    import hashlib
+    import threading
+
+    import torch
+
+    g, spec = golden_configs["C3"], golden_configs["_meta"]["configs"]["C3"]
+    img = S.synth_image(3, 0)
+    cfg = S.RunConfig(dim=spec["dim"], alpha=spec["alpha"], clusters=spec["k"], iterations=spec["iterations"],
+                      early_stop=False)
+    world = 3
+    barrier = threading.Barrier(world)
+    slots, total = [None] * world, {}
+
+    def make_fn(rank):
+        def fn(ptr, n, stream):
+            t = torch.as_tensor(_Dev(ptr, n), device="cuda:0")
+            torch.cuda.synchronize()
+            slots[rank] = t.cpu().numpy()
+            if barrier.wait() == 0:
+                total["sum"] = np.sum(np.stack(slots).astype(np.int64), axis=0).astype(np.uint32).view(np.int32)
+            barrier.wait()
+            t.copy_(torch.from_numpy(total["sum"].copy()))
+            torch.cuda.synchronize()
+            barrier.wait()
+        return fn
+
+    ctxs = [S.Context(0) for _ in range(world)]
+    for r, c in enumerate(ctxs):
+        c.set_allreduce(make_fn(r), r, world)
+    out = [None] * world
+    ths = [threading.Thread(target=lambda r=r: out.__setitem__(r, ctxs[r].run_pipeline_sharded(img, cfg)))
+           for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    labels = np.concatenate([out[r]["labels"] for r in range(world)]).astype(np.uint32)
+    assert hashlib.sha256(labels.tobytes()).hexdigest() == g["labels_sha256"]
+    for r in range(world):
+        assert hashlib.sha256(out[r]["centroids"].astype(np.uint32).tobytes()).hexdigest() == g["centroids_sha256"]
+        assert out[r]["counts"].tolist() == g["counts"]
+    for c in ctxs:
+        c.close()
