@@ -84,11 +84,14 @@ constexpr uint32_t kEncRows = 32, kEncCols = 64;
 // 96 KB of colour tables leave room for one CTA per SM, so that CTA runs 24 warps
 template <int C>
 constexpr uint32_t enc_warps() { return C == 1 ? 8 : 24; }
+#ifndef SEGHDC_ENC_MINB
+#define SEGHDC_ENC_MINB 4  // resident CTAs per SM with one channel (64 registers, no spills; 3 CTAs: 113 vs 100 us at C1)
+#endif
 
 // H: weight-16 planes of the column-sum counters, the fewest that hold the pixels one warp
 // encodes (its ripple is 2 LOP3 per plane per 16 pixels on the ALU-bound path)
 template <int C, int H>
-__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? 3 : 1)
+__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB : 1)
     k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
              uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t* __restrict__ colsum, uint32_t W32) {
