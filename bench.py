@@ -461,7 +461,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": ("e2m1 x e2m1 -> f32 tcgen05 (exact integer digit products), u64/u128 argmax"
+        "scaling": "strong" if (sharded or batch) else "weak", "vs_baseline": None, "dtype": ("e2m1 x e2m1 -> f32 tcgen05 (exact integer digit products), u64/u128 argmax"
                                                                    if kernel_name == "k_round_tc" else
                                                                    "u8 x u8 -> s32 IMMA, u64/u128 argmax"),
         "data": "synthetic (seeded generator, SURVEY.md §8d)",
