@@ -222,13 +222,14 @@ def run_reference_arm(args, spec):
     total = sum(times)
     value = sh * w * args.steps / total
     what = ("the whole image" if sh == h else f"the first {sh} rows ({sh * w} of {full_px} px)")
-    _, _, img_ids, n_local, par = workload_layout(args.config, world, 0, h, w)
+    sh_, ba_, img_ids, n_local, par = workload_layout(args.config, world, 0, h, w)
     cfg = bench_config(args, spec, n_local, len(img_ids), par)
     cfg["sample"] = f"one assign_labels+update_centroids round of {what} per step"
     line = {
         "metric": METRIC, "value": value, "unit": "px·iter/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 (reference integer dot)", "data": "synthetic",
+        "scaling": "strong" if (sh_ or ba_) else "weak", "vs_baseline": None,
+        "dtype": "u32/u64 (reference integer dot)", "data": "synthetic",
         "impl": "reference", "config": cfg,
         "cpu_baseline": {"value": value, "unit": "px·iter/s", "cores": threads, "kind": kind, "host": host_cpu(),
                          "sample": f"{args.steps} chained rounds of {spec['name']} ({what}), one row-block per "
@@ -264,10 +265,21 @@ def main():
     import paper_2303_12753_b200 as S
 
     world, rank, local = dist_env()
+    # SEGHDC_BENCH_GLOO=1: a dry run of the N > 1 control flow on a one-GPU box (every rank on
+    # cuda:0, gloo for the host-side barrier / max; the data path has no collective for C0-C2).
+    # Not a measurement: ranks share one GPU. Row-sharded configs need NCCL and distinct GPUs.
+    dry = bool(os.environ.get("SEGHDC_BENCH_GLOO")) and world > 1
+    if dry:
+        assert not (args.config in (3, 4)), "SEGHDC_BENCH_GLOO dry runs cover the unsharded configs only"
+        local = 0
+    coll_dev = "cpu" if dry else None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     ctx = S.Context(local)
@@ -354,7 +366,7 @@ def main():
     launches = sum(g.kernel_launches for g in groups) - launches0 if batch else ctx.kernel_launches - launches0
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=coll_dev or dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     total_px_iter = (h * w if sharded else C2_IMAGES * h * w if batch else h * w * world) * iters * args.steps
@@ -411,7 +423,7 @@ def main():
         res = [call(None)] if batch else [call(im) for im in host_imgs]
     dt = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([dt], device=dev)
+        t = torch.tensor([dt], device=coll_dev or dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dt = float(t.item())
     wph = (dim + 63) // 64
