@@ -79,11 +79,15 @@ void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_
 // row, lane = word: coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane;
 // the CTA folds them in shared memory and adds 1024 column sums to the global array.
 // =============================================================================================
-constexpr uint32_t kEncRows = 32, kEncCols = 64;
+constexpr uint32_t kEncRows = 32;
+// image columns per CTA: 64 with one channel; 32 with three, so that two CTAs (2 x ~110 KB of
+// tables and tiles) share an SM
+template <int C>
+constexpr uint32_t enc_cols() { return C == 1 ? 64 : 32; }
 // warps per CTA: 8 with one channel (~46 KB of smem, 3 CTAs per SM); with three channels the
 // 96 KB of colour tables leave room for one CTA per SM, so that CTA runs 24 warps
 template <int C>
-constexpr uint32_t enc_warps() { return C == 1 ? 8 : 24; }
+constexpr uint32_t enc_warps() { return C == 1 ? 8 : 16; }
 #ifndef SEGHDC_ENC_MINB
 #define SEGHDC_ENC_MINB 4  // resident CTAs per SM with one channel (64 registers, no spills; 3 CTAs: 113 vs 100 us at C1)
 #endif
@@ -91,10 +95,11 @@ constexpr uint32_t enc_warps() { return C == 1 ? 8 : 24; }
 // H: weight-16 planes of the column-sum counters, the fewest that hold the pixels one warp
 // encodes (its ripple is 2 LOP3 per plane per 16 pixels on the ALU-bound path)
 template <int C, int H>
-__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB : 1)
+__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB : 2)
     k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
              uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t* __restrict__ colsum, uint32_t W32) {
+    constexpr uint32_t kEncCols = enc_cols<C>();
     extern __shared__ __align__(16) uint32_t es[];
     uint32_t* s_wid = es;                            // [C][256][32]
     uint32_t* s_col = s_wid + C * 256 * 32;          // [EC][32]
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB 
 
 template <int C, int H>
 static void launch_encode_ch(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
+    constexpr uint32_t kEncCols = enc_cols<C>();
     const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
     ensure_dynamic_smem((const void*)k_encode<C, H>, smem);
     k_encode<C, H><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
@@ -215,7 +221,7 @@ template <int C>
 static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
     const uint64_t rows_per = (uint64_t(row_end - row_begin) + g.z - 1) / g.z;
     const uint64_t per_warp = (rows_per + kEncRows - 1) / kEncRows * ((kEncRows + enc_warps<C>() - 1) / enc_warps<C>()) *
-                              kEncCols;
+                              enc_cols<C>();
     if (per_warp <= BitCounter<6>::capacity()) return launch_encode_ch<C, 6>(a, g, row_begin, row_end, s);
     if (per_warp <= BitCounter<8>::capacity()) return launch_encode_ch<C, 8>(a, g, row_begin, row_end, s);
     if (per_warp <= BitCounter<10>::capacity()) return launch_encode_ch<C, 10>(a, g, row_begin, row_end, s);
@@ -226,7 +232,8 @@ void launch_encode(const EncodeArgs& a, cudaStream_t s) {
     const uint64_t n = a.pix_end - a.pix_begin;
     if (n == 0) return;
     const uint32_t row_begin = uint32_t(a.pix_begin / a.w), row_end = uint32_t(a.pix_end / a.w);
-    const uint32_t gx = (a.w + kEncCols - 1) / kEncCols, gz = (a.S32 + 31) / 32;
+    const uint32_t ec = a.c == 1 ? enc_cols<1>() : enc_cols<3>();
+    const uint32_t gx = (a.w + ec - 1) / ec, gz = (a.S32 + 31) / 32;
     // row groups: up to ~6 CTAs per SM in total, but each CTA covers enough rows to amortise
     // staging its table chunk (C x 32 KB) over >= 32*C rows
     const uint32_t rows = row_end - row_begin;
