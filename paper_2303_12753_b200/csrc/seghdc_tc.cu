@@ -78,7 +78,14 @@ struct TcCfg {
 #else  // experiment: 3 A buffers and one accumulator set in the split layout (32 warps)
     static constexpr uint32_t AB = 3;
 #endif
+#ifdef SEGHDC_C3_UH2
+    // experiment: the K <= 4 layout (no fold warps) with two unpack warps per chunk
+    static constexpr bool FOLD = NCOL == 16 && SPLIT == 1;    // fold warps (incremental K == 2 schedule)
+    static constexpr uint32_t UH = (SPLIT > 1 || !FOLD) ? 2 : 1;  // unpack warps sharing one chunk (halves)
+#else
+    static constexpr bool FOLD = SPLIT == 1;                  // fold warps (incremental K == 2 schedule)
     static constexpr uint32_t UH = SPLIT > 1 ? 2 : 1;        // unpack warps sharing one chunk (halves)
+#endif
     static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
 #if defined(SEGHDC_SPLIT_AB3)
     static constexpr uint32_t DB = SPLIT > 1 ? 1 : 2;
@@ -96,9 +103,10 @@ struct TcCfg {
     static constexpr uint32_t NMW = (NCOL == 16 || (NCOL == 32 && SPLIT == 1)) ? 2 : 1;
 #endif
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
-    static constexpr uint32_t WMma0 = SPLIT > 1 ? WEpi + 4 : 18, WProd = SPLIT > 1 ? WEpi + 5 : 20;
+    static constexpr uint32_t WMma0 = (SPLIT > 1 || !FOLD) ? WEpi + 4 : 18;
+    static constexpr uint32_t WProd = (SPLIT > 1 || !FOLD) ? WEpi + 4 + NMW : 20;
     static constexpr uint32_t WFin = WEpi + 6;               // SPLIT: 2 finalizer warps (labels), by tile parity
-    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 8 : 23;
+    static constexpr uint32_t Warps = SPLIT > 1 ? WEpi + 8 : FOLD ? 23 : WEpi + 5 + NMW;
     static constexpr uint32_t ColD = 128 * AB;
     static constexpr uint32_t ColSF = ColD + DB * NMW * NCOL;  // after D[DB tile parities][NMW]
     static_assert(Stages % AB == 0, "ring slots follow the unpack phases");
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c) ccount[c] += best == c;
             }
-            if (SPLIT == 1) TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
+            if (SPLIT == 1 && Cfg::FOLD) TCW(4, it, &list_free[db], ((it >> 1) & 1) ^ 1);
             // incremental re-bundling: pixels whose membership of a tracked cluster c >= 1 changed
             // (old = 0xFFFFFFFF before round 1); entering pixels add their HV, leaving pixels their
             // complement (flag). Global lists (one per tracked cluster, n entries apart) for
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 SG_CHECK(!take || base + __popc(m & ((1u << lane) - 1)) < kTP);
                 if (take) s_list[db * kTP + base + __popc(m & ((1u << lane) - 1))] = (32 * qd + lane) | (leave ? 0x100u : 0u);
             }
-            if (SPLIT == 1) mbar_arrive(&list_ready[db]);
+            if (SPLIT == 1 && Cfg::FOLD) mbar_arrive(&list_ready[db]);
             if (qd == 0) TC_TR(5, it);
         }
         for (int o = 16; o; o >>= 1) {
@@ -838,7 +846,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 
     // ---------------------------------------------------------------------------- fold warps
     BitCounter<UPD ? H : 1> cnt[CPTMAX];
-    const int fw = SPLIT == 1 ? fold_index(warp) : -1;
+    const int fw = (SPLIT == 1 && Cfg::FOLD) ? fold_index(warp) : -1;
     const uint32_t rt = uint32_t(fw) * 32 + lane;
     const uint32_t cpt = (W32 + NRT - 1) / NRT;
     uint32_t nleave = 0;  // leaving pixels folded by this CTA (same count in every fold thread)
