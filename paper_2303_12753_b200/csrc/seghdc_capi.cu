@@ -1474,7 +1474,7 @@ int seghdc_run_pipeline_closed(seghdc_ctx* ctx, const uint8_t* pixels, size_t h,
         size_t rounds = 0;
         for (size_t r = 1; r <= iterations; ++r) {  // clusterer.cpp:208-216
             ck(cudaMemsetAsync(changed.p, 0, 8, ctx->stream), "clear changed");
-            st.wraps = ctx->wraps_hist.p + (r - 1);
+            st.wraps = ctx->count_wraps ? ctx->wraps_hist.p + (r - 1) : nullptr;  // opt-in counting
             launch_closed_assign(a, st, ctx->sms, ctx->stream);
             ctx->count();
             ctx->check_launch();

@@ -123,6 +123,8 @@ __global__ void k_closed_seed(ClosedArgs a, const uint64_t* __restrict__ seeds, 
 
 constexpr int kMaxK = 32;
 
+// WR: also count the comparisons whose 128-bit products wrapped (opt-in diagnostic)
+template <bool WR>
 __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState s) {
     __shared__ unsigned long long sP[kMaxK], sN[kMaxK];
     for (uint32_t k = threadIdx.x; k < a.K; k += blockDim.x) sP[k] = s.P[k], sN[k] = s.norm2[k];
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
             if (k == 0) {
                 best_dot = dot, best_n2 = n2;
             } else {
-                nwrap += compare_wraps(dot, n2, best_dot, best_n2);
+                if (WR) nwrap += compare_wraps(dot, n2, best_dot, best_n2);
                 if (strictly_closer_dev(dot, n2, best_dot, best_n2)) best = k, best_dot = dot, best_n2 = n2;
             }
         }
@@ -155,14 +157,15 @@ __global__ void __launch_bounds__(256) k_closed_assign(ClosedArgs a, ClosedState
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
-        nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
+        if (WR) nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
     }
     if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
-    if ((threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
+    if (WR && (threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
 }
 
 // assign_labels with the K prefix tables restricted to the L endpoint positions, staged once per
 // CTA in shared memory ([K][L] int64): 10 shared-memory loads per pixel and cluster.
+template <bool WR>
 __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, ClosedState s) {
     extern __shared__ long long sq[];
     __shared__ unsigned long long sP[kMaxK], sN[kMaxK];
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
             if (k == 0) {
                 best_dot = dot, best_n2 = n2;
             } else {
-                nwrap += compare_wraps(dot, n2, best_dot, best_n2);
+                if (WR) nwrap += compare_wraps(dot, n2, best_dot, best_n2);
                 if (strictly_closer_dev(dot, n2, best_dot, best_n2)) best = k, best_dot = dot, best_n2 = n2;
             }
         }
@@ -202,10 +205,10 @@ __global__ void __launch_bounds__(512) k_closed_assign_smem(ClosedArgs a, Closed
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         changed += __shfl_xor_sync(0xFFFFFFFFu, changed, o);
-        nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
+        if (WR) nwrap += __shfl_xor_sync(0xFFFFFFFFu, nwrap, o);
     }
     if ((threadIdx.x & 31) == 0 && changed) atomicAdd(s.changed, changed);
-    if ((threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
+    if (WR && (threadIdx.x & 31) == 0 && nwrap && s.wraps) atomicAdd(s.wraps, (unsigned long long)nwrap);
 }
 
 // grid = (blocks, cluster groups); group y owns clusters [y*G, y*G + G), one difference array
@@ -433,6 +436,116 @@ __global__ void __launch_bounds__(kFinT) k_closed_finish_smem(ClosedArgs a, Clos
 
 size_t fin_smem_bytes(uint32_t dim) { return (size_t(fin_skew(dim)) + 1 + fin_skew(dim)) * 4; }
 
+// ---- the finish spread over a thread-block cluster per centroid (round 2) -----------------------
+// k_closed_finish_smem runs one CTA per cluster: at K = 2 two SMs scan D positions through three
+// serial passes and the round waits on them (latency-bound, half of a C1 closed-form run). Here a
+// cluster of kFinG CTAs shares each centroid: CTA r owns positions [r seg, (r+1) seg), and the
+// two prefix sums (c, then Q) and the norm2 / P reductions combine their per-CTA totals through
+// distributed shared memory. Same integers in the same order of summation per position, so
+// bit-identical to k_closed_finish.
+constexpr int kFinG = 8, kFinCT = 256;
+__device__ __forceinline__ void fin_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ long long fin_peer_ll(const long long* local, uint32_t rank) {
+    uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(local)), peer;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(addr), "r"(rank));
+    long long v;
+    asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(peer) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kFinCT) k_closed_finish_cl(ClosedArgs a, ClosedState s) {
+    using ScanI = cub::BlockScan<long long, kFinCT>;
+    using RedU = cub::BlockReduce<unsigned long long, kFinCT>;
+    __shared__ union {
+        typename ScanI::TempStorage scan;
+        typename RedU::TempStorage red;
+    } tmp;
+    __shared__ long long xch[4];  // this CTA's totals: [c, Q increments, norm2, P]
+    extern __shared__ int32_t fcl_sm[];
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t k = blockIdx.x / kFinG, stride = a.dim + 1, tid = threadIdx.x;
+    const uint32_t seg = (a.dim + kFinG - 1) / kFinG, p0 = min(a.dim, rank * seg), p1 = min(a.dim, p0 + seg);
+    const uint32_t len = p1 - p0;
+    int32_t* sd = fcl_sm;                      // [seg + 1] counts of positions p0.., then z
+    uint8_t* sb = reinterpret_cast<uint8_t*>(fcl_sm + seg + 1);
+    const unsigned long long n = s.cnt[k];
+    fin_cluster_sync();  // every CTA of the cluster read cnt[k] before it is reset
+    if (rank == 0 && tid == 0) s.counts[k] = n, s.cnt[k] = 0;
+    if (n == 0) return;  // cluster-uniform
+    int32_t* d = s.diff + size_t(k) * stride;
+    for (uint32_t t = tid; t < len; t += kFinCT) {
+        sd[t] = __ldcg(d + p0 + t);
+        d[p0 + t] = 0;
+        sb[t] = __ldg(s.bflag + p0 + t);
+    }
+    if (rank == kFinG - 1 && tid == 0) d[a.dim] = 0;
+    __syncthreads();
+    if (s.diffc) {  // compressed counts of this CTA's positions
+        int32_t* dc = s.diffc + size_t(k) * a.L;
+        for (uint32_t t = tid; t < a.L; t += kFinCT) {
+            const uint32_t pos = closed_pos(a, t);
+            const bool mine = (pos >= p0 && pos < p1) || (pos == a.dim && rank == kFinG - 1);
+            if (!mine) continue;
+            const int32_t v = dc[t];
+            if (v) {
+                if (pos < a.dim) atomicAdd(sd + (pos - p0), v);
+                dc[t] = 0;
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t chunk = (len + kFinCT - 1) / kFinCT;
+    const uint32_t i0 = min(len, tid * chunk), i1 = min(len, i0 + chunk);
+    long long part = 0;
+    for (uint32_t i = i0; i < i1; ++i) part += sd[i];
+    long long c, ctot;
+    ScanI(tmp.scan).ExclusiveSum(part, c, ctot);
+    if (tid == 0) xch[0] = ctot;
+    fin_cluster_sync();
+    for (uint32_t r = 0; r < rank; ++r) c += fin_peer_ll(&xch[0], r);  // prefix of the lower CTAs
+    __syncthreads();
+    uint32_t* z = s.Z + size_t(k) * a.dim;
+    long long* q = s.Q + size_t(k) * stride;
+    unsigned long long n2 = 0, pb = 0;
+    long long sp = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+        c += sd[i];
+        const bool b = sb[i];
+        const unsigned long long zi = b ? n - (unsigned long long)c : (unsigned long long)c;
+        z[p0 + i] = uint32_t(zi);
+        sd[i] = int32_t(uint32_t(zi));
+        n2 += zi * zi;
+        if (b) pb += zi, sp -= (long long)zi;
+        else sp += (long long)zi;
+    }
+    long long qb, qtot;
+    ScanI(tmp.scan).ExclusiveSum(sp, qb, qtot);
+    __syncthreads();
+    n2 = RedU(tmp.red).Sum(n2);
+    __syncthreads();
+    pb = RedU(tmp.red).Sum(pb);
+    if (tid == 0) xch[1] = qtot, xch[2] = (long long)n2, xch[3] = (long long)pb;
+    fin_cluster_sync();
+    for (uint32_t r = 0; r < rank; ++r) qb += fin_peer_ll(&xch[1], r);
+    if (rank == 0 && tid == 0) {
+        unsigned long long tn2 = 0, tpb = 0;
+        for (uint32_t r = 0; r < kFinG; ++r)
+            tn2 += (unsigned long long)fin_peer_ll(&xch[2], r), tpb += (unsigned long long)fin_peer_ll(&xch[3], r);
+        s.norm2[k] = tn2;
+        s.P[k] = tpb;
+        q[0] = 0;
+    }
+    for (uint32_t i = i0; i < i1; ++i) {
+        const long long zi = uint32_t(sd[i]);
+        qb += sb[i] ? -zi : zi;
+        q[p0 + i + 1] = qb;
+    }
+    fin_cluster_sync();  // no CTA leaves while a peer may still read its totals
+}
+
 }  // namespace
 
 void launch_closed_seed(const ClosedArgs& a, const uint64_t* seeds, ClosedState s, cudaStream_t st) {
@@ -442,13 +555,15 @@ void launch_closed_seed(const ClosedArgs& a, const uint64_t* seeds, ClosedState 
 void launch_closed_assign(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
     const size_t smem = size_t(a.L) * a.K * 8;
     if (s.diffc) {  // compressed indices fit (seghdc_run_pipeline_closed decides)
-        ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_assign_smem), smem);
+        auto kern = s.wraps ? k_closed_assign_smem<true> : k_closed_assign_smem<false>;
+        ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
         const uint64_t blocks = std::min<uint64_t>((a.n + 511) / 512, uint64_t(sms) * (smem <= (100u << 10) ? 2 : 1));
-        k_closed_assign_smem<<<uint32_t(std::max<uint64_t>(blocks, 1)), 512, smem, st>>>(a, s);
+        kern<<<uint32_t(std::max<uint64_t>(blocks, 1)), 512, smem, st>>>(a, s);
         return;
     }
     const uint64_t blocks = std::min<uint64_t>((a.n + 255) / 256, uint64_t(sms) * 8);
-    k_closed_assign<<<uint32_t(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(a, s);
+    auto kern = s.wraps ? k_closed_assign<true> : k_closed_assign<false>;
+    kern<<<uint32_t(std::max<uint64_t>(blocks, 1)), 256, 0, st>>>(a, s);
 }
 
 void launch_closed_accumulate(const ClosedArgs& a, ClosedState s, int sms, cudaStream_t st) {
@@ -469,6 +584,27 @@ void launch_closed_accumulate(const ClosedArgs& a, ClosedState s, int sms, cudaS
 }
 
 void launch_closed_finish(const ClosedArgs& a, ClosedState s, cudaStream_t st) {
+    const char* fe = getenv("SEGHDC_CLOSED_FIN");  // "smem": the one-CTA kernels (read per launch)
+    if (!(fe && *fe) && !getenv("SEGHDC_CLOSED_FIN_GLOBAL")) {
+        const uint32_t seg = (a.dim + kFinG - 1) / kFinG;
+        const size_t smem = (size_t(seg) + 1) * 4 + seg;
+        if (ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_finish_cl), smem) == cudaSuccess) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(a.K * kFinG);
+            cfg.blockDim = dim3(kFinCT);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = kFinG;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, k_closed_finish_cl, a, s) == cudaSuccess) return;
+            cudaGetLastError();
+        }
+    }
     const size_t smem = fin_smem_bytes(a.dim);
     if (!getenv("SEGHDC_CLOSED_FIN_GLOBAL") && smem <= (200u << 10) &&
         ensure_dynamic_smem(reinterpret_cast<const void*>(k_closed_finish_smem), smem) == cudaSuccess) {

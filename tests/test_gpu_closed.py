@@ -117,3 +117,11 @@ def test_closed_global_finish_matches(ctx, port, case, monkeypatch):
     if case[0] < 25000:
         monkeypatch.setenv("SEGHDC_CLOSED_FIN_GLOBAL", "1")
     test_closed_matches_oracle(ctx, port, case)
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[4], CASES[8]])
+def test_closed_one_cta_shared_memory_finish_matches(ctx, port, case, monkeypatch):
+    """The one-CTA shared-memory finish (SEGHDC_CLOSED_FIN=smem; the default is the cluster
+    finish, k_closed_finish_cl) gives the same results."""
+    monkeypatch.setenv("SEGHDC_CLOSED_FIN", "smem")
+    test_closed_matches_oracle(ctx, port, case)
