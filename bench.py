@@ -266,11 +266,10 @@ def main():
 
     world, rank, local = dist_env()
     # SEGHDC_BENCH_GLOO=1: a dry run of the N > 1 control flow on a one-GPU box (every rank on
-    # cuda:0, gloo for the host-side barrier / max; the data path has no collective for C0-C2).
-    # Not a measurement: ranks share one GPU. Row-sharded configs need NCCL and distinct GPUs.
+    # cuda:0, gloo for the host-side barrier / max and, for C3/C4, a host-staged all-reduce
+    # callback instead of NCCL). Not a measurement: the ranks share one GPU.
     dry = bool(os.environ.get("SEGHDC_BENCH_GLOO")) and world > 1
-    if dry:
-        assert not (args.config in (3, 4)), "SEGHDC_BENCH_GLOO dry runs cover the unsharded configs only"
+    if dry:  # row-sharded configs exchange through the host-staged gloo callback instead of NCCL
         local = 0
     coll_dev = "cpu" if dry else None
     if world > 1:
@@ -300,9 +299,13 @@ def main():
     if sharded:
         # the library's own sharded loop: one ncclAllReduce per round inside the C-ABI, on the
         # context's stream (rank 0's NCCL unique id reaches the others through torch.distributed)
-        uid = [S.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(uid, src=0)
-        ctx.nccl_init(uid[0], rank, world)
+        if dry:
+            from paper_2303_12753_b200.sharded import gloo_collective
+            ctx.set_allreduce(gloo_collective(), rank, world)
+        else:
+            uid = [S.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(uid, src=0)
+            ctx.nccl_init(uid[0], rank, world)
         r0, r1 = S.shard_rows(h, rank, world)
 
         def step():
