@@ -353,3 +353,40 @@ def test_run_pipeline_large_golden(ctx, golden_configs, name):
         res = ctx.run_pipeline(img, cfg)
         assert sha(res.mask.astype(np.uint32).reshape(-1)) == g["labels_sha256"]
         assert res.iterations_run == g["rounds"]
+
+
+def test_run_pipeline_graph_switches(ctx, port):
+    """run_pipeline's CUDA-graph cache across changing call signatures: shape A (eager, then
+    captured, then replayed), shape B, back to A, then A with a per-round callback (eager path,
+    labels of every round) and with a pageable label buffer — every result equals the oracle."""
+    def case(h, w, c, k, its, seed):
+        rng = np.random.default_rng(seed)
+        img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+        img[: h // 2] //= 4
+        cfg = S.RunConfig(dim=4096, alpha=1.0, beta=3, gamma=1, clusters=k, iterations=its, seed=seed,
+                          early_stop=False)
+        cb = S.build_codebooks(4096, h, w, c, 1.0, 3, 1, seed)
+        exp = port.cluster(port.encode(img, 4096, *cb), img, 4096, k, its, False, per_round=True)
+        return img, cfg, exp
+
+    a, b = case(60, 70, 3, 3, 5, 1), case(33, 90, 1, 2, 4, 2)
+    for img, cfg, exp in (a, a, a, b, b, a, b, a):
+        res = ctx.run_pipeline(img, cfg)
+        assert (res.mask.reshape(-1) == exp["labels"]).all() and res.iterations_run == exp["rounds"]
+    img, cfg, exp = a
+    rounds = []
+    res = ctx.run_pipeline(img, cfg, on_iteration=lambda r, lab: rounds.append(lab.reshape(-1).copy()))
+    assert len(rounds) == exp["rounds"]
+    for r in range(exp["rounds"]):
+        assert (rounds[r] == exp["labels_rounds"][r]).all(), r
+    labels = np.zeros(img.shape[0] * img.shape[1], np.uint32)  # pageable: staged, not zero-copy
+    rc = ctx.run_pipeline(img, cfg)  # replayed graph (zero-copy into the pinned buffer)
+    assert (rc.mask.reshape(-1) == exp["labels"]).all()
+    lib = S.lib()
+    rounds_c = S._sz()
+    import ctypes as C
+    h, w, c = img.shape
+    ctx.check(lib.seghdc_run_pipeline(ctx.h, img, h, w, c, cfg.dim, float(cfg.alpha), cfg.beta, cfg.gamma,
+                                      cfg.clusters, cfg.iterations, cfg.seed, 0, 0, S.ROUND_CB(0), None, labels,
+                                      C.byref(rounds_c), None))
+    assert (labels == exp["labels"]).all() and rounds_c.value == exp["rounds"]
