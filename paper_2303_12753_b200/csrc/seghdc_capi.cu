@@ -155,10 +155,9 @@ struct Geometry {
     void set(size_t dim) {
         D = uint32_t(dim);
         W32 = uint32_t((dim + 31) / 32);
-        // rows padded to whole 128-byte lines once an HV spans a line: the encode's 128-byte
-        // stores then never straddle two lines (0.135 -> 0.126 ms at C1); short HVs keep 16-B rows
-        const uint32_t a = W32 >= 32 ? 32u : 4u;
-        S32 = (W32 + a - 1) / a * a;
+        // rows padded to whole 128-byte lines: the encode's 128-byte stores never straddle two
+        // lines (0.135 -> 0.126 ms at C1), and a short HV's row is one full TMA box of 32 words
+        S32 = (W32 + 31) / 32 * 32;
         SS = S32 + ((S32 % 32 == 0) ? 4 : 0);  // keep LDS.128 of adjacent rows on distinct banks
         nwarp_words = (W32 + 31) / 32;
         W32P = nwarp_words * 32;

@@ -52,6 +52,12 @@ constexpr uint32_t kP8 = 8;        // balanced base-8 digits per centroid entry 
 // sub-partition. The dimension-split kernel (SPLIT = 4, below) has no fold warps: [0, 8) unpack
 // (2 per lane quarter), [8, 12) epilogue, 12 MMA, 13 producer.
 constexpr uint32_t kNRW = 4;
+// chunks per tile: at least 2, so the two MMA warps of the K <= 2 layout (alternating chunks)
+// both write their accumulators; a short HV's second chunk is all zeros (TMA out-of-bounds fill)
+__host__ __device__ __forceinline__ uint32_t tc_chunks(uint32_t W32) {
+    const uint32_t c = (W32 + kCW - 1) / kCW;
+    return c < 2 ? 2u : c;
+}
 __device__ __forceinline__ int fold_index(uint32_t warp) {
     return warp == 16 ? 0 : warp == 17 ? 1 : warp == 21 ? 2 : warp == 22 ? 3 : -1;
 }
@@ -69,12 +75,12 @@ struct TcCfg {
     // the split layout uses balanced base 9 (digits -4..4: each digit and half-digit is still an
     // e2m1 value), so 8 digits cover entries up to 4 (9^8 - 1) / 8 = 21.5M (images of 2^24
     // pixels) with N = 8 x 8 = 64 columns instead of 9 base-8 digits (N = 72)
-    static constexpr uint32_t BASE = SPLIT > 1 ? 9 : 8;
+    static constexpr uint32_t BASE = (SPLIT > 1 || NCOL == 64) ? 9 : 8;
     static constexpr uint32_t NDIG = kP8;
     static constexpr uint32_t KC = NCOL / NDIG;              // clusters of the layout
     static constexpr uint32_t KB = NCOL * 32;                // B image bytes per k-step: N rows x 64 e2m1
 #ifndef SEGHDC_SPLIT_AB3
-    static constexpr uint32_t AB = SPLIT > 1 ? 2 : 3;        // A buffers in TMEM (128 columns each)
+    static constexpr uint32_t AB = (SPLIT > 1 || NCOL == 64) ? 2 : 3;  // A buffers in TMEM (128 columns each)
 #else  // experiment: 3 A buffers and one accumulator set in the split layout (32 warps)
     static constexpr uint32_t AB = 3;
 #endif
@@ -83,8 +89,8 @@ struct TcCfg {
     static constexpr bool FOLD = NCOL == 16 && SPLIT == 1;    // fold warps (incremental K == 2 schedule)
     static constexpr uint32_t UH = (SPLIT > 1 || !FOLD) ? 2 : 1;  // unpack warps sharing one chunk (halves)
 #else
-    static constexpr bool FOLD = SPLIT == 1;                  // fold warps (incremental K == 2 schedule)
-    static constexpr uint32_t UH = SPLIT > 1 ? 2 : 1;        // unpack warps sharing one chunk (halves)
+    static constexpr bool FOLD = SPLIT == 1 && NCOL <= 32;    // fold warps (incremental K == 2 schedule)
+    static constexpr uint32_t UH = (SPLIT > 1 || NCOL == 64) ? 2 : 1;  // unpack warps sharing one chunk (halves)
 #endif
     static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
 #if defined(SEGHDC_SPLIT_AB3)
@@ -94,7 +100,7 @@ struct TcCfg {
 #else
     static constexpr uint32_t DB = (NCOL == 32 && SPLIT == 1) ? 1 : 2;
 #endif
-    static constexpr uint32_t Stages = NCOL == 16 ? 9 : SPLIT > 1 ? (AB == 3 ? 3 : 4) : 3;  // smem ring depth (16 KB each):
+    static constexpr uint32_t Stages = NCOL == 16 ? 9 : (SPLIT > 1 || NCOL == 64) ? (AB == 3 ? 3 : 4) : 3;  // smem ring depth (16 KB each):
                                                              // the larger B image takes the rest; a multiple
                                                              // of AB, so slot g % Stages is unpacked by phase g % AB
 #ifndef SEGHDC_C3_NMW2
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     const uint32_t qrank = SPLIT > 1 ? cl_rank() : 0u;  // SPLIT: dimension quarter = rank in the cluster
     const uint32_t cid = blockIdx.x / SPLIT, ncl = gridDim.x / SPLIT;  // tiles go to clusters
 
-    const uint32_t nch_all = (W32 + kCW - 1) / kCW;  // chunks per tile
+    const uint32_t nch_all = tc_chunks(W32);  // chunks per tile
     // SPLIT: this CTA's chunks [ch0, ch0 + nch) of every tile; its B image slice starts at ch0
     const uint32_t ch0 = qrank * nch_all / SPLIT, nch = (qrank + 1) * nch_all / SPLIT - ch0;
     const uint64_t ntiles = (n + kTP - 1) / kTP;
@@ -1185,7 +1191,7 @@ template <bool UPD, int H, uint32_t NCOL, uint32_t SPLIT = 1, bool WR = false>
 cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
     using Cfg = TcCfg<NCOL, SPLIT>;
     auto kern = k_round_tc<UPD, H, NCOL, SPLIT, WR>;
-    const uint32_t nch = (a.W32 + kCW - 1) / kCW;
+    const uint32_t nch = tc_chunks(a.W32);
     const uint32_t nks = SPLIT > 1 ? (nch + SPLIT - 1) / SPLIT * kKS : a.nks;  // B k-steps resident per CTA
     const size_t smem = TcSmem<NCOL, SPLIT>::total(nks);
     cudaError_t e = ensure_dynamic_smem((const void*)kern, smem);
@@ -1235,17 +1241,25 @@ cudaError_t launch_tc_t(const RoundArgs& a, cudaStream_t s) {
 }  // namespace
 
 // Layout of the tcgen05 kernel for (K, W32): N = 16 digit columns (K <= 2) or 32 (K <= 4) with
-// the whole B image resident in one CTA; N = 64 (K <= 8, 8 base-9 digits) split over a cluster of 4
-// CTAs when the whole image does not fit; 0: no tcgen05 layout (IMMA kernels).
+// the whole B image resident in one CTA; N = 64 (K <= 8, 8 base-9 digits) in one CTA for short
+// HVs, split over a cluster of 4 CTAs otherwise; 0: no tcgen05 layout (IMMA kernels).
 constexpr size_t kSmemOptin = 232448;  // B200: 227 KB of dynamic shared memory per CTA
-static uint32_t tc_nchunks(uint32_t W32) { return (W32 + kCW - 1) / kCW; }
+static uint32_t tc_nchunks(uint32_t W32) { return tc_chunks(W32); }
+uint32_t tc_split(uint32_t K, uint32_t W32) {
+    const uint32_t nch = tc_nchunks(W32), nks = nch * kKS;
+    if (K < 1 || K > 8) return 0;
+    if (K <= 2 && W32 <= 3 * kNRW * 32 && TcSmem<16>::total(nks) <= kSmemOptin) return 1;
+    if (K <= 4 && TcSmem<32>::total(nks) <= kSmemOptin) return 1;
+    if (K > 4 && TcSmem<64>::total(nks) <= kSmemOptin) return 1;
+    if (nch >= 4 && TcSmem<64, 4>::total((nch + 3) / 4 * kKS) <= kSmemOptin) return 4;
+    return 0;
+}
 uint32_t tc_ncol(uint32_t K, uint32_t W32) {
     const uint32_t nch = tc_nchunks(W32), nks = nch * kKS;
-    if (K < 1 || W32 <= kCW) return 0;
+    if (K < 1 || K > 8) return 0;
     if (K <= 2 && W32 <= 3 * kNRW * 32 && TcSmem<16>::total(nks) <= kSmemOptin) return 16;
     if (K <= 4 && TcSmem<32>::total(nks) <= kSmemOptin) return 32;
-    if (K <= 8 && nch >= 4 && TcSmem<64, 4>::total((nch + 3) / 4 * kKS) <= kSmemOptin) return 64;
-    return 0;
+    return tc_split(K, W32) ? 64 : 0;
 }
 bool tc_supported(uint32_t K, uint32_t W32) { return tc_ncol(K, W32) != 0; }
 static uint32_t tc_ndig(uint32_t ncol) { return ncol == 64 ? TcCfg<64, 4>::NDIG : kP8; }
@@ -1263,7 +1277,8 @@ size_t tc_smem_bytes(uint32_t K, uint32_t W32) {
     const uint32_t nc = tc_ncol(K, W32), nch = tc_nchunks(W32);
     return nc == 16 ? TcSmem<16>::total(tc_ksteps(W32))
          : nc == 32 ? TcSmem<32>::total(tc_ksteps(W32))
-         : nc == 64 ? TcSmem<64, 4>::total((nch + 3) / 4 * kKS)
+         : nc == 64 ? (tc_split(K, W32) == 1 ? TcSmem<64>::total(tc_ksteps(W32))
+                                              : TcSmem<64, 4>::total((nch + 3) / 4 * kKS))
                     : ~size_t(0);
 }
 size_t tc_bimg_bytes(uint32_t K, uint32_t W32) { return size_t(tc_ksteps(W32)) * tc_ncol(K, W32) * 32; }
@@ -1314,7 +1329,10 @@ static cudaError_t launch_round_tc_sel(const RoundArgs& a, cudaStream_t s) {
             if (a.K == 2) return launch_round_tc_body(a, s);
             return a.wraps ? launch_tc_t<false, 1, 16, 1, true>(a, s) : launch_tc_t<false, 1, 16>(a, s);
         case 32: return a.wraps ? launch_tc_t<false, 1, 32, 1, true>(a, s) : launch_tc_t<false, 1, 32>(a, s);
-        case 64: return a.wraps ? launch_tc_t<false, 1, 64, 4, true>(a, s) : launch_tc_t<false, 1, 64, 4>(a, s);
+        case 64:
+            if (tc_split(a.K, a.W32) == 1)
+                return a.wraps ? launch_tc_t<false, 1, 64, 1, true>(a, s) : launch_tc_t<false, 1, 64, 1>(a, s);
+            return a.wraps ? launch_tc_t<false, 1, 64, 4, true>(a, s) : launch_tc_t<false, 1, 64, 4>(a, s);
         default: return cudaErrorInvalidConfiguration;
     }
 }

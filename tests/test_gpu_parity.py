@@ -390,3 +390,30 @@ def test_run_pipeline_graph_switches(ctx, port):
                                       cfg.clusters, cfg.iterations, cfg.seed, 0, 0, S.ROUND_CB(0), None, labels,
                                       C.byref(rounds_c), None))
     assert (labels == exp["labels"]).all() and rounds_c.value == exp["rounds"]
+
+
+@pytest.mark.parametrize("dim,k,kernel", [
+    (32, 2, "k_round_tc"), (700, 3, "k_round_tc"), (1024, 1, "k_round_tc"),  # one chunk, padded to two
+    (3000, 7, "k_round_tc"), (4096, 8, "k_round_tc"),     # K <= 8 on one CTA per tile (N = 64)
+    (16384, 5, "k_round_tc"),                              # K <= 8, split over 4 CTAs
+    (2000, 9, "k_round"), (40000, 2, "k_round"),           # the IMMA-only shapes: K > 8, very long HVs
+])
+def test_round_kernel_layouts(ctx, port, dim, k, kernel):
+    """Which round kernel serves which shape (tcgen05 everywhere a layout fits; the IMMA kernels
+    only for K > 8 and HVs too long for any tcgen05 B image), each bit-exact against the oracle
+    for four full rounds."""
+    rng = np.random.default_rng(dim + 17 * k)
+    h, w, c = 37, 45, 3
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    img[: h // 2] //= 3
+    if dim >= 2048:
+        grid = port.encode(img, dim, *S.build_codebooks(dim, h, w, c, 1.0, 2, 1, k))
+    else:  # too short for the codebooks' flip units at this size: random HVs
+        grid = _rand_grid(rng, h * w, dim)
+    got = []
+    res = ctx.cluster(grid, img, dim, k, 4, False, on_iteration=lambda r, lab: got.append(lab))
+    assert ctx.round_kernel == kernel
+    exp = port.cluster(grid, img, dim, k, 4, False, per_round=True)
+    for r in range(exp["rounds"]):
+        assert (got[r] == exp["labels_rounds"][r]).all(), r
+    assert (res["centroids"] == exp["centroids"]).all() and (res["counts"] == exp["counts"]).all()
