@@ -93,6 +93,16 @@ struct TcCfg {
     static constexpr uint32_t UH = (SPLIT > 1 || NCOL == 64) ? 2 : 1;  // unpack warps sharing one chunk (halves)
 #endif
     static constexpr uint32_t UW = AB * UH;                  // unpack warps per TMEM lane quarter
+#ifndef SEGHDC_NO_HALVES
+    // in the layouts with two unpack warps per chunk (split, N = 64), each half chunk is its own
+    // hand-off (full / free barriers per half, 8 MMAs + a commit per half): the MMAs of a half
+    // start as soon as its two warps are done (C4 rounds 5-8 % faster; measured slower where one
+    // warp unpacks a whole chunk, so those layouts keep whole-chunk hand-offs)
+    static constexpr bool HALVES = UH == 2;
+#else
+    static constexpr bool HALVES = false;
+#endif
+    static constexpr uint32_t NAF = HALVES ? 2 * AB : AB;    // a_free barriers
 #if defined(SEGHDC_SPLIT_AB3)
     static constexpr uint32_t DB = SPLIT > 1 ? 1 : 2;
 #elif !defined(SEGHDC_C3_NMW2)
@@ -163,6 +173,17 @@ __device__ __forceinline__ void tc_mma_chunk(uint32_t d_t, uint32_t a_t, uint64_
         "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
             SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
                 SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
+        "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(KB >> 4), "r"(accum)
+        : "memory");
+}
+template <uint32_t KB>
+__device__ __forceinline__ void tc_mma_half(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                            uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
+            SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
         "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(KB >> 4), "r"(accum)
         : "memory");
 }
@@ -253,7 +274,8 @@ struct TcSmem {
     __host__ __device__ static size_t bars(uint32_t nks) {
         return (xb(nks) + (SPLIT > 1 ? 2 * size_t(SPLIT) * 32 * Cfg::KC * 8 : 0) + 7) & ~size_t(7);
     }
-    static constexpr uint32_t nbars = 2 * Cfg::Stages + 3 * Cfg::AB + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
+    static constexpr uint32_t nbars =
+        2 * Cfg::Stages + 2 * Cfg::AB + Cfg::NAF + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
 
@@ -376,8 +398,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     // per (buffer, consumer) keeps every parity wait in order (a shared barrier consumed by two
     // warps alternately would alias phases)
     uint64_t* a_full = bars + 2 * kStages;      // [kAB][2] A buffer written (tcgen05.st)
-    uint64_t* a_free = a_full + 2 * kAB;        // [kAB] MMAs on the A buffer done (commit)
-    uint64_t* d_full = a_free + kAB;            // [2] tile accumulator complete (commit)
+    uint64_t* a_free = a_full + 2 * kAB;        // [kAB] MMAs on the A buffer done (commit); [2 kAB] by half
+    uint64_t* d_full = a_free + Cfg::NAF;       // [2] tile accumulator complete (commit)
     uint64_t* d_free = d_full + 2;              // [2] epilogue read the accumulator
     uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
     uint64_t* list_free = list_ready + 2;       // [2] fold warps done with the list
@@ -406,11 +428,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_init(&slot_full[s], 1);
             mbar_init(&slot_free[s], 4 * 32 * kUH);
         }
-        for (uint32_t b = 0; b < kAB; ++b) {
-            mbar_init(&a_full[2 * b], 4 * 32 * kUH);
-            mbar_init(&a_full[2 * b + 1], 4 * 32 * kUH);
-            mbar_init(&a_free[b], 1);
+        for (uint32_t b = 0; b < kAB; ++b) {  // HALVES: a_full[2 b + half], one MMA warp
+            mbar_init(&a_full[2 * b], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
+            mbar_init(&a_full[2 * b + 1], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
         }
+        for (uint32_t b = 0; b < Cfg::NAF; ++b) mbar_init(&a_free[b], 1);
         for (uint32_t b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], NMW);  // every MMA warp commits
             mbar_init(&d_free[b], 4 * 32);
@@ -510,7 +532,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             if (!kLdg) TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
             TC_CLK(c1);
             if (warp == 0 && g == 0) TC_TG(3);
-            TCW(2, g, &a_free[ab], ((g / kAB) & 1) ^ 1);
+            TCW(2, g, &a_free[Cfg::HALVES ? 2 * ab + hf : ab], ((g / kAB) & 1) ^ 1);
             __syncwarp();  // lanes leave the spin loops independently; tcgen05.st is .sync.aligned
             TC_CLK(c2);
             if (warp == 0) { TC_ACC(0, c1 - c0); TC_ACC(1, c2 - c1); }
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             PRG(11 * 100000 + g);
             if (!kLdg) mbar_arrive(&slot_free[s]);
             tc_fence_before();
-            mbar_arrive(&a_full[2 * ab + (g % NMW)]);
+            mbar_arrive(&a_full[Cfg::HALVES ? 2 * ab + hf : 2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
     } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp >= Cfg::WFin)) {
@@ -789,6 +811,22 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 TC_CLK(c0);
                 // a_full[2 ab + m] carries chunks g = x + lcm(NMW, kAB) t
                 constexpr uint32_t kLcm = (kAB % NMW == 0) ? kAB : NMW * kAB;
+                if constexpr (Cfg::HALVES) {  // each half chunk as soon as its unpack warps are done
+                    static_assert(!Cfg::HALVES || NMW == 1, "half-chunk hand-offs assume one MMA warp");
+#pragma unroll
+                    for (uint32_t hf = 0; hf < 2; ++hf) {
+                        TCW(7, g, &a_full[2 * ab + hf], (g / kLcm) & 1);
+                        __syncwarp();
+                        tc_fence_after();
+#ifndef SEGHDC_EXP_NOMMA
+                        tc_mma_half<Cfg::KB>(d_t, tbase + ab * 128 + hf * 64,
+                                             bdesc_at(b0 + (ch * kKS + hf * (kKS / 2)) * Cfg::KB), idesc,
+                                             tbase + Cfg::ColSF, (ch >= NMW || hf) ? 1u : 0u);
+#endif
+                        tc_commit(&a_free[2 * ab + hf]);
+                    }
+                    continue;
+                }
                 TCW(7, g, &a_full[2 * ab + m], (g / kLcm) & 1);
                 __syncwarp();  // converge before elect.sync / tcgen05.mma
                 TC_CLK(c1);
