@@ -102,7 +102,12 @@ struct TcCfg {
 #else
     static constexpr bool HALVES = false;
 #endif
-    static constexpr uint32_t NAF = HALVES ? 2 * AB : AB;    // a_free barriers
+#ifdef SEGHDC_QUARTERS  // experiment: quarter-chunk hand-offs (4 MMAs + a commit each)
+    static constexpr uint32_t PARTS = HALVES ? 4 : 1;
+#else
+    static constexpr uint32_t PARTS = HALVES ? 2 : 1;        // hand-offs per chunk
+#endif
+    static constexpr uint32_t NAF = PARTS * AB;              // a_free barriers
 #if defined(SEGHDC_SPLIT_AB3)
     static constexpr uint32_t DB = SPLIT > 1 ? 1 : 2;
 #elif !defined(SEGHDC_C3_NMW2)
@@ -184,6 +189,16 @@ __device__ __forceinline__ void tc_mma_half(uint32_t d_t, uint32_t a_t, uint64_t
         "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
         "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP
             SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
+        "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(KB >> 4), "r"(accum)
+        : "memory");
+}
+template <uint32_t KB>
+__device__ __forceinline__ void tc_mma_quarter(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                               uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t" SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP SEGHDC_KSTEP "}" ::"r"(d_t),
         "r"(a_t), "l"(bdesc), "r"(idesc), "r"(sf), "r"(sf + 4), "n"(KB >> 4), "r"(accum)
         : "memory");
 }
@@ -275,7 +290,8 @@ struct TcSmem {
         return (xb(nks) + (SPLIT > 1 ? 2 * size_t(SPLIT) * 32 * Cfg::KC * 8 : 0) + 7) & ~size_t(7);
     }
     static constexpr uint32_t nbars =
-        2 * Cfg::Stages + 2 * Cfg::AB + Cfg::NAF + 2 + 2 + 2 + 2 + 1 + (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
+        2 * Cfg::Stages + (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * Cfg::AB + Cfg::NAF + 2 + 2 + 2 + 2 + 1 +
+        (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
 
@@ -398,7 +414,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     // per (buffer, consumer) keeps every parity wait in order (a shared barrier consumed by two
     // warps alternately would alias phases)
     uint64_t* a_full = bars + 2 * kStages;      // [kAB][2] A buffer written (tcgen05.st)
-    uint64_t* a_free = a_full + 2 * kAB;        // [kAB] MMAs on the A buffer done (commit); [2 kAB] by half
+    uint64_t* a_free = a_full + (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * kAB;  // [kAB] MMAs on the A buffer done; [PARTS kAB] by part
     uint64_t* d_full = a_free + Cfg::NAF;       // [2] tile accumulator complete (commit)
     uint64_t* d_free = d_full + 2;              // [2] epilogue read the accumulator
     uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
@@ -428,10 +444,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_init(&slot_full[s], 1);
             mbar_init(&slot_free[s], 4 * 32 * kUH);
         }
-        for (uint32_t b = 0; b < kAB; ++b) {  // HALVES: a_full[2 b + half], one MMA warp
-            mbar_init(&a_full[2 * b], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
-            mbar_init(&a_full[2 * b + 1], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
-        }
+        for (uint32_t b = 0; b < (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * kAB; ++b)  // PARTS > 1: a_full[PARTS b + part]
+            mbar_init(&a_full[b], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
         for (uint32_t b = 0; b < Cfg::NAF; ++b) mbar_init(&a_free[b], 1);
         for (uint32_t b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], NMW);  // every MMA warp commits
@@ -532,7 +546,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             if (!kLdg) TCW(1, g, &slot_full[s], (g / kStages) & 1);  // slot s only ever carries this warp's chunks
             TC_CLK(c1);
             if (warp == 0 && g == 0) TC_TG(3);
-            TCW(2, g, &a_free[Cfg::HALVES ? 2 * ab + hf : ab], ((g / kAB) & 1) ^ 1);
+            constexpr uint32_t kPPW = Cfg::PARTS > 1 ? Cfg::PARTS / 2 : 1;  // parts per unpack warp
+            TCW(2, g, &a_free[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf : ab], ((g / kAB) & 1) ^ 1);
             __syncwarp();  // lanes leave the spin loops independently; tcgen05.st is .sync.aligned
             TC_CLK(c2);
             if (warp == 0) { TC_ACC(0, c1 - c0); TC_ACC(1, c2 - c1); }
@@ -568,13 +583,24 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 #else
                 if (a[0] == 0x12345678u) tc_st16(lane_addr + ab * 128 + c16 * 16, a);
 #endif
+                if constexpr (Cfg::PARTS == 4) {  // quarter done: hand it off, claim the next one
+                    if (((c16 + 1) & 1) == 0 && c16 + 1 < (hf + 1) * (8 / kUH)) {
+                        const uint32_t qp = Cfg::PARTS * ab + c16 / 2;
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        tc_fence_before();
+                        mbar_arrive(&a_full[qp]);
+                        TCW(2, g, &a_free[qp + 1], ((g / kAB) & 1) ^ 1);
+                        __syncwarp();
+                        tc_fence_after();
+                    }
+                }
             }
             PRG(10 * 100000 + g);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             PRG(11 * 100000 + g);
             if (!kLdg) mbar_arrive(&slot_free[s]);
             tc_fence_before();
-            mbar_arrive(&a_full[Cfg::HALVES ? 2 * ab + hf : 2 * ab + (g % NMW)]);
+            mbar_arrive(&a_full[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf + (kPPW - 1) : 2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
     } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp >= Cfg::WFin)) {
@@ -814,16 +840,20 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 if constexpr (Cfg::HALVES) {  // each half chunk as soon as its unpack warps are done
                     static_assert(!Cfg::HALVES || NMW == 1, "half-chunk hand-offs assume one MMA warp");
 #pragma unroll
-                    for (uint32_t hf = 0; hf < 2; ++hf) {
-                        TCW(7, g, &a_full[2 * ab + hf], (g / kLcm) & 1);
+                    for (uint32_t pt = 0; pt < Cfg::PARTS; ++pt) {
+                        TCW(7, g, &a_full[Cfg::PARTS * ab + pt], (g / kLcm) & 1);
                         __syncwarp();
                         tc_fence_after();
 #ifndef SEGHDC_EXP_NOMMA
-                        tc_mma_half<Cfg::KB>(d_t, tbase + ab * 128 + hf * 64,
-                                             bdesc_at(b0 + (ch * kKS + hf * (kKS / 2)) * Cfg::KB), idesc,
-                                             tbase + Cfg::ColSF, (ch >= NMW || hf) ? 1u : 0u);
+                        constexpr uint32_t kStepsPP = kKS / Cfg::PARTS;
+                        const uint32_t acc = (ch >= NMW || pt) ? 1u : 0u;
+                        const uint64_t bd = bdesc_at(b0 + (ch * kKS + pt * kStepsPP) * Cfg::KB);
+                        if constexpr (Cfg::PARTS == 4)
+                            tc_mma_quarter<Cfg::KB>(d_t, tbase + ab * 128 + pt * 32, bd, idesc, tbase + Cfg::ColSF, acc);
+                        else
+                            tc_mma_half<Cfg::KB>(d_t, tbase + ab * 128 + pt * 64, bd, idesc, tbase + Cfg::ColSF, acc);
 #endif
-                        tc_commit(&a_free[2 * ab + hf]);
+                        tc_commit(&a_free[Cfg::PARTS * ab + pt]);
                     }
                     continue;
                 }
