@@ -210,6 +210,33 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
         : "memory");
 }
+// Lean issue (the default): ONE elected thread issues NSTEP k-steps from warp-uniform operands, so
+// ptxas keeps every address in uniform registers (UTCOMMA + UIADD3 per k-step). The asm-block
+// variants above predicate each MMA on the per-thread elect result, which costs ~15 instructions
+// and 5 R2UR per MMA: measured 48-60 cycles per MMA inside the busy round kernel against the
+// tensor pipe's 12 / 16 / 32 (N = 16 / 32 / 64; tools/probes/mma_floor.cu).
+__device__ __forceinline__ bool tc_elect() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    return e != 0;
+}
+template <uint32_t KB, uint32_t NSTEP>
+__device__ __forceinline__ void tc_mma_steps(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                             uint32_t accum) {
+#pragma unroll
+    for (uint32_t ks = 0; ks < NSTEP; ++ks)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_t),
+            "r"(a_t + 8 * ks), "l"(bdesc + uint64_t(ks) * (KB >> 4)), "r"(idesc), "r"(sf), "r"(sf + 4),
+            "r"(ks ? 1u : accum)
+            : "memory");
+}
+// commit by the calling (already elected) thread
+__device__ __forceinline__ void tc_commit_one(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -398,7 +425,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     StateView st = StateView::at(state, K);
 
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // the warp index through a shuffle: ptxas then knows it is warp-uniform and keeps the role
+    // branches and the MMA warps' operand addresses on the uniform datapath
+    const uint32_t tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
     const uint32_t parity = round & 1;
     uint32_t* tail = xchg + size_t(K) * Dp;  // [K counts | changed]
     if (warp == 0) TC_TG(0);
@@ -848,10 +877,20 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                         constexpr uint32_t kStepsPP = kKS / Cfg::PARTS;
                         const uint32_t acc = (ch >= NMW || pt) ? 1u : 0u;
                         const uint64_t bd = bdesc_at(b0 + (ch * kKS + pt * kStepsPP) * Cfg::KB);
+#ifdef SEGHDC_OLD_ISSUE
                         if constexpr (Cfg::PARTS == 4)
                             tc_mma_quarter<Cfg::KB>(d_t, tbase + ab * 128 + pt * 32, bd, idesc, tbase + Cfg::ColSF, acc);
                         else
                             tc_mma_half<Cfg::KB>(d_t, tbase + ab * 128 + pt * 64, bd, idesc, tbase + Cfg::ColSF, acc);
+#else
+                        if (tc_elect()) {
+                            tc_mma_steps<Cfg::KB, kStepsPP>(d_t, tbase + ab * 128 + pt * (128 / Cfg::PARTS), bd, idesc,
+                                                            tbase + Cfg::ColSF, acc);
+                            tc_commit_one(&a_free[Cfg::PARTS * ab + pt]);
+                        }
+                        __syncwarp();
+                        continue;
+#endif
 #endif
                         tc_commit(&a_free[Cfg::PARTS * ab + pt]);
                     }
@@ -863,11 +902,20 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 if (m == 0) TC_ACC(2, c1 - c0);
                 tc_fence_after();
                 PRG(12 * 100000 + g);
-#ifndef SEGHDC_EXP_NOMMA  // timing experiment only: the pipeline without the tensor-core work
+#if defined(SEGHDC_EXP_NOMMA)  // timing experiment only: the pipeline without the tensor-core work
+                tc_commit(&a_free[ab]);
+#elif defined(SEGHDC_OLD_ISSUE)
                 tc_mma_chunk<Cfg::KB>(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * Cfg::KB), idesc,
                                       tbase + Cfg::ColSF, ch >= NMW);
-#endif
                 tc_commit(&a_free[ab]);
+#else
+                if (tc_elect()) {
+                    tc_mma_steps<Cfg::KB, kKS>(d_t, tbase + ab * 128, bdesc_at(b0 + ch * kKS * Cfg::KB), idesc,
+                                               tbase + Cfg::ColSF, ch >= NMW ? 1u : 0u);
+                    tc_commit_one(&a_free[ab]);
+                }
+                __syncwarp();
+#endif
                 PRG(13 * 100000 + g);
                 {
                     TC_CLK(c2);

@@ -1,0 +1,95 @@
+// probe (not product code): the tensor-side rate of tcgen05.mma kind::mxf4 M128 N16/32/64 K64 (A in
+// TMEM, B in smem) when the issue is lean (operands in uniform registers, UTCOMMA back to back),
+// alone and with STW warps per sub-partition streaming tcgen05.st into other columns.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+#ifndef PN
+#define PN 16
+#endif
+constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t(PN) >> 3) << 17) | ((128u >> 4) << 24);
+template <int SAMEA>
+__global__ void k(long long* out, int iters, int stw) {
+  extern __shared__ __align__(1024) uint8_t sB[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ volatile int stop;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  for (int i = tid; i < 65536; i += blockDim.x) sB[i] = uint8_t(i * 7) & 0x77;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) { stop = 0; for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i]))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tb = tmem_base;
+  if (warp < 4) {
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = ((tid * 7 + i) * 2654435761u) & 0x22222222u;
+    for (int c = 0; c < 384; c += 16)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(tb + ((32 * warp) << 16) + c), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+    const uint32_t s = 0x7F7F7F7Fu;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(tb + ((32 * warp) << 16) + 500), "r"(s), "r"(s), "r"(s), "r"(s));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) {
+    const uint32_t saddr = smem_u32(sB);
+    const uint64_t bdesc = uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(128 >> 4) << 16) | (uint64_t(256 >> 4) << 32) | (1ull << 46);
+    long long t0 = clock64();
+    uint32_t el;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(el));
+    if (el) {
+      for (int i = 0; i < iters; i += 32) {
+#pragma unroll
+        for (int ks = 0; ks < 32; ++ks)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], p;\n\t}"
+            :: "r"(tb + 400), "r"(tb + (SAMEA ? 0 : 8 * ks)), "l"(bdesc + (PN * 2) * (ks % 16)), "r"(IDESC), "r"(tb + 500), "r"(tb + 502) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar[0])));
+    }
+    __syncwarp();
+    asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W;\n\t}" ::"r"(smem_u32(&bar[0])));
+    long long t1 = clock64();
+    if ((tid & 31) == 0) out[blockIdx.x] = t1 - t0;
+    if ((tid & 31) == 0) stop = 1;
+  } else if (warp >= 4 && warp < 4 + 4 * stw) {  // st warps: columns [256, 384) of their lane quarter
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = ((tid * 7 + i) * 2654435761u) & 0x22222222u;
+    long long n = 0;
+    long long t0 = clock64();
+    while (!stop) {
+#pragma unroll
+      for (int c = 0; c < 128; c += 16)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+          ::"r"(tb + ((32 * (warp & 3)) << 16) + 256 + c), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      ++n;
+    }
+    long long t1 = clock64();
+    if (warp == 4 && (tid & 31) == 0) out[148 + blockIdx.x] = n ? (t1 - t0) / n : 0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb));
+}
+template <int SAMEA> void run(int stw) {
+  long long* d; cudaMalloc(&d, 8 * 296); cudaMemset(d, 0, 8 * 296); long long h = 0, hs = 0;
+  const int iters = 32 * 300;
+  cudaFuncSetAttribute(k<SAMEA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  k<SAMEA><<<148, 128 + 128 * stw, 65536>>>(d, iters, stw); cudaDeviceSynchronize();
+  k<SAMEA><<<148, 128 + 128 * stw, 65536>>>(d, iters, stw); cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(&h, d + 3, 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&hs, d + 148 + 3, 8, cudaMemcpyDeviceToHost);
+  printf("mxf4 M128 N%d K64 lean issue, %s, st warps/SMSP=%d: %.2f cycles per MMA; st: %lld cyc per 16 KB (%s)\n", PN,
+         SAMEA ? "same A columns" : "A walks 256 columns", stw, double(h) / iters, hs, cudaGetErrorString(e));
+}
+int main() { for (int stw = 0; stw <= 3; ++stw) { run<0>(stw); run<1>(stw); } }
