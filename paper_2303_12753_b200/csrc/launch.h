@@ -36,6 +36,8 @@ struct EncodeArgs {
     uint32_t w, c;
     uint64_t pix_begin, pix_end;  // global pixel range encoded into grid[0..)
     const uint32_t *row, *col, *wid;
+    const uint8_t* sup;  // [wref] channel set per HV word (bit ch: wid[ch][*] may be non-zero there)
+    uint32_t nl_max;     // most channels any word has
     uint32_t wref;  // u32 words per table entry (2 * ceil(dim/64))
     uint32_t S32, W32;
     uint32_t* grid;
@@ -148,7 +150,20 @@ struct ExpandArgs {  // closed-form Manhattan codebooks (seghdc_host::manhattan_
     uint32_t off[3], unit[3];
 };
 void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_t* row, uint32_t* col, uint32_t* wid,
-                             cudaStream_t s);
+                             uint8_t* sup, cudaStream_t s);
+// Channels whose dimension segment [off[ch], off[ch + 1] or dim) overlaps HV word q (a superset
+// of the support of the widened Manhattan tables, pixel_pipeline.cpp:66-88), as a bit set.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint8_t manhattan_word_channels(uint32_t dim, uint32_t c, const uint32_t* off, uint32_t q) {
+    uint8_t m = 0;
+    for (uint32_t ch = 0; ch < c && ch < 3; ++ch) {
+        const uint32_t lo = off[ch], hi = (ch + 1 < c && ch + 1 < 3) ? off[ch + 1] : dim;
+        if (lo < hi && lo < 32 * q + 32 && hi > 32 * q) m |= uint8_t(1u << ch);
+    }
+    return m;
+}
 uint64_t tc_max_value(uint32_t K, uint32_t W32);
 uint32_t tc_ncol(uint32_t K, uint32_t W32);  // 16 / 32 (one CTA), 64 (4-CTA dimension split), 0
 // incremental K == 2 schedule of the tcgen05 kernel: xchg row 1 holds the round's delta of

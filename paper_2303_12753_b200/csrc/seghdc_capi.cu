@@ -183,6 +183,9 @@ struct seghdc_ctx {
     size_t h = 0, w = 0, c = 0;
     // codebooks
     DevBuf<uint32_t> row, col, wid;
+    DevBuf<uint8_t> wid_sup;            // channel set per HV word of wid (EncodeArgs::sup)
+    std::vector<uint8_t> wid_sup_host;  // its host copy while an upload may be in flight
+    uint32_t enc_nl = 1;                // most channels any HV word has
     DevBuf<uint64_t> cb_bases;  // closed-form Manhattan codebooks: bases expanded on the device
     size_t cb_dim = 0, cb_h = 0, cb_w = 0, cb_c = 0;
     // grid (rows [row_begin,row_end) of an h_total x w image)
@@ -292,7 +295,7 @@ void require(bool cond, const std::string& msg) {
 // ---- resident data ---------------------------------------------------------------------------
 void load_image(seghdc_ctx& x, const uint8_t* px, size_t h, size_t w, size_t c) {
     seghdc_host::validate_image(h, w, c);
-    x.img.ensure(h * w * c);
+    x.img.ensure(h * w * c + 64);  // the encode kernel reads whole 4-pixel groups (up to 16 bytes past a ragged row end)
     // host or device pointer (unified addressing): a batch kept resident in HBM loads D2D
     ck(cudaMemcpyAsync(x.img.p, px, h * w * c, cudaMemcpyDefault, x.stream), "upload image");
     x.h = h;
@@ -309,6 +312,20 @@ void load_codebooks(seghdc_ctx& x, size_t dim, size_t h, size_t w, size_t c, con
     ck(cudaMemcpyAsync(x.row.p, row, h * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload rows");
     ck(cudaMemcpyAsync(x.col.p, col, w * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload cols");
     ck(cudaMemcpyAsync(x.wid.p, wid, c * 256 * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload colour tables");
+    // channel set per 32-bit HV word, from the tables themselves (any caller tables stay exact)
+    ck(cudaStreamSynchronize(x.stream), "sync");  // a previous upload may still read wid_sup_host
+    x.wid_sup_host.assign(wref, 0);
+    for (size_t ch = 0; ch < c && ch < 3; ++ch)
+        for (size_t q = 0; q < wph; ++q) {
+            uint64_t any = 0;
+            for (size_t v = 0; v < 256; ++v) any |= wid[(ch * 256 + v) * wph + q];
+            if (uint32_t(any)) x.wid_sup_host[2 * q] |= uint8_t(1u << ch);
+            if (any >> 32) x.wid_sup_host[2 * q + 1] |= uint8_t(1u << ch);
+        }
+    x.enc_nl = 1;
+    for (uint8_t m : x.wid_sup_host) x.enc_nl = std::max<uint32_t>(x.enc_nl, uint32_t(__builtin_popcount(m)));
+    x.wid_sup.ensure(wref);
+    ck(cudaMemcpyAsync(x.wid_sup.p, x.wid_sup_host.data(), wref, cudaMemcpyHostToDevice, x.stream), "upload support");
     x.cb_dim = dim;
     x.cb_h = h;
     x.cb_w = w;
@@ -323,6 +340,11 @@ void upload_bases(seghdc_ctx& x, const seghdc_host::ManhattanParams& p, const ui
     x.col.ensure(size_t(p.w) * wref);
     x.wid.ensure(size_t(p.c) * 256 * wref);
     x.cb_bases.ensure((2 + p.c) * wph);
+    x.wid_sup.ensure(wref);  // written by the expansion kernel
+    x.enc_nl = 1;
+    for (size_t q = 0; q < wref; ++q)
+        x.enc_nl = std::max<uint32_t>(
+            x.enc_nl, uint32_t(__builtin_popcount(manhattan_word_channels(p.dim, p.c, p.off, uint32_t(q)))));
     ck(cudaMemcpyAsync(x.cb_bases.p, bases, (2 + p.c) * wph * 8, cudaMemcpyHostToDevice, x.stream), "upload bases");
     x.cb_dim = p.dim;
     x.cb_h = p.h;
@@ -345,7 +367,8 @@ void expand_codebooks(seghdc_ctx& x, const seghdc_host::ManhattanParams& p) {
         a.off[i] = p.off[i];
         a.unit[i] = p.unit[i];
     }
-    launch_expand_codebooks(reinterpret_cast<const uint32_t*>(x.cb_bases.p), a, x.row.p, x.col.p, x.wid.p, x.stream);
+    launch_expand_codebooks(reinterpret_cast<const uint32_t*>(x.cb_bases.p), a, x.row.p, x.col.p, x.wid.p, x.wid_sup.p,
+                            x.stream);
     x.count();
     x.check_launch();
 }
@@ -376,6 +399,8 @@ void encode_rows(seghdc_ctx& x, size_t r0, size_t r1) {
     a.row = x.row.p;
     a.col = x.col.p;
     a.wid = x.wid.p;
+    a.sup = x.wid_sup.p;
+    a.nl_max = x.enc_nl;
     a.wref = uint32_t(2 * x.g.wph());
     a.S32 = x.g.S32;
     a.W32 = x.g.W32;

@@ -41,10 +41,11 @@ __device__ __forceinline__ uint32_t run_mask32(uint32_t q, uint32_t s, uint32_t 
     return (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << sh;
 }
 __global__ void k_expand_codebooks(const uint32_t* __restrict__ bases, ExpandArgs a, uint32_t* __restrict__ row,
-                                   uint32_t* __restrict__ col, uint32_t* __restrict__ wid) {
+                                   uint32_t* __restrict__ col, uint32_t* __restrict__ wid, uint8_t* __restrict__ sup) {
     const uint32_t ne = a.h + a.w + a.c * 256;
     const size_t total = size_t(ne) * a.wref;
     for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total; t += size_t(gridDim.x) * blockDim.x) {
+        if (t < a.wref) sup[t] = manhattan_word_channels(a.dim, a.c, a.off, uint32_t(t));
         const uint32_t e = uint32_t(t / a.wref), q = uint32_t(t % a.wref);
         uint32_t b, s, len;
         uint32_t* out;
@@ -61,10 +62,10 @@ __global__ void k_expand_codebooks(const uint32_t* __restrict__ bases, ExpandArg
     }
 }
 void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_t* row, uint32_t* col, uint32_t* wid,
-                             cudaStream_t s) {
+                             uint8_t* sup, cudaStream_t s) {
     const size_t total = size_t(a.h + a.w + a.c * 256) * a.wref;
     const uint32_t blocks = uint32_t(std::min<size_t>((total + 255) / 256, 148 * 8));
-    k_expand_codebooks<<<blocks, 256, 0, s>>>(bases, a, row, col, wid);
+    k_expand_codebooks<<<blocks, 256, 0, s>>>(bases, a, row, col, wid, sup);
 }
 
 // =============================================================================================
@@ -72,137 +73,244 @@ void launch_expand_codebooks(const uint32_t* bases, const ExpandArgs& a, uint32_
 // fused with the column sums of the grid (the Harley-Seal counter of every pixel), which the
 // round schedule needs to derive the largest cluster's sums without accumulating them.
 //
-// CTA = (64-column tile, group of rows, chunk of 32 HV words). The chunk's slice of the colour
-// tables (C x 256 entries) and of the tile's 64 column codes is staged once per CTA; row codes
-// and image bytes are staged per batch of 32 rows, so the inner loop touches shared memory only
-// (L2 serves ~30 B per pixel-chunk instead of ~4 table words per output word). Warp = one image
-// row, lane = word: coalesced 128-byte stores. Each warp keeps a Harley-Seal counter per lane;
-// the CTA folds them in shared memory and adds 1024 column sums to the global array.
+// The widened colour tables of different channels have disjoint supports
+// (pixel_pipeline.cpp:66-69): HV word q is touched by the channels whose dimension segment
+// overlaps it, one for all but C - 1 boundary words. `sup[q]` holds that channel set (any
+// superset of the true support is exact: the other channels' entries are zero in word q), so a
+// lane looks up ONE table entry per pixel, a CTA stages one 32 KB table slice (two where its
+// word chunk straddles a channel boundary) and three channels cost what one does.
+//
+// CTA = (64-column tile, group of rows, chunk of 32 HV words); lane = word, so every pixel is one
+// coalesced 128-byte store. A warp owns 8 image columns for the whole kernel (their column
+// codes live in registers) and walks 4-row x 8-column patches: 4 row-code loads and 4 8-byte
+// loads of its channel's image bytes (staged planar) per 32 pixels, then one table load and one
+// store per pixel. Each lane keeps a Harley-Seal counter; the CTA folds them in shared memory
+// and adds 1024 column sums to the global array.
 // =============================================================================================
-constexpr uint32_t kEncRows = 32;
-// image columns per CTA: 64 with one channel; 32 with three, so that two CTAs (2 x ~110 KB of
-// tables and tiles) share an SM
-template <int C>
-constexpr uint32_t enc_cols() { return C == 1 ? 64 : 32; }
-// warps per CTA: 8 with one channel (~46 KB of smem, 3 CTAs per SM); with three channels the
-// 96 KB of colour tables leave room for one CTA per SM, so that CTA runs 24 warps
+constexpr uint32_t kEncRows = 64, kEncCols = 64;  // image tile (and its row codes) staged per batch
+// warps per CTA: 8 (4 CTAs per SM) with one channel; 16 (2 CTAs per SM, up to two table
+// slices each) with three
 template <int C>
 constexpr uint32_t enc_warps() { return C == 1 ? 8 : 16; }
-#ifndef SEGHDC_ENC_MINB
-#define SEGHDC_ENC_MINB 4  // resident CTAs per SM with one channel (64 registers, no spills; 3 CTAs: 113 vs 100 us at C1)
-#endif
+template <int C>
+constexpr uint32_t enc_ctas_per_sm() { return C == 1 ? 4 : 2; }
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(uint32_t(__cvta_generic_to_shared(smem_dst))), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// One 4 x 8 patch: rows rr0..rr0+3 of the staged batch, columns 8 cg..8 cg+7 of the tile.
+// FULL: every row and column of the patch exists.
+template <int NL, int H, bool FULL>
+__device__ __forceinline__ void encode_patch(const uint32_t* s_row_l, const uint8_t* const (&px)[NL],
+                                             const uint32_t* const (&tab)[NL], const uint32_t (&colr)[8],
+                                             uint32_t rr0, uint32_t nrows, uint32_t ncols, char* o,
+                                             ptrdiff_t pix_bytes, ptrdiff_t row_skip_bytes, BitCounter<H>& cnt) {
+    uint32_t x[16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const bool rok = FULL || uint32_t(r) < nrows;
+        const uint32_t rv = s_row_l[(rr0 + r) * 32];
+        uint2 pk[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) pk[k] = *reinterpret_cast<const uint2*>(px[k] + (rr0 + r) * kEncCols);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            uint32_t v = rv ^ colr[u];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                const uint32_t b = __byte_perm(u < 4 ? pk[k].x : pk[k].y, 0, 0x4440 + (u & 3));
+                v ^= tab[k][b * 32];
+            }
+            if (!FULL && !(rok && uint32_t(u) < ncols)) v = 0;
+            x[(r & 1) * 8 + u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // one running pointer: a 64-bit add per store, no multiplies
+            if (FULL || (rok && uint32_t(u) < ncols)) *reinterpret_cast<uint32_t*>(o) = x[(r & 1) * 8 + u];
+            o += pix_bytes;
+        }
+        o += row_skip_bytes;
+        if (r & 1) cnt.add16(x);
+    }
+}
 
 // H: weight-16 planes of the column-sum counters, the fewest that hold the pixels one warp
-// encodes (its ripple is 2 LOP3 per plane per 16 pixels on the ALU-bound path)
+// encodes (its ripple is 2 LOP3 per plane per 16 pixels)
+template <int C, int NL, int H>
+__device__ __forceinline__ void encode_rows_loop(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin,
+                                                 uint32_t r0, uint32_t r1, const uint32_t* __restrict__ row,
+                                                 uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t w0,
+                                                 uint32_t c0, uint32_t nc, const uint32_t (&ch)[3],
+                                                 const uint32_t (&colr)[8], const uint32_t* s_tab, uint32_t* s_row,
+                                                 uint8_t* s_img, BitCounter<H>& cnt) {
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr uint32_t kWarps = enc_warps<C>(), kRgStep = kWarps / 8;
+    const uint32_t cg = warp & 7;                               // the warp's 8 columns of the tile
+    const uint32_t ncols = nc > cg * 8 ? min(8u, nc - cg * 8) : 0u;
+    const bool ld = w0 + lane < wref;  // every lane stores: S32 is a multiple of 32 (launch_encode)
+    const uint32_t* s_row_l = s_row + lane;
+    const ptrdiff_t pix_bytes = ptrdiff_t(S32) * 4, row_skip_bytes = (ptrdiff_t(w) - 8) * ptrdiff_t(S32) * 4;
+    const uint8_t* px[NL];
+    const uint32_t* tab[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        px[k] = s_img + ch[k] * (kEncRows * kEncCols) + cg * 8;  // planar: [channel][row][column]
+        tab[k] = s_tab + k * 8192 + lane;
+    }
+    bool first = true;
+    for (uint32_t rb = r0; rb < r1; rb += kEncRows) {
+        const uint32_t nrb = min(kEncRows, r1 - rb);
+        __syncthreads();  // previous batch's row codes and image bytes consumed
+        for (uint32_t e = tid; e < nrb * 32; e += blockDim.x) {  // e & 31 == lane
+            if (ld) cp_async4(s_row + e, row + size_t(rb + (e >> 5)) * wref + w0 + lane);
+            else s_row[e] = 0;
+        }
+        // image tile -> planar bytes, 4 pixels (4 C bytes) per item: C + 1 aligned words, funnel
+        // shifts to the group's first byte, then byte permutes to one word per channel. A group
+        // that starts inside the row may read up to 16 bytes past a ragged row end (the image
+        // allocation is padded); its extra columns are never stored.
+        for (uint32_t e = tid; e < nrb * (kEncCols / 4); e += blockDim.x) {
+            const uint32_t rr = e / (kEncCols / 4), g = e % (kEncCols / 4);
+            if (g * 4 >= nc) continue;
+            const uint8_t* p = img + (size_t(rb + rr) * w + c0 + g * 4) * C;
+            const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(p) & 3);
+            const uint32_t* pw = reinterpret_cast<const uint32_t*>(p - mis);
+            uint32_t wv[C + 1], f[C];
+#pragma unroll
+            for (int j = 0; j <= C; ++j) wv[j] = (j < C || mis) ? __ldg(pw + j) : 0u;
+#pragma unroll
+            for (int j = 0; j < C; ++j) f[j] = __funnelshift_r(wv[j], wv[j + 1], mis * 8);
+            uint32_t* dst = reinterpret_cast<uint32_t*>(s_img + rr * kEncCols + g * 4);
+            if (C == 1) {
+                dst[0] = f[0];
+            } else {  // f = [R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3]
+                dst[0] = __byte_perm(__byte_perm(f[0], f[1], 0x0630), f[2], 0x5210);
+                dst[kEncRows * kEncCols / 4] = __byte_perm(__byte_perm(f[0], f[1], 0x0741), f[2], 0x6210);
+                dst[2 * kEncRows * kEncCols / 4] = __byte_perm(__byte_perm(f[0], f[1], 0x0052), f[2], 0x7410);
+            }
+        }
+        cp_async_wait_all();  // row codes (and, the first time, the table slices)
+        first = false;
+        __syncthreads();
+        if (ncols == 0) continue;
+        for (uint32_t rg = warp >> 3; rg * 4 < nrb; rg += kRgStep) {  // the warp's 4-row groups of the batch
+            const uint32_t rr0 = rg * 4, nrows = min(4u, nrb - rr0);
+            char* o = reinterpret_cast<char*>(grid + (size_t(rb + rr0 - row_begin) * w + c0 + cg * 8) * S32 + w0 + lane);
+            if (nrows == 4 && ncols == 8)
+                encode_patch<NL, H, true>(s_row_l, px, tab, colr, rr0, 4, 8, o, pix_bytes, row_skip_bytes, cnt);
+            else
+                encode_patch<NL, H, false>(s_row_l, px, tab, colr, rr0, nrows, ncols, o, pix_bytes, row_skip_bytes, cnt);
+        }
+    }
+    if (first) cp_async_wait_all();
+}
+
 template <int C, int H>
-__global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB : 2)
+__global__ void __launch_bounds__(enc_warps<C>() * 32, enc_ctas_per_sm<C>())
     k_encode(const uint8_t* __restrict__ img, uint32_t w, uint32_t row_begin, uint32_t row_end,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ col, const uint32_t* __restrict__ wid,
-             uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid, uint32_t* __restrict__ colsum, uint32_t W32) {
-    constexpr uint32_t kEncCols = enc_cols<C>();
+             const uint8_t* __restrict__ sup, uint32_t wref, uint32_t S32, uint32_t* __restrict__ grid,
+             uint32_t* __restrict__ colsum, uint32_t W32, uint32_t nl_max) {
     extern __shared__ __align__(16) uint32_t es[];
-    uint32_t* s_wid = es;                            // [C][256][32]
-    uint32_t* s_col = s_wid + C * 256 * 32;          // [EC][32]
-    uint32_t* s_row = s_col + kEncCols * 32;         // [ER][32]
-    uint32_t* s_sum = s_row + kEncRows * 32;         // [32 bits][32 words]
-    uint8_t* s_img = reinterpret_cast<uint8_t*>(s_sum + 1024);  // [ER][EC][C]
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // chunk index varies fastest, so the CTAs writing the same pixel rows run together and L2
-    // assembles full lines before they are written back
     const uint32_t w0 = blockIdx.x * 32;             // first word of the chunk
     const uint32_t rows_per = (row_end - row_begin + gridDim.z - 1) / gridDim.z;
     const uint32_t r0 = row_begin + blockIdx.z * rows_per, r1 = min(row_end, r0 + rows_per);
     const uint32_t c0 = blockIdx.y * kEncCols, nc = min(kEncCols, w - c0);
 
-    for (uint32_t e0 = tid; e0 < C * 256 * 32; e0 += blockDim.x * 8) {  // 8 loads in flight
-        uint32_t v[8];
+    // the lane's channels: set bits of sup[word], lowest first; nl = the most any lane needs
+    uint32_t ch[3] = {0, 0, 0}, nl_lane = 1;
+    if (C > 1) {
+        uint32_t m = (w0 + lane < wref) ? sup[w0 + lane] & ((1u << C) - 1) : 0u;
+        nl_lane = __popc(m);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t e = e0 + k * blockDim.x, wd = e & 31;
-            v[k] = (e < C * 256 * 32 && w0 + wd < wref) ? __ldg(wid + size_t(e >> 5) * wref + w0 + wd) : 0u;
+        for (int k = 0; k < 3; ++k) {
+            ch[k] = m ? __ffs(m) - 1 : 0;
+            m &= m - 1;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (e0 + k * blockDim.x < C * 256 * 32) s_wid[e0 + k * blockDim.x] = v[k];
     }
-    for (uint32_t e = tid; e < kEncCols * 32; e += blockDim.x) {
-        const uint32_t wd = e & 31, cc = e >> 5;
-        s_col[e] = (cc < nc && w0 + wd < wref) ? __ldg(col + size_t(c0 + cc) * wref + w0 + wd) : 0u;
-    }
-    for (uint32_t e = tid; e < 1024; e += blockDim.x) s_sum[e] = 0;
+    const uint32_t nl = C > 1 ? max(1u, __reduce_max_sync(0xffffffffu, nl_lane)) : 1u;
+    if (nl > nl_max) __trap();  // the launch sized shared memory for nl_max table slices
+    uint32_t* s_tab = es;                             // [nl][256][32]: the lane's k-th channel
+    uint32_t* s_sum = s_tab + nl * 8192;              // [32 bits][32 words]
+    uint32_t* s_row = s_sum + 1024;                   // [ER][32]
+    uint8_t* s_img = reinterpret_cast<uint8_t*>(s_row + kEncRows * 32);  // [C][ER][EC], planar
 
-    BitCounter<H> cnt;  // <= ceil(rows_per / kEncRows) * ceil(kEncRows / warps) * kEncCols pixels per warp
-    cnt.reset();
-    const bool st = w0 + lane < S32;
-    // staged tables hold 0 for words >= wref, so lanes past the HV need no masking below
-    const uint32_t* s_col_l = s_col + lane;
-    const uint32_t* s_wid_l = s_wid + lane;
-    for (uint32_t rb = r0; rb < r1; rb += kEncRows) {
-        const uint32_t nrb = min(kEncRows, r1 - rb);
-        __syncthreads();  // previous batch's row codes / image bytes consumed (and tables staged)
-        for (uint32_t e = tid; e < nrb * 32; e += blockDim.x) {
-            const uint32_t wd = e & 31;
-            s_row[e] = (w0 + wd < wref) ? __ldg(row + size_t(rb + (e >> 5)) * wref + w0 + wd) : 0u;
+    // table slices: 4-byte async copies, all in flight at once (e & 31 == lane); words past the
+    // HV and unused slices hold 0, and so do the column codes below: no masking in the loop
+    for (uint32_t e = tid; e < nl * 8192; e += blockDim.x) {
+        const uint32_t k = e >> 13, val = (e >> 5) & 255;
+        const uint32_t chk = k == 0 ? ch[0] : (k == 1 ? ch[1] : ch[2]);
+        if (k < nl_lane && w0 + lane < wref)
+            cp_async4(s_tab + e, wid + size_t(chk * 256 + val) * wref + w0 + lane);
+        else
+            s_tab[e] = 0;
+    }
+    uint32_t colr[8];
+    {
+        const uint32_t cg = warp & 7;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t cc = cg * 8 + u;
+            colr[u] = (cc < nc && w0 + lane < wref) ? __ldg(col + size_t(c0 + cc) * wref + w0 + lane) : 0u;
         }
-        for (uint32_t e = tid; e < nrb * nc * C; e += blockDim.x) {
-            const uint32_t rr = e / (nc * C), k = e - rr * nc * C;
-            s_img[rr * kEncCols * C + k] = __ldg(img + (size_t(rb + rr) * w + c0) * C + k);
+    }
+    BitCounter<H> cnt;  // <= ceil(rows_per / 4 / (warps / 8)) * 32 pixels per warp
+    cnt.reset();
+    if (nl == 1)
+        encode_rows_loop<C, 1, H>(img, w, row_begin, r0, r1, row, wref, S32, grid, w0, c0, nc, ch, colr, s_tab, s_row, s_img, cnt);
+    else if (C > 1 && nl == 2)
+        encode_rows_loop<C, 2, H>(img, w, row_begin, r0, r1, row, wref, S32, grid, w0, c0, nc, ch, colr, s_tab, s_row, s_img, cnt);
+    else if (C > 1)
+        encode_rows_loop<C, 3, H>(img, w, row_begin, r0, r1, row, wref, S32, grid, w0, c0, nc, ch, colr, s_tab, s_row, s_img, cnt);
+    // fold the warps' counters: a tree of bit-sliced adds (2 LOP3 per plane) through shared
+    // memory (the table slices are dead by now), then warp 0 expands the CTA totals and every
+    // thread adds its share of the 1024 column sums to the global array
+    {
+        constexpr int kWarps = int(enc_warps<C>()), kLv = kWarps == 16 ? 4 : 3, kP0 = 4 + H, kPmax = kP0 + kLv;
+        uint32_t pl[kPmax];
+        pl[0] = cnt.o, pl[1] = cnt.t, pl[2] = cnt.f, pl[3] = cnt.e;
+#pragma unroll
+        for (int m = 0; m < H; ++m) pl[4 + m] = cnt.hi[m];
+#pragma unroll
+        for (int m = kP0; m < kPmax; ++m) pl[m] = 0;
+        uint32_t* scratch = s_tab;  // [kWarps / 2][kPmax][32] <= 8 * 20 * 128 B
+#pragma unroll
+        for (int lv = 0; lv < kLv; ++lv) {
+            const uint32_t half = kWarps >> (lv + 1);
+            __syncthreads();  // main loop done / previous level's readers done
+            if (warp >= half && warp < 2 * half) {
+#pragma unroll
+                for (int m = 0; m < kP0 + lv; ++m) scratch[((warp - half) * kPmax + m) * 32 + lane] = pl[m];
+            }
+            __syncthreads();
+            if (warp < half) {
+                uint32_t carry = 0;
+#pragma unroll
+                for (int m = 0; m < kP0 + lv; ++m) {
+                    const uint32_t a = pl[m], bb = scratch[(warp * kPmax + m) * 32 + lane];
+                    pl[m] = a ^ bb ^ carry;
+                    carry = (a & bb) | ((a ^ bb) & carry);
+                }
+                pl[kP0 + lv] = carry;
+            }
+        }
+        if (warp == 0) {
+#pragma unroll 4
+            for (int b = 0; b < 32; ++b) {
+                uint32_t val = 0;
+#pragma unroll
+                for (int m = 0; m < kPmax; ++m) val |= ((pl[m] >> b) & 1u) << m;
+                s_sum[b * 32 + lane] = val;
+            }
         }
         __syncthreads();
-        for (uint32_t rr = warp; rr < nrb; rr += enc_warps<C>()) {  // warp = one image row
-            const uint32_t rv = s_row[rr * 32 + lane];
-            const uint8_t* px = s_img + rr * kEncCols * C;
-            uint32_t* o = grid + (size_t(rb + rr - row_begin) * w + c0) * S32 + w0 + lane;
-            uint32_t c16 = 0;
-            for (; c16 + 16 <= nc; c16 += 16) {  // full groups of 16 pixels: no bounds per word
-                uint32_t x[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t cc = c16 + u;
-                    uint32_t v = rv ^ s_col_l[cc * 32];
-#pragma unroll
-                    for (int ch = 0; ch < C; ++ch) v ^= s_wid_l[(ch * 256 + px[cc * C + ch]) * 32];
-                    x[u] = v;
-                }
-                if (st) {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) o[size_t(u) * S32] = x[u];
-                }
-                o += size_t(16) * S32;
-                cnt.add16(x);
-            }
-            if (c16 < nc) {  // the ragged last group of a tile
-                const uint32_t lim = nc - c16;
-                uint32_t x[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const uint32_t cc = c16 + u;
-                    uint32_t v = 0;
-                    if (uint32_t(u) < lim) {
-                        v = rv ^ s_col_l[cc * 32];
-#pragma unroll
-                        for (int ch = 0; ch < C; ++ch) v ^= s_wid_l[(ch * 256 + px[cc * C + ch]) * 32];
-                    }
-                    x[u] = v;
-                }
-                if (st) {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u)
-                        if (uint32_t(u) < lim) o[size_t(u) * S32] = x[u];
-                }
-                cnt.add16(x);
-            }
-        }
     }
-    // fold the warps' counters in shared memory (bit-major: lanes hit distinct banks), then
-    // one global atomic per column sum
-    __syncthreads();
-#pragma unroll 4
-    for (int b = 0; b < 32; ++b) {
-        const uint32_t val = cnt.value(b);
-        if (val) atomicAdd(&s_sum[b * 32 + lane], val);
-    }
-    __syncthreads();
     for (uint32_t e = tid; e < 1024; e += blockDim.x) {
         const uint32_t wd = e & 31, b = e >> 5, word = w0 + wd;
         if (word < W32 && s_sum[e]) atomicAdd(colsum + size_t(word) * 32 + b, s_sum[e]);
@@ -211,17 +319,37 @@ __global__ void __launch_bounds__(enc_warps<C>() * 32, C == 1 ? SEGHDC_ENC_MINB 
 
 template <int C, int H>
 static void launch_encode_ch(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
-    constexpr uint32_t kEncCols = enc_cols<C>();
-    const size_t smem = (size_t(C) * 256 * 32 + kEncCols * 32 + kEncRows * 32 + 1024) * 4 + kEncRows * kEncCols * C;
+    const uint32_t nl = C == 1 ? 1 : std::min<uint32_t>(std::max<uint32_t>(a.nl_max, 1), 3);
+    const size_t smem = (size_t(nl) * 8192 + 1024 + kEncRows * 32) * 4 + size_t(C) * kEncRows * kEncCols;
     ensure_dynamic_smem((const void*)k_encode<C, H>, smem);
-    k_encode<C, H><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.wref,
-                                                       a.S32, a.grid, a.colsum, a.W32);
+    k_encode<C, H><<<g, enc_warps<C>() * 32, smem, s>>>(a.img, a.w, row_begin, row_end, a.row, a.col, a.wid, a.sup,
+                                                       a.wref, a.S32, a.grid, a.colsum, a.W32, nl);
 }
 template <int C>
-static void launch_encode_c(const EncodeArgs& a, dim3 g, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
-    const uint64_t rows_per = (uint64_t(row_end - row_begin) + g.z - 1) / g.z;
-    const uint64_t per_warp = (rows_per + kEncRows - 1) / kEncRows * ((kEncRows + enc_warps<C>() - 1) / enc_warps<C>()) *
-                              enc_cols<C>();
+static void launch_encode_c(const EncodeArgs& a, uint32_t row_begin, uint32_t row_end, cudaStream_t s) {
+    const uint32_t gx = (a.w + kEncCols - 1) / kEncCols, gz = (a.S32 + 31) / 32, rows = row_end - row_begin;
+    // row groups per (column tile, chunk): the split that minimises waves x (rows per CTA + the
+    // rows' worth of time a CTA spends staging its table slice and folding its counters), over
+    // the resident CTA slots. From 1.5 waves on the SMs pick up CTAs as they free up, so waves
+    // count fractionally plus half a CTA of tail; a single wave runs its CTAs in lock step
+    // (all staging, then all storing) and is charged as 1.5.
+    // (Measured flat within ~5 % around the optimum: C1 100-111 us for 5..12 groups.)
+    const uint64_t slots = uint64_t(std::max<uint32_t>(a.sms, 1)) * enc_ctas_per_sm<C>();
+    constexpr uint64_t kStageRows = C == 1 ? 6 : 12;
+    uint32_t gy = 1;
+    uint64_t best = ~0ull;
+    for (uint32_t y = 1; y <= std::max<uint32_t>(1, (rows + 3) / 4) && y <= 65535; ++y) {
+        const uint64_t per = (rows + y - 1) / y, n = uint64_t(gx) * gz * y;
+        const uint64_t waves2 = 2 * n >= 3 * slots ? (2 * n + slots - 1) / slots + 1 : (n <= slots ? 3 : 4);
+        const uint64_t cost = waves2 * (per + kStageRows);  // in half waves
+        if (cost < best) best = cost, gy = y;
+        if (per <= 16) break;
+    }
+    static const char* gy_env = getenv("SEGHDC_ENC_GY");  // experiment switch
+    if (gy_env && atoi(gy_env) > 0) gy = std::min<uint32_t>(uint32_t(atoi(gy_env)), rows);
+    const dim3 g(gz, gx, gy);
+    const uint64_t rows_per = (uint64_t(rows) + gy - 1) / gy;
+    const uint64_t per_warp = (rows_per + 4 * (enc_warps<C>() / 8) - 1) / (4 * (enc_warps<C>() / 8)) * 32 + 32;
     if (per_warp <= BitCounter<6>::capacity()) return launch_encode_ch<C, 6>(a, g, row_begin, row_end, s);
     if (per_warp <= BitCounter<8>::capacity()) return launch_encode_ch<C, 8>(a, g, row_begin, row_end, s);
     if (per_warp <= BitCounter<10>::capacity()) return launch_encode_ch<C, 10>(a, g, row_begin, row_end, s);
@@ -232,17 +360,9 @@ void launch_encode(const EncodeArgs& a, cudaStream_t s) {
     const uint64_t n = a.pix_end - a.pix_begin;
     if (n == 0) return;
     const uint32_t row_begin = uint32_t(a.pix_begin / a.w), row_end = uint32_t(a.pix_end / a.w);
-    const uint32_t ec = a.c == 1 ? enc_cols<1>() : enc_cols<3>();
-    const uint32_t gx = (a.w + ec - 1) / ec, gz = (a.S32 + 31) / 32;
-    // row groups: up to ~6 CTAs per SM in total, but each CTA covers enough rows to amortise
-    // staging its table chunk (C x 32 KB) over >= 32*C rows
-    const uint32_t rows = row_end - row_begin;
-    const uint32_t min_rows = 32 * a.c;
-    const uint32_t gy = std::max<uint32_t>(
-        1, std::min<uint32_t>((rows + min_rows - 1) / min_rows, (6 * a.sms + gx * gz - 1) / (gx * gz)));
-    const dim3 g(gz, gx, gy);
-    if (a.c == 1) launch_encode_c<1>(a, g, row_begin, row_end, s);
-    else launch_encode_c<3>(a, g, row_begin, row_end, s);
+    if (a.S32 % 32 != 0) abort();  // grid rows are whole 128-byte lines (Geometry::set)
+    if (a.c == 1) launch_encode_c<1>(a, row_begin, row_end, s);
+    else launch_encode_c<3>(a, row_begin, row_end, s);
 }
 
 // =============================================================================================

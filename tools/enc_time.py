@@ -4,7 +4,10 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2303_12753_b200 as S
+only = [int(a) for a in sys.argv[1:]]  # optional config filter, e.g. "1 3" (used under ncu)
 for cid, dim, alpha in ((0, 10000, 0.2), (1, 10000, 0.2), (3, 10000, 1.0), (4, 16384, 1.0)):
+    if only and cid not in only:
+        continue
     img = S.synth_image(cid, 0)
     h, w, c = img.shape
     ctx = S.Context(0)
