@@ -161,6 +161,20 @@ __device__ __forceinline__ void tc_ld8(uint32_t taddr, uint32_t* r) {
                  : "memory");
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// dot_c = sum_p v_p BASE^p from the 8 digit-column dots of one cluster (f32 accumulators holding
+// exact integers, |v_p| <= 4 x the dimensions one CTA multiplies). Digits are first combined in
+// groups of 3, 3 and 2 with FFMA, which stays exact while 4 dims (1 + BASE + BASE^2) < 2^24
+// (dims < 46k at base 9; every tcgen05 layout keeps a CTA's dimensions below 25k), so a cluster
+// costs 5 FFMA + 3 F2I + 2 IMAD.WIDE instead of 8 conversions and 8 64-bit multiply-adds.
+template <uint32_t BASE>
+__device__ __forceinline__ long long combine_digits(const float (&v)[8]) {
+    constexpr float B = float(BASE);
+    const float g0 = fmaf(fmaf(v[2], B, v[1]), B, v[0]);
+    const float g1 = fmaf(fmaf(v[5], B, v[4]), B, v[3]);
+    const float g2 = fmaf(v[7], B, v[6]);
+    constexpr long long B3 = (long long)BASE * BASE * BASE, B6 = B3 * B3;
+    return (long long)__float2int_rn(g0) + (long long)__float2int_rn(g1) * B3 + (long long)__float2int_rn(g2) * B6;
+}
 // One chunk (kKS k-steps) of MMAs, issued by an elected lane of the calling warp from a single
 // asm block: addresses advance inside PTX, so the whole block runs on the uniform datapath.
 // Per k-step ONE block-scaled FP4 MMA: A = 8 TMEM columns (64 e2m1), B = kN x 64 e2m1 at b;
@@ -302,6 +316,31 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity, uint32_t
 #define TCW(id, it, bar, par) mbar_wait(bar, par)
 #define PRG(code) ((void)0)
 #endif
+// Hand-offs whose arrivals come from whole warps (slot_free, a_full, d_free): one elected arrival
+// per warp after a __syncwarp instead of 32 (128-256 serialised shared-memory atomics per hand-off
+// otherwise). SEGHDC_LANE_ARRIVE restores per-lane arrivals (A/B builds).
+#ifndef SEGHDC_LANE_ARRIVE
+constexpr uint32_t kArrivePerWarp = 1;
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+#else
+constexpr uint32_t kArrivePerWarp = 32;
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) { mbar_arrive(bar); }
+#endif
+// the A-buffer hand-offs (unpack <-> MMA): polling waits under SEGHDC_SPIN_AB=1/2/3 (experiment;
+// 1: MMA warp's a_full, 2: unpack warps' a_free, 3: both)
+#ifndef SEGHDC_SPIN_AB
+#define SEGHDC_SPIN_AB 0
+#endif
+#if !defined(SEGHDC_HANGDBG)
+#define TCW_AFULL(id, it, bar, par) ((SEGHDC_SPIN_AB & 1) ? mbar_wait_spin(bar, par) : mbar_wait(bar, par))
+#define TCW_AFREE(id, it, bar, par) ((SEGHDC_SPIN_AB & 2) ? mbar_wait_spin(bar, par) : mbar_wait(bar, par))
+#else
+#define TCW_AFULL TCW
+#define TCW_AFREE TCW
+#endif
 
 template <uint32_t NCOL, uint32_t SPLIT = 1>
 struct TcSmem {
@@ -336,6 +375,13 @@ __device__ __forceinline__ uint32_t cl_rank() {
 }
 __device__ __forceinline__ void cl_st_u64(uint32_t addr, unsigned long long a) {
     asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(a) : "memory");
+}
+// asynchronous remote store that completes `bytes` on the destination CTA's mbarrier when the data
+// has landed: the sender neither waits for an acknowledgement nor issues a release
+__device__ __forceinline__ void cl_st_async_u64(uint32_t addr, unsigned long long a, uint32_t remote_bar) {
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(a),
+                 "r"(remote_bar)
+                 : "memory");
 }
 __device__ __forceinline__ void cl_arrive(uint32_t remote_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
@@ -393,10 +439,18 @@ void read_trace_tc(void* dst) {
             atomicAdd(&g_trace_tc[(size_t(blockIdx.x) * 64 + 62) * 8 + (ev)], (cyc));  \
     } while (0)
 #define TC_CLK(v) const unsigned long long v = clock64()
+// more accumulated cycles in slot 60 (split layout): 0 epilogue TMEM loads, 1 digit recombination,
+// 2 remote stores + arrive, 3 finalizer x_full wait, 4 finalizer sum + argmax + labels, 5 lists
+#define TC_ACC2(ev, cyc)                                                              \
+    do {                                                                              \
+        if (lane == 0 && blockIdx.x < 148 && TC_ON)                                   \
+            atomicAdd(&g_trace_tc[(size_t(blockIdx.x) * 64 + 60) * 8 + (ev)], (cyc));  \
+    } while (0)
 #else
 #define TC_TR(ev, it) ((void)0)
 #define TC_TG(ev) ((void)0)
 #define TC_ACC(ev, cyc) ((void)0)
+#define TC_ACC2(ev, cyc) ((void)0)
 #define TC_CLK(v) ((void)0)
 #endif
 
@@ -471,21 +525,21 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     if (tid == 0) {
         for (uint32_t s = 0; s < kStages; ++s) {
             mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_free[s], 4 * 32 * kUH);
+            mbar_init(&slot_free[s], 4 * kArrivePerWarp * kUH);
         }
         for (uint32_t b = 0; b < (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * kAB; ++b)  // PARTS > 1: a_full[PARTS b + part]
-            mbar_init(&a_full[b], 4 * 32 * (Cfg::HALVES ? 1 : kUH));
+            mbar_init(&a_full[b], 4 * kArrivePerWarp * (Cfg::HALVES ? 1 : kUH));
         for (uint32_t b = 0; b < Cfg::NAF; ++b) mbar_init(&a_free[b], 1);
         for (uint32_t b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], NMW);  // every MMA warp commits
-            mbar_init(&d_free[b], 4 * 32);
+            mbar_init(&d_free[b], 4 * kArrivePerWarp);
             mbar_init(&list_ready[b], 4 * 32);
             mbar_init(&list_free[b], NRT);
         }
         mbar_init(b_full, 1);
         if (SPLIT > 1) {
             for (uint32_t b = 0; b < 2; ++b) {
-                mbar_init(&x_full[b], SPLIT * 32);
+                mbar_init(&x_full[b], 1);  // the finalizer arms it with the bytes of the 4 senders
                 for (uint32_t d = 0; d < SPLIT; ++d) mbar_init(&x_free[b * SPLIT + d], 1);
             }
         }
@@ -576,7 +630,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             TC_CLK(c1);
             if (warp == 0 && g == 0) TC_TG(3);
             constexpr uint32_t kPPW = Cfg::PARTS > 1 ? Cfg::PARTS / 2 : 1;  // parts per unpack warp
-            TCW(2, g, &a_free[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf : ab], ((g / kAB) & 1) ^ 1);
+            TCW_AFREE(2, g, &a_free[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf : ab], ((g / kAB) & 1) ^ 1);
             __syncwarp();  // lanes leave the spin loops independently; tcgen05.st is .sync.aligned
             TC_CLK(c2);
             if (warp == 0) { TC_ACC(0, c1 - c0); TC_ACC(1, c2 - c1); }
@@ -617,7 +671,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                         const uint32_t qp = Cfg::PARTS * ab + c16 / 2;
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         tc_fence_before();
-                        mbar_arrive(&a_full[qp]);
+                        warp_arrive(&a_full[qp]);
                         TCW(2, g, &a_free[qp + 1], ((g / kAB) & 1) ^ 1);
                         __syncwarp();
                         tc_fence_after();
@@ -627,10 +681,70 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             PRG(10 * 100000 + g);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             PRG(11 * 100000 + g);
-            if (!kLdg) mbar_arrive(&slot_free[s]);
+            if (!kLdg) warp_arrive(&slot_free[s]);
             tc_fence_before();
-            mbar_arrive(&a_full[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf + (kPPW - 1) : 2 * ab + (g % NMW)]);
+            warp_arrive(&a_full[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf + (kPPW - 1) : 2 * ab + (g % NMW)]);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
+        }
+    } else if (SPLIT > 1 && warp < kWEpi + 4) {
+        // ------------------------------------------------------- split layout: epilogue senders
+        // One warp per lane quarter qd: the partial dots of its 32 pixels (this CTA's quarter of
+        // the dimensions) go to CTA qd of the cluster, slot [tile parity][this CTA], with
+        // asynchronous remote stores that complete bytes on that CTA's x_full barrier. The warp
+        // never waits for the stores (a release + arrive cost a DSMEM round trip per tile, and
+        // this warp is the split layout's critical path).
+        if constexpr (SPLIT > 1) {
+            const uint32_t qd = warp & 3;
+            const uint32_t lane_addr = tbase + ((32 * qd) << 16);
+            long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));
+            const uint32_t xdst = cl_mapa(smem_u32(xbuf + (qrank * KC) * 32 + lane), qd);
+            const uint32_t xfull_dst = cl_mapa(smem_u32(x_full), qd);
+            static_assert(SPLIT == 1 || (NDIG == 8 && NCOL == 64), "two loads of 32 columns = 4 clusters each");
+            for (uint32_t it = 0; it < my_tiles; ++it) {
+                const uint32_t db = it & 1, dd = it % Cfg::DB, dpar = (it / Cfg::DB) & 1;
+                TC_CLK(c0);
+                TCW(3, it, &d_full[dd], dpar);
+                __syncwarp();  // converge before the .sync.aligned tcgen05.ld
+                TC_CLK(c1);
+                if (qd == 0) TC_ACC(5, c1 - c0);
+                tc_fence_after();
+                if (qd == 0) TC_TR(4, it);
+                long long d[KC];
+                TC_CLK(ce0);
+#pragma unroll
+                for (uint32_t grp = 0; grp < 2; ++grp) {
+                    uint32_t r32[32];
+                    tc_ld16(lane_addr + kColD + dd * NCOL + 32 * grp, r32);
+                    tc_ld16(lane_addr + kColD + dd * NCOL + 32 * grp + 16, r32 + 16);
+                    tc_wait_ld();
+                    if (grp == 1) {  // the accumulator set is free once the second group sits in registers
+                        tc_fence_before();
+                        warp_arrive(&d_free[dd]);
+                    }
+#pragma unroll
+                    for (uint32_t cc = 0; cc < 4; ++cc) {
+                        float v[8];
+#pragma unroll
+                        for (uint32_t p = 0; p < 8; ++p) v[p] = __uint_as_float(r32[8 * cc + p]);
+                        d[4 * grp + cc] = combine_digits<Cfg::BASE>(v);
+                    }
+                }
+                TC_CLK(cx0);
+                if (qd == 0) TC_ACC2(0, cx0 - ce0);
+                cl_wait(&x_free[db * SPLIT + qd], ((it >> 1) & 1) ^ 1);
+                TC_CLK(cx1);
+                if (qd == 0) TC_ACC(7, cx1 - cx0);
+                const uint32_t o = db * (SPLIT * KC * 32 * 8);
+#pragma unroll
+                for (uint32_t c = 0; c < KC; ++c)
+                    cl_st_async_u64(xdst + o + c * 256, (unsigned long long)d[c], xfull_dst + db * 8);
+                {
+                    TC_CLK(cs1);
+                    if (qd == 0) TC_ACC2(2, cs1 - cx1);
+                }
+                if (qd == 0) TC_TR(5, it);
+            }
+            if (qd == 0) TC_TG(4);
         }
     } else if (warp < kWEpi + 4 || (SPLIT > 1 && warp >= Cfg::WFin)) {
         // ---------------------------------------------------------------------- epilogue warps
@@ -638,7 +752,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         // pixels (this CTA's quarter of the dimensions) to CTA qd of the cluster; the finalizer
         // warp receives the 4 partials of this CTA's own lane quarter (qrank) and labels them.
         // The exchange buffer is double-buffered by tile parity, [2][src][KC][32] i64.
-        const bool finw = SPLIT > 1 && warp >= Cfg::WFin;  // finalizer warp f takes the tiles of parity f
+        const bool finw = SPLIT > 1;  // split layout: only the finalizers get here; warp f takes the tiles of parity f
         const uint32_t qd = finw ? qrank : (warp & 3);
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
         const bool fin = SPLIT == 1 || finw;  // this warp labels pixels
@@ -674,26 +788,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 tc_fence_after();
                 if (qd == 0) TC_TR(4, it);
                 if constexpr (SPLIT > 1) {
-                    // 64 columns in 4 groups of 16 (registers: 24 warps share the SM): column
-                    // n = NDIG c + p adds digit_dot * BASE^p to dot_c
-#pragma unroll
-                    for (uint32_t c = 0; c < KC; ++c) d[c] = 0;
-#pragma unroll
-                    for (uint32_t grp = 0; grp < NCOL / 16; ++grp) {
-                        uint32_t r16[16];
-                        tc_ld16(lane_addr + kColD + dd * NCOL + 16 * grp, r16);
-                        tc_wait_ld();
-#pragma unroll
-                        for (uint32_t j = 0; j < 16; ++j) {
-                            const uint32_t col = 16 * grp + j, c = col / NDIG, p = col % NDIG;
-                            long long pw = 1;
-#pragma unroll
-                            for (uint32_t q = 0; q < p; ++q) pw *= Cfg::BASE;
-                            d[c] += (long long)__float2int_rn(__uint_as_float(r16[j])) * pw;
-                        }
-                    }
-                    tc_fence_before();
-                    mbar_arrive(&d_free[dd]);
+                    // (the split layout's senders have their own branch above)
                 } else {
                     uint32_t acc[NMW][NCOL];  // the MMA warps' accumulators of this tile
 #pragma unroll
@@ -706,38 +801,32 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                         }
                     tc_wait_ld();
                     tc_fence_before();
-                    mbar_arrive(&d_free[dd]);
+                    warp_arrive(&d_free[dd]);
                     // exact dots: column n = NDIG * c + p holds sum_i y_i d_p(z_c[i]) (an integer in
-                    // f32); dot_c = sum_p digit_dot_p * 8^p
+                    // f32, summed over the MMA warps' accumulators); dot_c = sum_p digit_dot_p * BASE^p
+                    static_assert(NDIG == 8, "combine_digits takes 8 digit columns");
 #pragma unroll
                     for (uint32_t c = 0; c < KC; ++c) {
-                        d[c] = 0;
+                        float v[8];
 #pragma unroll
-                        for (int p = NDIG - 1; p >= 0; --p) {
-                            int v = 0;
+                        for (uint32_t p = 0; p < 8; ++p) {
+                            v[p] = __uint_as_float(acc[0][NDIG * c + p]);
 #pragma unroll
-                            for (uint32_t mw = 0; mw < NMW; ++mw) v += __float2int_rn(__uint_as_float(acc[mw][NDIG * c + p]));
-                            d[c] = d[c] * Cfg::BASE + v;
+                            for (uint32_t mw = 1; mw < NMW; ++mw) v[p] += __uint_as_float(acc[mw][NDIG * c + p]);
                         }
+                        d[c] = combine_digits<Cfg::BASE>(v);
                     }
                 }
             }
             if constexpr (SPLIT > 1) {
-                if (!finw) {  // partial dots of lane quarter qd -> CTA qd, slot [db][qrank]
-                    TC_CLK(cx0);
-                    cl_wait(&x_free[db * SPLIT + qd], ((it >> 1) & 1) ^ 1);
-                    {
-                        TC_CLK(cx1);
-                        if (qd == 0) TC_ACC(7, cx1 - cx0);
-                    }
-                    const uint32_t o = db * (SPLIT * KC * 32 * 8);
-#pragma unroll
-                    for (uint32_t c = 0; c < KC; ++c) cl_st_u64(xdst + o + c * 256, (unsigned long long)d[c]);
-                    cl_arrive(xfull_dst + db * 8);
-                    if (qd == 0) TC_TR(5, it);
-                    continue;
-                }
+                // arm this tile's phase with the bytes the 4 senders deliver, then wait for them
+                if (lane == 0) mbar_expect_tx(&x_full[db], SPLIT * 32 * KC * 8);
+                TC_CLK(cw0);
                 cl_wait(&x_full[db], (it >> 1) & 1);
+                {
+                    TC_CLK(cw1);
+                    TC_ACC2(3, cw1 - cw0);
+                }
                 SG_CHECK(Smem::xb(nks) + (size_t(db + 1) * SPLIT * KC * 32) * 8 <= Smem::bars(nks));
                 const long long* xb = xbuf + db * (SPLIT * KC * 32) + lane;
 #pragma unroll
@@ -870,7 +959,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     static_assert(!Cfg::HALVES || NMW == 1, "half-chunk hand-offs assume one MMA warp");
 #pragma unroll
                     for (uint32_t pt = 0; pt < Cfg::PARTS; ++pt) {
-                        TCW(7, g, &a_full[Cfg::PARTS * ab + pt], (g / kLcm) & 1);
+                        TCW_AFULL(7, g, &a_full[Cfg::PARTS * ab + pt], (g / kLcm) & 1);
                         __syncwarp();
                         tc_fence_after();
 #ifndef SEGHDC_EXP_NOMMA
@@ -896,7 +985,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     }
                     continue;
                 }
-                TCW(7, g, &a_full[2 * ab + m], (g / kLcm) & 1);
+                TCW_AFULL(7, g, &a_full[2 * ab + m], (g / kLcm) & 1);
                 __syncwarp();  // converge before elect.sync / tcgen05.mma
                 TC_CLK(c1);
                 if (m == 0) TC_ACC(2, c1 - c0);

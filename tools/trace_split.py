@@ -35,6 +35,9 @@ ncta = 33 if cfg == 4 else 148
 nchunk = 3 * ((tiles + ncta - 1) // ncta) * (((dim + 31) // 32 + 31) // 32 // (4 if cfg == 4 else 1))
 print("cycles per chunk (median over CTAs):", ", ".join(f"{n}={np.median(acc[:, i]) / nchunk:.0f}" for i, n in enumerate(
     ["unp_slotfull", "unp_afree", "mma_afull", "mma_issue", "prod_slotfree", "epi_dfull", "mma_dfree", "epi_xfree"])))
+acc2 = t[1:, 60, :].copy()
+print("more cycles per TILE (median over CTAs):", ", ".join(f"{n}={np.median(acc2[:, i]) / (nchunk / 4):.0f}" for i, n in enumerate(
+    ["epi_ld+combine", "-", "epi_remote_st", "fin_xfull_wait(2 warps)", "-", "-"])))
 t[:, 60:, :] = t[:, 59:60, :]
 t = t - t[:, :1, 0:1]
 names = ["prod_issue", "unpack_beg", "unpack_end", "mma_commit", "epi_D", "epi_list"]
