@@ -18,11 +18,12 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libseghdc_b200.so")
 
 SOURCES = ["seghdc_kernels.cu", "seghdc_tc.cu", "seghdc_closed.cu", "seghdc_capi.cu", "seghdc_host.cpp", "seghdc_dropin.cpp",
-           "seghdc_metrics.cpp"]
+           "seghdc_metrics.cpp", "seghdc_image_io.cpp"]
 HEADERS = ["kernels.cuh", "launch.h", "host_internal.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "seghdc_cuda.h"),
                   os.path.join(ROOT, "include", "seghdc", "seghdc.hpp"),
-                  os.path.join(ROOT, "include", "seghdc", "metrics.hpp")]
+                  os.path.join(ROOT, "include", "seghdc", "metrics.hpp"),
+                  os.path.join(ROOT, "include", "seghdc", "image_io.hpp")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -72,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra: lis
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = out + ".tmp"
-    r = subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"], capture_output=True, text=True)
+    r = subprocess.run([nvcc()] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-lz"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
@@ -84,6 +85,26 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra: lis
     if verbose:
         print("\n".join(logs))
     return out
+
+
+CLI = os.path.join(LIBDIR, "seghdc")
+CLI_SRC = os.path.join(ROOT, "tools", "seghdc_cli.cpp")
+
+
+def build_cli(force: bool = False) -> str:
+    """The reference's command-line tool over the drop-in (tools/seghdc_cli.cpp) as lib/seghdc."""
+    build()
+    if not force and not _stale(CLI, [CLI_SRC, LIB] + PUBLIC_HEADERS):
+        return CLI
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cuda_lib = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64")
+    cmd = [cxx, "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI, "-L", LIBDIR,
+           "-lseghdc_b200", "-L", cuda_lib, "-lcudart", "-lz", "-Wl,-rpath,$ORIGIN", "-Wl,-rpath," + cuda_lib]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("seghdc CLI build failed")
+    return CLI
 
 
 if __name__ == "__main__":

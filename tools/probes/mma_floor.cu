@@ -10,7 +10,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__
 #endif
 constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t(PN) >> 3) << 17) | ((128u >> 4) << 24);
 template <int SAMEA>
-__global__ void k(long long* out, int iters, int stw) {
+__global__ void k(long long* out, int iters, int stw, const uint4* gbuf = nullptr, size_t gcount = 0) {
   extern __shared__ __align__(1024) uint8_t sB[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar[2];
@@ -61,6 +61,44 @@ __global__ void k(long long* out, int iters, int stw) {
     long long t1 = clock64();
     if ((tid & 31) == 0) out[blockIdx.x] = t1 - t0;
     if ((tid & 31) == 0) stop = 1;
+#ifdef LDGW  // LDGW warps per sub-partition stream coalesced LDG.128 (8 rows x 64 B per instruction, 2 KB row stride)
+  } else if (warp >= 4 + 4 * stw && warp < 4 + 4 * stw + 4 * LDGW) {
+    const int lw = warp - 4 - 4 * stw, lane = tid & 31;
+    // this warp's stream: rows of 2 KB; instruction = rows r..r+7, 64 B each (4 lanes per row)
+    size_t row = (size_t(blockIdx.x) * 4 * LDGW + lw) * 4096;
+    const size_t nrows = gcount * 16 / 2048;
+    uint32_t acc = 0;
+    long long n = 0, t0 = clock64();
+    while (!stop) {
+      uint4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const size_t rr = (row + 8 * i + lane / 4) % nrows;
+        v[i] = __ldg(gbuf + rr * 128 + (n & 31) * 4 + (lane & 3));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
+      row += 64 * ((n & 31) == 31);
+      ++n;
+    }
+    long long t1 = clock64();
+    if (lw == 0 && lane == 0) out[148 + blockIdx.x] = n ? (t1 - t0) * 100 / (n * 8) : 0;  // centi-cycles per LDG.128
+    if (acc == 0x12345) out[0] = 1;
+#endif
+#ifdef LDSW  // LDSW warps per sub-partition stream LDS.128 from the B buffer (shared-memory bandwidth contention)
+  } else if (warp >= 4 + 4 * stw && warp < 4 + 4 * stw + 4 * LDSW) {
+    const uint4* p = reinterpret_cast<const uint4*>(sB) + (tid & 31);
+    uint32_t acc = 0;
+    long long n = 0, t0 = clock64();
+    while (!stop) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { const uint4 v = p[32 * ((i * 5 + n) & 127)]; acc ^= v.x ^ v.y ^ v.z ^ v.w; }
+      ++n;
+    }
+    long long t1 = clock64();
+    if (warp == 4 + 4 * stw && (tid & 31) == 0) out[148 + blockIdx.x] = n ? (t1 - t0) * 100 / (n * 32) : 0;  // centi-cycles per LDS.128
+    if (acc == 0x12345) out[0] = 1;
+#endif
   } else if (warp >= 4 && warp < 4 + 4 * stw) {  // st warps: columns [256, 384) of their lane quarter
     uint32_t r[16];
     for (int i = 0; i < 16; ++i) r[i] = ((tid * 7 + i) * 2654435761u) & 0x22222222u;
@@ -85,11 +123,27 @@ template <int SAMEA> void run(int stw) {
   long long* d; cudaMalloc(&d, 8 * 296); cudaMemset(d, 0, 8 * 296); long long h = 0, hs = 0;
   const int iters = 32 * 300;
   cudaFuncSetAttribute(k<SAMEA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  k<SAMEA><<<148, 128 + 128 * stw, 65536>>>(d, iters, stw); cudaDeviceSynchronize();
-  k<SAMEA><<<148, 128 + 128 * stw, 65536>>>(d, iters, stw); cudaError_t e = cudaDeviceSynchronize();
+#ifndef LDSW
+#define LDSW 0
+#endif
+#ifndef LDGW
+#define LDGW 0
+#endif
+  static uint4* gbuf = nullptr;
+  const size_t gcount = (size_t(96) << 20) / 16;  // 96 MB: L2-resident after the first pass
+  if (LDGW && !gbuf) { cudaMalloc(&gbuf, gcount * 16); cudaMemset(gbuf, 1, gcount * 16); }
+  k<SAMEA><<<148, 128 + 128 * stw + 128 * (LDSW + LDGW), 65536>>>(d, iters * (LDGW ? 20 : 1), stw, gbuf, gcount); cudaDeviceSynchronize();
+  k<SAMEA><<<148, 128 + 128 * stw + 128 * (LDSW + LDGW), 65536>>>(d, iters * (LDGW ? 20 : 1), stw, gbuf, gcount); cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(&h, d + 3, 8, cudaMemcpyDeviceToHost);
   cudaMemcpy(&hs, d + 148 + 3, 8, cudaMemcpyDeviceToHost);
   printf("mxf4 M128 N%d K64 lean issue, %s, st warps/SMSP=%d: %.2f cycles per MMA; st: %lld cyc per 16 KB (%s)\n", PN,
-         SAMEA ? "same A columns" : "A walks 256 columns", stw, double(h) / iters, hs, cudaGetErrorString(e));
+         SAMEA ? "same A columns" : "A walks 256 columns", stw, double(h) / (iters * (LDGW ? 20 : 1)), hs, cudaGetErrorString(e));
 }
-int main() { for (int stw = 0; stw <= 3; ++stw) { run<0>(stw); run<1>(stw); } }
+int main() {
+#if LDSW || LDGW
+  run<0>(0);  // second figure printed: centi-cycles per LDS.128 of the first LDS warp
+  run<0>(1);
+#else
+  for (int stw = 0; stw <= 3; ++stw) { run<0>(stw); run<1>(stw); }
+#endif
+}
