@@ -13,7 +13,8 @@
 #include <string>
 #include <vector>
 
-#include "../../include/seghdc/image_io.hpp"
+#include "seghdc/errors.hpp"
+#include "seghdc/image_io.hpp"
 
 namespace seghdc {
 
