@@ -109,7 +109,8 @@ template <int NL, int H, bool FULL>
 __device__ __forceinline__ void encode_patch(const uint32_t* s_row_l, const uint8_t* const (&px)[NL],
                                              const uint32_t* const (&tab)[NL], const uint32_t (&colr)[8],
                                              uint32_t rr0, uint32_t nrows, uint32_t ncols, char* o,
-                                             ptrdiff_t pix_bytes, ptrdiff_t row_skip_bytes, BitCounter<H>& cnt) {
+                                             ptrdiff_t pix_bytes, ptrdiff_t row_skip_bytes, BitCounter<H>& cnt,
+                                             const char* g_lo, const char* g_hi) {
     uint32_t x[16];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -131,7 +132,10 @@ __device__ __forceinline__ void encode_patch(const uint32_t* s_row_l, const uint
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {  // one running pointer: a 64-bit add per store, no multiplies
-            if (FULL || (rok && uint32_t(u) < ncols)) *reinterpret_cast<uint32_t*>(o) = x[(r & 1) * 8 + u];
+            if (FULL || (rok && uint32_t(u) < ncols)) {
+                SG_CHECK(o >= g_lo && o + 4 <= g_hi);  // inside this call's rows of the grid
+                *reinterpret_cast<uint32_t*>(o) = x[(r & 1) * 8 + u];
+            }
             o += pix_bytes;
         }
         o += row_skip_bytes;
@@ -155,6 +159,10 @@ __device__ __forceinline__ void encode_rows_loop(const uint8_t* __restrict__ img
     const bool ld = w0 + lane < wref;  // every lane stores: S32 is a multiple of 32 (launch_encode)
     const uint32_t* s_row_l = s_row + lane;
     const ptrdiff_t pix_bytes = ptrdiff_t(S32) * 4, row_skip_bytes = (ptrdiff_t(w) - 8) * ptrdiff_t(S32) * 4;
+    const char* g_lo = reinterpret_cast<const char*>(grid);  // checked build: the rows this launch encodes
+    const char* g_hi = reinterpret_cast<const char*>(grid + size_t(r1 - row_begin) * w * S32);
+    (void)g_lo;
+    (void)g_hi;
     const uint8_t* px[NL];
     const uint32_t* tab[NL];
 #pragma unroll
@@ -201,10 +209,12 @@ __device__ __forceinline__ void encode_rows_loop(const uint8_t* __restrict__ img
         for (uint32_t rg = warp >> 3; rg * 4 < nrb; rg += kRgStep) {  // the warp's 4-row groups of the batch
             const uint32_t rr0 = rg * 4, nrows = min(4u, nrb - rr0);
             char* o = reinterpret_cast<char*>(grid + (size_t(rb + rr0 - row_begin) * w + c0 + cg * 8) * S32 + w0 + lane);
+            SG_CHECK(rr0 + nrows <= kEncRows && cg * 8 + ncols <= kEncCols);  // inside the staged tile
             if (nrows == 4 && ncols == 8)
-                encode_patch<NL, H, true>(s_row_l, px, tab, colr, rr0, 4, 8, o, pix_bytes, row_skip_bytes, cnt);
+                encode_patch<NL, H, true>(s_row_l, px, tab, colr, rr0, 4, 8, o, pix_bytes, row_skip_bytes, cnt, g_lo, g_hi);
             else
-                encode_patch<NL, H, false>(s_row_l, px, tab, colr, rr0, nrows, ncols, o, pix_bytes, row_skip_bytes, cnt);
+                encode_patch<NL, H, false>(s_row_l, px, tab, colr, rr0, nrows, ncols, o, pix_bytes, row_skip_bytes, cnt, g_lo,
+                                           g_hi);
         }
     }
     if (first) cp_async_wait_all();

@@ -49,8 +49,13 @@ def _acceptance(binary, *args):
     path = os.path.join(SUITES_DIR, binary)
     if not os.path.exists(path):
         pytest.skip(f"{binary} not built (needs /root/reference and nlohmann/json at build time)")
-    r = subprocess.run([path, *args], capture_output=True, text=True, timeout=900)
+    # through an intermediate shell: criterion 8 reads getrusage().ru_maxrss, which Linux carries
+    # over exec from the mm the child was forked from (here: pytest with torch and the goldens
+    # loaded, > 1 GB); a grandchild starts from the small shell instead
     import re
+    import shlex
+    cmd = " ".join(shlex.quote(a) for a in (path, *args)) + "; rc=$?; exit $rc"
+    r = subprocess.run(["/bin/sh", "-c", cmd], capture_output=True, text=True, timeout=900)
     out = {}
     for m in re.finditer(r"\[(PASS|FAIL)\] criterion (\d+): ([^(]+)\((.*)\)$", r.stdout, re.M):
         out[int(m.group(2))] = (m.group(1), m.group(3).strip(), m.group(4))
