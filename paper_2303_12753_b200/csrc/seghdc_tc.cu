@@ -123,6 +123,15 @@ struct TcCfg {
 #else
     static constexpr uint32_t NMW = (NCOL == 16 || (NCOL == 32 && SPLIT == 1)) ? 2 : 1;
 #endif
+#ifdef SEGHDC_PAIR
+    // CTA pairs (cta_group::2, M = 256): the 4-CTA cluster is two pairs; pair p multiplies the two
+    // tiles of a 256-pixel super-tile (one per CTA, in that CTA's TMEM) against dimension half p,
+    // each CTA holding half of the digit columns of B, so every MMA reads 1 KB of B per SM, not 2
+    static constexpr bool PAIR = SPLIT == 4;
+#else
+    static constexpr bool PAIR = false;
+#endif
+    static constexpr uint32_t DS = PAIR ? 2 : SPLIT;         // dimension split of the cluster
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
     static constexpr uint32_t WMma0 = (SPLIT > 1 || !FOLD) ? WEpi + 4 : 18;
     static constexpr uint32_t WProd = (SPLIT > 1 || !FOLD) ? WEpi + 4 + NMW : 20;
@@ -246,6 +255,26 @@ __device__ __forceinline__ void tc_mma_steps(uint32_t d_t, uint32_t a_t, uint64_
             "r"(ks ? 1u : accum)
             : "memory");
 }
+// the pair forms: M = 256 over both CTAs' TMEM, issued by the leader; the commit arrives on the
+// same barrier of every CTA in `mask` (cluster ranks)
+template <uint32_t KB, uint32_t NSTEP>
+__device__ __forceinline__ void tc_mma_steps_pair(uint32_t d_t, uint32_t a_t, uint64_t bdesc, uint32_t idesc, uint32_t sf,
+                                                  uint32_t accum) {
+#pragma unroll
+    for (uint32_t ks = 0; ks < NSTEP; ++ks)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_t),
+            "r"(a_t + 8 * ks), "l"(bdesc + uint64_t(ks) * (KB >> 5)), "r"(idesc), "r"(sf), "r"(sf + 4),
+            "r"(ks ? 1u : accum)
+            : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
 // commit by the calling (already elected) thread
 __device__ __forceinline__ void tc_commit_one(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -329,6 +358,8 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
 constexpr uint32_t kArrivePerWarp = 32;
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) { mbar_arrive(bar); }
 #endif
+// the same towards CTA `rank` of the cluster (pairs: the peer's warps report to the leader's barriers)
+__device__ __forceinline__ void warp_arrive_at(uint64_t* bar, uint32_t rank, bool remote);
 // the A-buffer hand-offs (unpack <-> MMA): polling waits under SEGHDC_SPIN_AB=1/2/3 (experiment;
 // 1: MMA warp's a_full, 2: unpack warps' a_free, 3: both)
 #ifndef SEGHDC_SPIN_AB
@@ -357,7 +388,7 @@ struct TcSmem {
     }
     static constexpr uint32_t nbars =
         2 * Cfg::Stages + (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * Cfg::AB + Cfg::NAF + 2 + 2 + 2 + 2 + 1 +
-        (SPLIT > 1 ? 2 * (1 + SPLIT) : 0);
+        (SPLIT > 1 ? 2 * (2 + SPLIT) + 1 : 0);  // x_full [2][2] (pairs; [2] otherwise), x_free [2][SPLIT], b_peer
     __host__ __device__ static size_t total(uint32_t nks) { return bars(nks) + nbars * 8; }
 };
 
@@ -393,6 +424,13 @@ __device__ __forceinline__ void cl_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra CLW_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+__device__ __forceinline__ void warp_arrive_at(uint64_t* bar, uint32_t rank, bool remote) {
+    __syncwarp();
+    if (kArrivePerWarp == 32 || (threadIdx.x & 31) == 0) {
+        if (remote) cl_arrive(cl_mapa(smem_u32(bar), rank));
+        else mbar_arrive(bar);
+    }
 }
 __device__ __forceinline__ void cl_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -503,15 +541,22 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     uint64_t* list_ready = d_free + 2;          // [2] labels + update list written
     uint64_t* list_free = list_ready + 2;       // [2] fold warps done with the list
     uint64_t* b_full = list_free + 2;           // B image landed
-    uint64_t* x_full = b_full + 1;              // SPLIT: [2] the 4 partial dots of this CTA's lane quarter landed
-    uint64_t* x_free = x_full + 2;              // SPLIT: [2][dest] dest CTA consumed what this CTA's epilogue warp sent
+    uint64_t* x_full = b_full + 1;              // SPLIT: [2] the 4 partial dots of this CTA's lane quarter landed (pairs: [2][2], by quarter)
+    uint64_t* x_free = x_full + 4;              // SPLIT: [2][dest] dest CTA consumed what this CTA's epilogue warp sent
+    uint64_t* b_peer = x_free + 2 * SPLIT;      // pairs (leader): the peer's half of the B slice landed
     const uint32_t qrank = SPLIT > 1 ? cl_rank() : 0u;  // SPLIT: dimension quarter = rank in the cluster
     const uint32_t cid = blockIdx.x / SPLIT, ncl = gridDim.x / SPLIT;  // tiles go to clusters
+    // pairs: CTA (pr, pe) = rank 2 pr + pe multiplies tile pe of every super-tile (256 pixels)
+    // against dimension half pr; pe == 0 leads the pair (issues the MMAs)
+    constexpr bool kPair = Cfg::PAIR;
+    const uint32_t pr = qrank >> 1, pe = qrank & 1, leader_rank = qrank & ~1u;
+    const uint32_t dq = kPair ? pr : qrank;     // this CTA's part of the dimension split
 
     const uint32_t nch_all = tc_chunks(W32);  // chunks per tile
     // SPLIT: this CTA's chunks [ch0, ch0 + nch) of every tile; its B image slice starts at ch0
-    const uint32_t ch0 = qrank * nch_all / SPLIT, nch = (qrank + 1) * nch_all / SPLIT - ch0;
-    const uint64_t ntiles = (n + kTP - 1) / kTP;
+    const uint32_t ch0 = dq * nch_all / Cfg::DS, nch = (dq + 1) * nch_all / Cfg::DS - ch0;
+    const uint64_t ntiles_px = (n + kTP - 1) / kTP;
+    const uint64_t ntiles = kPair ? (ntiles_px + 1) / 2 : ntiles_px;  // pairs: super-tiles of two tiles
     const uint32_t my_tiles = cid < ntiles ? uint32_t((ntiles - 1 - cid) / ncl + 1) : 0;
     // serpentine traversal: odd rounds walk the tiles from the end of the grid, even rounds from
     // the start, so each round begins with the ~100 MB the previous pass (the encode, or the
@@ -519,7 +564,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     const bool reverse = serpentine && (round & 1) != 0;
     auto tile_px0 = [&](uint32_t it) -> uint64_t {
         const uint64_t t = cid + uint64_t(it) * ncl;
-        return (reverse ? ntiles - 1 - t : t) * kTP;
+        return ((reverse ? ntiles - 1 - t : t) * (kPair ? 2 : 1) + (kPair ? pe : 0)) * kTP;
     };
 
     if (tid == 0) {
@@ -528,28 +573,37 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             mbar_init(&slot_free[s], 4 * kArrivePerWarp * kUH);
         }
         for (uint32_t b = 0; b < (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * kAB; ++b)  // PARTS > 1: a_full[PARTS b + part]
-            mbar_init(&a_full[b], 4 * kArrivePerWarp * (Cfg::HALVES ? 1 : kUH));
+            mbar_init(&a_full[b], (kPair ? 2 : 1) * 4 * kArrivePerWarp * (Cfg::HALVES ? 1 : kUH));  // pairs: both CTAs' warps
         for (uint32_t b = 0; b < Cfg::NAF; ++b) mbar_init(&a_free[b], 1);
         for (uint32_t b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], NMW);  // every MMA warp commits
-            mbar_init(&d_free[b], 4 * kArrivePerWarp);
+            mbar_init(&d_free[b], (kPair ? 2 : 1) * 4 * kArrivePerWarp);
             mbar_init(&list_ready[b], 4 * 32);
             mbar_init(&list_free[b], NRT);
         }
         mbar_init(b_full, 1);
         if (SPLIT > 1) {
-            for (uint32_t b = 0; b < 2; ++b) {
-                mbar_init(&x_full[b], 1);  // the finalizer arms it with the bytes of the 4 senders
-                for (uint32_t d = 0; d < SPLIT; ++d) mbar_init(&x_free[b * SPLIT + d], 1);
-            }
+            for (uint32_t b = 0; b < 4; ++b) mbar_init(&x_full[b], 1);  // the finalizer arms it with the senders' bytes
+            for (uint32_t b = 0; b < 2 * SPLIT; ++b) mbar_init(&x_free[b], 1);
+            mbar_init(b_peer, 1);
         }
         mbar_fence_init();
         s_listn[0] = s_listn[1] = 0;
     }
+    if (kPair) {  // both CTAs of a pair are resident before either allocates the pair's TMEM
+        __syncthreads();
+        cl_sync();
+    }
     if (warp == kWMma0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_misc)),
-                     "n"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_misc)),
+                         "n"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_misc)),
+                         "n"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -575,8 +629,15 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     __syncthreads();
     tc_fence_after();
     if (done) {  // early stop reached (clusterer.cpp:213): nothing left to do
+        if (kPair) cl_sync();  // the pair's TMEM is freed once both CTAs are here
         if (warp == kWMma0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+        {
+            if constexpr (kPair) {
+                asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+            } else {
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+            }
+        }
         return;
     }
     if (blockIdx.x == 0 && tid == 0) st.hdr->rounds_run = round;
@@ -671,7 +732,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                         const uint32_t qp = Cfg::PARTS * ab + c16 / 2;
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         tc_fence_before();
-                        warp_arrive(&a_full[qp]);
+                        warp_arrive_at(&a_full[qp], leader_rank, kPair && pe != 0);
                         TCW(2, g, &a_free[qp + 1], ((g / kAB) & 1) ^ 1);
                         __syncwarp();
                         tc_fence_after();
@@ -683,7 +744,8 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             PRG(11 * 100000 + g);
             if (!kLdg) warp_arrive(&slot_free[s]);
             tc_fence_before();
-            warp_arrive(&a_full[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf + (kPPW - 1) : 2 * ab + (g % NMW)]);
+            warp_arrive_at(&a_full[Cfg::HALVES ? Cfg::PARTS * ab + kPPW * hf + (kPPW - 1) : 2 * ab + (g % NMW)], leader_rank,
+                           kPair && pe != 0);
             if (warp == 0 && g % nch == nch - 1) TC_TR(2, g / nch);
         }
     } else if (SPLIT > 1 && warp < kWEpi + 4) {
@@ -697,8 +759,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint32_t qd = warp & 3;
             const uint32_t lane_addr = tbase + ((32 * qd) << 16);
             long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));
-            const uint32_t xdst = cl_mapa(smem_u32(xbuf + (qrank * KC) * 32 + lane), qd);
-            const uint32_t xfull_dst = cl_mapa(smem_u32(x_full), qd);
+            // destination of lane quarter qd's partial dots: CTA qd, slot [this CTA]; pairs: the CTA
+            // with this CTA's tile (same pe) in pair qd / 2, which finalizes quarters 2 (qd / 2) and
+            // 2 (qd / 2) + 1 of it: slot [quarter qd % 2][this pair]
+            const uint32_t xrank = kPair ? 2 * (qd >> 1) + pe : qd;
+            const uint32_t xslot = kPair ? (qd & 1) * 2 + pr : qrank;
+            const uint32_t xdst = cl_mapa(smem_u32(xbuf + (xslot * KC) * 32 + lane), xrank);
+            const uint32_t xfull_dst = cl_mapa(smem_u32(x_full), xrank) + (kPair ? (qd & 1) * 8 : 0);
             static_assert(SPLIT == 1 || (NDIG == 8 && NCOL == 64), "two loads of 32 columns = 4 clusters each");
             for (uint32_t it = 0; it < my_tiles; ++it) {
                 const uint32_t db = it & 1, dd = it % Cfg::DB, dpar = (it / Cfg::DB) & 1;
@@ -719,7 +786,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                     tc_wait_ld();
                     if (grp == 1) {  // the accumulator set is free once the second group sits in registers
                         tc_fence_before();
-                        warp_arrive(&d_free[dd]);
+                        warp_arrive_at(&d_free[dd], leader_rank, kPair && pe != 0);
                     }
 #pragma unroll
                     for (uint32_t cc = 0; cc < 4; ++cc) {
@@ -737,7 +804,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 const uint32_t o = db * (SPLIT * KC * 32 * 8);
 #pragma unroll
                 for (uint32_t c = 0; c < KC; ++c)
-                    cl_st_async_u64(xdst + o + c * 256, (unsigned long long)d[c], xfull_dst + db * 8);
+                    cl_st_async_u64(xdst + o + c * 256, (unsigned long long)d[c], xfull_dst + db * (kPair ? 16 : 8));
                 {
                     TC_CLK(cs1);
                     if (qd == 0) TC_ACC2(2, cs1 - cx1);
@@ -753,7 +820,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         // warp receives the 4 partials of this CTA's own lane quarter (qrank) and labels them.
         // The exchange buffer is double-buffered by tile parity, [2][src][KC][32] i64.
         const bool finw = SPLIT > 1;  // split layout: only the finalizers get here; warp f takes the tiles of parity f
-        const uint32_t qd = finw ? qrank : (warp & 3);
+        // finalizer lane quarter: this CTA's own (rank) one; pairs: quarters 2 pr and 2 pr + 1 of
+        // this CTA's tile, one per finalizer warp
+        const uint32_t fq = finw ? warp - Cfg::WFin : 0u;
+        const uint32_t qd = finw ? (kPair ? 2 * pr + fq : qrank) : (warp & 3);
         const uint32_t lane_addr = tbase + ((32 * qd) << 16);
         const bool fin = SPLIT == 1 || finw;  // this warp labels pixels
         long long* xbuf = reinterpret_cast<long long*>(smem + Smem::xb(nks));
@@ -771,7 +841,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         for (uint32_t c = 0; c < KC; ++c) ccount[c] = 0;
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it & 1;  // exchange slot / finalizer
-            if (finw && db != warp - Cfg::WFin) continue;
+            if (finw && !kPair && db != fq) continue;  // (pairs: both warps take every tile, a quarter each)
             const uint32_t dd = it % Cfg::DB, dpar = (it / Cfg::DB) & 1;  // accumulator set, its phase
             const uint64_t px0 = tile_px0(it);
             const uint64_t px = px0 + 32 * qd + lane;
@@ -820,9 +890,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             }
             if constexpr (SPLIT > 1) {
                 // arm this tile's phase with the bytes the 4 senders deliver, then wait for them
-                if (lane == 0) mbar_expect_tx(&x_full[db], SPLIT * 32 * KC * 8);
+                constexpr uint32_t kSrc = kPair ? 2 : SPLIT;  // CTAs sharing this tile
+                uint64_t* xf = &x_full[kPair ? db * 2 + fq : db];
+                if (lane == 0) mbar_expect_tx(xf, kSrc * 32 * KC * 8);
                 TC_CLK(cw0);
-                cl_wait(&x_full[db], (it >> 1) & 1);
+                cl_wait(xf, (it >> 1) & 1);
                 {
                     TC_CLK(cw1);
                     TC_ACC2(3, cw1 - cw0);
@@ -833,11 +905,13 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 for (uint32_t c = 0; c < KC; ++c) {
                     long long t = 0;
 #pragma unroll
-                    for (uint32_t src = 0; src < SPLIT; ++src) t += xb[(src * KC + c) * 32];
+                    for (uint32_t src = 0; src < kSrc; ++src) t += xb[(((kPair ? fq * 2 : 0) + src) * KC + c) * 32];
                     d[c] = t;
                 }
                 __syncwarp();
-                if (lane < SPLIT) cl_arrive(cl_mapa(smem_u32(&x_free[db * SPLIT + qrank]), lane));  // slots free again
+                // slots free again: tell every sender of this quarter
+                if (lane < kSrc)
+                    cl_arrive(cl_mapa(smem_u32(&x_free[db * SPLIT + qd]), kPair ? 2 * lane + pe : lane));
             }
             // assign_labels (clusterer.cpp:146-158): first strictly closer centroid wins
             uint32_t best = 0;
@@ -939,6 +1013,46 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         TCW(5, 0, b_full, 0);
         __syncwarp();
         TC_TG(2);
+        if constexpr (kPair) {
+            // the leader issues M = 256 MMAs over both CTAs' A buffers and accumulators; its commits
+            // arrive on the a_free / d_full barriers of both CTAs. The peer's warps report to the
+            // leader's a_full / d_free barriers; its MMA warp only reports its B half.
+            if (pe != 0) {
+                if (lane == 0) cl_arrive(cl_mapa(smem_u32(b_peer), leader_rank));
+            } else {
+                cl_wait(b_peer, 0);
+                __syncwarp();
+                constexpr uint32_t idesc2 = idesc_mxf4(NCOL, 2 * kTP);
+                constexpr uint32_t kStepsPP = kKS / Cfg::PARTS, kKBH = Cfg::KB / 2;  // B bytes per k-step and CTA
+                const uint16_t mask = uint16_t(3u << leader_rank);
+                for (uint32_t it = 0; it < my_tiles; ++it) {
+                    const uint32_t db = it % Cfg::DB;
+                    const uint32_t d_t = tbase + kColD + db * NCOL;
+                    cl_wait(&d_free[db], ((it / Cfg::DB) & 1) ^ 1);
+                    __syncwarp();
+                    for (uint32_t ch = 0; ch < nch; ++ch) {
+                        const uint32_t g = it * nch + ch, ab = g % kAB;
+#pragma unroll
+                        for (uint32_t pt = 0; pt < Cfg::PARTS; ++pt) {
+                            cl_wait(&a_full[Cfg::PARTS * ab + pt], (g / kAB) & 1);
+                            __syncwarp();
+                            tc_fence_after();
+                            if (tc_elect()) {
+                                tc_mma_steps_pair<Cfg::KB, kStepsPP>(
+                                    d_t, tbase + ab * 128 + pt * (128 / Cfg::PARTS),
+                                    bdesc_at(b0 + (ch * kKS + pt * kStepsPP) * kKBH), idesc2, tbase + Cfg::ColSF,
+                                    (ch || pt) ? 1u : 0u);
+                                tc_commit_pair(&a_free[Cfg::PARTS * ab + pt], mask);
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    if (tc_elect()) tc_commit_pair(&d_full[db], mask);
+                    __syncwarp();
+                    if (m == 0) TC_TR(3, it);
+                }
+            }
+        } else
         for (uint32_t it = 0; it < my_tiles; ++it) {
             const uint32_t db = it % Cfg::DB;  // accumulator set
             const uint32_t d_t = tbase + kColD + (NMW * db + m) * NCOL;
@@ -1018,12 +1132,16 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     } else if (warp == kWProd) {
         // ----------------------------------------------------------------------- producer warp
         if (lane == 0) {
-            const uint32_t bbytes = nch * kKS * Cfg::KB;  // this CTA's slice (SPLIT) or the whole image
+            // this CTA's slice (SPLIT) or the whole image; pairs: half of the digit columns of the
+            // pair's dimension half, contiguous in the pair layout [column half][k-step][KB / 2]
+            const uint32_t bbytes = nch * kKS * (kPair ? Cfg::KB / 2 : Cfg::KB);
+            const size_t boff = kPair ? size_t(pe) * (size_t(nch_all) * kKS * (Cfg::KB / 2)) + size_t(ch0) * kKS * (Cfg::KB / 2)
+                                      : size_t(ch0) * kKS * Cfg::KB;
             // the grid streams through L2 with evict_first (measured: evict_last on the tiles read
             // last slows every round; evict_first takes round 1 from 98 to 82 us at C1)
             const uint64_t pol_stream = policy_evict_first();
             mbar_expect_tx(b_full, bbytes);
-            bulk_g2s(sB, bimg + size_t(ch0) * kKS * Cfg::KB, bbytes, b_full);
+            bulk_g2s(sB, bimg + boff, bbytes, b_full);
             uint32_t g = 0;
             const uint32_t nchunks = kLdg ? 0u : my_tiles * nch;  // kLdg: the unpack warps load A
             for (uint32_t q = 0; q < pf && q < nchunks; ++q)
@@ -1138,7 +1256,11 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     if (fw == 0) TC_TG(7);
     if (warp == kWMma0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+        if constexpr (kPair) {
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+        } else {
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols));
+        }
 #ifdef SEGHDC_TRACE
         if (lane == 0 && blockIdx.x < 148) {  // slot 61: [0] stamp before, [1] after dealloc, [2] stamp after
             unsigned long long t_;
@@ -1176,12 +1298,15 @@ __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint
     const uint32_t code = (c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u);
     return code | (d < 0 ? 8u : 0u);
 }
+// pair: the CTA-pair layout [column half][k-step][kb / 2] (each CTA of a pair copies one contiguous
+// half of the digit columns of its k-steps) instead of [k-step][kb]
 __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
-                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state) {
+                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state, uint32_t pair) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
-    const uint32_t total = nks * kb;
+    const uint32_t total = nks * kb, half = kb / 2;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t ks = i / kb, rem = i % kb;
+        const uint32_t ks = pair ? (i / half) % nks : i / kb;
+        const uint32_t rem = pair ? (i / (nks * half)) * half + i % half : i % kb;
         const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
         const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
         bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k, ndig, base) | (b_nibble(Z, K, D, ks, n, k + 1, ndig, base) << 4));
@@ -1506,7 +1631,8 @@ void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, 
                        cudaStream_t s) {
     const uint32_t nc = tc_ncol(K, W32), nks = tc_ksteps(W32), kb = nc * 32;
     const uint32_t total = nks * kb;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state);
+    const uint32_t pair = (nc == 64 && tc_split(K, W32) > 1 && TcCfg<64, 4>::PAIR) ? 1u : 0u;
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state, pair);
 }
 
 #ifdef SEGHDC_HANGDBG
