@@ -45,6 +45,47 @@ def test_encode_matches_reference(ctx, port, dim, h, w, c, enc, beta):
     assert (grid == port.encode(img, dim, *cb)).all()
 
 
+@pytest.mark.parametrize("dim,h,w,c,overlap", [
+    (1000, 9, 70, 3, "all"),      # every channel non-zero in every word: three lookups per word (nl = 3)
+    (2100, 5, 3, 3, "pairs"),     # channels 0/1 share the low words, 1/2 the high ones (nl = 2 everywhere)
+    (4200, 130, 9, 3, "disjoint"),  # the reference's structure; rows beyond one staged batch, a ragged 9-column tile
+    (777, 3, 131, 1, "all"),      # one channel, three column tiles, the last ragged
+])
+def test_encode_with_arbitrary_caller_tables(ctx, port, dim, h, w, c, overlap):
+    """seghdc_encode takes the caller's tables as they are: the kernel's one-lookup-per-word fast
+    path must stay exact when the widened colour tables are NOT channel-disjoint (it derives the
+    channel set of every word from the tables). Checked against a direct numpy XOR, and the fused
+    column sums (cluster 0 = column sums - cluster 1) through two rounds on the resident grid."""
+    rng = np.random.default_rng(dim + w)
+    wph = (dim + 63) // 64
+    tail = np.uint64((1 << (dim % 64)) - 1) if dim % 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+
+    def rand(n):
+        t = rng.integers(0, 1 << 63, (n, wph), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, (n, wph), dtype=np.uint64)
+        t[:, -1] &= tail
+        return t
+
+    row, col, wid = rand(h), rand(w), rand(c * 256).reshape(c, 256, wph)
+    if overlap != "all" and c == 3:
+        third = wph // 3
+        keep = np.zeros((3, wph), bool)
+        if overlap == "pairs":
+            keep[0, : wph // 2], keep[1, :], keep[2, wph // 2:] = True, True, True
+        else:
+            keep[0, :third], keep[1, third: 2 * third], keep[2, 2 * third:] = True, True, True
+        wid = wid * keep[:, None, :].astype(np.uint64)
+    img = rng.integers(0, 256, (h, w, c), dtype=np.uint8)
+    grid = ctx.encode_image(img, dim, row, col, wid)
+    exp = (row[:, None, :] ^ col[None, :, :]).reshape(h * w, wph)
+    for ch in range(c):
+        exp = exp ^ wid[ch][img[:, :, ch].reshape(-1)]
+    assert (grid == exp).all()
+    res = ctx.cluster(None, img, dim, 2, 2, False)
+    ref = port.cluster(exp, img, dim, 2, 2, False)
+    assert (res["labels"] == ref["labels"]).all() and (res["centroids"] == ref["centroids"]).all()
+    assert (res["counts"] == ref["counts"]).all()
+
+
 # ---------------------------------------------------------------- assign / update
 def _rand_grid(rng, n, dim, density=0.5):
     bits = (rng.random((n, dim)) < density).astype(np.uint8)
