@@ -132,6 +132,14 @@ struct TcCfg {
     static constexpr bool PAIR = false;
 #endif
     static constexpr uint32_t DS = PAIR ? 2 : SPLIT;         // dimension split of the cluster
+#ifdef SEGHDC_COOP
+    // the unpack warps of a lane quarter share EVERY chunk (16-byte pieces u, u + AB, ... each)
+    // instead of owning whole chunks: a chunk is complete after a third of the time, so its MMAs
+    // overlap the next chunk's unpack instead of all AB buffers filling, then all draining
+    static constexpr bool COOP = !HALVES;
+#else
+    static constexpr bool COOP = false;
+#endif
     static constexpr uint32_t WEpi = 4 * UW;                 // first epilogue warp
     static constexpr uint32_t WMma0 = (SPLIT > 1 || !FOLD) ? WEpi + 4 : 18;
     static constexpr uint32_t WProd = (SPLIT > 1 || !FOLD) ? WEpi + 4 + NMW : 20;
@@ -570,10 +578,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
     if (tid == 0) {
         for (uint32_t s = 0; s < kStages; ++s) {
             mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_free[s], 4 * kArrivePerWarp * kUH);
+            mbar_init(&slot_free[s], 4 * kArrivePerWarp * (Cfg::COOP ? Cfg::UW : kUH));
         }
         for (uint32_t b = 0; b < (Cfg::PARTS > 2 ? Cfg::PARTS : 2) * kAB; ++b)  // PARTS > 1: a_full[PARTS b + part]
-            mbar_init(&a_full[b], (kPair ? 2 : 1) * 4 * kArrivePerWarp * (Cfg::HALVES ? 1 : kUH));  // pairs: both CTAs' warps
+            mbar_init(&a_full[b], (kPair ? 2 : 1) * 4 * kArrivePerWarp * (Cfg::HALVES ? 1 : Cfg::COOP ? Cfg::UW : kUH));  // pairs: both CTAs' warps
         for (uint32_t b = 0; b < Cfg::NAF; ++b) mbar_init(&a_free[b], 1);
         for (uint32_t b = 0; b < 2; ++b) {
             mbar_init(&d_full[b], NMW);  // every MMA warp commits
@@ -678,7 +686,7 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
         if constexpr (kLdg) {
             if (ph < nchunks) ld_row(ph, nv);
         }
-        for (uint32_t g = ph; g < nchunks; g += kAB) {
+        for (uint32_t g = Cfg::COOP ? 0 : ph; g < nchunks; g += Cfg::COOP ? 1 : kAB) {
             const uint32_t s = g % kStages, ab = g % kAB;
             uint4 cv[4];
             if constexpr (kLdg) {
@@ -702,7 +710,10 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             // ALU pipe the four masks per word
             const uint32_t half = opaque(0x80000000u), two = opaque(2u);
 #pragma unroll
-            for (uint32_t c16 = hf * (8 / kUH); c16 < (hf + 1) * (8 / kUH); ++c16) {  // 16-byte pieces: 4 words = 2 k-steps
+            for (uint32_t c16i = hf * (8 / kUH); c16i < (hf + 1) * (8 / kUH); ++c16i) {  // 16-byte pieces: 4 words = 2 k-steps
+                // COOP: this warp's pieces u, u + AB, ... of every chunk
+                const uint32_t c16 = Cfg::COOP ? u + c16i * kAB : c16i;
+                if (Cfg::COOP && (c16i >= (8 + kAB - 1) / kAB || c16 >= 8)) continue;
 #if defined(SEGHDC_EXP_NOGRID)  // timing experiment: no grid at all (no TMA, no smem), words from a hash
                 const uint32_t hq = uint32_t(tile_px0(g / nch) + r) * 2654435761u ^ ((g % nch) * 8 + c16) * 40503u;
                 const uint4 v = make_uint4(hq, hq * 3u, hq ^ 0x9E3779B9u, hq + 0x7F4A7C15u);
@@ -740,7 +751,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
                 }
             }
             PRG(10 * 100000 + g);
+#ifndef SEGHDC_EXP_NOWAITST  // timing experiment only: hand the buffer off without waiting for the stores
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#endif
             PRG(11 * 100000 + g);
             if (!kLdg) warp_arrive(&slot_free[s]);
             tc_fence_before();

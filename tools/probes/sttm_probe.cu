@@ -62,7 +62,14 @@ __global__ void k(long long* out, int iters, int STW, int AW, int mma, int stbat
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
       for (int j = 0; j < per; ++j) {
-        if (ALU) {  // X registers from X / 4 words: 4 LOP3 + 2 IMAD per word
+        if (ALU == 2) {  // one cheap ALU op per stored register (is the store rate data-dependent?)
+#pragma unroll
+          for (int q = 0; q < X; q += 2) { r[q] += w; r[q + 1] ^= w; }
+          w += 0x9E3779B9u;
+        } else if (ALU == 3) {  // one FMA-pipe op per stored register
+#pragma unroll
+          for (int q = 0; q < X; ++q) r[q] = r[q] * 3u + w;
+        } else if (ALU) {  // X registers from X / 4 words: 4 LOP3 + 2 IMAD per word
 #pragma unroll
           for (int q = 0; q < X / 4; ++q) {
             w = w * 1664525u + 1013904223u;
@@ -155,6 +162,10 @@ template <int X, int ALU> void run(int STW, int AW, int mma, int stbatch, int dc
 }
 
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'r') {  // store rate with changing data: 0 no ALU, 2 one ALU op, 3 one FMA op per register
+    for (int stw = 1; stw <= 4; ++stw) { run<16, 0>(stw, 0, 0, 0); run<16, 2>(stw, 0, 0, 0); run<16, 3>(stw, 0, 0, 0); }
+    return 0;
+  }
   if (argc > 1) {  // MMA-only placement sweep
     for (int dcol : {0, 16, 384, 400, 448}) for (int nab : {1, 3}) for (int a0 : {0, 128, 256}) {
       if (nab == 3 && a0) continue;
