@@ -1447,7 +1447,10 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
     SG_CHECK(M <= n);
     // at least kMinRows rows per CTA: a short list (late rounds) occupies a few CTAs, whose
     // flush (one atomic per entry of D) dominates, instead of all of them
-    constexpr uint32_t kMinRows = 64;
+#ifndef SEGHDC_FOLD_MINROWS
+#define SEGHDC_FOLD_MINROWS 32  // 16 / 32 / 64 / 128 / 256 / 512 measured: C0 step 296.6 / 296.0 / 298.8 / 305.5 / 321 / 350 us
+#endif
+    constexpr uint32_t kMinRows = SEGHDC_FOLD_MINROWS;
     const uint32_t per = max(kMinRows, (M + gridDim.x - 1) / gridDim.x);
     const uint32_t r0 = min(M, blockIdx.x * per), r1 = min(M, r0 + per);
     if (r0 >= r1) return;
