@@ -54,7 +54,10 @@ struct SeedArgs {
     uint64_t* seeds;
     unsigned long long* slots;
     RoundState* hdr;
+    bool slots_cleared;  // the caller already set the slots to all ones (launch_init_clear)
 };
+void launch_init_clear(void* state, size_t state_bytes, void* run1, size_t run1_bytes, unsigned long long* slots,
+                       uint32_t nslots, cudaStream_t s);
 void launch_select_seeds(const SeedArgs& a, cudaStream_t s);
 
 struct InitSeedArgs {
@@ -64,6 +67,8 @@ struct InitSeedArgs {
     const uint64_t* seeds;
     uint32_t K, W32, Dp;
     int32_t* xchg;
+    const int32_t* colsum_src;  // nullable: local column sums, copied to colsum_dst (the exchange tail)
+    int32_t* colsum_dst;
 };
 void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s);
 

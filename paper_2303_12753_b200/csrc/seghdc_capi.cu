@@ -183,6 +183,7 @@ struct seghdc_ctx {
     size_t h = 0, w = 0, c = 0;
     // codebooks
     DevBuf<uint32_t> row, col, wid;
+    bool slots_cleared = false;         // cluster_begin's clear kernel already reset the seed slots
     DevBuf<uint8_t> wid_sup;            // channel set per HV word of wid (EncodeArgs::sup)
     std::vector<uint8_t> wid_sup_host;  // its host copy while an upload may be in flight
     uint32_t enc_nl = 1;                // most channels any HV word has
@@ -527,6 +528,8 @@ void select_seeds_dev(seghdc_ctx& x, size_t K) {
     a.seeds = x.seeds.p;
     a.slots = x.slots.p;
     a.hdr = reinterpret_cast<RoundState*>(x.state.p);
+    a.slots_cleared = x.slots_cleared;
+    x.slots_cleared = false;
     launch_select_seeds(a, x.stream);
     x.count(2 + (K > 2 ? (K - 2) + 1 : 0));
     x.check_launch();
@@ -542,7 +545,8 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
         return;
     }
     const uint32_t np = (round & 1) ^ 1;
-    launch_prep_finish(x.state.p, uint32_t(x.K), np, x.stream);
+    // (init: cluster_begin has just cleared the whole state, norm2 included)
+    if (mode != 1) launch_prep_finish(x.state.p, uint32_t(x.K), np, x.stream);
     FinishArgs f{};
     f.mode = mode;
     f.K = uint32_t(x.K);
@@ -560,7 +564,7 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     f.early_stop = x.early_stop;
     f.run = (mode == 0 && x.incremental()) ? x.run1.p : nullptr;
     launch_finish(f, x.stream);
-    x.count(2);
+    x.count(mode != 1 ? 2 : 1);
     if (x.plan.tc) {
         launch_build_bimg(x.Z.p, uint32_t(x.K), x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr, x.stream);
         x.count();
@@ -575,15 +579,18 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     x.iterations = iterations;
     alloc_cluster(x, K);
     x.early_stop = early_stop;
-    ck(cudaMemsetAsync(x.state.p, 0, StateView::bytes(uint32_t(K), iterations), x.stream), "clear state");
+    // one launch clears the round state, the running sums and the seed slots (was three memsets)
+    launch_init_clear(x.state.p, StateView::bytes(uint32_t(K), iterations), x.run1.p,
+                      x.incremental() ? 2 * x.K * size_t(x.g.Dp) * 4 : 0, x.slots.p, uint32_t(2 + K), x.stream);
+    x.count();
+    x.slots_cleared = true;
     x.wraps_src = StateView::at(x.state.p, uint32_t(K)).wraps;
     x.wraps_rounds = 0;
-    ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
-    if (x.incremental()) ck(cudaMemsetAsync(x.run1.p, 0, 2 * x.K * size_t(x.g.Dp) * 4, x.stream), "clear running sums");
+    // labels start at 0xFFFFFFFF ("no cluster"); the tcgen05 round kernel takes that as given in
+    // round 1 instead of reading them, so only the other kernels need the buffer cleared
+    if (!x.plan.tc) ck(cudaMemsetAsync(x.labels.p, 0xFF, x.n_local() * 4, x.stream), "clear labels");
     select_seeds_dev(x, K);
     if (!x.colsum_valid) compute_colsum(x);
-    // local column sums into the exchange tail; the init all-reduce makes them global
-    ck(cudaMemcpyAsync(x.colsum_ptr(), x.colsum.p, x.g.Dp * 4, cudaMemcpyDeviceToDevice, x.stream), "colsum");
     InitSeedArgs a{};
     a.grid = x.grid.p;
     a.S32 = x.g.S32;
@@ -594,6 +601,10 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     a.W32 = x.g.W32;
     a.Dp = x.g.Dp;
     a.xchg = x.xchg.p;
+    // local column sums into the exchange tail (inside the same kernel); the init all-reduce
+    // makes them global
+    a.colsum_src = reinterpret_cast<const int32_t*>(x.colsum.p);
+    a.colsum_dst = reinterpret_cast<int32_t*>(x.colsum_ptr());
     launch_init_seeds(a, x.stream);
     x.count();
     x.check_launch();

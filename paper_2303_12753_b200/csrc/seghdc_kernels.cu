@@ -484,7 +484,7 @@ __global__ void k_seed_collect(uint64_t* seeds, const unsigned long long* slots,
 }
 
 void launch_select_seeds(const SeedArgs& a, cudaStream_t s) {
-    cudaMemsetAsync(a.slots, 0xFF, (2 + a.K) * sizeof(unsigned long long), s);
+    if (!a.slots_cleared) cudaMemsetAsync(a.slots, 0xFF, (2 + a.K) * sizeof(unsigned long long), s);
     const uint32_t blocks = uint32_t(std::min<uint64_t>((a.n + 255) / 256, 148 * 2));
     k_seed_minmax<<<blocks, 256, 0, s>>>(a.img, a.n, a.c, a.slots);
     k_seed_post<<<1, 1, 0, s>>>(a.slots, a.seeds, a.K, a.h, a.w, a.hdr);
@@ -497,8 +497,11 @@ void launch_select_seeds(const SeedArgs& a, cudaStream_t s) {
 // Seed centroids (clusterer.cpp:197-205): xchg[c][i] = bit i of the seed pixel's HV when the
 // pixel lies in this rank's shard, else 0 (an all-reduce then yields the full seed HVs).
 // =============================================================================================
+// colsum_src (nullable): the local column sums are copied into the exchange tail here as well
+// (their init all-reduce makes them global), saving a device-to-device copy in the init chain.
 __global__ void k_init_seeds(const uint32_t* __restrict__ grid, uint32_t S32, uint64_t pix_begin, uint64_t n_local,
-                             const uint64_t* seeds, uint32_t K, uint32_t W32, uint32_t Dp, int32_t* xchg) {
+                             const uint64_t* seeds, uint32_t K, uint32_t W32, uint32_t Dp, int32_t* xchg,
+                             const int32_t* __restrict__ colsum_src, int32_t* __restrict__ colsum_dst) {
     const uint32_t c = blockIdx.y;
     const uint64_t sp = seeds[c];
     const bool local = sp >= pix_begin && sp < pix_begin + n_local;
@@ -506,12 +509,31 @@ __global__ void k_init_seeds(const uint32_t* __restrict__ grid, uint32_t S32, ui
         uint32_t bit = 0;
         if (local && (i >> 5) < W32) bit = (grid[(sp - pix_begin) * S32 + (i >> 5)] >> (i & 31)) & 1u;
         xchg[size_t(c) * Dp + i] = int32_t(bit);
+        if (c == 0 && colsum_src) colsum_dst[i] = colsum_src[i];
     }
 }
 
 void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s) {
     dim3 g((a.Dp + 255) / 256, a.K);
-    k_init_seeds<<<g, 256, 0, s>>>(a.grid, a.S32, a.pix_begin, a.n_local, a.seeds, a.K, a.W32, a.Dp, a.xchg);
+    k_init_seeds<<<g, 256, 0, s>>>(a.grid, a.S32, a.pix_begin, a.n_local, a.seeds, a.K, a.W32, a.Dp, a.xchg, a.colsum_src,
+                                   a.colsum_dst);
+}
+
+// One launch instead of three memsets at the start of a cluster call: the round state and the
+// running sums to zero, the seed-selection slots to all ones.
+__global__ void k_init_clear(uint32_t* state, uint32_t state_words, uint32_t* run1, uint32_t run1_words,
+                             unsigned long long* slots, uint32_t nslots) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = t; i < state_words; i += nt) state[i] = 0;
+    for (uint32_t i = t; i < run1_words; i += nt) run1[i] = 0;
+    for (uint32_t i = t; i < nslots; i += nt) slots[i] = ~0ull;
+}
+void launch_init_clear(void* state, size_t state_bytes, void* run1, size_t run1_bytes, unsigned long long* slots,
+                       uint32_t nslots, cudaStream_t s) {
+    const uint32_t words = uint32_t((state_bytes + 3) / 4 + run1_bytes / 4 + nslots);
+    k_init_clear<<<std::max(1u, std::min(148u, (words + 1023) / 1024)), 256, 0, s>>>(
+        static_cast<uint32_t*>(state), uint32_t((state_bytes + 3) / 4), static_cast<uint32_t*>(run1),
+        uint32_t(run1_bytes / 4), slots, nslots);
 }
 
 // =============================================================================================

@@ -860,7 +860,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
             const uint64_t px = px0 + 32 * qd + lane;
             const bool live = px < n;
             SG_CHECK(!(fin && live) || px < n);
-            const uint32_t old = (fin && live) ? labels[px] : 0u;
+            // round 1: every label is 0xFFFFFFFF ("no cluster") by definition; the buffer is not read
+            // (and not cleared beforehand for tcgen05 plans)
+            const uint32_t old = (fin && live) ? (round == 1 ? 0xFFFFFFFFu : labels[px]) : 0u;
             long long d[KC];
             if (!finw) {
                 TC_CLK(c0);
