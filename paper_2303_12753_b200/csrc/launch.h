@@ -55,6 +55,7 @@ struct SeedArgs {
     unsigned long long* slots;
     RoundState* hdr;
     bool slots_cleared;  // the caller already set the slots to all ones (launch_init_clear)
+    bool defer_post;     // K <= 2: k_init_seeds decides the seeds from the slots (InitSeedArgs::post_slots)
 };
 void launch_init_clear(void* state, size_t state_bytes, void* run1, size_t run1_bytes, unsigned long long* slots,
                        uint32_t nslots, cudaStream_t s);
@@ -64,9 +65,12 @@ struct InitSeedArgs {
     const uint32_t* grid;
     uint32_t S32;
     uint64_t pix_begin, n_local;
-    const uint64_t* seeds;
+    uint64_t* seeds;
     uint32_t K, W32, Dp;
     int32_t* xchg;
+    const unsigned long long* post_slots;  // nullable (K <= 2): derive the seeds here (see SeedArgs::defer_post)
+    uint32_t h, w;
+    RoundState* hdr;
     const int32_t* colsum_src;  // nullable: local column sums, copied to colsum_dst (the exchange tail)
     int32_t* colsum_dst;
 };

@@ -529,9 +529,10 @@ void select_seeds_dev(seghdc_ctx& x, size_t K) {
     a.slots = x.slots.p;
     a.hdr = reinterpret_cast<RoundState*>(x.state.p);
     a.slots_cleared = x.slots_cleared;
+    a.defer_post = x.slots_cleared;  // inside cluster_begin: k_init_seeds follows
     x.slots_cleared = false;
     launch_select_seeds(a, x.stream);
-    x.count(2 + (K > 2 ? (K - 2) + 1 : 0));
+    x.count((a.defer_post && K <= 2 ? 1 : 2) + (K > 2 ? (K - 2) + 1 : 0));
     x.check_launch();
 }
 
@@ -603,6 +604,10 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     a.xchg = x.xchg.p;
     // local column sums into the exchange tail (inside the same kernel); the init all-reduce
     // makes them global
+    a.post_slots = K <= 2 ? x.slots.p : nullptr;
+    a.h = uint32_t(x.h);
+    a.w = uint32_t(x.w);
+    a.hdr = reinterpret_cast<RoundState*>(x.state.p);
     a.colsum_src = reinterpret_cast<const int32_t*>(x.colsum.p);
     a.colsum_dst = reinterpret_cast<int32_t*>(x.colsum_ptr());
     launch_init_seeds(a, x.stream);

@@ -423,12 +423,13 @@ __global__ void k_seed_minmax(const uint8_t* __restrict__ img, uint64_t n, uint3
     }
 }
 
-// Decide min/max seeds or the uniform fallback (clusterer.cpp:83-99). Single thread.
-__global__ void k_seed_post(unsigned long long* slots, uint64_t* seeds, uint32_t K, uint32_t h, uint32_t w,
-                            RoundState* hdr) {
+// Decide min/max seeds or the uniform fallback (clusterer.cpp:83-99). Single thread; `seeds` may be
+// a global or a shared array, `uniform` receives the fallback flag.
+__device__ __forceinline__ void seed_post(const unsigned long long* slots, uint64_t* seeds, uint32_t K, uint32_t h,
+                                          uint32_t w, uint32_t* uniform) {
     const uint64_t mn_key = slots[0] >> 32, mx_key = 0xFFFFull - (slots[1] >> 32);
     if (mn_key == mx_key) {
-        hdr->uniform = 1;
+        *uniform = 1;
         uint32_t nch = 0;
         const uint64_t corners[4] = {0, uint64_t(w) - 1, uint64_t(h - 1) * w, uint64_t(h - 1) * w + w - 1};
         for (int i = 0; i < 4 && nch < K; ++i) {
@@ -443,9 +444,13 @@ __global__ void k_seed_post(unsigned long long* slots, uint64_t* seeds, uint32_t
         }
         return;
     }
-    hdr->uniform = 0;
+    *uniform = 0;
     seeds[0] = slots[0] & 0xFFFFFFFFull;
     if (K >= 2) seeds[1] = slots[1] & 0xFFFFFFFFull;
+}
+__global__ void k_seed_post(unsigned long long* slots, uint64_t* seeds, uint32_t K, uint32_t h, uint32_t w,
+                            RoundState* hdr) {
+    seed_post(slots, seeds, K, h, w, &hdr->uniform);
 }
 
 // Greedy step s (>= 2): relax min_dist with seed s-1 (or both first seeds at s == 2) and pick
@@ -487,7 +492,8 @@ void launch_select_seeds(const SeedArgs& a, cudaStream_t s) {
     if (!a.slots_cleared) cudaMemsetAsync(a.slots, 0xFF, (2 + a.K) * sizeof(unsigned long long), s);
     const uint32_t blocks = uint32_t(std::min<uint64_t>((a.n + 255) / 256, 148 * 2));
     k_seed_minmax<<<blocks, 256, 0, s>>>(a.img, a.n, a.c, a.slots);
-    k_seed_post<<<1, 1, 0, s>>>(a.slots, a.seeds, a.K, a.h, a.w, a.hdr);
+    // K <= 2 inside a cluster call: k_init_seeds decides the seeds itself (one launch fewer)
+    if (!(a.defer_post && a.K <= 2)) k_seed_post<<<1, 1, 0, s>>>(a.slots, a.seeds, a.K, a.h, a.w, a.hdr);
     for (uint32_t st = 2; st < a.K; ++st)
         k_seed_greedy<<<blocks, 256, 0, s>>>(a.img, a.n, a.c, st, a.min_dist, a.seeds, a.slots, a.hdr);
     if (a.K > 2) k_seed_collect<<<1, 32, 0, s>>>(a.seeds, a.slots, a.K, a.hdr);
@@ -500,10 +506,25 @@ void launch_select_seeds(const SeedArgs& a, cudaStream_t s) {
 // colsum_src (nullable): the local column sums are copied into the exchange tail here as well
 // (their init all-reduce makes them global), saving a device-to-device copy in the init chain.
 __global__ void k_init_seeds(const uint32_t* __restrict__ grid, uint32_t S32, uint64_t pix_begin, uint64_t n_local,
-                             const uint64_t* seeds, uint32_t K, uint32_t W32, uint32_t Dp, int32_t* xchg,
-                             const int32_t* __restrict__ colsum_src, int32_t* __restrict__ colsum_dst) {
+                             uint64_t* seeds, uint32_t K, uint32_t W32, uint32_t Dp, int32_t* xchg,
+                             const int32_t* __restrict__ colsum_src, int32_t* __restrict__ colsum_dst,
+                             const unsigned long long* post_slots, uint32_t h, uint32_t w, RoundState* hdr) {
     const uint32_t c = blockIdx.y;
-    const uint64_t sp = seeds[c];
+    // post_slots (K <= 2): the min/max slots of k_seed_minmax; every block derives the seeds (the
+    // work of k_seed_post) and block (0, 0) publishes them
+    __shared__ uint64_t s_seeds[2];
+    __shared__ uint32_t s_uniform;
+    if (post_slots) {
+        if (threadIdx.x == 0) {
+            seed_post(post_slots, s_seeds, K, h, w, &s_uniform);
+            if (blockIdx.x == 0 && blockIdx.y == 0) {
+                hdr->uniform = s_uniform;
+                for (uint32_t q = 0; q < K; ++q) seeds[q] = s_seeds[q];
+            }
+        }
+        __syncthreads();
+    }
+    const uint64_t sp = post_slots ? s_seeds[c] : seeds[c];
     const bool local = sp >= pix_begin && sp < pix_begin + n_local;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < Dp; i += gridDim.x * blockDim.x) {
         uint32_t bit = 0;
@@ -516,7 +537,7 @@ __global__ void k_init_seeds(const uint32_t* __restrict__ grid, uint32_t S32, ui
 void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s) {
     dim3 g((a.Dp + 255) / 256, a.K);
     k_init_seeds<<<g, 256, 0, s>>>(a.grid, a.S32, a.pix_begin, a.n_local, a.seeds, a.K, a.W32, a.Dp, a.xchg, a.colsum_src,
-                                   a.colsum_dst);
+                                   a.colsum_dst, a.K <= 2 ? a.post_slots : nullptr, a.h, a.w, a.hdr);
 }
 
 // One launch instead of three memsets at the start of a cluster call: the round state and the
