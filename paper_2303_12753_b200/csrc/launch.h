@@ -58,7 +58,7 @@ struct SeedArgs {
     bool defer_post;     // K <= 2: k_init_seeds decides the seeds from the slots (InitSeedArgs::post_slots)
 };
 void launch_init_clear(void* state, size_t state_bytes, void* run1, size_t run1_bytes, unsigned long long* slots,
-                       uint32_t nslots, cudaStream_t s);
+                       uint32_t nslots, uint32_t* list_counts, uint32_t nlists, cudaStream_t s);
 void launch_select_seeds(const SeedArgs& a, cudaStream_t s);
 
 struct InitSeedArgs {
@@ -186,7 +186,8 @@ void launch_finish_tc(uint32_t D, uint32_t W32, uint32_t Dp, int32_t* xchg, cons
                       uint32_t* run1, uint8_t* bimg, void* state, uint32_t round, int early_stop, uint32_t* ticket,
                       cudaStream_t s);  // centroid entries above this need the IMMA kernels
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
-                       cudaStream_t s);
+                       cudaStream_t s,
+                       uint32_t* clear = nullptr, uint32_t clear_n = 0);
 cudaError_t launch_round_tc(const RoundArgs& a, cudaStream_t s);
 #ifdef SEGHDC_CHECKED
 unsigned int check_line_tc();       // first violated SG_CHECK line per translation unit (0: none)

@@ -184,6 +184,7 @@ struct seghdc_ctx {
     // codebooks
     DevBuf<uint32_t> row, col, wid;
     bool slots_cleared = false;         // cluster_begin's clear kernel already reset the seed slots
+    bool flist_cleared = false;         // ... and round 1's changed-pixel list counts
     DevBuf<uint8_t> wid_sup;            // channel set per HV word of wid (EncodeArgs::sup)
     std::vector<uint8_t> wid_sup_host;  // its host copy while an upload may be in flight
     uint32_t enc_nl = 1;                // most channels any HV word has
@@ -567,8 +568,12 @@ void finish(seghdc_ctx& x, int mode, uint32_t round) {
     launch_finish(f, x.stream);
     x.count(mode != 1 ? 2 : 1);
     if (x.plan.tc) {
-        launch_build_bimg(x.Z.p, uint32_t(x.K), x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr, x.stream);
+        // init (mode 1): the same kernel zeroes the exchange buffer k_finish has just consumed
+        launch_build_bimg(x.Z.p, uint32_t(x.K), x.g.D, x.g.W32, x.bimg.p, mode == 0 ? x.state.p : nullptr, x.stream,
+                          mode == 1 ? reinterpret_cast<uint32_t*>(x.xchg.p) : nullptr,
+                          mode == 1 ? uint32_t(x.xchg_round_ints()) : 0u);
         x.count();
+        if (mode == 1) x.xchg_clean = true;
     }
     x.check_launch();
 }
@@ -582,9 +587,12 @@ void cluster_begin(seghdc_ctx& x, size_t K, size_t iterations, int early_stop) {
     x.early_stop = early_stop;
     // one launch clears the round state, the running sums and the seed slots (was three memsets)
     launch_init_clear(x.state.p, StateView::bytes(uint32_t(K), iterations), x.run1.p,
-                      x.incremental() ? 2 * x.K * size_t(x.g.Dp) * 4 : 0, x.slots.p, uint32_t(2 + K), x.stream);
+                      x.incremental() ? 2 * x.K * size_t(x.g.Dp) * 4 : 0, x.slots.p, uint32_t(2 + K),
+                      x.incremental() ? x.flist.p + (x.K - 1) * x.n_local() : nullptr,
+                      x.incremental() ? uint32_t(x.K - 1) : 0u, x.stream);
     x.count();
     x.slots_cleared = true;
+    x.flist_cleared = x.incremental();  // round 1's list counts are zero already
     x.wraps_src = StateView::at(x.state.p, uint32_t(K)).wraps;
     x.wraps_rounds = 0;
     // labels start at 0xFFFFFFFF ("no cluster"); the tcgen05 round kernel takes that as given in
@@ -671,7 +679,9 @@ void round_assign(seghdc_ctx& x, uint32_t r) {
     a.labels_host_slot = (x.in_pipeline && r == x.iterations) ? x.zc_slot.p : nullptr;
     a.flist = use_flist ? x.flist.p : nullptr;
     a.flist_count = use_flist ? x.flist.p + (x.K - 1) * x.n_local() : nullptr;
-    if (use_flist) ck(cudaMemsetAsync(a.flist_count, 0, (x.K - 1) * 4, x.stream), "clear fold lists");
+    if (use_flist && !(r == 1 && x.flist_cleared))
+        ck(cudaMemsetAsync(a.flist_count, 0, (x.K - 1) * 4, x.stream), "clear fold lists");
+    x.flist_cleared = false;
     // the round's CTAs fold their exact sums, member counts and changes into the exchange buffer
     if (!x.xchg_clean) ck(cudaMemsetAsync(x.xchg.p, 0, x.xchg_round_ints() * 4, x.stream), "clear exchange");
     x.xchg_clean = false;

@@ -543,18 +543,19 @@ void launch_init_seeds(const InitSeedArgs& a, cudaStream_t s) {
 // One launch instead of three memsets at the start of a cluster call: the round state and the
 // running sums to zero, the seed-selection slots to all ones.
 __global__ void k_init_clear(uint32_t* state, uint32_t state_words, uint32_t* run1, uint32_t run1_words,
-                             unsigned long long* slots, uint32_t nslots) {
+                             unsigned long long* slots, uint32_t nslots, uint32_t* list_counts, uint32_t nlists) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    for (uint32_t i = t; i < nlists; i += nt) list_counts[i] = 0;  // round 1's changed-pixel lists
     for (uint32_t i = t; i < state_words; i += nt) state[i] = 0;
     for (uint32_t i = t; i < run1_words; i += nt) run1[i] = 0;
     for (uint32_t i = t; i < nslots; i += nt) slots[i] = ~0ull;
 }
 void launch_init_clear(void* state, size_t state_bytes, void* run1, size_t run1_bytes, unsigned long long* slots,
-                       uint32_t nslots, cudaStream_t s) {
+                       uint32_t nslots, uint32_t* list_counts, uint32_t nlists, cudaStream_t s) {
     const uint32_t words = uint32_t((state_bytes + 3) / 4 + run1_bytes / 4 + nslots);
     k_init_clear<<<std::max(1u, std::min(148u, (words + 1023) / 1024)), 256, 0, s>>>(
         static_cast<uint32_t*>(state), uint32_t((state_bytes + 3) / 4), static_cast<uint32_t*>(run1),
-        uint32_t(run1_bytes / 4), slots, nslots);
+        uint32_t(run1_bytes / 4), slots, nslots, list_counts, nlists);
 }
 
 // =============================================================================================

@@ -1316,8 +1316,12 @@ __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint
 // pair: the CTA-pair layout [column half][k-step][kb / 2] (each CTA of a pair copies one contiguous
 // half of the digit columns of its k-steps) instead of [k-step][kb]
 __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
-                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state, uint32_t pair) {
+                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state, uint32_t pair,
+                             uint32_t* __restrict__ clear, uint32_t clear_n) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
+    // init only: the exchange buffer the previous kernel (k_finish) consumed is zeroed here, so
+    // round 1 needs no memset of its own
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < clear_n; i += gridDim.x * blockDim.x) clear[i] = 0;
     const uint32_t total = nks * kb, half = kb / 2;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t ks = pair ? (i / half) % nks : i / kb;
@@ -1646,11 +1650,11 @@ bool tc_make_grid_map(void* map, const uint32_t* grid, uint64_t rows, uint32_t S
 }
 
 void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, uint8_t* bimg, const void* state,
-                       cudaStream_t s) {
+                       cudaStream_t s, uint32_t* clear, uint32_t clear_n) {
     const uint32_t nc = tc_ncol(K, W32), nks = tc_ksteps(W32), kb = nc * 32;
     const uint32_t total = nks * kb;
     const uint32_t pair = (nc == 64 && tc_split(K, W32) > 1 && TcCfg<64, 4>::PAIR) ? 1u : 0u;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state, pair);
+    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state, pair, clear, clear_n);
 }
 
 #ifdef SEGHDC_HANGDBG
