@@ -124,30 +124,41 @@ ImageBuffer load_png(const std::vector<std::uint8_t>& file, const std::string& p
     return img;
 }
 
-// minimal P5 reader: "P5" <ws> width <ws> height <ws> maxval <single ws> data, '#' comments
-ImageBuffer load_pgm(std::FILE* fp, const std::string& path) {
-    auto next_token = [&]() -> std::string {
+// Binary PGM (P5), parsed from the file's bytes: magic, width, height, maxval as whitespace-
+// separated decimal tokens ('#' starts a comment that runs to the end of the line), exactly one
+// whitespace byte after maxval, then width x height samples.
+struct PgmCursor {
+    const std::vector<std::uint8_t>& bytes;
+    std::size_t at = 0;
+    static bool space(std::uint8_t ch) { return ch == ' ' || (ch >= '\t' && ch <= '\r'); }
+    // next token, leaving the cursor just past the single byte that ended it; empty at end of file
+    std::string token() {
         std::string tok;
-        int ch;
-        while ((ch = std::fgetc(fp)) != EOF) {
+        while (at < bytes.size()) {
+            const std::uint8_t ch = bytes[at++];
             if (ch == '#') {
-                while ((ch = std::fgetc(fp)) != EOF && ch != '\n') {
+                while (at < bytes.size() && bytes[at++] != '\n') {
                 }
-                continue;
+            } else if (!space(ch)) {
+                tok.push_back(char(ch));
+            } else if (!tok.empty()) {
+                break;
             }
-            if (ch == ' ' || ch == '\t' || ch == '\n' || ch == '\r' || ch == '\v' || ch == '\f') {
-                if (!tok.empty()) break;
-                continue;
-            }
-            tok.push_back(char(ch));
         }
-        if (tok.empty()) throw IoError("truncated PGM header in '" + path + "'");
         return tok;
-    };
-    if (next_token() != "P5") throw IoError("'" + path + "' is not a binary PGM (P5) file");
-    const long width = std::strtol(next_token().c_str(), nullptr, 10);
-    const long height = std::strtol(next_token().c_str(), nullptr, 10);
-    const long maxval = std::strtol(next_token().c_str(), nullptr, 10);
+    }
+};
+
+ImageBuffer load_pgm(const std::vector<std::uint8_t>& file, const std::string& path) {
+    PgmCursor cur{file};
+    long field[3] = {0, 0, 0};  // width, height, maxval
+    if (cur.token() != "P5") throw IoError("'" + path + "' is not a binary PGM (P5) file");
+    for (long& f : field) {
+        const std::string tok = cur.token();
+        if (tok.empty()) throw IoError("truncated PGM header in '" + path + "'");
+        f = std::strtol(tok.c_str(), nullptr, 10);
+    }
+    const long width = field[0], height = field[1], maxval = field[2];
     if (width <= 0 || height <= 0) throw IoError("invalid PGM dimensions in '" + path + "'");
     if (maxval > 255)
         throw IoError("unsupported bit depth in '" + path + "' (PGM maxval " + std::to_string(maxval) + " exceeds 255)");
@@ -156,9 +167,9 @@ ImageBuffer load_pgm(std::FILE* fp, const std::string& path) {
     img.height = std::size_t(height);
     img.width = std::size_t(width);
     img.channels = 1;
-    img.pixels.resize(img.height * img.width);
-    if (std::fread(img.pixels.data(), 1, img.pixels.size(), fp) != img.pixels.size())
-        throw IoError("truncated PGM pixel data in '" + path + "'");
+    const std::size_t count = img.height * img.width;
+    if (file.size() - cur.at < count) throw IoError("truncated PGM pixel data in '" + path + "'");
+    img.pixels.assign(file.begin() + std::ptrdiff_t(cur.at), file.begin() + std::ptrdiff_t(cur.at + count));
     return img;
 }
 
@@ -177,12 +188,9 @@ std::uint8_t level_value(std::size_t label, std::size_t k) {
 }  // namespace
 
 ImageBuffer load_image(const std::string& path) {
-    auto fp = open_file(path, "rb");
-    unsigned char magic[8] = {0};
-    const std::size_t got = std::fread(magic, 1, sizeof(magic), fp.get());
-    std::rewind(fp.get());
-    if (got >= 8 && std::memcmp(magic, kPngSig, 8) == 0) return load_png(read_all(fp.get()), path);
-    if (got >= 2 && magic[0] == 'P' && magic[1] == '5') return load_pgm(fp.get(), path);
+    const std::vector<std::uint8_t> file = read_all(open_file(path, "rb").get());
+    if (file.size() >= 8 && std::memcmp(file.data(), kPngSig, 8) == 0) return load_png(file, path);
+    if (file.size() >= 2 && file[0] == 'P' && file[1] == '5') return load_pgm(file, path);
     throw IoError("'" + path + "' is neither a PNG nor a binary PGM (P5) file");
 }
 

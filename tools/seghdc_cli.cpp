@@ -284,54 +284,63 @@ int run_eval(const std::string& pred_path, const std::string& gt_path, std::size
     return kExitOk;
 }
 
-double median(std::vector<double> v) {
-    std::sort(v.begin(), v.end());
-    const std::size_t n = v.size();
-    return n % 2 == 1 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+// ---- bench (seghdc_main.cpp:116-161): fixed iterations, early stop off, median of the repeats ----------
+// One configuration of the sweep: `repeats` pipeline runs, every stage's median time.
+MetricsRecord bench_one(const seghdc::ImageBuffer& img, const seghdc::RunConfig& cfg, std::size_t repeats,
+                        const std::string& gt_path) {
+    cfg.validate(img);
+    std::map<std::string, std::vector<double>> samples;
+    seghdc::PipelineResult last;
+    for (std::size_t r = 0; r < repeats; ++r) {
+        last = seghdc::run_pipeline(img, cfg);
+        for (const auto& [stage, ms] : last.timings.as_map()) samples[stage].push_back(ms);
+    }
+    const auto mid = [&](const char* stage) {
+        std::vector<double>& v = samples[stage];
+        std::sort(v.begin(), v.end());
+        return v.size() % 2 ? v[v.size() / 2] : 0.5 * (v[v.size() / 2 - 1] + v[v.size() / 2]);
+    };
+    MetricsRecord record;
+    record.iterations_run = last.iterations_run;
+    record.config = cfg;
+    record.timings.encode_position_ms = mid("encode_position");
+    record.timings.encode_color_ms = mid("encode_color");
+    record.timings.produce_pixels_ms = mid("produce_pixels");
+    record.timings.cluster_ms = mid("cluster");
+    record.timings.total_ms = mid("total");
+    if (!gt_path.empty()) record.iou = score_against_gt(last.mask, gt_path, cfg.clusters);
+    return record;
 }
 
-// ---- bench (seghdc_main.cpp:116-161): fixed iterations, early stop off, median of the repeats ----------
 int run_bench(CommonOptions& o, std::size_t repeats, std::vector<std::size_t> sweep_dim, std::vector<std::size_t> sweep_iters) {
-    o.config.early_stop = false;
+    o.config.early_stop = false;  // the fixed-iteration protocol
     if (repeats == 0) throw seghdc::ConfigError("bench: --repeats must be >= 1");
     const seghdc::ImageBuffer img = seghdc::load_image(o.input);
-    if (sweep_dim.empty()) sweep_dim = {o.config.dim};
-    if (sweep_iters.empty()) sweep_iters = {o.config.iterations};
-    std::string records = "[";
-    bool first = true;
-    for (const std::size_t d : sweep_dim) {
+    if (sweep_dim.empty()) sweep_dim.push_back(o.config.dim);
+    if (sweep_iters.empty()) sweep_iters.push_back(o.config.iterations);
+    std::vector<std::string> records;
+    for (const std::size_t d : sweep_dim)
         for (const std::size_t iters : sweep_iters) {
             seghdc::RunConfig cfg = o.config;
             cfg.dim = d;
             cfg.iterations = iters;
-            cfg.validate(img);
-            std::map<std::string, std::vector<double>> samples;
-            seghdc::PipelineResult last;
-            for (std::size_t r = 0; r < repeats; ++r) {
-                last = seghdc::run_pipeline(img, cfg);
-                for (const auto& [stage, ms] : last.timings.as_map()) samples[stage].push_back(ms);
-            }
-            seghdc::StageTimings med;
-            med.encode_position_ms = median(samples["encode_position"]);
-            med.encode_color_ms = median(samples["encode_color"]);
-            med.produce_pixels_ms = median(samples["produce_pixels"]);
-            med.cluster_ms = median(samples["cluster"]);
-            med.total_ms = median(samples["total"]);
-            MetricsRecord record{{}, last.iterations_run, med, cfg};
-            if (!o.gt.empty()) record.iou = score_against_gt(last.mask, o.gt, cfg.clusters);
-            records += std::string(first ? "\n  " : ",\n  ") + record.to_json("  ");
-            first = false;
-            std::printf("d=%zu iterations=%zu total=%.1f ms cluster=%.1f ms", d, iters, med.total_ms, med.cluster_ms);
+            const MetricsRecord record = bench_one(img, cfg, repeats, o.gt);
+            records.push_back(record.to_json("  "));
+            std::printf("d=%zu iterations=%zu total=%.1f ms cluster=%.1f ms", d, iters, record.timings.total_ms,
+                        record.timings.cluster_ms);
             if (record.iou) std::printf(" iou=%.4f", *record.iou);
             std::printf("\n");
         }
+    if (!o.metrics.empty()) {
+        std::string text = "[";
+        for (std::size_t i = 0; i < records.size(); ++i) text += std::string(i ? ",\n  " : "\n  ") + records[i];
+        write_text(text + (records.empty() ? "]" : "\n]"), o.metrics);
     }
-    records += first ? "]" : "\n]";
-    if (!o.metrics.empty()) write_text(records, o.metrics);
     return kExitOk;
 }
 
 // ---- batch (seghdc_main.cpp:163-225): inputs and ground truths paired by filename stem --------------------
+// Regular files of `dir` by stem, first path (in sorted order) winning a duplicate stem.
 std::map<std::string, fs::path> stem_index(const std::string& dir) {
     if (!fs::is_directory(dir)) throw seghdc::IoError("'" + dir + "' is not a directory");
     std::vector<fs::path> files;
@@ -348,37 +357,41 @@ std::map<std::string, fs::path> stem_index(const std::string& dir) {
 int run_batch(CommonOptions& o) {
     const auto inputs = stem_index(o.input);
     const auto gts = stem_index(o.gt);
-    for (const auto& [stem, path] : inputs)
-        if (!gts.count(stem)) std::cerr << "warning: no ground truth for '" << path.string() << "', skipped\n";
+    struct Pair {
+        std::string stem;
+        fs::path input, gt;
+    };
+    std::vector<Pair> pairs;  // in sorted-stem order
+    for (const auto& [stem, path] : inputs) {
+        const auto gt = gts.find(stem);
+        if (gt == gts.end()) std::cerr << "warning: no ground truth for '" << path.string() << "', skipped\n";
+        else pairs.push_back({stem, path, gt->second});
+    }
     for (const auto& [stem, path] : gts)
         if (!inputs.count(stem)) std::cerr << "warning: no input for ground truth '" << path.string() << "', skipped\n";
-    std::string per_image;
-    double iou_sum = 0.0;
-    std::size_t count = 0;
-    for (const auto& [stem, path] : inputs) {
-        const auto gt_it = gts.find(stem);
-        if (gt_it == gts.end()) continue;
-        const seghdc::ImageBuffer img = seghdc::load_image(path.string());
-        o.config.validate(img);
-        const seghdc::PipelineResult result = seghdc::run_pipeline(img, o.config);
-        const double score = score_against_gt(result.mask, gt_it->second.string(), o.config.clusters);
-        per_image += std::string(count ? ",\n" : "\n") + "    {\n      \"iou\": " + json_number(score) +
-                     ",\n      \"iterations_run\": " + std::to_string(result.iterations_run) +
-                     ",\n      \"stem\": " + json_string(stem) + "\n    }";
-        iou_sum += score;
-        ++count;
-        std::printf("%s  iou=%.4f\n", stem.c_str(), score);
-    }
-    if (count == 0) {
+    if (pairs.empty()) {
         std::cerr << "error: no input/ground-truth pairs matched by filename stem\n";
         return kExitConfig;
     }
-    const double mean = iou_sum / static_cast<double>(count);
+    std::string per_image;
+    double iou_sum = 0.0;
+    for (const Pair& pr : pairs) {
+        const seghdc::ImageBuffer img = seghdc::load_image(pr.input.string());
+        o.config.validate(img);
+        const seghdc::PipelineResult result = seghdc::run_pipeline(img, o.config);
+        const double score = score_against_gt(result.mask, pr.gt.string(), o.config.clusters);
+        per_image += std::string(per_image.empty() ? "\n" : ",\n") + "    {\n      \"iou\": " + json_number(score) +
+                     ",\n      \"iterations_run\": " + std::to_string(result.iterations_run) +
+                     ",\n      \"stem\": " + json_string(pr.stem) + "\n    }";
+        iou_sum += score;
+        std::printf("%s  iou=%.4f\n", pr.stem.c_str(), score);
+    }
+    const double mean = iou_sum / static_cast<double>(pairs.size());
     if (!o.metrics.empty())
-        write_text("{\n  \"count\": " + std::to_string(count) + ",\n  \"mean_iou\": " + json_number(mean) +
+        write_text("{\n  \"count\": " + std::to_string(pairs.size()) + ",\n  \"mean_iou\": " + json_number(mean) +
                        ",\n  \"per_image\": [" + per_image + "\n  ]\n}",
                    o.metrics);
-    std::printf("mean iou over %zu images: %.4f\n", count, mean);
+    std::printf("mean iou over %zu images: %.4f\n", pairs.size(), mean);
     return kExitOk;
 }
 
