@@ -241,6 +241,46 @@ struct PipelineResult {
 };
 PipelineResult run_pipeline(const ImageBuffer& img, const RunConfig& config, const IterationCallback& on_iteration = {});
 
+// ---- scoring (reference metrics.hpp / metrics.cpp:42-101; csrc/seghdc_metrics.cpp) ---------------
+/// Foreground flags, row-major.
+struct BinaryMask {
+    std::size_t height = 0;
+    std::size_t width = 0;
+    std::vector<std::uint8_t> bits;  // 0 or 1
+    bool at(std::size_t i, std::size_t j) const { return bits[i * width + j] != 0; }
+};
+
+/// Any nonzero channel counts as foreground (0/255 ground-truth images).
+BinaryMask binarize_ground_truth(const ImageBuffer& img);
+
+/// |pred AND gt| / |pred OR gt|; 1.0 when both masks are empty. ConfigError on shape mismatch.
+double iou(const BinaryMask& pred, const BinaryMask& gt);
+
+struct ForegroundMatch {
+    double iou = 0.0;
+    std::vector<std::uint32_t> subset;  // cluster labels binarized to foreground
+};
+
+/// Max IoU over every non-empty proper subset of cluster labels (k = 1: the whole image);
+/// ties go to the smallest subset, then the lexicographically smallest. k must be <= 4.
+ForegroundMatch best_foreground_iou(const SegmentationMask& mask, const BinaryMask& gt, std::size_t k);
+
+// ---- image and mask files (reference image_io.hpp / image_io.cpp:31-217; csrc/seghdc_image_io.cpp:
+// a PNG codec over zlib and the P5 reader, the reference's error contract) -----------------------
+/// Reads an 8-bit grayscale or RGB PNG, or a binary PGM (P5). The format is detected from the
+/// magic bytes, not the extension. 16-bit files, PNG colour types other than gray / RGB and
+/// interlaced PNGs are rejected with IoError.
+ImageBuffer load_image(const std::string& path);
+
+/// 8-bit PNG, grayscale for 1 channel, RGB for 3. Deterministic bytes for identical inputs.
+void save_image(const ImageBuffer& img, const std::string& path);
+
+/// 8-bit grayscale PNG with label l mapped to floor(255 l / (k - 1)); k = 1 writes zeros.
+void save_mask(const SegmentationMask& mask, std::size_t k, const std::string& path);
+
+/// Inverse of save_mask's level mapping: every pixel snaps to the nearest of the k levels.
+SegmentationMask labels_from_mask_image(const ImageBuffer& img, std::size_t k);
+
 // ---- B200 extras ------------------------------------------------------------------------------
 // The drop-in uses one CUDA context per host thread on this device (default 0).
 void set_device(int device);
