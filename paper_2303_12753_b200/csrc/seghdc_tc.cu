@@ -1293,7 +1293,9 @@ __global__ void __launch_bounds__(TcCfg<NCOL, SPLIT>::Warps * 32, 1)
 // 4j+1 / 4j as 1.0, c = 1 / 3 carry bits 4j+2 / 4j+3 as 2.0. Row n = kP8 * cluster + p holds
 // digit p of the centroid entry (weight 1) or half of it (weight 2), so every product is bit * d.
 // balanced base 8 (digits [-4, 3]) or base 9 (digits [-4, 4])
-__device__ __forceinline__ int digit_b(long long z, uint32_t p, uint32_t base) {
+// (BASE is a compile-time constant: the divisions become multiplies)
+template <uint32_t base>
+__device__ __forceinline__ int digit_b(long long z, uint32_t p) {
     for (uint32_t q = 0;; ++q) {
         int r = int(z % base);
         if (r >= int(base) - 4) r -= int(base);
@@ -1301,13 +1303,14 @@ __device__ __forceinline__ int digit_b(long long z, uint32_t p, uint32_t base) {
         z = (z - r) / base;
     }
 }
+template <uint32_t base>
 __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t ks, uint32_t n,
-                                             uint32_t k, uint32_t ndig, uint32_t base) {
+                                             uint32_t k, uint32_t ndig) {
     const uint32_t col = k >> 3, j = k & 7, h = col >> 2, c = col & 3;
     const uint32_t dim = 32 * (2 * ks + h) + 4 * j + (c == 0 ? 1u : c == 1 ? 2u : c == 2 ? 0u : 3u);
     const uint32_t cl = n / ndig, p = n % ndig;
     if (cl >= K || dim >= D) return 0;
-    const int d = digit_b((long long)Z[size_t(cl) * D + dim], p, base);
+    const int d = digit_b<base>((long long)Z[size_t(cl) * D + dim], p);
     const uint32_t a = uint32_t(d < 0 ? -d : d);
     // weight 1: |d| in 0..4 -> e2m1 {0, 1, 2, 3, 4}; weight 2: |d|/2 in {0, .5, 1, 1.5, 2}
     const uint32_t code = (c & 1) ? a : (a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : a == 3 ? 5u : 6u);
@@ -1315,8 +1318,9 @@ __device__ __forceinline__ uint32_t b_nibble(const uint32_t* Z, uint32_t K, uint
 }
 // pair: the CTA-pair layout [column half][k-step][kb / 2] (each CTA of a pair copies one contiguous
 // half of the digit columns of its k-steps) instead of [k-step][kb]
+template <uint32_t BASE>
 __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_t D, uint32_t nks, uint32_t kb,
-                             uint32_t ndig, uint32_t base, uint8_t* __restrict__ bimg, const void* state, uint32_t pair,
+                             uint32_t ndig, uint8_t* __restrict__ bimg, const void* state, uint32_t pair,
                              uint32_t* __restrict__ clear, uint32_t clear_n) {
     if (state && StateView::at(const_cast<void*>(state), K).hdr->done) return;
     // init only: the exchange buffer the previous kernel (k_finish) consumed is zeroed here, so
@@ -1328,7 +1332,7 @@ __global__ void k_build_bimg(const uint32_t* __restrict__ Z, uint32_t K, uint32_
         const uint32_t rem = pair ? (i / (nks * half)) * half + i % half : i % kb;
         const uint32_t grp = rem / 256, r2 = rem % 256, cm = r2 / 128, row = (r2 % 128) / 16, b = r2 % 16;
         const uint32_t n = grp * 8 + row, k = 32 * cm + 2 * b;
-        bimg[i] = uint8_t(b_nibble(Z, K, D, ks, n, k, ndig, base) | (b_nibble(Z, K, D, ks, n, k + 1, ndig, base) << 4));
+        bimg[i] = uint8_t(b_nibble<BASE>(Z, K, D, ks, n, k, ndig) | (b_nibble<BASE>(Z, K, D, ks, n, k + 1, ndig) << 4));
     }
 }
 
@@ -1654,7 +1658,10 @@ void launch_build_bimg(const uint32_t* Z, uint32_t K, uint32_t D, uint32_t W32, 
     const uint32_t nc = tc_ncol(K, W32), nks = tc_ksteps(W32), kb = nc * 32;
     const uint32_t total = nks * kb;
     const uint32_t pair = (nc == 64 && tc_split(K, W32) > 1 && TcCfg<64, 4>::PAIR) ? 1u : 0u;
-    k_build_bimg<<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), tc_base(nc), bimg, state, pair, clear, clear_n);
+    if (tc_base(nc) == 9)
+        k_build_bimg<9><<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), bimg, state, pair, clear, clear_n);
+    else
+        k_build_bimg<8><<<(total + 255) / 256, 256, 0, s>>>(Z, K, D, nks, kb, tc_ndig(nc), bimg, state, pair, clear, clear_n);
 }
 
 #ifdef SEGHDC_HANGDBG
