@@ -1499,11 +1499,12 @@ __global__ void __launch_bounds__(768) k_fold_list(const uint32_t* __restrict__ 
 void launch_fold_list(const uint32_t* list, const uint32_t* count, uint64_t max_rows, uint32_t nlists,
                       const uint32_t* grid, uint32_t S32, uint32_t W32, int32_t* dst, uint32_t dst_stride,
                       uint32_t sms, cudaStream_t s) {
-    const dim3 ctas(sms, nlists);
+    static const char* fc_env = getenv("SEGHDC_FOLD_CTAS");  // experiment switch: CTAs per list
+    const dim3 ctas(fc_env && atoi(fc_env) > 0 ? uint32_t(atoi(fc_env)) : sms, nlists);
     const uint32_t ng = W32 > 384 ? 1 : 2;  // row groups per CTA (768 threads at most)
     const uint32_t threads = ng * 32 * ((W32 + 31) / 32);
     const size_t smem = size_t(32) * W32 * 4;
-    const uint64_t per_group = (max_rows + ng * sms - 1) / (ng * sms) + 64;  // inputs per counter
+    const uint64_t per_group = (max_rows + ng * ctas.x - 1) / (ng * ctas.x) + 64;  // inputs per counter
     uint32_t* d = reinterpret_cast<uint32_t*>(dst);
     if (per_group <= BitCounter<8>::capacity()) {
         ensure_dynamic_smem((const void*)k_fold_list<8>, smem);
